@@ -1,0 +1,243 @@
+/*
+ * tuckerplan_b200 — C ABI of the B200-native HOOI engine.
+ *
+ * This is the drop-in boundary for the reference's header-only C++ API
+ * (`#include "tuckerplan/tuckerplan.hpp"`, reference proj/include/tuckerplan/).
+ * The reference has no FFI of its own; every entry point below names the
+ * reference function it replaces (file:line relative to
+ * /root/reference/proj/include/tuckerplan/).  The C++ wrappers in
+ * include/tuckerplan/ (this repo) re-create the reference signatures on top of
+ * these calls; INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *   - plain pointers and sizes only; the caller owns every host buffer, the
+ *     library owns device memory behind opaque handles;
+ *   - every function returns TP_OK (0) or an error code; codes 1..13 are the
+ *     reference's `Errc` ordinals + 1 (errors.hpp:16-30); the offending mode
+ *     and message are read with tp_last_error_mode() / tp_last_error();
+ *   - matrices are COLUMN-MAJOR (rows x cols, leading dimension = rows), the
+ *     layout of Eigen::MatrixXd in the reference signatures; tensors are
+ *     row-major, last index fastest (dense_tensor.hpp:19-30);
+ *   - trees are flat arrays kind/mode/parent in the reference's stored order
+ *     (parent first, node 0 = root, children in insertion order,
+ *     ttm_tree.hpp:36-57); kinds are 0 root, 1 mode, 2 leaf (ttm_tree.hpp:27);
+ *   - a context is bound to one CUDA device and is not thread-safe;
+ *   - there is NO CPU fallback: device entry points fail with TP_ERR_CUDA when
+ *     no sm_100 device / driver is present.
+ */
+#ifndef TUCKERPLAN_B200_H
+#define TUCKERPLAN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef uint64_t tp_u64;
+
+/* errors.hpp:16-30 (ordinal + 1) */
+enum {
+  TP_OK = 0,
+  TP_ERR_BAD_DIMS = 1,
+  TP_ERR_K_TOO_LARGE = 2,
+  TP_ERR_OVERFLOW = 3,
+  TP_ERR_BAD_TREE = 4,
+  TP_ERR_BAD_MODE = 5,
+  TP_ERR_SHAPE_MISMATCH = 6,
+  TP_ERR_INVALID_GRID = 7,
+  TP_ERR_NO_VALID_GRID = 8,
+  TP_ERR_MISSING_ASSIGNMENT = 9,
+  TP_ERR_TOO_LARGE = 10,
+  TP_ERR_ZERO_TENSOR = 11,
+  TP_ERR_NEEDS_CHAIN_TREE = 12,
+  TP_ERR_BAD_ARGUMENT = 13,
+  /* outside the reference enum */
+  TP_ERR_CUDA = 100,      /* CUDA / cuSOLVER runtime failure, or no device */
+  TP_ERR_NCCL = 101,      /* NCCL failure */
+  TP_ERR_CAPACITY = 102,  /* caller-provided output array too small */
+  TP_ERR_INTERNAL = 103
+};
+
+enum { TP_NODE_ROOT = 0, TP_NODE_MODE = 1, TP_NODE_LEAF = 2 };      /* ttm_tree.hpp:27 */
+enum { TP_CHAIN_INPUT = 0, TP_CHAIN_BY_COST = 1, TP_CHAIN_BY_RATIO = 2 }; /* tree_builders.hpp:25 */
+enum { TP_SWEEP_JACOBI = 0, TP_SWEEP_GAUSS_SEIDEL = 1 };            /* hooi.hpp:132 */
+/* bench.hpp:115 TreeStrategy */
+enum { TP_TREE_CHAIN_INPUT = 0, TP_TREE_CHAIN_BY_COST = 1, TP_TREE_CHAIN_BY_RATIO = 2,
+       TP_TREE_BALANCED = 3, TP_TREE_OPTIMAL = 4 };
+
+#define TP_MAX_MODES 16        /* mode_set.hpp:15 */
+#define TP_MAX_GRAM_ROWS 2048  /* hooi.hpp:32 */
+
+const char* tp_last_error(void);   /* message of the last failure on this thread */
+int tp_last_error_mode(void);      /* Error::mode() of that failure, -1 if none */
+const char* tp_version(void);
+
+/* ------------------------------------------------------------------ planner
+ * Pure host code, exact u64 arithmetic, selections bit-identical to the
+ * reference. */
+
+/* validate_spec — problem.hpp:37-53 */
+int tp_validate_spec(int n_modes, const tp_u64* L, const tp_u64* K);
+/* input/core/partial_cardinality — problem.hpp:67-86 (done_mask bit m = mode m multiplied) */
+int tp_partial_cardinality(int n_modes, const tp_u64* L, const tp_u64* K, uint32_t done_mask, tp_u64* out);
+
+/* optimal_tree — tree_opt.hpp:126-138.  Writes up to `cap` nodes. */
+int tp_optimal_tree(int n_modes, const tp_u64* L, const tp_u64* K, int cap, int* kind, int* mode, int* parent,
+                    int* n_nodes, tp_u64* total_macs, tp_u64* dp_states);
+/* optimal_cost_reuse_greedy — tree_opt.hpp:143-150 */
+int tp_reuse_greedy_cost(int n_modes, const tp_u64* L, const tp_u64* K, tp_u64* cost);
+/* chain_tree — tree_builders.hpp:49-60 */
+int tp_chain_tree(int n_modes, const tp_u64* L, const tp_u64* K, int order, int cap, int* kind, int* mode,
+                  int* parent, int* n_nodes);
+/* balanced_tree — tree_builders.hpp:85-91 */
+int tp_balanced_tree(int n_modes, const tp_u64* L, const tp_u64* K, int cap, int* kind, int* mode, int* parent,
+                     int* n_nodes);
+/* build_tree — bench.hpp:128-137 */
+int tp_build_tree(int n_modes, const tp_u64* L, const tp_u64* K, int strategy, int cap, int* kind, int* mode,
+                  int* parent, int* n_nodes);
+/* validate_tree — ttm_tree.hpp:103-119 */
+int tp_validate_tree(int n_modes, const tp_u64* L, const tp_u64* K, int n_nodes, const int* kind,
+                     const int* mode, const int* parent);
+/* is_canonical / canonicalize / tree_depth — ttm_tree.hpp:123-187 */
+int tp_tree_is_canonical(int n_nodes, const int* kind, const int* mode, const int* parent, int* out);
+int tp_canonicalize(int n_modes, int n_nodes, const int* kind, const int* mode, const int* parent, int cap,
+                    int* out_kind, int* out_mode, int* out_parent, int* out_n_nodes);
+int tp_tree_depth(int n_nodes, const int* kind, const int* mode, const int* parent, int* depth);
+/* node_cardinalities + tree_cost — tree_cost.hpp:25-63.  card_in/card_out/per_node_macs have n_nodes entries
+ * (any may be NULL). */
+int tp_tree_cost(int n_modes, const tp_u64* L, const tp_u64* K, int n_nodes, const int* kind, const int* mode,
+                 const int* parent, tp_u64* total_macs, tp_u64* per_node_macs, tp_u64* card_in, tp_u64* card_out,
+                 int* n_internal, int* depth);
+
+/* grid_count psi(P,N) — grid.hpp:49-70 */
+int tp_grid_count(tp_u64 procs, int n_modes, tp_u64* out);
+/* validate_grid — grid.hpp:36-45 */
+int tp_validate_grid(int n_modes, const tp_u64* L, const tp_u64* K, const tp_u64* q, tp_u64 procs);
+/* enumerate_grids — grid.hpp:96-111.  grids_out is cap_grids x n_modes, lexicographic order. */
+int tp_enumerate_grids(int n_modes, const tp_u64* L, const tp_u64* K, tp_u64 procs, size_t cap_grids,
+                       tp_u64* grids_out, size_t* n_grids);
+/* block_bounds / block_of — grid.hpp:114-125.  cuts has parts+1 entries. */
+int tp_block_bounds(tp_u64 len, tp_u64 parts, tp_u64* cuts);
+int tp_block_of(tp_u64 c, tp_u64 len, tp_u64 parts, tp_u64* out);
+/* static_volume — grid_volume.hpp:32-46.  per_node_ttm has n_nodes entries (0 for root/leaves), may be NULL. */
+int tp_static_volume(int n_modes, const tp_u64* L, const tp_u64* K, int n_nodes, const int* kind, const int* mode,
+                     const int* parent, const tp_u64* q, tp_u64 procs, tp_u64* total, tp_u64* per_node_ttm);
+/* optimal_static_grid — grid_volume.hpp:56-110 (first minimum in lexicographic order). */
+int tp_optimal_static_grid(int n_modes, const tp_u64* L, const tp_u64* K, int n_nodes, const int* kind,
+                           const int* mode, const int* parent, tp_u64 procs, int threads, tp_u64* q_out,
+                           tp_u64* total, tp_u64* per_node_ttm);
+
+/* --------------------------------------------------------- seeded host data
+ * libstdc++ mt19937_64 + ONE normal_distribution<double>(0,1) object. */
+
+/* random_tensor — dense_tensor.hpp:43-49.  out has prod(dims) entries. */
+int tp_random_tensor(int n_modes, const size_t* dims, tp_u64 seed, double* out);
+/* the factor part of random_decomposition — hooi.hpp:109-120: per mode an L_n x K_n gaussian matrix filled column
+ * by column from one shared stream, thin Q of its Householder QR.  factors_out[n] is L_n x K_n column-major. */
+int tp_random_orthonormal_factors(int n_modes, const tp_u64* L, const tp_u64* K, tp_u64 seed,
+                                  double* const* factors_out);
+/* frobenius_norm — dense_tensor.hpp:51-55 (host data; same left-to-right sum) */
+int tp_frobenius_norm_host(size_t n, const double* data, double* out);
+
+/* ------------------------------------------------------------ device engine */
+typedef struct tp_ctx tp_ctx;
+typedef struct tp_tensor tp_tensor;   /* row-major FP64 tensor resident in HBM */
+typedef struct tp_plan tp_plan;       /* spec + tree + arena + launch schedule for repeated sweeps */
+
+int tp_ctx_create(int device, tp_ctx** out);
+int tp_ctx_destroy(tp_ctx* ctx);
+int tp_ctx_synchronize(tp_ctx* ctx);
+/* the CUDA stream the engine launches on (cudaStream_t as void*), for event timing by the caller */
+int tp_ctx_stream(tp_ctx* ctx, void** stream_out);
+/* number of kernels this context has launched so far (own kernels + cuSOLVER calls counted separately) */
+int tp_ctx_launch_counts(tp_ctx* ctx, tp_u64* own_kernels, tp_u64* library_calls);
+
+/* pinned host staging buffers for callers that want full-speed PCIe copies */
+int tp_host_alloc(size_t bytes, void** out);
+int tp_host_free(void* p);
+
+/* DenseTensor upload/download (dense_tensor.hpp:19-30 value type <-> device handle) */
+int tp_tensor_upload(tp_ctx* ctx, int n_modes, const size_t* dims, const double* host, tp_tensor** out);
+int tp_tensor_alloc(tp_ctx* ctx, int n_modes, const size_t* dims, tp_tensor** out);   /* zeros(), :32-39 */
+int tp_tensor_download(tp_ctx* ctx, const tp_tensor* t, double* host);
+int tp_tensor_free(tp_ctx* ctx, tp_tensor* t);
+int tp_tensor_dims(const tp_tensor* t, int* n_modes, size_t* dims /* TP_MAX_MODES entries */);
+void* tp_tensor_device_ptr(const tp_tensor* t);
+/* frobenius_norm — dense_tensor.hpp:51-55, on the device (deterministic pairwise reduction) */
+int tp_tensor_norm(tp_ctx* ctx, const tp_tensor* t, double* out);
+
+/* ttm — ttm.hpp:73-96.  m is new_len x dims[mode], column-major host matrix.  *macs (may be NULL) is
+ * ACCUMULATED with the exact new_len * size(t), overflow-checked. */
+int tp_ttm(tp_ctx* ctx, const tp_tensor* t, const double* m, size_t m_rows, size_t m_cols, int mode, tp_u64* macs,
+           tp_tensor** out);
+/* same with the matrix already on the device as a ROW-major m_rows x m_cols array (== column-major transpose,
+ * i.e. a reference factor F (L x K col-major) passed as F^T without any copy, hooi.hpp:98,153) */
+int tp_ttm_device(tp_ctx* ctx, const tp_tensor* t, const double* m_dev_rowmajor, size_t m_rows, size_t m_cols,
+                  int mode, tp_u64* macs, tp_tensor** out);
+
+/* leading_left_factors — hooi.hpp:45-76.  m is rows x cols column-major on the host; vectors_out rows x k
+ * column-major; *degenerate 0/1. */
+int tp_leading_left_factors(tp_ctx* ctx, const double* m, size_t rows, size_t cols, int k, double* vectors_out,
+                            int* degenerate);
+/* Gram + truncated basis of the mode-n unfolding of a device tensor, without materialising the unfolding
+ * (unfold ttm.hpp:43-53 + leading_left_factors hooi.hpp:45-76 as used at hooi.hpp:147-151) */
+int tp_leaf_factor(tp_ctx* ctx, const tp_tensor* t, int mode, int k, double* vectors_out, int* degenerate);
+/* Gram matrix Y_(n) Y_(n)^T only (rows x rows, symmetric, column-major, full storage) */
+int tp_gram(tp_ctx* ctx, const tp_tensor* t, int mode, double* gram_out);
+
+typedef struct tp_sweep_stats {   /* SweepStats, hooi.hpp:125-130 */
+  tp_u64 tree_macs;
+  tp_u64 core_macs;
+  int peak_live;
+  int degenerate;
+} tp_sweep_stats;
+
+typedef struct tp_sweep_timing {  /* device milliseconds of the last sweep, CUDA events on the engine stream */
+  float total_ms;
+  float tree_ms;   /* TTM-tree phase: every tree TTM (+ the factor-fragment prep kernels) */
+  float gram_ms;
+  float evd_ms;    /* eigen-solve + sign/gap kernel */
+  float core_ms;
+} tp_sweep_timing;
+
+/* Build the launch schedule for hooi_sweep (hooi.hpp:189-229) on a fixed spec/tree: validates, sizes the arena from
+ * node_cardinalities, allocates device factors.  kind: TP_SWEEP_JACOBI or TP_SWEEP_GAUSS_SEIDEL (chain trees only,
+ * TP_ERR_NEEDS_CHAIN_TREE otherwise). */
+int tp_plan_create(tp_ctx* ctx, int n_modes, const tp_u64* L, const tp_u64* K, int n_nodes, const int* kind,
+                   const int* mode, const int* parent, int sweep_kind, tp_plan** out);
+int tp_plan_destroy(tp_ctx* ctx, tp_plan* plan);
+/* Decomposition::factors (hooi.hpp:78-81) <-> device: factors[n] is L_n x K_n column-major on the host */
+int tp_plan_set_factors(tp_ctx* ctx, tp_plan* plan, const double* const* factors);
+int tp_plan_get_factors(tp_ctx* ctx, tp_plan* plan, double* const* factors_out);
+/* Decomposition::core — prod(K) doubles, row-major */
+int tp_plan_get_core(tp_ctx* ctx, tp_plan* plan, double* core_out);
+int tp_plan_core_norm(tp_ctx* ctx, tp_plan* plan, double* out);
+/* core_from_factors — hooi.hpp:93-100 with the plan's current factors (used by random_decomposition, :121) */
+int tp_plan_compute_core(tp_ctx* ctx, tp_plan* plan, const tp_tensor* t);
+/* One hooi_sweep on the device-resident tensor: the plan's factors are the input Decomposition and are replaced by
+ * the output one; the core is recomputed (hooi.hpp:227).  stats may be NULL. */
+int tp_plan_sweep(tp_ctx* ctx, tp_plan* plan, const tp_tensor* t, tp_sweep_stats* stats);
+int tp_plan_last_timing(tp_ctx* ctx, tp_plan* plan, tp_sweep_timing* out);
+/* reconstruction_error — hooi.hpp:232-245, full expansion on the device (materialises |T| elements). */
+int tp_plan_reconstruction_error(tp_ctx* ctx, tp_plan* plan, const tp_tensor* t, double* out);
+/* same quantity from ||T||^2 - ||G||^2 (valid for orthonormal factors and the core of those factors) */
+int tp_plan_fit_from_norms(tp_ctx* ctx, tp_plan* plan, const tp_tensor* t, double* out);
+
+/* reconstruction_error for an arbitrary host Decomposition (core row-major with dims core_dims, factors[n]
+ * dims[n] x core_dims[n] column-major) */
+int tp_reconstruction_error(tp_ctx* ctx, const tp_tensor* t, const size_t* core_dims, const double* core,
+                            const double* const* factors, double* out);
+
+/* By-value hooi_sweep (hooi.hpp:189-191): host tensor + host factors in, host factors + core out; uploads, runs,
+ * downloads.  This is the call the reference-facing C++ wrapper makes. */
+int tp_hooi_sweep_host(tp_ctx* ctx, int n_modes, const size_t* dims, const double* tensor, const tp_u64* K,
+                       const double* const* factors_in, int n_nodes, const int* kind, const int* mode,
+                       const int* parent, int sweep_kind, double* const* factors_out, double* core_out,
+                       tp_sweep_stats* stats);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TUCKERPLAN_B200_H */
