@@ -167,6 +167,8 @@ int tp_tensor_dims(const tp_tensor* t, int* n_modes, size_t* dims /* TP_MAX_MODE
 void* tp_tensor_device_ptr(const tp_tensor* t);
 /* frobenius_norm — dense_tensor.hpp:51-55, on the device (deterministic pairwise reduction) */
 int tp_tensor_norm(tp_ctx* ctx, const tp_tensor* t, double* out);
+/* y = beta * y + alpha * x, elementwise on the device (input assembly: T = X + sigma E; no reference counterpart) */
+int tp_tensor_axpby(tp_ctx* ctx, tp_tensor* y, double beta, double alpha, const tp_tensor* x);
 
 /* ttm — ttm.hpp:73-96.  m is new_len x dims[mode], column-major host matrix.  *macs (may be NULL) is
  * ACCUMULATED with the exact new_len * size(t), overflow-checked. */
@@ -220,6 +222,10 @@ int tp_plan_compute_core(tp_ctx* ctx, tp_plan* plan, const tp_tensor* t);
  * the output one; the core is recomputed (hooi.hpp:227).  stats may be NULL. */
 int tp_plan_sweep(tp_ctx* ctx, tp_plan* plan, const tp_tensor* t, tp_sweep_stats* stats);
 int tp_plan_last_timing(tp_ctx* ctx, tp_plan* plan, tp_sweep_timing* out);
+/* per tree node of the last sweep (n_nodes entries each, either may be NULL): node_ms = device time of the node's
+ * TTM launch (mode nodes) or Gram kernels (leaves); evd_ms = eigen-solve + basis selection (leaves, else 0).
+ * Jacobi plans only. */
+int tp_plan_node_timing(tp_ctx* ctx, tp_plan* plan, int n_nodes, float* node_ms, float* evd_ms);
 /* reconstruction_error — hooi.hpp:232-245, full expansion on the device (materialises |T| elements). */
 int tp_plan_reconstruction_error(tp_ctx* ctx, tp_plan* plan, const tp_tensor* t, double* out);
 /* same quantity from ||T||^2 - ||G||^2 (valid for orthonormal factors and the core of those factors) */

@@ -1,0 +1,1065 @@
+// Device engine behind the C ABI: context, HBM-resident tensors, the TTM-tree
+// executor (hooi_sweep), Gram + eigen-solve leaf updates, core and fit.
+//
+// Reference behaviour followed (proj/include/tuckerplan): ttm.hpp:73-96,
+// hooi.hpp:45-76 (leaf update), :93-100 (core), :136-159 (Jacobi walk),
+// :163-229 (Gauss-Seidel + sweep driver), :232-245 (reconstruction error).
+//
+// HBM layout: tensors are row-major FP64, exactly the reference's
+// DenseTensor::data order; factors are L_n x K_n column-major (Eigen::MatrixXd
+// order), which read as row-major is the K_n x L_n matrix F^T a tree TTM needs.
+// A sweep never allocates: intermediates live in one buffer per tree depth
+// (depth-first execution frees in tree order, so depth d has one live tensor),
+// sized from the planner's node cardinalities.
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.hpp"
+#include "kernels.cuh"
+#include "planner.hpp"
+
+namespace tpb {
+
+[[noreturn]] static void cuda_fail(cudaError_t e, const char* what) {
+  raise(TP_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define TPB_CUDA(expr)                               \
+  do {                                               \
+    cudaError_t tpb_e_ = (expr);                     \
+    if (tpb_e_ != cudaSuccess) cuda_fail(tpb_e_, #expr); \
+  } while (0)
+#define TPB_SOLVER(expr)                                                                        \
+  do {                                                                                          \
+    cusolverStatus_t tpb_s_ = (expr);                                                           \
+    if (tpb_s_ != CUSOLVER_STATUS_SUCCESS)                                                      \
+      raise(TP_ERR_CUDA, std::string(#expr) + ": cusolver status " + std::to_string(static_cast<int>(tpb_s_))); \
+  } while (0)
+
+}  // namespace tpb
+
+using namespace tpb;
+
+struct tp_ctx {
+  int device = 0;
+  int sm_count = 148;
+  cudaStream_t stream = nullptr;
+  cusolverDnHandle_t solver = nullptr;
+  u64 own_kernels = 0;
+  u64 library_calls = 0;
+  double* reduce_scratch = nullptr;  // reduce_scratch_doubles() + 1 result slot
+  double* frag_scratch = nullptr;    // fragment buffer for one-off TTMs
+  size_t frag_capacity = 0;
+};
+
+struct tp_tensor {
+  std::vector<size_t> dims;
+  size_t size = 0;
+  double* data = nullptr;
+};
+
+namespace tpb {
+namespace {
+
+void bind(const tp_ctx* ctx) {
+  if (!ctx) raise(TP_ERR_BAD_ARGUMENT, "null context");
+  TPB_CUDA(cudaSetDevice(ctx->device));
+}
+
+double* device_alloc(size_t doubles) {
+  double* p = nullptr;
+  const cudaError_t e = cudaMalloc(&p, std::max<size_t>(doubles, 1) * sizeof(double));
+  if (e != cudaSuccess) raise(TP_ERR_CUDA, std::string("cudaMalloc of ") + std::to_string(doubles * 8) + " bytes: " +
+                                               cudaGetErrorString(e));
+  return p;
+}
+
+size_t checked_size(int n_modes, const size_t* dims) {
+  if (n_modes <= 0 || n_modes > kMaxModes || !dims) raise(TP_ERR_BAD_DIMS, "tensor needs 1..16 modes");
+  u64 total = 1;
+  for (int m = 0; m < n_modes; ++m) {
+    if (dims[m] == 0) raise(TP_ERR_BAD_DIMS, "zero extent", m);  // zeros(), dense_tensor.hpp:35-36
+    total = mul_or_throw(total, dims[m]);
+  }
+  return static_cast<size_t>(total);
+}
+
+tp_tensor* new_tensor(const std::vector<size_t>& dims) {
+  tp_tensor* t = new tp_tensor;
+  t->dims = dims;
+  t->size = checked_size(static_cast<int>(dims.size()), dims.data());
+  try {
+    t->data = device_alloc(t->size);
+  } catch (...) {
+    delete t;
+    throw;
+  }
+  return t;
+}
+
+void mode_extents(const std::vector<size_t>& dims, int mode, long long& outer, long long& inner) {
+  if (mode < 0 || mode >= static_cast<int>(dims.size())) raise(TP_ERR_BAD_MODE, "mode out of range", mode);
+  outer = inner = 1;
+  for (int m = 0; m < mode; ++m) outer *= static_cast<long long>(dims[m]);
+  for (int m = mode + 1; m < static_cast<int>(dims.size()); ++m) inner *= static_cast<long long>(dims[m]);
+}
+
+double* ensure_frag_scratch(tp_ctx* ctx, size_t doubles) {
+  if (doubles > ctx->frag_capacity) {
+    if (ctx->frag_scratch) {
+      TPB_CUDA(cudaStreamSynchronize(ctx->stream));
+      TPB_CUDA(cudaFree(ctx->frag_scratch));
+      ctx->frag_scratch = nullptr;
+      ctx->frag_capacity = 0;
+    }
+    ctx->frag_scratch = device_alloc(doubles);
+    ctx->frag_capacity = doubles;
+  }
+  return ctx->frag_scratch;
+}
+
+// One TTM with an arbitrary-stride device matrix (prep + contraction), out preallocated.
+void run_ttm(tp_ctx* ctx, const double* x, const std::vector<size_t>& dims, int mode, const double* m_dev,
+             long long row_stride, long long col_stride, long long new_len, double* frag, double* out) {
+  long long outer, inner;
+  mode_extents(dims, mode, outer, inner);
+  const long long len = static_cast<long long>(dims[mode]);
+  const TtmFragmentLayout f = ttm_fragment_layout(new_len, len);
+  if (!frag) frag = ensure_frag_scratch(ctx, f.doubles);
+  TPB_CUDA(prep_factor_fragments(ctx->stream, m_dev, row_stride, col_stride, new_len, len, f, frag));
+  TPB_CUDA(launch_ttm(ctx->stream, x, outer, len, inner, frag, f, new_len, out));
+  ctx->own_kernels += 2;
+}
+
+double device_scalar(tp_ctx* ctx, const double* dev) {
+  double v = 0.0;
+  TPB_CUDA(cudaMemcpyAsync(&v, dev, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  TPB_CUDA(cudaStreamSynchronize(ctx->stream));
+  return v;
+}
+
+double sum_squares(tp_ctx* ctx, const double* x, size_t n) {
+  double* result = ctx->reduce_scratch + reduce_scratch_doubles();
+  TPB_CUDA(launch_sum_squares(ctx->stream, x, n, ctx->reduce_scratch, result));
+  ctx->own_kernels += 2;
+  return device_scalar(ctx, result);
+}
+
+double diff_sum_squares(tp_ctx* ctx, const double* x, const double* y, size_t n) {
+  double* result = ctx->reduce_scratch + reduce_scratch_doubles();
+  TPB_CUDA(launch_diff_sum_squares(ctx->stream, x, y, n, ctx->reduce_scratch, result));
+  ctx->own_kernels += 2;
+  return device_scalar(ctx, result);
+}
+
+// Eigen-solve scratch shared by every leaf update of a plan / one-off call.
+struct LeafScratch {
+  long long max_rows = 0;
+  double* gram = nullptr;      // rows x rows, overwritten with eigenvectors
+  double* gram_ws = nullptr;   // split-k partials
+  size_t gram_ws_doubles = 0;
+  double* w = nullptr;         // eigenvalues
+  double* work = nullptr;
+  int lwork = 0;
+  int* info = nullptr;
+  int* flag = nullptr;         // degenerate flag, OR-ed by leaves
+
+  void release() {
+    cudaFree(gram);
+    cudaFree(gram_ws);
+    cudaFree(w);
+    cudaFree(work);
+    cudaFree(info);
+    cudaFree(flag);
+    *this = LeafScratch{};
+  }
+};
+
+void leaf_scratch_reserve(tp_ctx* ctx, LeafScratch& s, long long rows, size_t gram_ws_doubles) {
+  if (rows > s.max_rows) {
+    cudaFree(s.gram);
+    cudaFree(s.w);
+    cudaFree(s.work);
+    s.gram = device_alloc(static_cast<size_t>(rows) * rows);
+    s.w = device_alloc(static_cast<size_t>(rows));
+    int lwork = 0;
+    TPB_SOLVER(cusolverDnDsyevd_bufferSize(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
+                                           static_cast<int>(rows), s.gram, static_cast<int>(rows), s.w, &lwork));
+    s.work = device_alloc(static_cast<size_t>(lwork));
+    s.lwork = lwork;
+    s.max_rows = rows;
+  }
+  if (gram_ws_doubles > s.gram_ws_doubles) {
+    cudaFree(s.gram_ws);
+    s.gram_ws = device_alloc(gram_ws_doubles);
+    s.gram_ws_doubles = gram_ws_doubles;
+  }
+  if (!s.info) {
+    TPB_CUDA(cudaMalloc(&s.info, sizeof(int)));
+    TPB_CUDA(cudaMalloc(&s.flag, sizeof(int)));
+    TPB_CUDA(cudaMemsetAsync(s.flag, 0, sizeof(int), ctx->stream));
+  }
+}
+
+void check_leaf_args(long long rows, long long cols, int k) {  // hooi.hpp:46-51
+  if (rows == 0 || cols == 0) raise(TP_ERR_SHAPE_MISMATCH, "empty matrix");
+  if (rows > TP_MAX_GRAM_ROWS) raise(TP_ERR_TOO_LARGE, "unfolding has too many rows for the Gram route");
+  if (k < 1 || k > rows) raise(TP_ERR_BAD_ARGUMENT, "need 1 <= k <= rows");
+}
+
+// Gram of the mode-`mode` unfolding of y into s.gram (hooi.hpp:53-54 without the unfold copy of :148-149).
+long long leaf_gram(tp_ctx* ctx, LeafScratch& s, const double* y, const std::vector<size_t>& dims, int mode, int k) {
+  long long outer, inner;
+  mode_extents(dims, mode, outer, inner);
+  const long long rows = static_cast<long long>(dims[mode]);
+  check_leaf_args(rows, outer * inner, k);
+  const GramLayout g = gram_layout(outer, rows, inner, ctx->sm_count);
+  leaf_scratch_reserve(ctx, s, rows, g.workspace_doubles);
+  TPB_CUDA(launch_gram(ctx->stream, y, outer, rows, inner, g, s.gram_ws, s.gram));
+  ctx->own_kernels += 2;
+  return rows;
+}
+
+// Top-k eigenvectors of s.gram into factor_out (rows x k column-major): full symmetric eigen-solve (hooi.hpp:55),
+// then the sign / gap rules (hooi.hpp:60-74).  The eigen-solve is cuSOLVER's (off the hot path per the spec).
+void leaf_solve(tp_ctx* ctx, LeafScratch& s, long long rows, int k, double* factor_out) {
+  TPB_SOLVER(cusolverDnDsyevd(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, static_cast<int>(rows),
+                              s.gram, static_cast<int>(rows), s.w, s.work, s.lwork, s.info));
+  ctx->library_calls += 1;
+  TPB_CUDA(launch_select_basis(ctx->stream, s.gram, s.w, static_cast<int>(rows), k, factor_out, s.flag));
+  ctx->own_kernels += 1;
+}
+
+void leaf_update(tp_ctx* ctx, LeafScratch& s, const double* y, const std::vector<size_t>& dims, int mode, int k,
+                 double* factor_out) {
+  const long long rows = leaf_gram(ctx, s, y, dims, mode, k);
+  leaf_solve(ctx, s, rows, k, factor_out);
+}
+
+int read_and_clear_flag(tp_ctx* ctx, LeafScratch& s) {
+  int host[2] = {0, 0};
+  TPB_CUDA(cudaMemcpyAsync(&host[0], s.flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  TPB_CUDA(cudaMemcpyAsync(&host[1], s.info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  TPB_CUDA(cudaMemsetAsync(s.flag, 0, sizeof(int), ctx->stream));
+  TPB_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (host[1] != 0) raise(TP_ERR_TOO_LARGE, "eigensolver did not converge");  // hooi.hpp:56-57
+  return host[0];
+}
+
+}  // namespace
+}  // namespace tpb
+
+// ------------------------------------------------------------------------ plan
+struct tp_plan {
+  Spec spec;
+  Tree tree;
+  int sweep_kind = TP_SWEEP_JACOBI;
+  int n = 0;
+  std::vector<std::vector<int>> gs_paths;
+  std::vector<double*> cur, fresh;            // device factors, L_n x K_n column-major
+  std::vector<TtmFragmentLayout> frag_layout; // for F_n^T (K_n x L_n) as the TTM matrix
+  std::vector<double*> frag;                  // fragment-ordered copies, rebuilt when a factor changes
+  std::vector<double*> depth_buf;             // one intermediate per tree depth
+  std::vector<size_t> depth_cap;
+  double* core = nullptr;
+  double* core_tmp[2] = {nullptr, nullptr};
+  size_t core_size = 0, core_tmp_cap = 0;
+  LeafScratch leaf;
+  tp_sweep_stats model{};   // analytic SweepStats (tree_macs, core_macs, peak_live)
+  tp_sweep_timing timing{};
+  // event pool for phase timing: triples (phase, begin, end)
+  std::vector<cudaEvent_t> events;
+  std::vector<int> event_phase;
+  std::vector<int> event_node;   // tree node a span belongs to, -1 if none
+  size_t events_used = 0;
+  std::vector<float> node_ms, node_evd_ms;
+};
+
+namespace tpb {
+namespace {
+
+enum Phase { kTree = 0, kGram = 1, kEvd = 2, kCore = 3 };
+
+cudaEvent_t next_event(tp_plan* p) {
+  if (p->events_used == p->events.size()) {
+    cudaEvent_t e;
+    TPB_CUDA(cudaEventCreate(&e));
+    p->events.push_back(e);
+  }
+  return p->events[p->events_used++];
+}
+
+struct Span {
+  tp_ctx* ctx;
+  tp_plan* plan;
+  Span(tp_ctx* c, tp_plan* p, int phase, int node = -1) : ctx(c), plan(p) {
+    plan->event_phase.push_back(phase);
+    plan->event_node.push_back(node);
+    TPB_CUDA(cudaEventRecord(next_event(plan), ctx->stream));
+  }
+  void close() { TPB_CUDA(cudaEventRecord(next_event(plan), ctx->stream)); }
+};
+
+void plan_refresh_fragments(tp_ctx* ctx, tp_plan* p, int mode, const double* factor) {
+  // F (L x K col-major) read as M = F^T: M(k, l) = F[k * L + l]
+  const long long L = static_cast<long long>(p->spec.L[mode]), K = static_cast<long long>(p->spec.K[mode]);
+  TPB_CUDA(prep_factor_fragments(ctx->stream, factor, L, 1, K, L, p->frag_layout[mode], p->frag[mode]));
+  ctx->own_kernels += 1;
+}
+
+void plan_ttm(tp_ctx* ctx, tp_plan* p, const double* x, const std::vector<size_t>& dims, int mode, double* out) {
+  long long outer, inner;
+  mode_extents(dims, mode, outer, inner);
+  TPB_CUDA(launch_ttm(ctx->stream, x, outer, static_cast<long long>(dims[mode]), inner, p->frag[mode],
+                      p->frag_layout[mode], static_cast<long long>(p->spec.K[mode]), out));
+  ctx->own_kernels += 1;
+}
+
+void plan_leaf(tp_ctx* ctx, tp_plan* p, const double* y, const std::vector<size_t>& dims, int mode, double* dst,
+               int node = -1) {
+  const int k = static_cast<int>(p->spec.K[mode]);
+  Span gram(ctx, p, kGram, node);
+  const long long rows = leaf_gram(ctx, p->leaf, y, dims, mode, k);
+  gram.close();
+  Span evd(ctx, p, kEvd, node);
+  leaf_solve(ctx, p->leaf, rows, k, dst);
+  evd.close();
+}
+
+void jacobi_walk(tp_ctx* ctx, tp_plan* p, int node, const double* tensor, std::vector<size_t>& dims, int depth) {
+  for (int c : p->tree.kids[node]) {
+    const int mode = p->tree.mode[c];
+    if (p->tree.kind[c] == TP_NODE_LEAF) {
+      plan_leaf(ctx, p, tensor, dims, mode, p->fresh[mode], c);
+    } else {
+      double* out = p->depth_buf[depth];
+      {
+        Span s(ctx, p, kTree, c);
+        plan_ttm(ctx, p, tensor, dims, mode, out);
+        s.close();
+      }
+      const size_t saved = dims[mode];
+      dims[mode] = static_cast<size_t>(p->spec.K[mode]);
+      jacobi_walk(ctx, p, c, out, dims, depth + 1);
+      dims[mode] = saved;
+    }
+  }
+}
+
+// core_from_factors (hooi.hpp:93-100): T x_0 F_0^T x_1 F_1^T ... in mode order, ping-pong buffers.
+void plan_core(tp_ctx* ctx, tp_plan* p, const double* tensor, const std::vector<double*>& factors) {
+  Span s(ctx, p, kCore);
+  std::vector<size_t> dims(p->spec.L.begin(), p->spec.L.end());
+  const double* src = tensor;
+  for (int m = 0; m < p->n; ++m) {
+    plan_refresh_fragments(ctx, p, m, factors[m]);
+    double* dst = (m == p->n - 1) ? p->core : p->core_tmp[m & 1];
+    plan_ttm(ctx, p, src, dims, m, dst);
+    dims[m] = static_cast<size_t>(p->spec.K[m]);
+    src = dst;
+  }
+  s.close();
+}
+
+void check_tensor_matches(const tp_plan* p, const tp_tensor* t) {  // hooi.hpp:85-91
+  if (!t) raise(TP_ERR_BAD_ARGUMENT, "null tensor");
+  if (static_cast<int>(t->dims.size()) != p->n) raise(TP_ERR_SHAPE_MISMATCH, "tensor and spec mode counts differ");
+  for (int m = 0; m < p->n; ++m)
+    if (t->dims[m] != p->spec.L[m]) raise(TP_ERR_SHAPE_MISMATCH, "tensor extent differs from L", m);
+}
+
+void plan_collect_timing(tp_ctx* ctx, tp_plan* p) {
+  TPB_CUDA(cudaStreamSynchronize(ctx->stream));
+  tp_sweep_timing t{};
+  float* slot[4] = {&t.tree_ms, &t.gram_ms, &t.evd_ms, &t.core_ms};
+  p->node_ms.assign(p->tree.size(), 0.f);
+  p->node_evd_ms.assign(p->tree.size(), 0.f);
+  for (size_t i = 0; i < p->event_phase.size(); ++i) {
+    float ms = 0.f;
+    TPB_CUDA(cudaEventElapsedTime(&ms, p->events[2 * i], p->events[2 * i + 1]));
+    *slot[p->event_phase[i]] += ms;
+    const int node = p->event_node[i];
+    if (node >= 0) (p->event_phase[i] == kEvd ? p->node_evd_ms : p->node_ms)[node] += ms;
+  }
+  if (!p->event_phase.empty()) {
+    float ms = 0.f;
+    TPB_CUDA(cudaEventElapsedTime(&ms, p->events[0], p->events[p->events_used - 1]));
+    t.total_ms = ms;
+  }
+  p->timing = t;
+}
+
+}  // namespace
+}  // namespace tpb
+
+extern "C" {
+
+int tp_ctx_create(int device, tp_ctx** out) {
+  return guarded([&] {
+    if (!out) raise(TP_ERR_BAD_ARGUMENT, "null output");
+    int count = 0;
+    const cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0)
+      raise(TP_ERR_CUDA, std::string("no CUDA device available (this engine has no CPU fallback): ") +
+                             cudaGetErrorString(e));
+    if (device < 0 || device >= count) raise(TP_ERR_BAD_ARGUMENT, "device index out of range");
+    cudaDeviceProp prop;
+    TPB_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+      raise(TP_ERR_CUDA, std::string("device '") + prop.name + "' is not sm_100: this library carries sm_100a code only");
+    tp_ctx* ctx = new tp_ctx;
+    ctx->device = device;
+    ctx->sm_count = prop.multiProcessorCount;
+    try {
+      TPB_CUDA(cudaSetDevice(device));
+      TPB_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+      TPB_SOLVER(cusolverDnCreate(&ctx->solver));
+      TPB_SOLVER(cusolverDnSetStream(ctx->solver, ctx->stream));
+      ctx->reduce_scratch = device_alloc(reduce_scratch_doubles() + 1);
+    } catch (...) {
+      delete ctx;
+      throw;
+    }
+    *out = ctx;
+  });
+}
+
+int tp_ctx_destroy(tp_ctx* ctx) {
+  return guarded([&] {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->solver) cusolverDnDestroy(ctx->solver);
+    cudaFree(ctx->reduce_scratch);
+    cudaFree(ctx->frag_scratch);
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+  });
+}
+
+int tp_ctx_synchronize(tp_ctx* ctx) {
+  return guarded([&] {
+    bind(ctx);
+    TPB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int tp_ctx_stream(tp_ctx* ctx, void** stream_out) {
+  return guarded([&] {
+    bind(ctx);
+    *stream_out = static_cast<void*>(ctx->stream);
+  });
+}
+
+int tp_ctx_launch_counts(tp_ctx* ctx, tp_u64* own_kernels, tp_u64* library_calls) {
+  return guarded([&] {
+    if (!ctx) raise(TP_ERR_BAD_ARGUMENT, "null context");
+    if (own_kernels) *own_kernels = ctx->own_kernels;
+    if (library_calls) *library_calls = ctx->library_calls;
+  });
+}
+
+int tp_host_alloc(size_t bytes, void** out) {
+  return guarded([&] { TPB_CUDA(cudaHostAlloc(out, std::max<size_t>(bytes, 1), cudaHostAllocDefault)); });
+}
+
+int tp_host_free(void* p) {
+  return guarded([&] {
+    if (p) TPB_CUDA(cudaFreeHost(p));
+  });
+}
+
+int tp_tensor_upload(tp_ctx* ctx, int n_modes, const size_t* dims, const double* host, tp_tensor** out) {
+  return guarded([&] {
+    bind(ctx);
+    if (!host || !out) raise(TP_ERR_BAD_ARGUMENT, "null buffer");
+    checked_size(n_modes, dims);
+    tp_tensor* t = new_tensor(std::vector<size_t>(dims, dims + n_modes));
+    const cudaError_t e = cudaMemcpyAsync(t->data, host, t->size * sizeof(double), cudaMemcpyHostToDevice, ctx->stream);
+    if (e != cudaSuccess) {
+      cudaFree(t->data);
+      delete t;
+      cuda_fail(e, "tensor upload");
+    }
+    TPB_CUDA(cudaStreamSynchronize(ctx->stream));
+    *out = t;
+  });
+}
+
+int tp_tensor_alloc(tp_ctx* ctx, int n_modes, const size_t* dims, tp_tensor** out) {
+  return guarded([&] {
+    bind(ctx);
+    if (!out) raise(TP_ERR_BAD_ARGUMENT, "null output");
+    checked_size(n_modes, dims);
+    tp_tensor* t = new_tensor(std::vector<size_t>(dims, dims + n_modes));
+    TPB_CUDA(cudaMemsetAsync(t->data, 0, t->size * sizeof(double), ctx->stream));
+    *out = t;
+  });
+}
+
+int tp_tensor_download(tp_ctx* ctx, const tp_tensor* t, double* host) {
+  return guarded([&] {
+    bind(ctx);
+    if (!t || !host) raise(TP_ERR_BAD_ARGUMENT, "null buffer");
+    TPB_CUDA(cudaMemcpyAsync(host, t->data, t->size * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    TPB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int tp_tensor_free(tp_ctx* ctx, tp_tensor* t) {
+  return guarded([&] {
+    if (!t) return;
+    bind(ctx);
+    TPB_CUDA(cudaStreamSynchronize(ctx->stream));
+    cudaFree(t->data);
+    delete t;
+  });
+}
+
+int tp_tensor_dims(const tp_tensor* t, int* n_modes, size_t* dims) {
+  return guarded([&] {
+    if (!t) raise(TP_ERR_BAD_ARGUMENT, "null tensor");
+    if (n_modes) *n_modes = static_cast<int>(t->dims.size());
+    if (dims) std::copy(t->dims.begin(), t->dims.end(), dims);
+  });
+}
+
+void* tp_tensor_device_ptr(const tp_tensor* t) { return t ? t->data : nullptr; }
+
+int tp_tensor_norm(tp_ctx* ctx, const tp_tensor* t, double* out) {
+  return guarded([&] {
+    bind(ctx);
+    if (!t || !out) raise(TP_ERR_BAD_ARGUMENT, "null argument");
+    *out = std::sqrt(sum_squares(ctx, t->data, t->size));
+  });
+}
+
+static void ttm_common(tp_ctx* ctx, const tp_tensor* t, const double* m_dev, long long row_stride,
+                       long long col_stride, size_t m_rows, size_t m_cols, int mode, tp_u64* macs, tp_tensor** out) {
+  if (!t || !out) raise(TP_ERR_BAD_ARGUMENT, "null argument");
+  long long outer, inner;
+  mode_extents(t->dims, mode, outer, inner);  // bad_mode, ttm.hpp:26-27
+  if (m_cols != t->dims[mode]) raise(TP_ERR_SHAPE_MISMATCH, "matrix columns must match the mode extent");
+  if (m_rows == 0) raise(TP_ERR_SHAPE_MISMATCH, "empty matrix");
+  std::vector<size_t> out_dims = t->dims;
+  out_dims[mode] = m_rows;
+  tp_tensor* z = new_tensor(out_dims);
+  try {
+    run_ttm(ctx, t->data, t->dims, mode, m_dev, row_stride, col_stride, static_cast<long long>(m_rows), nullptr,
+            z->data);
+    if (macs) *macs = add_or_throw(*macs, mul_or_throw(m_rows, t->size));  // ttm.hpp:92-94
+  } catch (...) {
+    cudaFree(z->data);
+    delete z;
+    throw;
+  }
+  *out = z;
+}
+
+int tp_ttm(tp_ctx* ctx, const tp_tensor* t, const double* m, size_t m_rows, size_t m_cols, int mode, tp_u64* macs,
+           tp_tensor** out) {
+  return guarded([&] {
+    bind(ctx);
+    if (!m || !t) raise(TP_ERR_BAD_ARGUMENT, "null argument");
+    {  // argument errors in the reference's order (ttm.hpp:75-80) before any device work
+      long long o, i;
+      mode_extents(t->dims, mode, o, i);
+      if (m_cols != t->dims[mode]) raise(TP_ERR_SHAPE_MISMATCH, "matrix columns must match the mode extent");
+      if (m_rows == 0) raise(TP_ERR_SHAPE_MISMATCH, "empty matrix");
+    }
+    double* m_dev = device_alloc(m_rows * m_cols);
+    try {
+      TPB_CUDA(cudaMemcpyAsync(m_dev, m, m_rows * m_cols * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+      // column-major host matrix: M(k, l) at m[l * m_rows + k]
+      ttm_common(ctx, t, m_dev, 1, static_cast<long long>(m_rows), m_rows, m_cols, mode, macs, out);
+      TPB_CUDA(cudaStreamSynchronize(ctx->stream));
+    } catch (...) {
+      cudaStreamSynchronize(ctx->stream);
+      cudaFree(m_dev);
+      throw;
+    }
+    cudaFree(m_dev);
+  });
+}
+
+int tp_ttm_device(tp_ctx* ctx, const tp_tensor* t, const double* m_dev_rowmajor, size_t m_rows, size_t m_cols,
+                  int mode, tp_u64* macs, tp_tensor** out) {
+  return guarded([&] {
+    bind(ctx);
+    if (!m_dev_rowmajor) raise(TP_ERR_BAD_ARGUMENT, "null matrix");
+    ttm_common(ctx, t, m_dev_rowmajor, static_cast<long long>(m_cols), 1, m_rows, m_cols, mode, macs, out);
+  });
+}
+
+int tp_gram(tp_ctx* ctx, const tp_tensor* t, int mode, double* gram_out) {
+  return guarded([&] {
+    bind(ctx);
+    if (!t || !gram_out) raise(TP_ERR_BAD_ARGUMENT, "null argument");
+    long long outer, inner;
+    mode_extents(t->dims, mode, outer, inner);
+    const long long rows = static_cast<long long>(t->dims[mode]);
+    const GramLayout g = gram_layout(outer, rows, inner, ctx->sm_count);
+    double* ws = device_alloc(g.workspace_doubles);
+    double* gram = device_alloc(static_cast<size_t>(rows) * rows);
+    cudaError_t e = launch_gram(ctx->stream, t->data, outer, rows, inner, g, ws, gram);
+    ctx->own_kernels += 2;
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(gram_out, gram, sizeof(double) * rows * rows, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    cudaFree(ws);
+    cudaFree(gram);
+    if (e != cudaSuccess) cuda_fail(e, "gram");
+  });
+}
+
+int tp_leaf_factor(tp_ctx* ctx, const tp_tensor* t, int mode, int k, double* vectors_out, int* degenerate) {
+  return guarded([&] {
+    bind(ctx);
+    if (!t || !vectors_out) raise(TP_ERR_BAD_ARGUMENT, "null argument");
+    long long outer, inner;
+    mode_extents(t->dims, mode, outer, inner);
+    const long long rows = static_cast<long long>(t->dims[mode]);
+    check_leaf_args(rows, outer * inner, k);
+    LeafScratch s;
+    double* factor = nullptr;
+    try {
+      factor = device_alloc(static_cast<size_t>(rows) * k);
+      leaf_update(ctx, s, t->data, t->dims, mode, k, factor);
+      TPB_CUDA(cudaMemcpyAsync(vectors_out, factor, sizeof(double) * rows * k, cudaMemcpyDeviceToHost, ctx->stream));
+      const int flag = read_and_clear_flag(ctx, s);
+      if (degenerate) *degenerate = flag;
+    } catch (...) {
+      cudaStreamSynchronize(ctx->stream);
+      cudaFree(factor);
+      s.release();
+      throw;
+    }
+    cudaFree(factor);
+    s.release();
+  });
+}
+
+int tp_leading_left_factors(tp_ctx* ctx, const double* m, size_t rows, size_t cols, int k, double* vectors_out,
+                            int* degenerate) {
+  return guarded([&] {
+    bind(ctx);
+    check_leaf_args(static_cast<long long>(rows), static_cast<long long>(cols), k);
+    if (!m || !vectors_out) raise(TP_ERR_BAD_ARGUMENT, "null argument");
+    // a column-major rows x cols matrix is, in memory, the row-major tensor (cols, rows); its mode-1 Gram is m m^T
+    const size_t dims[2] = {cols, rows};
+    tp_tensor* t = nullptr;
+    int status = tp_tensor_upload(ctx, 2, dims, m, &t);
+    if (status != TP_OK) raise(status, tp_last_error(), tp_last_error_mode());
+    status = tp_leaf_factor(ctx, t, 1, k, vectors_out, degenerate);
+    const std::string msg = status != TP_OK ? tp_last_error() : "";
+    const int bad_mode = tp_last_error_mode();
+    tp_tensor_free(ctx, t);
+    if (status != TP_OK) raise(status, msg, bad_mode);
+  });
+}
+
+int tp_plan_create(tp_ctx* ctx, int n_modes, const tp_u64* L, const tp_u64* K, int n_nodes, const int* kind,
+                   const int* mode, const int* parent, int sweep_kind, tp_plan** out) {
+  return guarded([&] {
+    bind(ctx);
+    if (!out) raise(TP_ERR_BAD_ARGUMENT, "null output");
+    if (sweep_kind != TP_SWEEP_JACOBI && sweep_kind != TP_SWEEP_GAUSS_SEIDEL)
+      raise(TP_ERR_BAD_ARGUMENT, "unknown sweep kind");
+    tp_plan* p = new tp_plan;
+    try {
+      p->spec = make_spec(n_modes, L, K);
+      validate_spec(p->spec);
+      p->n = n_modes;
+      p->tree = tree_from_arrays(n_modes, n_nodes, kind, mode, parent);
+      validate_tree(p->tree, p->spec);
+      p->sweep_kind = sweep_kind;
+      Cards cards;
+      const Cost cost = tree_cost(p->tree, p->spec, &cards);
+      for (int m = 0; m < n_modes; ++m)
+        if (p->spec.L[m] > TP_MAX_GRAM_ROWS)
+          raise(TP_ERR_TOO_LARGE, "unfolding has too many rows for the Gram route", m);  // hooi.hpp:48-49
+
+      // SweepStats are properties of (spec, tree, kind): tree_macs == tree_cost, core_macs in mode order
+      p->model.tree_macs = cost.total_macs;
+      u64 card = partial_cardinality(p->spec, 0), core_macs = 0;
+      for (int m = 0; m < n_modes; ++m) {
+        core_macs = add_or_throw(core_macs, mul_or_throw(p->spec.K[m], card));
+        card = scale_exact(card, p->spec.K[m], p->spec.L[m]);
+      }
+      p->model.core_macs = core_macs;
+      p->core_size = static_cast<size_t>(card);
+      if (sweep_kind == TP_SWEEP_JACOBI) {
+        p->model.peak_live = cost.depth + 1;  // hooi.hpp:143-144: live grows by one per mode node on the path
+      } else {
+        p->gs_paths = chain_paths(p->tree);  // needs_chain_tree
+        u64 macs = 0;
+        int peak = 1;
+        for (int leaf = 0; leaf < n_modes; ++leaf) {
+          u64 c = partial_cardinality(p->spec, 0);
+          for (size_t i = 0; i < p->gs_paths[leaf].size(); ++i) {
+            const int m = p->gs_paths[leaf][i];
+            macs = add_or_throw(macs, mul_or_throw(p->spec.K[m], c));
+            c = scale_exact(c, p->spec.K[m], p->spec.L[m]);
+            peak = std::max(peak, (i == 0 ? 1 : 2) + 1);  // hooi.hpp:213-214
+          }
+        }
+        p->model.tree_macs = macs;
+        p->model.peak_live = peak;
+      }
+
+      // one intermediate buffer per depth
+      std::vector<int> depth(p->tree.size(), 0);
+      for (int id = 1; id < p->tree.size(); ++id) {
+        depth[id] = depth[p->tree.parent[id]] + (p->tree.internal(id) ? 1 : 0);
+        if (!p->tree.internal(id)) continue;
+        const size_t d = depth[id] - 1;
+        if (p->depth_cap.size() <= d) p->depth_cap.resize(d + 1, 0);
+        p->depth_cap[d] = std::max(p->depth_cap[d], static_cast<size_t>(cards.out[id]));
+      }
+      p->depth_buf.assign(p->depth_cap.size(), nullptr);
+      for (size_t d = 0; d < p->depth_cap.size(); ++d) p->depth_buf[d] = device_alloc(p->depth_cap[d]);
+
+      // core chain ping-pong: the largest partial product of the mode-order chain
+      card = partial_cardinality(p->spec, 0);
+      for (int m = 0; m + 1 < n_modes; ++m) {
+        card = scale_exact(card, p->spec.K[m], p->spec.L[m]);
+        p->core_tmp_cap = std::max(p->core_tmp_cap, static_cast<size_t>(card));
+      }
+      p->core = device_alloc(p->core_size);
+      if (n_modes > 1) p->core_tmp[0] = device_alloc(p->core_tmp_cap);
+      if (n_modes > 2) p->core_tmp[1] = device_alloc(p->core_tmp_cap);
+
+      p->cur.assign(n_modes, nullptr);
+      p->fresh.assign(n_modes, nullptr);
+      p->frag.assign(n_modes, nullptr);
+      p->frag_layout.resize(n_modes);
+      long long max_rows = 0;
+      for (int m = 0; m < n_modes; ++m) {
+        const size_t elems = static_cast<size_t>(p->spec.L[m] * p->spec.K[m]);
+        p->cur[m] = device_alloc(elems);
+        p->fresh[m] = device_alloc(elems);
+        TPB_CUDA(cudaMemsetAsync(p->cur[m], 0, elems * sizeof(double), ctx->stream));
+        p->frag_layout[m] = ttm_fragment_layout(static_cast<long long>(p->spec.K[m]), static_cast<long long>(p->spec.L[m]));
+        p->frag[m] = device_alloc(p->frag_layout[m].doubles);
+        max_rows = std::max(max_rows, static_cast<long long>(p->spec.L[m]));
+      }
+      // worst-case Gram split workspace over the leaves
+      size_t ws = 0;
+      for (int id = 0; id < p->tree.size(); ++id) {
+        if (!p->tree.leaf(id)) continue;
+        const std::vector<u64> ext = node_extents(p->tree, p->spec, id);
+        const int m = p->tree.mode[id];
+        long long outer = 1, inner = 1;
+        for (int i = 0; i < m; ++i) outer *= static_cast<long long>(ext[i]);
+        for (int i = m + 1; i < n_modes; ++i) inner *= static_cast<long long>(ext[i]);
+        ws = std::max(ws, gram_layout(outer, static_cast<long long>(ext[m]), inner, ctx->sm_count).workspace_doubles);
+      }
+      leaf_scratch_reserve(ctx, p->leaf, max_rows, ws);
+      TPB_CUDA(cudaStreamSynchronize(ctx->stream));
+    } catch (...) {
+      tp_plan_destroy(ctx, p);
+      throw;
+    }
+    *out = p;
+  });
+}
+
+int tp_plan_destroy(tp_ctx* ctx, tp_plan* p) {
+  return guarded([&] {
+    if (!p) return;
+    if (ctx) {
+      cudaSetDevice(ctx->device);
+      cudaStreamSynchronize(ctx->stream);
+    }
+    for (double* d : p->cur) cudaFree(d);
+    for (double* d : p->fresh) cudaFree(d);
+    for (double* d : p->frag) cudaFree(d);
+    for (double* d : p->depth_buf) cudaFree(d);
+    cudaFree(p->core);
+    cudaFree(p->core_tmp[0]);
+    cudaFree(p->core_tmp[1]);
+    p->leaf.release();
+    for (cudaEvent_t e : p->events)
+      if (e) cudaEventDestroy(e);
+    delete p;
+  });
+}
+
+int tp_plan_set_factors(tp_ctx* ctx, tp_plan* p, const double* const* factors) {
+  return guarded([&] {
+    bind(ctx);
+    if (!p || !factors) raise(TP_ERR_BAD_ARGUMENT, "null argument");
+    for (int m = 0; m < p->n; ++m) {
+      if (!factors[m]) raise(TP_ERR_SHAPE_MISMATCH, "factor count differs from mode count");
+      TPB_CUDA(cudaMemcpyAsync(p->cur[m], factors[m], sizeof(double) * p->spec.L[m] * p->spec.K[m],
+                               cudaMemcpyHostToDevice, ctx->stream));
+    }
+    TPB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int tp_plan_get_factors(tp_ctx* ctx, tp_plan* p, double* const* factors_out) {
+  return guarded([&] {
+    bind(ctx);
+    if (!p || !factors_out) raise(TP_ERR_BAD_ARGUMENT, "null argument");
+    for (int m = 0; m < p->n; ++m)
+      TPB_CUDA(cudaMemcpyAsync(factors_out[m], p->cur[m], sizeof(double) * p->spec.L[m] * p->spec.K[m],
+                               cudaMemcpyDeviceToHost, ctx->stream));
+    TPB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int tp_plan_get_core(tp_ctx* ctx, tp_plan* p, double* core_out) {
+  return guarded([&] {
+    bind(ctx);
+    if (!p || !core_out) raise(TP_ERR_BAD_ARGUMENT, "null argument");
+    TPB_CUDA(cudaMemcpyAsync(core_out, p->core, sizeof(double) * p->core_size, cudaMemcpyDeviceToHost, ctx->stream));
+    TPB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int tp_plan_core_norm(tp_ctx* ctx, tp_plan* p, double* out) {
+  return guarded([&] {
+    bind(ctx);
+    if (!p || !out) raise(TP_ERR_BAD_ARGUMENT, "null argument");
+    *out = std::sqrt(sum_squares(ctx, p->core, p->core_size));
+  });
+}
+
+int tp_plan_compute_core(tp_ctx* ctx, tp_plan* p, const tp_tensor* t) {
+  return guarded([&] {
+    bind(ctx);
+    if (!p) raise(TP_ERR_BAD_ARGUMENT, "null plan");
+    check_tensor_matches(p, t);
+    p->events_used = 0;
+    p->event_phase.clear();
+    p->event_node.clear();
+    plan_core(ctx, p, t->data, p->cur);
+    plan_collect_timing(ctx, p);
+  });
+}
+
+int tp_plan_sweep(tp_ctx* ctx, tp_plan* p, const tp_tensor* t, tp_sweep_stats* stats) {
+  return guarded([&] {
+    bind(ctx);
+    if (!p) raise(TP_ERR_BAD_ARGUMENT, "null plan");
+    check_tensor_matches(p, t);
+    if (stats) *stats = tp_sweep_stats{};  // hooi.hpp:198
+    p->events_used = 0;
+    p->event_phase.clear();
+    p->event_node.clear();
+    std::vector<size_t> dims(p->spec.L.begin(), p->spec.L.end());
+    if (p->sweep_kind == TP_SWEEP_JACOBI) {
+      {
+        Span s(ctx, p, kTree);  // start-of-sweep factors -> fragment order, once per mode
+        for (int m = 0; m < p->n; ++m) plan_refresh_fragments(ctx, p, m, p->cur[m]);
+        s.close();
+      }
+      jacobi_walk(ctx, p, 0, t->data, dims, 0);
+      plan_core(ctx, p, t->data, p->fresh);
+      std::swap(p->cur, p->fresh);
+    } else {
+      {
+        Span s(ctx, p, kTree);
+        for (int m = 0; m < p->n; ++m) plan_refresh_fragments(ctx, p, m, p->cur[m]);
+        s.close();
+      }
+      for (int leaf = 0; leaf < p->n; ++leaf) {  // hooi.hpp:206-224
+        const double* at = t->data;
+        std::vector<size_t> d = dims;
+        size_t step = 0;
+        for (int m : p->gs_paths[leaf]) {
+          Span s(ctx, p, kTree);
+          double* out = p->depth_buf[step];
+          plan_ttm(ctx, p, at, d, m, out);
+          s.close();
+          d[m] = static_cast<size_t>(p->spec.K[m]);
+          at = out;
+          ++step;
+        }
+        plan_leaf(ctx, p, at, d, leaf, p->fresh[leaf]);
+        std::swap(p->cur[leaf], p->fresh[leaf]);  // later chains see the fresh factor
+        Span s(ctx, p, kTree);
+        plan_refresh_fragments(ctx, p, leaf, p->cur[leaf]);
+        s.close();
+      }
+      plan_core(ctx, p, t->data, p->cur);
+    }
+    const int flag = read_and_clear_flag(ctx, p->leaf);
+    plan_collect_timing(ctx, p);
+    if (stats) {
+      *stats = p->model;
+      stats->degenerate = flag;
+    }
+  });
+}
+
+int tp_plan_node_timing(tp_ctx* ctx, tp_plan* p, int n_nodes, float* node_ms, float* evd_ms) {
+  return guarded([&] {
+    (void)ctx;
+    if (!p) raise(TP_ERR_BAD_ARGUMENT, "null plan");
+    if (n_nodes != p->tree.size()) raise(TP_ERR_SHAPE_MISMATCH, "node count differs from the plan's tree");
+    for (int i = 0; i < n_nodes; ++i) {
+      if (node_ms) node_ms[i] = i < static_cast<int>(p->node_ms.size()) ? p->node_ms[i] : 0.f;
+      if (evd_ms) evd_ms[i] = i < static_cast<int>(p->node_evd_ms.size()) ? p->node_evd_ms[i] : 0.f;
+    }
+  });
+}
+
+int tp_tensor_axpby(tp_ctx* ctx, tp_tensor* y, double beta, double alpha, const tp_tensor* x) {
+  return guarded([&] {
+    bind(ctx);
+    if (!y || !x) raise(TP_ERR_BAD_ARGUMENT, "null tensor");
+    if (y->dims != x->dims) raise(TP_ERR_SHAPE_MISMATCH, "tensor shapes differ");
+    TPB_CUDA(launch_axpby(ctx->stream, y->data, beta, alpha, x->data, y->size));
+    ctx->own_kernels += 1;
+  });
+}
+
+int tp_plan_last_timing(tp_ctx* ctx, tp_plan* p, tp_sweep_timing* out) {
+  return guarded([&] {
+    (void)ctx;
+    if (!p || !out) raise(TP_ERR_BAD_ARGUMENT, "null argument");
+    *out = p->timing;
+  });
+}
+
+// core x_0 F_0 ... x_{N-1} F_{N-1} on the device, then ||t - z|| / ||t||  (hooi.hpp:232-245)
+static double expansion_error(tp_ctx* ctx, const tp_tensor* t, const std::vector<size_t>& core_dims,
+                              const double* core_dev, const std::vector<const double*>& factors_dev) {
+  const double norm = std::sqrt(sum_squares(ctx, t->data, t->size));
+  if (norm == 0.0) raise(TP_ERR_ZERO_TENSOR, "relative error undefined at zero");
+  const int n = static_cast<int>(core_dims.size());
+  std::vector<size_t> dims = core_dims;
+  const double* src = core_dev;
+  double* owned = nullptr;
+  try {
+    for (int m = 0; m < n; ++m) {
+      const size_t rows = t->dims[m], cols = core_dims[m];
+      std::vector<size_t> out_dims = dims;
+      out_dims[m] = rows;
+      size_t out_size = 1;
+      for (size_t d : out_dims) out_size *= d;
+      double* dst = device_alloc(out_size);
+      // ttm(z, F_m, m): matrix rows x cols with F column-major -> M(r, c) = F[c * rows + r]
+      try {
+        run_ttm(ctx, src, dims, m, factors_dev[m], 1, static_cast<long long>(rows), static_cast<long long>(rows),
+                nullptr, dst);
+        TPB_CUDA(cudaStreamSynchronize(ctx->stream));
+      } catch (...) {
+        cudaFree(dst);
+        throw;
+      }
+      (void)cols;
+      cudaFree(owned);
+      owned = dst;
+      src = dst;
+      dims = out_dims;
+    }
+    if (dims != t->dims) raise(TP_ERR_SHAPE_MISMATCH, "reconstruction shape differs");
+    const double diff = diff_sum_squares(ctx, t->data, src, t->size);
+    cudaFree(owned);
+    return std::sqrt(diff) / norm;
+  } catch (...) {
+    cudaStreamSynchronize(ctx->stream);
+    cudaFree(owned);
+    throw;
+  }
+}
+
+int tp_plan_reconstruction_error(tp_ctx* ctx, tp_plan* p, const tp_tensor* t, double* out) {
+  return guarded([&] {
+    bind(ctx);
+    if (!p || !out) raise(TP_ERR_BAD_ARGUMENT, "null argument");
+    if (!t) raise(TP_ERR_BAD_ARGUMENT, "null tensor");
+    check_tensor_matches(p, t);
+    std::vector<size_t> core_dims(p->spec.K.begin(), p->spec.K.end());
+    std::vector<const double*> factors(p->cur.begin(), p->cur.end());
+    *out = expansion_error(ctx, t, core_dims, p->core, factors);
+  });
+}
+
+int tp_plan_fit_from_norms(tp_ctx* ctx, tp_plan* p, const tp_tensor* t, double* out) {
+  return guarded([&] {
+    bind(ctx);
+    if (!p || !out || !t) raise(TP_ERR_BAD_ARGUMENT, "null argument");
+    check_tensor_matches(p, t);
+    const double t2 = sum_squares(ctx, t->data, t->size);
+    if (t2 == 0.0) raise(TP_ERR_ZERO_TENSOR, "relative error undefined at zero");
+    const double g2 = sum_squares(ctx, p->core, p->core_size);
+    *out = std::sqrt(std::max(t2 - g2, 0.0) / t2);
+  });
+}
+
+int tp_reconstruction_error(tp_ctx* ctx, const tp_tensor* t, const size_t* core_dims, const double* core,
+                            const double* const* factors, double* out) {
+  return guarded([&] {
+    bind(ctx);
+    if (!t || !out) raise(TP_ERR_BAD_ARGUMENT, "null argument");
+    const double norm2 = sum_squares(ctx, t->data, t->size);
+    if (norm2 == 0.0) raise(TP_ERR_ZERO_TENSOR, "relative error undefined at zero");  // hooi.hpp:233-234 comes first
+    if (!core_dims || !core || !factors) raise(TP_ERR_SHAPE_MISMATCH, "reconstruction shape differs");
+    const int n = static_cast<int>(t->dims.size());
+    std::vector<size_t> cd(core_dims, core_dims + n);
+    const size_t core_size = checked_size(n, core_dims);
+    std::vector<double*> owned;
+    auto cleanup = [&] {
+      cudaStreamSynchronize(ctx->stream);
+      for (double* d : owned) cudaFree(d);
+    };
+    try {
+      double* core_dev = device_alloc(core_size);
+      owned.push_back(core_dev);
+      TPB_CUDA(cudaMemcpyAsync(core_dev, core, core_size * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+      std::vector<const double*> f(n);
+      for (int m = 0; m < n; ++m) {
+        if (!factors[m]) raise(TP_ERR_SHAPE_MISMATCH, "reconstruction shape differs");
+        double* d = device_alloc(t->dims[m] * cd[m]);
+        owned.push_back(d);
+        TPB_CUDA(cudaMemcpyAsync(d, factors[m], t->dims[m] * cd[m] * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        f[m] = d;
+      }
+      *out = expansion_error(ctx, t, cd, core_dev, f);
+    } catch (...) {
+      cleanup();
+      throw;
+    }
+    cleanup();
+  });
+}
+
+int tp_hooi_sweep_host(tp_ctx* ctx, int n_modes, const size_t* dims, const double* tensor, const tp_u64* K,
+                       const double* const* factors_in, int n_nodes, const int* kind, const int* mode,
+                       const int* parent, int sweep_kind, double* const* factors_out, double* core_out,
+                       tp_sweep_stats* stats) {
+  return guarded([&] {
+    bind(ctx);
+    if (!dims || !tensor || !K || !factors_in) raise(TP_ERR_BAD_ARGUMENT, "null argument");
+    std::vector<u64> L(dims, dims + std::max(n_modes, 0));
+    tp_plan* plan = nullptr;
+    tp_tensor* t = nullptr;
+    auto forward = [&](int status) {
+      if (status == TP_OK) return;
+      const std::string msg = tp_last_error();
+      const int bad = tp_last_error_mode();
+      if (plan) tp_plan_destroy(ctx, plan);
+      if (t) tp_tensor_free(ctx, t);
+      raise(status, msg, bad);
+    };
+    forward(tp_plan_create(ctx, n_modes, L.data(), K, n_nodes, kind, mode, parent, sweep_kind, &plan));
+    forward(tp_tensor_upload(ctx, n_modes, dims, tensor, &t));
+    forward(tp_plan_set_factors(ctx, plan, factors_in));
+    forward(tp_plan_sweep(ctx, plan, t, stats));
+    if (factors_out) forward(tp_plan_get_factors(ctx, plan, factors_out));
+    if (core_out) forward(tp_plan_get_core(ctx, plan, core_out));
+    tp_plan_destroy(ctx, plan);
+    tp_tensor_free(ctx, t);
+  });
+}
+
+}  // extern "C"

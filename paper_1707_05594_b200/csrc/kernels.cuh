@@ -1,0 +1,55 @@
+// Launchers of the hand-written sm_100a kernels (definitions in *_kernels.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+
+namespace tpb {
+
+// ---- mode-n TTM (ttm_kernels.cu) -------------------------------------------
+struct TtmFragmentLayout {
+  int kt = 1;        // 8-row output tiles per CTA (rows of the new mode handled per K block = 8 * kt)
+  int k_blocks = 1;  // ceil(new_len / (8 kt))
+  int kc = 16;       // contraction steps per pipeline stage
+  int n_chunks = 1;  // ceil(len / kc)
+  size_t doubles = 0;
+};
+
+int ttm_pick_kt(long long new_len);
+TtmFragmentLayout ttm_fragment_layout(long long new_len, long long len);
+
+// M(k, l) = m[k * row_stride + l * col_stride], k < new_len, l < len  ->  fragment order, zero padded.
+cudaError_t prep_factor_fragments(cudaStream_t stream, const double* m, long long row_stride, long long col_stride,
+                                  long long new_len, long long len, const TtmFragmentLayout& f, double* out);
+
+// Z(a,k,b) = sum_l M(k,l) X(a,l,b); x is (outer, len, inner) row-major, z is (outer, new_len, inner).
+cudaError_t launch_ttm(cudaStream_t stream, const double* x, long long outer, long long len, long long inner,
+                       const double* mfrag, const TtmFragmentLayout& f, long long new_len, double* z);
+
+// ---- Gram of the mode-n unfolding, read in place (gram_kernels.cu) -----------
+struct GramLayout {
+  int tiles = 1;     // ceil(rows / 64)
+  int splits = 1;    // deterministic split of the column (contraction) range
+  long long chunks = 0;
+  size_t workspace_doubles = 0;  // splits * rows * rows
+};
+GramLayout gram_layout(long long outer, long long rows, long long inner, int sm_count);
+// gram (rows x rows, full symmetric storage) = sum_{a,b} Y(a,:,b) Y(a,:,b)^T, y viewed as (outer, rows, inner).
+cudaError_t launch_gram(cudaStream_t stream, const double* y, long long outer, long long rows, long long inner,
+                        const GramLayout& g, double* workspace, double* gram);
+
+// ---- small helpers (misc_kernels.cu) ------------------------------------------
+// out[0] = sum x[i]^2 (deterministic two-level reduction); scratch needs reduce_scratch_doubles() entries.
+size_t reduce_scratch_doubles();
+cudaError_t launch_sum_squares(cudaStream_t stream, const double* x, size_t n, double* scratch, double* out);
+cudaError_t launch_diff_sum_squares(cudaStream_t stream, const double* x, const double* y, size_t n, double* scratch,
+                                    double* out);
+// y[i] = beta * y[i] + alpha * x[i]
+cudaError_t launch_axpby(cudaStream_t stream, double* y, double beta, double alpha, const double* x, size_t n);
+// Top-k eigenvectors from an ascending syevd result (vectors column-major rows x rows, eigenvalues w) with the
+// reference's sign rule and degenerate-gap flag (hooi.hpp:60-74).  factor is rows x k column-major; *flag is OR-ed.
+cudaError_t launch_select_basis(cudaStream_t stream, const double* vectors, const double* w, int rows, int k,
+                                double* factor, int* flag);
+
+}  // namespace tpb

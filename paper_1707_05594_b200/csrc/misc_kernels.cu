@@ -1,0 +1,136 @@
+// Small device helpers around the two hot kernels: deterministic norms and the
+// eigenvector selection with the reference's sign / gap rules.
+#include <cuda_runtime.h>
+
+#include <cfloat>
+
+#include "kernels.cuh"
+
+namespace tpb {
+namespace {
+
+constexpr int kReduceBlocks = 1184;  // 8 per SM on a 148-SM part
+constexpr int kReduceThreads = 256;
+
+__device__ __forceinline__ double block_sum(double v) {
+  __shared__ double warp_sums[kReduceThreads / 32];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  if ((threadIdx.x & 31) == 0) warp_sums[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double total = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < kReduceThreads / 32; ++w) total += warp_sums[w];
+  return total;  // valid on thread 0
+}
+
+// Every block accumulates a fixed, index-determined subset, so the result does not depend on scheduling.
+template <bool DIFF>
+__global__ void __launch_bounds__(kReduceThreads) partial_sum_squares(const double* __restrict__ x,
+                                                                       const double* __restrict__ y, size_t n,
+                                                                       double* __restrict__ partial) {
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+  for (; i + 3 * stride < n; i += 4 * stride) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double v = DIFF ? x[i + u * stride] - y[i + u * stride] : x[i + u * stride];
+      acc[u] = fma(v, v, acc[u]);
+    }
+  }
+  for (; i < n; i += stride) {
+    const double v = DIFF ? x[i] - y[i] : x[i];
+    acc[0] = fma(v, v, acc[0]);
+  }
+  const double total = block_sum((acc[0] + acc[1]) + (acc[2] + acc[3]));
+  if (threadIdx.x == 0) partial[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(kReduceThreads) final_sum(const double* __restrict__ partial, int n,
+                                                            double* __restrict__ out) {
+  double v = 0.0;
+  for (int i = threadIdx.x; i < n; i += kReduceThreads) v += partial[i];
+  const double total = block_sum(v);
+  if (threadIdx.x == 0) *out = total;
+}
+
+// One block per kept eigenvector j: column rows-1-j of the ascending eigenvector matrix, sign chosen so the
+// largest-magnitude entry (first on ties) is positive (reference hooi.hpp:60-68).  Block 0 also evaluates the
+// spectral-gap flag (hooi.hpp:70-74).
+__global__ void __launch_bounds__(256) select_basis_kernel(const double* __restrict__ vectors,
+                                                           const double* __restrict__ w, int rows, int k,
+                                                           double* __restrict__ factor, int* __restrict__ flag) {
+  const int j = blockIdx.x;
+  const double* col = vectors + static_cast<long long>(rows - 1 - j) * rows;
+  __shared__ double best_abs[256];
+  __shared__ int best_idx[256];
+  double ba = -1.0;
+  int bi = 0x7fffffff;
+  for (int i = threadIdx.x; i < rows; i += blockDim.x) {
+    const double a = fabs(col[i]);
+    if (a > ba) {  // strict: keeps the first index within this thread's ascending walk
+      ba = a;
+      bi = i;
+    }
+  }
+  best_abs[threadIdx.x] = ba;
+  best_idx[threadIdx.x] = bi;
+  __syncthreads();
+  for (int off = blockDim.x / 2; off > 0; off >>= 1) {
+    if (threadIdx.x < off) {
+      const double oa = best_abs[threadIdx.x + off];
+      const int oi = best_idx[threadIdx.x + off];
+      if (oa > best_abs[threadIdx.x] || (oa == best_abs[threadIdx.x] && oi < best_idx[threadIdx.x])) {
+        best_abs[threadIdx.x] = oa;
+        best_idx[threadIdx.x] = oi;
+      }
+    }
+    __syncthreads();
+  }
+  const double sign = col[best_idx[0]] < 0.0 ? -1.0 : 1.0;
+  double* dst = factor + static_cast<long long>(j) * rows;
+  for (int i = threadIdx.x; i < rows; i += blockDim.x) dst[i] = sign * col[i];
+  if (j == 0 && threadIdx.x == 0 && k < rows) {
+    const double top = fmax(w[rows - 1], 0.0);
+    const double gap = w[rows - k] - w[rows - 1 - k];
+    if (gap <= 1e-10 * fmax(top, 1e-300)) atomicOr(flag, 1);
+  }
+}
+
+__global__ void __launch_bounds__(256) axpby_kernel(double* __restrict__ y, double beta, double alpha,
+                                                    const double* __restrict__ x, size_t n) {
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n; i += stride)
+    y[i] = fma(alpha, x[i], beta * y[i]);
+}
+
+}  // namespace
+
+cudaError_t launch_axpby(cudaStream_t stream, double* y, double beta, double alpha, const double* x, size_t n) {
+  axpby_kernel<<<kReduceBlocks, 256, 0, stream>>>(y, beta, alpha, x, n);
+  return cudaGetLastError();
+}
+
+size_t reduce_scratch_doubles() { return kReduceBlocks; }
+
+cudaError_t launch_sum_squares(cudaStream_t stream, const double* x, size_t n, double* scratch, double* out) {
+  partial_sum_squares<false><<<kReduceBlocks, kReduceThreads, 0, stream>>>(x, nullptr, n, scratch);
+  final_sum<<<1, kReduceThreads, 0, stream>>>(scratch, kReduceBlocks, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_diff_sum_squares(cudaStream_t stream, const double* x, const double* y, size_t n, double* scratch,
+                                    double* out) {
+  partial_sum_squares<true><<<kReduceBlocks, kReduceThreads, 0, stream>>>(x, y, n, scratch);
+  final_sum<<<1, kReduceThreads, 0, stream>>>(scratch, kReduceBlocks, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_select_basis(cudaStream_t stream, const double* vectors, const double* w, int rows, int k,
+                                double* factor, int* flag) {
+  select_basis_kernel<<<k, 256, 0, stream>>>(vectors, w, rows, k, factor, flag);
+  return cudaGetLastError();
+}
+
+}  // namespace tpb

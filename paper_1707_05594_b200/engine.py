@@ -1,0 +1,403 @@
+"""Device engine: host-side mirror of the reference's dense API (ttm.hpp, hooi.hpp) over the C ABI.
+
+Two levels, as in include/tuckerplan_b200.h:
+  * by-value functions with the reference's names and argument meaning (`ttm`, `leading_left_factors`,
+    `hooi_sweep`, `reconstruction_error`, `random_decomposition`) — NumPy arrays in, NumPy arrays out, the
+    tensor uploaded per call, exactly what the reference signatures imply;
+  * handles (`Context`, `DeviceTensor`, `HooiPlan`) that keep the tensor and the factors resident in HBM across
+    sweeps — what a caller doing many sweeps should use.
+
+Nothing here computes on the CPU: every call goes to the CUDA library and fails with Errc.cuda without a B200.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from ._lib import TuckerplanError, Errc, check, dbl_p, lib, size_array, u64, u64_array
+from .planner import ProblemSpec, TtmTree, validate_spec
+from . import hostgen
+
+JACOBI, GAUSS_SEIDEL = 0, 1
+_KINDS = {"jacobi": JACOBI, "gauss_seidel": GAUSS_SEIDEL, "gauss-seidel": GAUSS_SEIDEL, JACOBI: JACOBI,
+          GAUSS_SEIDEL: GAUSS_SEIDEL}
+
+lib.tp_tensor_device_ptr.restype = ctypes.c_void_p
+
+
+class _SweepStatsC(ctypes.Structure):
+    _fields_ = [("tree_macs", ctypes.c_uint64), ("core_macs", ctypes.c_uint64), ("peak_live", ctypes.c_int),
+                ("degenerate", ctypes.c_int)]
+
+
+class _SweepTimingC(ctypes.Structure):
+    _fields_ = [("total_ms", ctypes.c_float), ("tree_ms", ctypes.c_float), ("gram_ms", ctypes.c_float),
+                ("evd_ms", ctypes.c_float), ("core_ms", ctypes.c_float)]
+
+
+@dataclass
+class SweepStats:
+    """hooi.hpp:125-130."""
+    tree_macs: int = 0
+    core_macs: int = 0
+    peak_live: int = 0
+    degenerate: bool = False
+
+
+@dataclass
+class Decomposition:
+    """hooi.hpp:78-81: core (extents K, row-major) and factors[n] (L_n x K_n)."""
+    core: np.ndarray
+    factors: List[np.ndarray]
+
+
+def _f64(a: np.ndarray) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _colmajor(a: np.ndarray) -> np.ndarray:
+    return np.asfortranarray(a, dtype=np.float64)
+
+
+class Context:
+    """One CUDA device + stream + cuSOLVER handle (tp_ctx)."""
+
+    def __init__(self, device: int = 0):
+        self._h = ctypes.c_void_p()
+        check(lib.tp_ctx_create(device, ctypes.byref(self._h)))
+
+    def close(self):
+        if self._h:
+            lib.tp_ctx_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def synchronize(self):
+        check(lib.tp_ctx_synchronize(self._h))
+
+    @property
+    def stream(self) -> int:
+        s = ctypes.c_void_p()
+        check(lib.tp_ctx_stream(self._h, ctypes.byref(s)))
+        return s.value or 0
+
+    def launch_counts(self):
+        a, b = u64(), u64()
+        check(lib.tp_ctx_launch_counts(self._h, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
+
+_default_ctx: Optional[Context] = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+class DeviceTensor:
+    """DenseTensor (dense_tensor.hpp:19-30) resident in HBM."""
+
+    def __init__(self, ctx: Context, handle, dims):
+        self.ctx, self._h, self.dims = ctx, handle, tuple(int(d) for d in dims)
+
+    @staticmethod
+    def upload(ctx: Context, array: np.ndarray) -> "DeviceTensor":
+        a = _f64(array)
+        h = ctypes.c_void_p()
+        check(lib.tp_tensor_upload(ctx._h, a.ndim, size_array(a.shape), a.ctypes.data_as(dbl_p), ctypes.byref(h)))
+        return DeviceTensor(ctx, h, a.shape)
+
+    @staticmethod
+    def upload_raw(ctx: Context, dims: Sequence[int], host_ptr: int) -> "DeviceTensor":
+        h = ctypes.c_void_p()
+        check(lib.tp_tensor_upload(ctx._h, len(dims), size_array(dims), ctypes.cast(host_ptr, dbl_p), ctypes.byref(h)))
+        return DeviceTensor(ctx, h, dims)
+
+    @staticmethod
+    def zeros(ctx: Context, dims: Sequence[int]) -> "DeviceTensor":
+        h = ctypes.c_void_p()
+        check(lib.tp_tensor_alloc(ctx._h, len(dims), size_array(dims), ctypes.byref(h)))
+        return DeviceTensor(ctx, h, dims)
+
+    @property
+    def size(self) -> int:
+        return int(np.prod(self.dims, dtype=np.int64))
+
+    @property
+    def device_ptr(self) -> int:
+        return lib.tp_tensor_device_ptr(self._h) or 0
+
+    def download(self) -> np.ndarray:
+        out = np.empty(self.dims, dtype=np.float64)
+        check(lib.tp_tensor_download(self.ctx._h, self._h, out.ctypes.data_as(dbl_p)))
+        return out
+
+    def norm(self) -> float:
+        out = ctypes.c_double()
+        check(lib.tp_tensor_norm(self.ctx._h, self._h, ctypes.byref(out)))
+        return out.value
+
+    def ttm(self, m: np.ndarray, mode: int, macs: Optional[list] = None) -> "DeviceTensor":
+        m = _colmajor(m)
+        if m.ndim != 2:
+            raise TuckerplanError(int(Errc.shape_mismatch), "matrix expected")
+        h = ctypes.c_void_p()
+        c = u64(macs[0]) if macs is not None else None
+        check(lib.tp_ttm(self.ctx._h, self._h, m.ctypes.data_as(dbl_p), ctypes.c_size_t(m.shape[0]),
+                         ctypes.c_size_t(m.shape[1]), int(mode), ctypes.byref(c) if c is not None else None,
+                         ctypes.byref(h)))
+        if macs is not None:
+            macs[0] = c.value
+        dims = list(self.dims)
+        dims[mode] = m.shape[0]
+        return DeviceTensor(self.ctx, h, dims)
+
+    def axpby(self, beta: float, alpha: float, x: "DeviceTensor") -> None:
+        """self = beta * self + alpha * x (input assembly helper)."""
+        check(lib.tp_tensor_axpby(self.ctx._h, self._h, ctypes.c_double(beta), ctypes.c_double(alpha), x._h))
+
+    def download_into(self, host_ptr: int) -> None:
+        check(lib.tp_tensor_download(self.ctx._h, self._h, ctypes.cast(host_ptr, dbl_p)))
+
+    def gram(self, mode: int) -> np.ndarray:
+        if not 0 <= mode < len(self.dims):
+            raise TuckerplanError(int(Errc.bad_mode), "mode out of range", mode)
+        rows = self.dims[mode]
+        out = np.empty((rows, rows), dtype=np.float64)
+        check(lib.tp_gram(self.ctx._h, self._h, int(mode), out.ctypes.data_as(dbl_p)))
+        return out
+
+    def leaf_factor(self, mode: int, k: int):
+        if not 0 <= mode < len(self.dims):
+            raise TuckerplanError(int(Errc.bad_mode), "mode out of range", mode)
+        out = np.zeros((self.dims[mode], max(int(k), 0)), dtype=np.float64, order="F")
+        deg = ctypes.c_int()
+        check(lib.tp_leaf_factor(self.ctx._h, self._h, int(mode), int(k), out.ctypes.data_as(dbl_p), ctypes.byref(deg)))
+        return out, bool(deg.value)
+
+    def free(self):
+        if self._h:
+            lib.tp_tensor_free(self.ctx._h, self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class HooiPlan:
+    """hooi_sweep (hooi.hpp:189-229) on a fixed (spec, tree, kind) with everything resident in HBM."""
+
+    def __init__(self, ctx: Context, spec: ProblemSpec, tree: TtmTree, kind="jacobi"):
+        self.ctx, self.spec, self.tree = ctx, spec, tree
+        if tree.n_modes != spec.n_modes():
+            raise TuckerplanError(int(Errc.shape_mismatch), "tree and spec mode counts differ")
+        self._h = ctypes.c_void_p()
+        n, L, K = spec._c()
+        nn, kind_a, mode_a, parent_a = tree._c()
+        check(lib.tp_plan_create(ctx._h, n, L, K, nn, kind_a, mode_a, parent_a, _KINDS[kind], ctypes.byref(self._h)))
+
+    def _factor_ptrs(self, arrays):
+        return (dbl_p * len(arrays))(*[a.ctypes.data_as(dbl_p) for a in arrays])
+
+    def set_factors(self, factors: Sequence[np.ndarray]):
+        if len(factors) != self.spec.n_modes():
+            raise TuckerplanError(int(Errc.shape_mismatch), "factor count differs from mode count")
+        fs = []
+        for f, l, k in zip(factors, self.spec.L, self.spec.K):
+            if tuple(f.shape) != (l, k):
+                raise TuckerplanError(int(Errc.shape_mismatch), "factor shape differs from L x K")
+            fs.append(_colmajor(f))
+        check(lib.tp_plan_set_factors(self.ctx._h, self._h, self._factor_ptrs(fs)))
+
+    def get_factors(self) -> List[np.ndarray]:
+        outs = [np.zeros((l, k), dtype=np.float64, order="F") for l, k in zip(self.spec.L, self.spec.K)]
+        check(lib.tp_plan_get_factors(self.ctx._h, self._h, self._factor_ptrs(outs)))
+        return outs
+
+    def get_core(self) -> np.ndarray:
+        out = np.empty(tuple(self.spec.K), dtype=np.float64)
+        check(lib.tp_plan_get_core(self.ctx._h, self._h, out.ctypes.data_as(dbl_p)))
+        return out
+
+    def core_norm(self) -> float:
+        out = ctypes.c_double()
+        check(lib.tp_plan_core_norm(self.ctx._h, self._h, ctypes.byref(out)))
+        return out.value
+
+    def compute_core(self, t: DeviceTensor):
+        check(lib.tp_plan_compute_core(self.ctx._h, self._h, t._h))
+
+    def sweep(self, t: DeviceTensor) -> SweepStats:
+        st = _SweepStatsC()
+        check(lib.tp_plan_sweep(self.ctx._h, self._h, t._h, ctypes.byref(st)))
+        return SweepStats(st.tree_macs, st.core_macs, st.peak_live, bool(st.degenerate))
+
+    def last_timing(self) -> dict:
+        tm = _SweepTimingC()
+        check(lib.tp_plan_last_timing(self.ctx._h, self._h, ctypes.byref(tm)))
+        return {"total_ms": tm.total_ms, "tree_ms": tm.tree_ms, "gram_ms": tm.gram_ms, "evd_ms": tm.evd_ms,
+                "core_ms": tm.core_ms}
+
+    def node_timing(self):
+        """(node_ms, evd_ms) per tree node of the last sweep: TTM launch time for mode nodes, Gram for leaves."""
+        nn = len(self.tree.kind)
+        a, b = (ctypes.c_float * nn)(), (ctypes.c_float * nn)()
+        check(lib.tp_plan_node_timing(self.ctx._h, self._h, nn, a, b))
+        return list(a), list(b)
+
+    def reconstruction_error(self, t: DeviceTensor) -> float:
+        out = ctypes.c_double()
+        check(lib.tp_plan_reconstruction_error(self.ctx._h, self._h, t._h, ctypes.byref(out)))
+        return out.value
+
+    def fit_from_norms(self, t: DeviceTensor) -> float:
+        out = ctypes.c_double()
+        check(lib.tp_plan_fit_from_norms(self.ctx._h, self._h, t._h, ctypes.byref(out)))
+        return out.value
+
+    def close(self):
+        if self._h:
+            lib.tp_plan_destroy(self.ctx._h, self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ------------------------------------------------------------------ by-value API (reference signatures)
+def ttm(t: np.ndarray, m: np.ndarray, mode: int, macs: Optional[list] = None, ctx: Optional[Context] = None):
+    """ttm(t, m, mode, macs*) — ttm.hpp:73-96."""
+    ctx = ctx or default_context()
+    dt = DeviceTensor.upload(ctx, t)
+    try:
+        out = dt.ttm(m, mode, macs)
+        try:
+            return out.download()
+        finally:
+            out.free()
+    finally:
+        dt.free()
+
+
+def leading_left_factors(m: np.ndarray, k: int, ctx: Optional[Context] = None):
+    """leading_left_factors(m, k) — hooi.hpp:45-76.  Returns (vectors rows x k, degenerate)."""
+    ctx = ctx or default_context()
+    m = np.asarray(m, dtype=np.float64)
+    if m.ndim != 2:
+        m = m.reshape(m.shape[0] if m.ndim else 0, -1) if m.size else np.zeros((0, 0))
+    mf = _colmajor(m)
+    rows, cols = mf.shape
+    out = np.zeros((rows, max(int(k), 0)), dtype=np.float64, order="F")
+    deg = ctypes.c_int()
+    check(lib.tp_leading_left_factors(ctx._h, mf.ctypes.data_as(dbl_p), ctypes.c_size_t(rows), ctypes.c_size_t(cols),
+                                      int(k), out.ctypes.data_as(dbl_p), ctypes.byref(deg)))
+    return out, bool(deg.value)
+
+
+def _check_engine_shapes(t: np.ndarray, s: ProblemSpec):
+    if t.ndim != s.n_modes():
+        raise TuckerplanError(int(Errc.shape_mismatch), "tensor and spec mode counts differ")
+    for m in range(t.ndim):
+        if t.shape[m] != s.L[m]:
+            raise TuckerplanError(int(Errc.shape_mismatch), "tensor extent differs from L", m)
+
+
+def hooi_sweep(t: np.ndarray, s: ProblemSpec, d: Decomposition, tree: TtmTree, kind="jacobi",
+               stats: Optional[SweepStats] = None, ctx: Optional[Context] = None) -> Decomposition:
+    """hooi_sweep(t, s, d, tree, kind, stats*) — hooi.hpp:189-229, by value through tp_hooi_sweep_host."""
+    ctx = ctx or default_context()
+    t = _f64(t)
+    _check_engine_shapes(t, s)
+    if tree.n_modes != s.n_modes():
+        raise TuckerplanError(int(Errc.shape_mismatch), "tree and spec mode counts differ")
+    # validate_tree precedes the factor-count check in the reference (hooi.hpp:193-195)
+    from .planner import validate_tree
+    validate_tree(tree, s)
+    if len(d.factors) != s.n_modes():
+        raise TuckerplanError(int(Errc.shape_mismatch), "factor count differs from mode count")
+    fin = [_colmajor(f) for f in d.factors]
+    fout = [np.zeros((l, k), dtype=np.float64, order="F") for l, k in zip(s.L, s.K)]
+    core = np.empty(tuple(s.K), dtype=np.float64)
+    st = _SweepStatsC()
+    nn, kind_a, mode_a, parent_a = tree._c()
+    n = s.n_modes()
+    check(lib.tp_hooi_sweep_host(ctx._h, n, size_array(t.shape), t.ctypes.data_as(dbl_p), u64_array(s.K),
+                                 (dbl_p * n)(*[a.ctypes.data_as(dbl_p) for a in fin]), nn, kind_a, mode_a, parent_a,
+                                 _KINDS[kind], (dbl_p * n)(*[a.ctypes.data_as(dbl_p) for a in fout]),
+                                 core.ctypes.data_as(dbl_p), ctypes.byref(st)))
+    if stats is not None:
+        stats.tree_macs, stats.core_macs = st.tree_macs, st.core_macs
+        stats.peak_live, stats.degenerate = st.peak_live, bool(st.degenerate)
+    return Decomposition(core, fout)
+
+
+def core_from_factors(t: np.ndarray, factors: Sequence[np.ndarray], ctx: Optional[Context] = None) -> np.ndarray:
+    """detail::core_from_factors — hooi.hpp:93-100."""
+    ctx = ctx or default_context()
+    dt = DeviceTensor.upload(ctx, t)
+    try:
+        cur = dt
+        for n, f in enumerate(factors):
+            nxt = cur.ttm(np.asarray(f).T, n)
+            if cur is not dt:
+                cur.free()
+            cur = nxt
+        out = cur.download()
+        if cur is not dt:
+            cur.free()
+        return out
+    finally:
+        dt.free()
+
+
+def random_decomposition(t: np.ndarray, s: ProblemSpec, seed: int, ctx: Optional[Context] = None) -> Decomposition:
+    """random_decomposition(t, s, seed) — hooi.hpp:106-123."""
+    validate_spec(s)
+    t = _f64(t)
+    _check_engine_shapes(t, s)
+    factors = hostgen.random_orthonormal_factors(s.L, s.K, seed)
+    return Decomposition(core_from_factors(t, factors, ctx), factors)
+
+
+def reconstruction_error(t: np.ndarray, d: Decomposition, ctx: Optional[Context] = None) -> float:
+    """reconstruction_error(t, d) — hooi.hpp:232-245."""
+    ctx = ctx or default_context()
+    t = _f64(t)
+    dt = DeviceTensor.upload(ctx, t)
+    try:
+        out = ctypes.c_double()
+        n = t.ndim
+        if d.core is None or len(d.factors) != n or np.ndim(d.core) != n:
+            # the reference evaluates the norm first (zero_tensor), then fails on the shape
+            if dt.norm() == 0.0:
+                raise TuckerplanError(int(Errc.zero_tensor), "relative error undefined at zero")
+            raise TuckerplanError(int(Errc.shape_mismatch), "reconstruction shape differs")
+        core = _f64(d.core)
+        fs = [_colmajor(f) for f in d.factors]
+        for m, f in enumerate(fs):
+            if f.shape != (t.shape[m], core.shape[m]):
+                if dt.norm() == 0.0:
+                    raise TuckerplanError(int(Errc.zero_tensor), "relative error undefined at zero")
+                raise TuckerplanError(int(Errc.shape_mismatch), "reconstruction shape differs")
+        check(lib.tp_reconstruction_error(ctx._h, dt._h, size_array(core.shape), core.ctypes.data_as(dbl_p),
+                                          (dbl_p * n)(*[a.ctypes.data_as(dbl_p) for a in fs]), ctypes.byref(out)))
+        return out.value
+    finally:
+        dt.free()

@@ -1,0 +1,302 @@
+"""GPU parity tests: the CUDA engine (through the C ABI) against the oracle on the same seeded inputs.
+Mirrors reference tests/test_engine.cpp; bounds are stated next to each check."""
+import numpy as np
+import pytest
+
+from oracle import hooi_oracle as ho
+from paper_1707_05594_b200 import Errc, TuckerplanError, engine as E, hostgen, planner as P, workloads as W
+
+pytestmark = pytest.mark.gpu
+EPS = np.finfo(np.float64).eps
+
+
+def otree(t):
+    return ho.Tree(t.n_modes, t.kind, t.mode, t.parent)
+
+
+def code_of(fn):
+    with pytest.raises(TuckerplanError) as e:
+        fn()
+    return e.value.code
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = E.Context(0)
+    yield c
+    c.close()
+
+
+def ttm_bound(t, m, mode):
+    # forward error of a length-L dot product in any summation order is <= L eps sum|m||x|; oracle (BLAS) and
+    # DMMA both obey it, so they differ by at most twice that.  sum|m||x| <= L max|m| max|x|.
+    L = t.shape[mode]
+    return 2 * L * EPS * L * np.max(np.abs(m)) * np.max(np.abs(t)) + 1e-300
+
+
+TTM_SHAPES = [
+    # dims, mode, new_len
+    ((4, 3, 5), 0, 1), ((4, 3, 5), 0, 2), ((4, 3, 5), 0, 6), ((4, 3, 5), 1, 1), ((4, 3, 5), 1, 2), ((4, 3, 5), 1, 6),
+    ((4, 3, 5), 2, 1), ((4, 3, 5), 2, 2), ((4, 3, 5), 2, 6),            # test_engine.cpp:109-125
+    ((1,), 0, 1), ((7,), 0, 3), ((1, 1, 1), 1, 1), ((9, 1), 0, 4), ((1, 9), 1, 4),
+    ((37, 41), 0, 5), ((37, 41), 1, 5), ((64, 64, 64), 1, 8), ((64, 64, 64), 0, 8), ((64, 64, 64), 2, 8),
+    ((33, 50, 6), 1, 20), ((33, 50, 5), 1, 20), ((33, 50, 2), 1, 20), ((33, 50, 3), 1, 7),   # tiny / odd inner
+    ((10, 100, 48), 1, 10), ((10, 96, 100), 1, 10), ((17, 23, 129), 1, 13), ((5, 200, 200), 1, 20),
+    ((200, 4000), 0, 20), ((4000, 200), 1, 20), ((4001, 201), 1, 20), ((1000, 50), 1, 5), ((999, 49), 1, 5),
+    ((2, 160, 130), 1, 100), ((130, 160), 1, 100), ((160, 2, 70), 0, 100), ((3, 300, 16), 1, 130),
+    ((6, 5, 4, 3, 2), 2, 3), ((6, 5, 4, 3, 2), 4, 2), ((6, 5, 4, 3, 2), 0, 6), ((8, 8, 8, 8), 3, 8),
+    ((40, 48, 48), 0, 8), ((12, 48, 2304), 1, 8), ((3, 96, 96), 1, 10), ((24, 11, 16), 1, 33), ((3, 70, 10), 1, 70),
+]
+
+
+@pytest.mark.parametrize("dims,mode,new_len", TTM_SHAPES)
+def test_ttm_matches_oracle(ctx, dims, mode, new_len):
+    seed = (sum(dims) * 31 + mode * 7 + new_len) % 10000
+    t = hostgen.random_tensor(dims, seed)
+    m = hostgen.random_tensor([new_len, dims[mode]], seed + 1)
+    macs = [5]
+    got = E.ttm(t, m, mode, macs, ctx=ctx)
+    want = ho.ttm(t, m, mode)
+    assert got.shape == want.shape
+    assert macs[0] == 5 + new_len * t.size                      # exact MAC ledger, accumulating (ttm.hpp:92-94)
+    assert np.max(np.abs(got - want)) <= ttm_bound(t, m, mode)
+    # and far tighter in the typical case: a few ulps of the result scale
+    assert np.max(np.abs(got - want)) <= 64 * EPS * np.sqrt(dims[mode]) * np.max(np.abs(m)) * np.max(np.abs(t))
+
+
+def test_ttm_linearity_and_identity(ctx):
+    """Size-independent properties at a size the oracle would not finish quickly: identity and linearity."""
+    dims = (96, 96, 96, 12)
+    t = hostgen.random_tensor(dims, 3)
+    for mode in range(4):
+        eye = np.eye(dims[mode])
+        assert np.array_equal(E.ttm(t, eye, mode, ctx=ctx), t)  # multiplying by exact 0/1 is exact
+    a = hostgen.random_tensor([10, 96], 4)
+    b = hostgen.random_tensor([10, 96], 5)
+    lhs = E.ttm(t, a + b, 1, ctx=ctx)
+    rhs = E.ttm(t, a, 1, ctx=ctx) + E.ttm(t, b, 1, ctx=ctx)
+    assert np.max(np.abs(lhs - rhs)) <= 8 * 96 * EPS * np.max(np.abs(t)) * 4
+
+
+def test_ttm_error_codes(ctx):
+    t = hostgen.random_tensor((4, 3, 5), 2)
+    assert code_of(lambda: E.ttm(t, np.eye(4), 1, ctx=ctx)) == Errc.shape_mismatch       # test_engine.cpp:134-135
+    assert code_of(lambda: E.ttm(t, np.eye(4), 3, ctx=ctx)) == Errc.bad_mode
+    assert code_of(lambda: E.ttm(t, np.eye(4), -1, ctx=ctx)) == Errc.bad_mode
+    assert code_of(lambda: E.ttm(t, np.zeros((0, 3)), 1, ctx=ctx)) == Errc.shape_mismatch
+    macs = [2 ** 64 - 10]
+    assert code_of(lambda: E.ttm(t, np.eye(4), 0, macs, ctx=ctx)) == Errc.overflow
+
+
+GRAM_SHAPES = [((6, 40), 0), ((40, 6), 1), ((5, 7, 3), 1), ((5, 7, 3), 0), ((5, 7, 3), 2), ((20, 200, 20), 1),
+               ((200, 20, 20), 0), ((20, 20, 200), 2), ((10, 130, 33), 1), ((3, 65, 64), 1), ((10, 10, 96, 10), 2),
+               ((129, 100), 0), ((100, 129), 1), ((8, 48, 8, 8), 1), ((400, 7, 11), 0), ((2, 2, 2, 2, 50), 4)]
+
+
+@pytest.mark.parametrize("dims,mode", GRAM_SHAPES)
+def test_gram_matches_oracle(ctx, dims, mode):
+    t = hostgen.random_tensor(dims, 17 + mode)
+    dt = E.DeviceTensor.upload(ctx, t)
+    got = dt.gram(mode)
+    dt.free()
+    u = ho.unfold(t, mode)
+    want = u @ u.T
+    cols = u.shape[1]
+    assert np.array_equal(got, got.T)                                   # full symmetric storage
+    assert np.max(np.abs(got - want)) <= 64 * EPS * np.sqrt(cols) * np.max(np.abs(t)) ** 2 * np.sqrt(cols)
+
+
+def test_truncated_basis(ctx):
+    rng = np.random.default_rng(3)
+    u, _ = np.linalg.qr(rng.standard_normal((6, 6)))
+    v, _ = np.linalg.qr(rng.standard_normal((40, 6)))
+    m = u @ np.diag([5, 4, 3, 2, 1, 0.5]) @ v.T
+    uu = np.linalg.svd(m)[0]
+    for k in range(1, 6):                                               # test_engine.cpp:138-155
+        b, deg = E.leading_left_factors(m, k, ctx=ctx)
+        assert not deg
+        assert np.max(np.abs(b.T @ b - np.eye(k))) < 1e-9
+        assert ho.projector_gap(b, uu[:, :k]) < 1e-9
+        ob, _ = ho.leading_left_factors(m, k)
+        assert np.max(np.abs(b - ob)) < 1e-9                            # same signs as the oracle
+    b, _ = E.leading_left_factors(np.array([[0.0], [-3.0]]), 1, ctx=ctx)  # test_engine.cpp:157-162
+    assert abs(b[0, 0]) < 1e-12 and abs(b[1, 0] - 1) < 1e-12
+    a, _ = np.linalg.qr(rng.standard_normal((4, 3)))
+    for k in (1, 2, 3):                                                 # Gram ignores the sign of the data
+        assert np.array_equal(E.leading_left_factors(a, k, ctx=ctx)[0], E.leading_left_factors(-a, k, ctx=ctx)[0])
+    d = np.diag([2.0, 1.0, 1.0])                                        # test_engine.cpp:172-176
+    assert not E.leading_left_factors(d, 1, ctx=ctx)[1]
+    assert E.leading_left_factors(d, 2, ctx=ctx)[1]
+    eye = np.eye(3)                                                     # test_engine.cpp:178-188
+    assert code_of(lambda: E.leading_left_factors(eye, 0, ctx=ctx)) == Errc.bad_argument
+    assert code_of(lambda: E.leading_left_factors(eye, 4, ctx=ctx)) == Errc.bad_argument
+    assert code_of(lambda: E.leading_left_factors(np.zeros((0, 0)), 1, ctx=ctx)) == Errc.shape_mismatch
+    assert code_of(lambda: E.leading_left_factors(np.zeros((2049, 1)), 1, ctx=ctx)) == Errc.too_large
+
+
+def test_random_start_and_exact_reconstruction(ctx):
+    s = P.ProblemSpec([6, 5, 4], [3, 2, 2])                             # test_engine.cpp:190-204
+    t = hostgen.random_tensor([6, 5, 4], 31)
+    a = E.random_decomposition(t, s, 7, ctx=ctx)
+    b = E.random_decomposition(t, s, 7, ctx=ctx)
+    assert a.core.shape == (3, 2, 2)
+    for n in range(3):
+        assert np.max(np.abs(a.factors[n].T @ a.factors[n] - np.eye(s.K[n]))) < 1e-12
+        assert np.array_equal(a.factors[n], b.factors[n])
+    assert np.array_equal(a.core, b.core)                               # bit-reproducible reruns
+    want = ho.core_from_factors(t, a.factors)
+    assert np.max(np.abs(a.core - want)) < 1e-13
+    s = P.ProblemSpec([4, 3, 5], [4, 3, 5])                             # test_engine.cpp:206-211
+    t = hostgen.random_tensor([4, 3, 5], 13)
+    d = E.random_decomposition(t, s, 5, ctx=ctx)
+    assert E.reconstruction_error(t, d, ctx=ctx) < 1e-12
+
+
+def test_readme_transcript_on_gpu(ctx, readme_kat):
+    """proj/README.md:122-126 through the CUDA engine: Gauss-Seidel on the chain-input tree."""
+    L, K = readme_kat["dims"], readme_kat["K"]
+    s = P.ProblemSpec(L, K)
+    t = hostgen.random_tensor(L, readme_kat["tensor_seed"])
+    d = E.random_decomposition(t, s, readme_kat["init_seed"], ctx=ctx)
+    assert "%.12f" % E.reconstruction_error(t, d, ctx=ctx) == readme_kat["start_error"]
+    st = E.SweepStats()
+    d = E.hooi_sweep(t, s, d, P.chain_tree(s), "gauss_seidel", st, ctx=ctx)
+    assert "%.12f" % E.reconstruction_error(t, d, ctx=ctx) == readme_kat["sweep1_error"]
+    assert st.tree_macs == readme_kat["tree_macs"] and st.peak_live == readme_kat["peak_live"]
+
+
+def test_sweep_integer_goldens(ctx):
+    L, K = [6, 5, 4], [3, 2, 2]                                         # test_engine.cpp:213-227
+    s = P.ProblemSpec(L, K)
+    t = hostgen.random_tensor(L, 41)
+    d = E.random_decomposition(t, s, 1, ctx=ctx)
+    for tree in (P.chain_tree(s), P.optimal_tree(s).tree):
+        st = E.SweepStats()
+        E.hooi_sweep(t, s, d, tree, "jacobi", st, ctx=ctx)
+        assert st.tree_macs == P.tree_cost(tree, s).total_macs
+    st = E.SweepStats()
+    E.hooi_sweep(t, s, d, P.chain_tree(s), "gauss_seidel", st, ctx=ctx)
+    assert st.tree_macs == 1296
+    assert st.core_macs == 3 * 120 + 2 * 60 + 2 * 24
+    s = P.ProblemSpec([5, 4, 3, 2], [2, 2, 2, 2])                       # test_engine.cpp:229-242
+    t = hostgen.random_tensor(s.L, 3)
+    d = E.random_decomposition(t, s, 9, ctx=ctx)
+    cases = [(P.chain_tree(s), "jacobi"), (P.balanced_tree(s), "jacobi"), (P.optimal_tree(s).tree, "jacobi"),
+             (P.chain_tree(s), "gauss_seidel")]
+    for tree, kind in cases:
+        st, ost = E.SweepStats(), ho.SweepStats()
+        E.hooi_sweep(t, s, d, tree, kind, st, ctx=ctx)
+        ho.hooi_sweep(t, s.L, s.K, d.factors, otree(tree), kind, ost)
+        assert st.peak_live <= P.tree_depth(tree) + 1
+        assert (st.tree_macs, st.core_macs, st.peak_live) == (ost.tree_macs, ost.core_macs, ost.peak_live)
+
+
+def test_jacobi_tree_independence_and_gs_monotone(ctx):
+    L, K = [8, 7, 6], [3, 3, 2]                                         # test_engine.cpp:244-271
+    s = P.ProblemSpec(L, K)
+    t = hostgen.random_tensor(L, 77)
+    d = E.random_decomposition(t, s, 2, ctx=ctx)
+    on_chain = E.hooi_sweep(t, s, d, P.chain_tree(s), "jacobi", ctx=ctx)
+    for tree in (P.balanced_tree(s), P.optimal_tree(s).tree):
+        other = E.hooi_sweep(t, s, d, tree, "jacobi", ctx=ctx)
+        for n in range(3):
+            assert ho.projector_gap(on_chain.factors[n], other.factors[n]) < 1e-9
+    t = hostgen.random_tensor(L, 55)
+    d = E.random_decomposition(t, s, 4, ctx=ctx)
+    prev = E.reconstruction_error(t, d, ctx=ctx)
+    for _ in range(6):
+        d = E.hooi_sweep(t, s, d, P.chain_tree(s), "gauss_seidel", ctx=ctx)
+        err = E.reconstruction_error(t, d, ctx=ctx)
+        assert err <= prev + 1e-12
+        prev = err
+
+
+def test_sweep_error_codes(ctx):
+    s = P.ProblemSpec([5, 4, 3], [2, 2, 2])                             # test_engine.cpp:273-300
+    t = hostgen.random_tensor(s.L, 6)
+    d = E.random_decomposition(t, s, 8, ctx=ctx)
+    assert code_of(lambda: E.hooi_sweep(t, s, d, P.balanced_tree(s), "gauss_seidel", ctx=ctx)) == Errc.needs_chain_tree
+    E.hooi_sweep(t, s, d, P.chain_tree(s), "gauss_seidel", ctx=ctx)
+    short = E.Decomposition(d.core, d.factors[:-1])
+    assert code_of(lambda: E.hooi_sweep(t, s, short, P.chain_tree(s), "jacobi", ctx=ctx)) == Errc.shape_mismatch
+    wrong = hostgen.random_tensor([5, 4, 4], 6)
+    assert code_of(lambda: E.random_decomposition(wrong, s, 1, ctx=ctx)) == Errc.shape_mismatch
+    assert code_of(lambda: E.reconstruction_error(np.zeros((2, 2)), E.Decomposition(None, []), ctx=ctx)) == Errc.zero_tensor
+    big = P.ProblemSpec([2049, 2], [2, 2])
+    tree = P.optimal_tree(big).tree
+    assert code_of(lambda: E.HooiPlan(ctx, big, tree, "jacobi")) == Errc.too_large
+
+
+def run_both(ctx, cfg, sweeps, kind="jacobi", tree=None):
+    """GPU (resident plan) and oracle on the same bits; returns per-sweep comparisons."""
+    spec = cfg.spec
+    tree = tree or P.optimal_tree(spec).tree
+    t = W.build_tensor_host(cfg)
+    f0 = W.start_factors(cfg)
+    dt = E.DeviceTensor.upload(ctx, t)
+    plan = E.HooiPlan(ctx, spec, tree, kind)
+    plan.set_factors(f0)
+    of = [f.copy() for f in f0]
+    tnorm = ho.frobenius_norm(t)
+    assert abs(dt.norm() - tnorm) <= 1e-13 * tnorm
+    rows = []
+    ocore = None
+    for _ in range(sweeps):
+        st = plan.sweep(dt)
+        ost = ho.SweepStats()
+        ocore, of = ho.hooi_sweep(t, spec.L, spec.K, of, otree(tree), kind, ost)
+        gf = plan.get_factors()
+        gcore = plan.get_core()
+        assert (st.tree_macs, st.core_macs, st.peak_live, st.degenerate) == \
+               (ost.tree_macs, ost.core_macs, ost.peak_live, ost.degenerate)
+        assert not st.degenerate                      # a degenerate cut has no unique subspace to compare
+        angle = max(ho.sin_largest_principal_angle(a, b) for a, b in zip(gf, of))
+        gn, on = np.sqrt(np.sum(gcore * gcore)), np.sqrt(np.sum(ocore * ocore))
+        assert abs(plan.core_norm() - gn) <= 1e-13 * gn
+        ofit = np.sqrt(max(tnorm ** 2 - on ** 2, 0.0)) / tnorm
+        rows.append(dict(angle=angle, core_rel=abs(gn - on) / on, fit_gpu=plan.fit_from_norms(dt), fit_oracle=ofit))
+    err_gpu = plan.reconstruction_error(dt)
+    err_oracle = ho.reconstruction_error(t, ocore, of)
+    plan.close()
+    dt.free()
+    return rows, err_gpu, err_oracle
+
+
+SWEEP_CASES = [
+    W.scaled_config(1, [40, 40, 40], [6, 6, 6], 3),
+    W.scaled_config(2, [20, 20, 20, 20], [4, 4, 4, 4], 3),
+    W.scaled_config(3, [40, 20, 20, 10], [8, 3, 5, 2], 3),
+    W.scaled_config(4, [10, 10, 10, 10, 10], [3, 3, 3, 3, 3], 3),
+    W.scaled_config(5, [130, 130, 130], [20, 20, 20], 2),
+    W.scaled_config(3, [33, 17, 9, 5], [5, 2, 3, 1], 2),
+]
+
+
+@pytest.mark.parametrize("cfg", SWEEP_CASES, ids=lambda c: c.name)
+def test_sweep_parity_small(ctx, cfg):
+    """north_star bar: subspaces up to column sign, core norm and relative fit within 1e-10 relative, stats exact."""
+    rows, err_gpu, err_oracle = run_both(ctx, cfg, cfg.iterations)
+    for r in rows:
+        assert r["angle"] < 1e-9                     # reference kProjectorTol (tolerances.hpp:17)
+        assert r["core_rel"] < 1e-10
+        assert abs(r["fit_gpu"] - r["fit_oracle"]) <= 1e-10 * max(r["fit_oracle"], 1e-3)
+    assert abs(err_gpu - err_oracle) <= 1e-10 * max(err_oracle, 1e-3)
+
+
+def test_sweep_parity_gauss_seidel(ctx):
+    cfg = W.scaled_config(1, [30, 24, 18], [5, 4, 3], 3)
+    rows, err_gpu, err_oracle = run_both(ctx, cfg, 3, "gauss_seidel", P.chain_tree(cfg.spec))
+    for r in rows:
+        assert r["angle"] < 1e-9 and r["core_rel"] < 1e-10
+    assert abs(err_gpu - err_oracle) <= 1e-10 * max(err_oracle, 1e-3)
+
+
+def test_sweep_parity_config1_full(ctx):
+    """BASELINE.json configs[0] at full size (200^3 -> 20^3, 5 Jacobi iterations on the optimal tree)."""
+    cfg = W.CONFIGS[1]
+    rows, err_gpu, err_oracle = run_both(ctx, cfg, cfg.iterations)
+    for r in rows:
+        assert r["angle"] < 1e-9 and r["core_rel"] < 1e-10
+        assert abs(r["fit_gpu"] - r["fit_oracle"]) <= 1e-10 * max(r["fit_oracle"], 1e-3)
+    assert abs(err_gpu - err_oracle) <= 1e-10 * max(err_oracle, 1e-3)
+    assert err_gpu < 2e-3                             # the noise floor: sigma * sqrt(|T|) / ||T||
