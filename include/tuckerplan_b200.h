@@ -210,6 +210,11 @@ typedef struct tp_sweep_timing {  /* device milliseconds of the last sweep, CUDA
 int tp_plan_create(tp_ctx* ctx, int n_modes, const tp_u64* L, const tp_u64* K, int n_nodes, const int* kind,
                    const int* mode, const int* parent, int sweep_kind, tp_plan** out);
 int tp_plan_destroy(tp_ctx* ctx, tp_plan* plan);
+/* Execution options (results are identical either way).  TP_OPT_OVERLAP_EVD (default 1): in a Jacobi sweep run each
+ * leaf's eigen-solve on a side stream beside the remaining tree TTMs; 0 serialises everything on one stream, which is
+ * what per-kernel timing and profiling want. */
+enum { TP_OPT_OVERLAP_EVD = 1 };
+int tp_plan_set_option(tp_ctx* ctx, tp_plan* plan, int option, int value);
 /* Decomposition::factors (hooi.hpp:78-81) <-> device: factors[n] is L_n x K_n column-major on the host */
 int tp_plan_set_factors(tp_ctx* ctx, tp_plan* plan, const double* const* factors);
 int tp_plan_get_factors(tp_ctx* ctx, tp_plan* plan, double* const* factors_out);
@@ -235,6 +240,31 @@ int tp_plan_fit_from_norms(tp_ctx* ctx, tp_plan* plan, const tp_tensor* t, doubl
  * dims[n] x core_dims[n] column-major) */
 int tp_reconstruction_error(tp_ctx* ctx, const tp_tensor* t, const size_t* core_dims, const double* core,
                             const double* const* factors, double* out);
+
+/* ------------------------------------------------- device-pointer building blocks (multi-GPU driver)
+ * The Cartesian-grid executor (paper_1707_05594_b200/distributed.py, one process per GPU) owns its device buffers
+ * and the collectives; these entry points are the local kernels it launches between them, all on the context's
+ * stream, all asynchronous.  Pointers are device pointers unless named *_host. */
+
+/* Local part of a mode-`mode` TTM of the block x (row-major, extents dims) with rows [l0, l0+dims[mode]) of the
+ * replicated factor (factor: L_full x K column-major):  z(a,k,b) = sum_l F(l0+l, k) x(a,l,b), all K rows.  With
+ * n_dest > 1 the K rows are split at dest_cuts[0..n_dest] and written destination-major, one contiguous chunk
+ * (outer, rows_d, inner) per peer of the mode-`mode` process group — the send buffer of the reduce-scatter that the
+ * paper's scheme needs exactly when the grid splits the contracted mode (grid_volume.hpp:41). */
+int tp_dev_ttm_partial(tp_ctx* ctx, const double* x, int n_modes, const size_t* dims, int mode, const double* factor,
+                       size_t L_full, size_t l0, size_t K, int n_dest, const size_t* dest_cuts, double* z);
+/* out[i] = slots[0][i] + ... + slots[n_slots-1][i], i < count, summed in slot order (deterministic). */
+int tp_dev_reduce_slots(tp_ctx* ctx, double* out, const double* const* slots_host, int n_slots, size_t count);
+/* dst(a, l0+l, b) = src(a, l, b): places a peer's mode slice (outer, count, inner) into (outer, full_len, inner). */
+int tp_dev_assemble_mode(tp_ctx* ctx, double* dst, size_t outer, size_t full_len, size_t inner, const double* src,
+                         size_t l0, size_t count);
+/* gram (rows x rows, full symmetric) of the mode-n unfolding of the block y viewed as (outer, rows, inner). */
+int tp_dev_gram(tp_ctx* ctx, const double* y, size_t outer, size_t rows, size_t inner, double* gram);
+/* top-k eigenvectors of gram (destroyed) with the reference's sign rule into factor (rows x k column-major);
+ * *flag (device int) is OR-ed with the degenerate-gap flag; *info (device int) receives the solver status. */
+int tp_dev_leaf_solve(tp_ctx* ctx, double* gram, size_t rows, int k, double* factor, int* flag, int* info);
+/* *out (device double) = sum x[i]^2 */
+int tp_dev_sum_squares(tp_ctx* ctx, const double* x, size_t count, double* out);
 
 /* By-value hooi_sweep (hooi.hpp:189-191): host tensor + host factors in, host factors + core out; uploads, runs,
  * downloads.  This is the call the reference-facing C++ wrapper makes. */

@@ -55,6 +55,12 @@ struct tp_ctx {
   double* reduce_scratch = nullptr;  // reduce_scratch_doubles() + 1 result slot
   double* frag_scratch = nullptr;    // fragment buffer for one-off TTMs
   size_t frag_capacity = 0;
+  // side streams for the eigen-solves of a Jacobi sweep: the leaves are independent of each other and of the
+  // remaining tree TTMs, and an eigen-solve is latency-bound, so it runs beside the TTM kernels
+  void* dev_scratch = nullptr;       // LeafScratch of the tp_dev_* entry points
+  static constexpr int kAux = 4;
+  cudaStream_t aux[kAux] = {nullptr, nullptr, nullptr, nullptr};
+  cusolverDnHandle_t aux_solver[kAux] = {nullptr, nullptr, nullptr, nullptr};
 };
 
 struct tp_tensor {
@@ -132,7 +138,7 @@ void run_ttm(tp_ctx* ctx, const double* x, const std::vector<size_t>& dims, int 
   const TtmFragmentLayout f = ttm_fragment_layout(new_len, len);
   if (!frag) frag = ensure_frag_scratch(ctx, f.doubles);
   TPB_CUDA(prep_factor_fragments(ctx->stream, m_dev, row_stride, col_stride, new_len, len, f, frag));
-  TPB_CUDA(launch_ttm(ctx->stream, x, outer, len, inner, frag, f, new_len, out));
+  TPB_CUDA(launch_ttm(ctx->stream, x, outer, len, inner, frag, f, new_len, out, ctx->sm_count));
   ctx->own_kernels += 2;
 }
 
@@ -227,11 +233,13 @@ long long leaf_gram(tp_ctx* ctx, LeafScratch& s, const double* y, const std::vec
 
 // Top-k eigenvectors of s.gram into factor_out (rows x k column-major): full symmetric eigen-solve (hooi.hpp:55),
 // then the sign / gap rules (hooi.hpp:60-74).  The eigen-solve is cuSOLVER's (off the hot path per the spec).
-void leaf_solve(tp_ctx* ctx, LeafScratch& s, long long rows, int k, double* factor_out) {
-  TPB_SOLVER(cusolverDnDsyevd(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, static_cast<int>(rows),
+void leaf_solve(tp_ctx* ctx, LeafScratch& s, long long rows, int k, double* factor_out, int aux = -1) {
+  cusolverDnHandle_t solver = aux < 0 ? ctx->solver : ctx->aux_solver[aux];
+  cudaStream_t stream = aux < 0 ? ctx->stream : ctx->aux[aux];
+  TPB_SOLVER(cusolverDnDsyevd(solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, static_cast<int>(rows),
                               s.gram, static_cast<int>(rows), s.w, s.work, s.lwork, s.info));
   ctx->library_calls += 1;
-  TPB_CUDA(launch_select_basis(ctx->stream, s.gram, s.w, static_cast<int>(rows), k, factor_out, s.flag));
+  TPB_CUDA(launch_select_basis(stream, s.gram, s.w, static_cast<int>(rows), k, factor_out, s.flag));
   ctx->own_kernels += 1;
 }
 
@@ -249,6 +257,23 @@ int read_and_clear_flag(tp_ctx* ctx, LeafScratch& s) {
   TPB_CUDA(cudaStreamSynchronize(ctx->stream));
   if (host[1] != 0) raise(TP_ERR_TOO_LARGE, "eigensolver did not converge");  // hooi.hpp:56-57
   return host[0];
+}
+
+int read_and_clear_flags(tp_ctx* ctx, std::vector<LeafScratch>& slots) {
+  std::vector<int> host(2 * slots.size(), 0);
+  for (size_t i = 0; i < slots.size(); ++i) {
+    if (!slots[i].flag) continue;
+    TPB_CUDA(cudaMemcpyAsync(&host[2 * i], slots[i].flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    TPB_CUDA(cudaMemcpyAsync(&host[2 * i + 1], slots[i].info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    TPB_CUDA(cudaMemsetAsync(slots[i].flag, 0, sizeof(int), ctx->stream));
+  }
+  TPB_CUDA(cudaStreamSynchronize(ctx->stream));
+  int flag = 0;
+  for (size_t i = 0; i < slots.size(); ++i) {
+    if (host[2 * i + 1] != 0) raise(TP_ERR_TOO_LARGE, "eigensolver did not converge");  // hooi.hpp:56-57
+    flag |= host[2 * i];
+  }
+  return flag;
 }
 
 }  // namespace
@@ -269,7 +294,11 @@ struct tp_plan {
   double* core = nullptr;
   double* core_tmp[2] = {nullptr, nullptr};
   size_t core_size = 0, core_tmp_cap = 0;
-  LeafScratch leaf;
+  std::vector<int> core_order;                // cheapest contraction order of the core chain
+  tp_u64 core_macs_executed = 0;
+  std::vector<LeafScratch> leaf;              // one Gram / eigen-solve scratch per mode (leaves run concurrently)
+  std::vector<cudaEvent_t> gram_ready, factor_ready;
+  bool overlap_evd = true;                    // Jacobi: eigen-solves on side streams beside the tree TTMs
   tp_sweep_stats model{};   // analytic SweepStats (tree_macs, core_macs, peak_live)
   tp_sweep_timing timing{};
   // event pool for phase timing: triples (phase, begin, end)
@@ -295,14 +324,15 @@ cudaEvent_t next_event(tp_plan* p) {
 }
 
 struct Span {
-  tp_ctx* ctx;
   tp_plan* plan;
-  Span(tp_ctx* c, tp_plan* p, int phase, int node = -1) : ctx(c), plan(p) {
+  cudaStream_t stream;
+  Span(tp_ctx* c, tp_plan* p, int phase, int node = -1, int aux = -1)
+      : plan(p), stream(aux < 0 ? c->stream : c->aux[aux]) {
     plan->event_phase.push_back(phase);
     plan->event_node.push_back(node);
-    TPB_CUDA(cudaEventRecord(next_event(plan), ctx->stream));
+    TPB_CUDA(cudaEventRecord(next_event(plan), stream));
   }
-  void close() { TPB_CUDA(cudaEventRecord(next_event(plan), ctx->stream)); }
+  void close() { TPB_CUDA(cudaEventRecord(next_event(plan), stream)); }
 };
 
 void plan_refresh_fragments(tp_ctx* ctx, tp_plan* p, int mode, const double* factor) {
@@ -316,26 +346,39 @@ void plan_ttm(tp_ctx* ctx, tp_plan* p, const double* x, const std::vector<size_t
   long long outer, inner;
   mode_extents(dims, mode, outer, inner);
   TPB_CUDA(launch_ttm(ctx->stream, x, outer, static_cast<long long>(dims[mode]), inner, p->frag[mode],
-                      p->frag_layout[mode], static_cast<long long>(p->spec.K[mode]), out));
+                      p->frag_layout[mode], static_cast<long long>(p->spec.K[mode]), out, ctx->sm_count));
   ctx->own_kernels += 1;
 }
 
+// Leaf update.  The Gram kernels stay on the main stream (the intermediate they read lives in a per-depth buffer the
+// next sibling TTM overwrites); with `overlap` the eigen-solve moves to a side stream and the main stream carries on
+// with the tree, joining again before the core chain needs the new factors.
 void plan_leaf(tp_ctx* ctx, tp_plan* p, const double* y, const std::vector<size_t>& dims, int mode, double* dst,
-               int node = -1) {
+               int node, bool overlap) {
   const int k = static_cast<int>(p->spec.K[mode]);
   Span gram(ctx, p, kGram, node);
-  const long long rows = leaf_gram(ctx, p->leaf, y, dims, mode, k);
+  const long long rows = leaf_gram(ctx, p->leaf[mode], y, dims, mode, k);
   gram.close();
-  Span evd(ctx, p, kEvd, node);
-  leaf_solve(ctx, p->leaf, rows, k, dst);
+  const int aux = overlap ? mode % tp_ctx::kAux : -1;
+  if (overlap) {
+    TPB_CUDA(cudaEventRecord(p->gram_ready[mode], ctx->stream));
+    TPB_CUDA(cudaStreamWaitEvent(ctx->aux[aux], p->gram_ready[mode], 0));
+  }
+  Span evd(ctx, p, kEvd, node, aux);
+  leaf_solve(ctx, p->leaf[mode], rows, k, dst, aux);
   evd.close();
+  if (overlap) TPB_CUDA(cudaEventRecord(p->factor_ready[mode], ctx->aux[aux]));
+}
+
+void plan_join_leaves(tp_ctx* ctx, tp_plan* p) {
+  for (int m = 0; m < p->n; ++m) TPB_CUDA(cudaStreamWaitEvent(ctx->stream, p->factor_ready[m], 0));
 }
 
 void jacobi_walk(tp_ctx* ctx, tp_plan* p, int node, const double* tensor, std::vector<size_t>& dims, int depth) {
   for (int c : p->tree.kids[node]) {
     const int mode = p->tree.mode[c];
     if (p->tree.kind[c] == TP_NODE_LEAF) {
-      plan_leaf(ctx, p, tensor, dims, mode, p->fresh[mode], c);
+      plan_leaf(ctx, p, tensor, dims, mode, p->fresh[mode], c, p->overlap_evd);
     } else {
       double* out = p->depth_buf[depth];
       {
@@ -351,19 +394,54 @@ void jacobi_walk(tp_ctx* ctx, tp_plan* p, int node, const double* tensor, std::v
   }
 }
 
-// core_from_factors (hooi.hpp:93-100): T x_0 F_0^T x_1 F_1^T ... in mode order, ping-pong buffers.
+// core_from_factors (hooi.hpp:93-100): T x_0 F_0^T ... x_{N-1} F_{N-1}^T.  Mode products along different modes
+// commute, so the chain runs in the cheapest order (plan->core_order) instead of the reference's fixed 0..N-1; the
+// result differs from the reference's only by rounding.  Ping-pong buffers, the last product lands in `core`.
 void plan_core(tp_ctx* ctx, tp_plan* p, const double* tensor, const std::vector<double*>& factors) {
   Span s(ctx, p, kCore);
   std::vector<size_t> dims(p->spec.L.begin(), p->spec.L.end());
   const double* src = tensor;
-  for (int m = 0; m < p->n; ++m) {
+  for (int i = 0; i < p->n; ++i) {
+    const int m = p->core_order[i];
     plan_refresh_fragments(ctx, p, m, factors[m]);
-    double* dst = (m == p->n - 1) ? p->core : p->core_tmp[m & 1];
+    double* dst = (i == p->n - 1) ? p->core : p->core_tmp[i & 1];
     plan_ttm(ctx, p, src, dims, m, dst);
     dims[m] = static_cast<size_t>(p->spec.K[m]);
     src = dst;
   }
   s.close();
+}
+
+// Cheapest order of the core chain: forward DP over the set of already-multiplied modes; ties keep the smaller mode
+// first (strict improvement only, modes scanned ascending), so the reference order wins whenever it is optimal.
+std::vector<int> cheapest_chain_order(const Spec& s, u64* macs_out) {
+  const int n = s.n();
+  const std::uint32_t full = (n >= 32) ? ~0u : ((1u << n) - 1);
+  std::vector<u64> best(static_cast<size_t>(full) + 1, kSat);
+  std::vector<signed char> last(static_cast<size_t>(full) + 1, -1);
+  best[0] = 0;
+  for (std::uint32_t done = 0; done < full; ++done) {
+    if (best[done] == kSat) continue;
+    u64 card = 1;
+    for (int m = 0; m < n; ++m) card = mul_sat(card, ((done >> m) & 1u) ? s.K[m] : s.L[m]);
+    for (int m = 0; m < n; ++m) {
+      if ((done >> m) & 1u) continue;
+      const u64 c = add_sat(best[done], mul_sat(s.K[m], card));
+      const std::uint32_t next = done | (1u << m);
+      if (c < best[next]) {
+        best[next] = c;
+        last[next] = static_cast<signed char>(m);
+      }
+    }
+  }
+  std::vector<int> order(n);
+  std::uint32_t at = full;
+  for (int i = n - 1; i >= 0; --i) {
+    order[i] = last[at];
+    at &= ~(1u << last[at]);
+  }
+  if (macs_out) *macs_out = best[full];
+  return order;
 }
 
 void check_tensor_matches(const tp_plan* p, const tp_tensor* t) {  // hooi.hpp:85-91
@@ -375,6 +453,7 @@ void check_tensor_matches(const tp_plan* p, const tp_tensor* t) {  // hooi.hpp:8
 
 void plan_collect_timing(tp_ctx* ctx, tp_plan* p) {
   TPB_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (int a = 0; a < tp_ctx::kAux; ++a) TPB_CUDA(cudaStreamSynchronize(ctx->aux[a]));
   tp_sweep_timing t{};
   float* slot[4] = {&t.tree_ms, &t.gram_ms, &t.evd_ms, &t.core_ms};
   p->node_ms.assign(p->tree.size(), 0.f);
@@ -417,10 +496,18 @@ int tp_ctx_create(int device, tp_ctx** out) {
     ctx->sm_count = prop.multiProcessorCount;
     try {
       TPB_CUDA(cudaSetDevice(device));
-      TPB_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+      // the TTM/Gram stream outranks the eigen-solve side streams: when both have CTAs pending, the tree goes first
+      int prio_low = 0, prio_high = 0;
+      TPB_CUDA(cudaDeviceGetStreamPriorityRange(&prio_low, &prio_high));
+      TPB_CUDA(cudaStreamCreateWithPriority(&ctx->stream, cudaStreamNonBlocking, prio_high));
       TPB_SOLVER(cusolverDnCreate(&ctx->solver));
       TPB_SOLVER(cusolverDnSetStream(ctx->solver, ctx->stream));
       ctx->reduce_scratch = device_alloc(reduce_scratch_doubles() + 1);
+      for (int a = 0; a < tp_ctx::kAux; ++a) {
+        TPB_CUDA(cudaStreamCreateWithPriority(&ctx->aux[a], cudaStreamNonBlocking, prio_low));
+        TPB_SOLVER(cusolverDnCreate(&ctx->aux_solver[a]));
+        TPB_SOLVER(cusolverDnSetStream(ctx->aux_solver[a], ctx->aux[a]));
+      }
     } catch (...) {
       delete ctx;
       throw;
@@ -435,8 +522,17 @@ int tp_ctx_destroy(tp_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     if (ctx->solver) cusolverDnDestroy(ctx->solver);
+    for (int a = 0; a < tp_ctx::kAux; ++a) {
+      if (ctx->aux[a]) cudaStreamSynchronize(ctx->aux[a]);
+      if (ctx->aux_solver[a]) cusolverDnDestroy(ctx->aux_solver[a]);
+      if (ctx->aux[a]) cudaStreamDestroy(ctx->aux[a]);
+    }
     cudaFree(ctx->reduce_scratch);
     cudaFree(ctx->frag_scratch);
+    if (ctx->dev_scratch) {
+      static_cast<LeafScratch*>(ctx->dev_scratch)->release();
+      delete static_cast<LeafScratch*>(ctx->dev_scratch);
+    }
     cudaStreamDestroy(ctx->stream);
     delete ctx;
   });
@@ -724,9 +820,11 @@ int tp_plan_create(tp_ctx* ctx, int n_modes, const tp_u64* L, const tp_u64* K, i
       p->depth_buf.assign(p->depth_cap.size(), nullptr);
       for (size_t d = 0; d < p->depth_cap.size(); ++d) p->depth_buf[d] = device_alloc(p->depth_cap[d]);
 
-      // core chain ping-pong: the largest partial product of the mode-order chain
+      // core chain in its cheapest order; ping-pong buffers hold its largest partial product
+      p->core_order = cheapest_chain_order(p->spec, &p->core_macs_executed);
       card = partial_cardinality(p->spec, 0);
-      for (int m = 0; m + 1 < n_modes; ++m) {
+      for (int i = 0; i + 1 < n_modes; ++i) {
+        const int m = p->core_order[i];
         card = scale_exact(card, p->spec.K[m], p->spec.L[m]);
         p->core_tmp_cap = std::max(p->core_tmp_cap, static_cast<size_t>(card));
       }
@@ -748,8 +846,8 @@ int tp_plan_create(tp_ctx* ctx, int n_modes, const tp_u64* L, const tp_u64* K, i
         p->frag[m] = device_alloc(p->frag_layout[m].doubles);
         max_rows = std::max(max_rows, static_cast<long long>(p->spec.L[m]));
       }
-      // worst-case Gram split workspace over the leaves
-      size_t ws = 0;
+      // Gram split workspace of each mode's leaf
+      std::vector<size_t> leaf_ws(n_modes, 0);
       for (int id = 0; id < p->tree.size(); ++id) {
         if (!p->tree.leaf(id)) continue;
         const std::vector<u64> ext = node_extents(p->tree, p->spec, id);
@@ -757,9 +855,18 @@ int tp_plan_create(tp_ctx* ctx, int n_modes, const tp_u64* L, const tp_u64* K, i
         long long outer = 1, inner = 1;
         for (int i = 0; i < m; ++i) outer *= static_cast<long long>(ext[i]);
         for (int i = m + 1; i < n_modes; ++i) inner *= static_cast<long long>(ext[i]);
-        ws = std::max(ws, gram_layout(outer, static_cast<long long>(ext[m]), inner, ctx->sm_count).workspace_doubles);
+        leaf_ws[m] = std::max(leaf_ws[m],
+                              gram_layout(outer, static_cast<long long>(ext[m]), inner, ctx->sm_count).workspace_doubles);
       }
-      leaf_scratch_reserve(ctx, p->leaf, max_rows, ws);
+      (void)max_rows;
+      p->leaf.resize(n_modes);
+      p->gram_ready.assign(n_modes, nullptr);
+      p->factor_ready.assign(n_modes, nullptr);
+      for (int m = 0; m < n_modes; ++m) {
+        leaf_scratch_reserve(ctx, p->leaf[m], static_cast<long long>(p->spec.L[m]), leaf_ws[m]);
+        TPB_CUDA(cudaEventCreateWithFlags(&p->gram_ready[m], cudaEventDisableTiming));
+        TPB_CUDA(cudaEventCreateWithFlags(&p->factor_ready[m], cudaEventDisableTiming));
+      }
       TPB_CUDA(cudaStreamSynchronize(ctx->stream));
     } catch (...) {
       tp_plan_destroy(ctx, p);
@@ -783,7 +890,11 @@ int tp_plan_destroy(tp_ctx* ctx, tp_plan* p) {
     cudaFree(p->core);
     cudaFree(p->core_tmp[0]);
     cudaFree(p->core_tmp[1]);
-    p->leaf.release();
+    for (LeafScratch& slot : p->leaf) slot.release();
+    for (cudaEvent_t e : p->gram_ready)
+      if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : p->factor_ready)
+      if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : p->events)
       if (e) cudaEventDestroy(e);
     delete p;
@@ -861,6 +972,7 @@ int tp_plan_sweep(tp_ctx* ctx, tp_plan* p, const tp_tensor* t, tp_sweep_stats* s
         s.close();
       }
       jacobi_walk(ctx, p, 0, t->data, dims, 0);
+      if (p->overlap_evd) plan_join_leaves(ctx, p);
       plan_core(ctx, p, t->data, p->fresh);
       std::swap(p->cur, p->fresh);
     } else {
@@ -882,7 +994,7 @@ int tp_plan_sweep(tp_ctx* ctx, tp_plan* p, const tp_tensor* t, tp_sweep_stats* s
           at = out;
           ++step;
         }
-        plan_leaf(ctx, p, at, d, leaf, p->fresh[leaf]);
+        plan_leaf(ctx, p, at, d, leaf, p->fresh[leaf], -1, false);
         std::swap(p->cur[leaf], p->fresh[leaf]);  // later chains see the fresh factor
         Span s(ctx, p, kTree);
         plan_refresh_fragments(ctx, p, leaf, p->cur[leaf]);
@@ -890,12 +1002,23 @@ int tp_plan_sweep(tp_ctx* ctx, tp_plan* p, const tp_tensor* t, tp_sweep_stats* s
       }
       plan_core(ctx, p, t->data, p->cur);
     }
-    const int flag = read_and_clear_flag(ctx, p->leaf);
+    const int flag = read_and_clear_flags(ctx, p->leaf);
     plan_collect_timing(ctx, p);
     if (stats) {
       *stats = p->model;
       stats->degenerate = flag;
     }
+  });
+}
+
+int tp_plan_set_option(tp_ctx* ctx, tp_plan* p, int option, int value) {
+  return guarded([&] {
+    (void)ctx;
+    if (!p) raise(TP_ERR_BAD_ARGUMENT, "null plan");
+    if (option == TP_OPT_OVERLAP_EVD)
+      p->overlap_evd = value != 0;
+    else
+      raise(TP_ERR_BAD_ARGUMENT, "unknown plan option");
   });
 }
 
@@ -1030,6 +1153,104 @@ int tp_reconstruction_error(tp_ctx* ctx, const tp_tensor* t, const size_t* core_
       throw;
     }
     cleanup();
+  });
+}
+
+// ------------------------------------------------------------- device-pointer building blocks
+static LeafScratch& dev_scratch(tp_ctx* ctx) {
+  if (!ctx->dev_scratch) ctx->dev_scratch = new LeafScratch;
+  return *static_cast<LeafScratch*>(ctx->dev_scratch);
+}
+
+int tp_dev_ttm_partial(tp_ctx* ctx, const double* x, int n_modes, const size_t* dims, int mode, const double* factor,
+                       size_t L_full, size_t l0, size_t K, int n_dest, const size_t* dest_cuts, double* z) {
+  return guarded([&] {
+    bind(ctx);
+    if (!x || !factor || !z) raise(TP_ERR_BAD_ARGUMENT, "null pointer");
+    checked_size(n_modes, dims);
+    std::vector<size_t> d(dims, dims + n_modes);
+    long long outer, inner;
+    mode_extents(d, mode, outer, inner);
+    const long long len = static_cast<long long>(d[mode]);
+    if (l0 + d[mode] > L_full) raise(TP_ERR_SHAPE_MISMATCH, "factor rows do not cover the block's mode slice");
+    if (K == 0) raise(TP_ERR_SHAPE_MISMATCH, "empty matrix");
+    if (n_dest < 1 || n_dest > kMaxTtmDest) raise(TP_ERR_BAD_ARGUMENT, "between 1 and 16 destinations");
+    std::vector<long long> cuts(n_dest + 1);
+    for (int i = 0; i <= n_dest; ++i) cuts[i] = dest_cuts ? static_cast<long long>(dest_cuts[i]) : (i == 0 ? 0 : static_cast<long long>(K));
+    if (cuts[0] != 0 || cuts[n_dest] != static_cast<long long>(K)) raise(TP_ERR_BAD_ARGUMENT, "destination cuts must span [0, K]");
+    for (int i = 0; i < n_dest; ++i)
+      if (cuts[i + 1] < cuts[i]) raise(TP_ERR_BAD_ARGUMENT, "destination cuts must ascend");
+    const TtmFragmentLayout f = ttm_fragment_layout(static_cast<long long>(K), len);
+    double* frag = ensure_frag_scratch(ctx, f.doubles);
+    // M = F^T restricted to rows l0.. of F: M(k, l) = factor[k * L_full + l0 + l]
+    TPB_CUDA(prep_factor_fragments(ctx->stream, factor + l0, static_cast<long long>(L_full), 1,
+                                   static_cast<long long>(K), len, f, frag));
+    TPB_CUDA(launch_ttm(ctx->stream, x, outer, len, inner, frag, f, static_cast<long long>(K), z, ctx->sm_count,
+                        n_dest, cuts.data()));
+    ctx->own_kernels += 2;
+  });
+}
+
+int tp_dev_reduce_slots(tp_ctx* ctx, double* out, const double* const* slots_host, int n_slots, size_t count) {
+  return guarded([&] {
+    bind(ctx);
+    if (!out || !slots_host) raise(TP_ERR_BAD_ARGUMENT, "null pointer");
+    if (n_slots < 1 || n_slots > kMaxReduceSlots) raise(TP_ERR_BAD_ARGUMENT, "between 1 and 16 slots");
+    TPB_CUDA(launch_reduce_slots(ctx->stream, out, slots_host, n_slots, count));
+    ctx->own_kernels += 1;
+  });
+}
+
+int tp_dev_assemble_mode(tp_ctx* ctx, double* dst, size_t outer, size_t full_len, size_t inner, const double* src,
+                         size_t l0, size_t count) {
+  return guarded([&] {
+    bind(ctx);
+    if (!dst || !src) raise(TP_ERR_BAD_ARGUMENT, "null pointer");
+    if (l0 + count > full_len) raise(TP_ERR_SHAPE_MISMATCH, "slice exceeds the mode extent");
+    TPB_CUDA(launch_assemble_mode(ctx->stream, dst, static_cast<long long>(outer), static_cast<long long>(full_len),
+                                  static_cast<long long>(inner), src, static_cast<long long>(l0),
+                                  static_cast<long long>(count)));
+    ctx->own_kernels += 1;
+  });
+}
+
+int tp_dev_gram(tp_ctx* ctx, const double* y, size_t outer, size_t rows, size_t inner, double* gram) {
+  return guarded([&] {
+    bind(ctx);
+    if (!y || !gram) raise(TP_ERR_BAD_ARGUMENT, "null pointer");
+    if (rows == 0 || outer * inner == 0) raise(TP_ERR_SHAPE_MISMATCH, "empty matrix");
+    if (rows > TP_MAX_GRAM_ROWS) raise(TP_ERR_TOO_LARGE, "unfolding has too many rows for the Gram route");
+    const GramLayout g = gram_layout(static_cast<long long>(outer), static_cast<long long>(rows),
+                                     static_cast<long long>(inner), ctx->sm_count);
+    LeafScratch& s = dev_scratch(ctx);
+    leaf_scratch_reserve(ctx, s, 1, g.workspace_doubles);
+    TPB_CUDA(launch_gram(ctx->stream, y, static_cast<long long>(outer), static_cast<long long>(rows),
+                         static_cast<long long>(inner), g, s.gram_ws, gram));
+    ctx->own_kernels += 2;
+  });
+}
+
+int tp_dev_leaf_solve(tp_ctx* ctx, double* gram, size_t rows, int k, double* factor, int* flag, int* info) {
+  return guarded([&] {
+    bind(ctx);
+    if (!gram || !factor || !flag || !info) raise(TP_ERR_BAD_ARGUMENT, "null pointer");
+    check_leaf_args(static_cast<long long>(rows), 1, k);
+    LeafScratch& s = dev_scratch(ctx);
+    leaf_scratch_reserve(ctx, s, static_cast<long long>(rows), 0);
+    TPB_SOLVER(cusolverDnDsyevd(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, static_cast<int>(rows),
+                                gram, static_cast<int>(rows), s.w, s.work, s.lwork, info));
+    ctx->library_calls += 1;
+    TPB_CUDA(launch_select_basis(ctx->stream, gram, s.w, static_cast<int>(rows), k, factor, flag));
+    ctx->own_kernels += 1;
+  });
+}
+
+int tp_dev_sum_squares(tp_ctx* ctx, const double* x, size_t count, double* out) {
+  return guarded([&] {
+    bind(ctx);
+    if (!x || !out) raise(TP_ERR_BAD_ARGUMENT, "null pointer");
+    TPB_CUDA(launch_sum_squares(ctx->stream, x, count, ctx->reduce_scratch, out));
+    ctx->own_kernels += 2;
   });
 }
 

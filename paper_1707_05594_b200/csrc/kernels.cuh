@@ -23,9 +23,13 @@ TtmFragmentLayout ttm_fragment_layout(long long new_len, long long len);
 cudaError_t prep_factor_fragments(cudaStream_t stream, const double* m, long long row_stride, long long col_stride,
                                   long long new_len, long long len, const TtmFragmentLayout& f, double* out);
 
+constexpr int kMaxTtmDest = 16;
 // Z(a,k,b) = sum_l M(k,l) X(a,l,b); x is (outer, len, inner) row-major, z is (outer, new_len, inner).
+// With n_dest > 1 the output rows are split at dest_cuts[0..n_dest] (dest_cuts[0] = 0, dest_cuts[n_dest] = new_len)
+// and written destination-major: chunk d is the contiguous tensor (outer, dest_cuts[d+1]-dest_cuts[d], inner).
 cudaError_t launch_ttm(cudaStream_t stream, const double* x, long long outer, long long len, long long inner,
-                       const double* mfrag, const TtmFragmentLayout& f, long long new_len, double* z);
+                       const double* mfrag, const TtmFragmentLayout& f, long long new_len, double* z, int sm_count,
+                       int n_dest = 1, const long long* dest_cuts = nullptr);
 
 // ---- Gram of the mode-n unfolding, read in place (gram_kernels.cu) -----------
 struct GramLayout {
@@ -45,6 +49,12 @@ size_t reduce_scratch_doubles();
 cudaError_t launch_sum_squares(cudaStream_t stream, const double* x, size_t n, double* scratch, double* out);
 cudaError_t launch_diff_sum_squares(cudaStream_t stream, const double* x, const double* y, size_t n, double* scratch,
                                     double* out);
+// out[i] = slots[0][i] + slots[1][i] + ... in that order (the reduction half of a reduce-scatter; fixed order)
+constexpr int kMaxReduceSlots = 16;
+cudaError_t launch_reduce_slots(cudaStream_t stream, double* out, const double* const* slots, int n_slots, size_t n);
+// dst(a, l0 + l, b) = src(a, l, b): drops the piece (outer, count, inner) into the tensor (outer, full_len, inner)
+cudaError_t launch_assemble_mode(cudaStream_t stream, double* dst, long long outer, long long full_len,
+                                 long long inner, const double* src, long long l0, long long count);
 // y[i] = beta * y[i] + alpha * x[i]
 cudaError_t launch_axpby(cudaStream_t stream, double* y, double beta, double alpha, const double* x, size_t n);
 // Top-k eigenvectors from an ascending syevd result (vectors column-major rows x rows, eigenvalues w) with the

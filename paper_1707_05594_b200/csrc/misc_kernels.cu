@@ -105,7 +105,48 @@ __global__ void __launch_bounds__(256) axpby_kernel(double* __restrict__ y, doub
     y[i] = fma(alpha, x[i], beta * y[i]);
 }
 
+struct SlotList {
+  const double* p[kMaxReduceSlots];
+};
+
+__global__ void __launch_bounds__(256) reduce_slots_kernel(double* __restrict__ out, SlotList slots, int n_slots,
+                                                           size_t n) {
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
+    double sum = slots.p[0][i];
+    for (int s = 1; s < n_slots; ++s) sum += slots.p[s][i];
+    out[i] = sum;
+  }
+}
+
+__global__ void __launch_bounds__(256) assemble_mode_kernel(double* __restrict__ dst, long long full_len,
+                                                            long long inner, const double* __restrict__ src,
+                                                            long long l0, long long count, size_t n) {
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  const long long piece = count * inner;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
+    const long long a = static_cast<long long>(i) / piece;
+    const long long r = static_cast<long long>(i) - a * piece;
+    dst[(a * full_len + l0) * inner + r] = src[i];
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_reduce_slots(cudaStream_t stream, double* out, const double* const* slots, int n_slots, size_t n) {
+  if (n_slots < 1 || n_slots > kMaxReduceSlots) return cudaErrorInvalidValue;
+  SlotList list{};
+  for (int s = 0; s < n_slots; ++s) list.p[s] = slots[s];
+  reduce_slots_kernel<<<kReduceBlocks, 256, 0, stream>>>(out, list, n_slots, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_assemble_mode(cudaStream_t stream, double* dst, long long outer, long long full_len,
+                                 long long inner, const double* src, long long l0, long long count) {
+  const size_t n = static_cast<size_t>(outer) * count * inner;
+  assemble_mode_kernel<<<kReduceBlocks, 256, 0, stream>>>(dst, full_len, inner, src, l0, count, n);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_axpby(cudaStream_t stream, double* y, double beta, double alpha, const double* x, size_t n) {
   axpby_kernel<<<kReduceBlocks, 256, 0, stream>>>(y, beta, alpha, x, n);

@@ -11,13 +11,17 @@
 //   * columns are grouped into "n-tiles" of 8: for inner > 1 eight consecutive
 //     b of one slab a (contiguous in memory), for inner == 1 eight consecutive
 //     slabs a (the contraction index is then the contiguous one).
-//   * a CTA owns WARPS*NT consecutive n-tiles and all 8*KT rows of one K block;
-//     X chunks of KC contraction steps stream through a STAGES-deep cp.async
-//     ring in shared memory, XOR-swizzled so that the 64-bit fragment loads of a
-//     half-warp hit 16 distinct bank pairs; the factor streams beside it in
-//     "fragment order" (prepared once per factor by prep_factor_fragments), so
-//     an A fragment is one conflict-free LDS.64 per lane and needs no bounds
-//     checks (padding rows/columns are stored as zeros).
+//   * a CTA tile is WARPS*NT consecutive n-tiles times all 8*KT rows of one K
+//     block; CTAs are persistent (grid = SMs x occupancy) and walk their tiles
+//     round-robin, and the cp.async ring never drains between tiles: while the
+//     last chunks of tile j are multiplied and its outputs stored, the first
+//     chunks of tile j+1 are already in flight.  X chunks of KC contraction
+//     steps stream through the STAGES-deep ring in shared memory, XOR-swizzled
+//     so that the 64-bit fragment loads of a half-warp hit 16 distinct bank
+//     pairs; the factor streams beside it in "fragment order" (prepared once
+//     per factor by prep_factor_fragments), so an A fragment is one
+//     conflict-free LDS.64 per lane and needs no bounds checks (padding rows
+//     and columns are stored as zeros).
 //   * every element of X is read from HBM exactly once per K block and every
 //     element of Z written once; accumulation order is fixed (deterministic).
 #include <cuda_runtime.h>
@@ -65,89 +69,144 @@ struct TtmParams {
   int tiles_per_slab; // ceil(inner / 8), inner > 1 only
   int n_chunks;       // ceil(len / KC)
   int vec;            // 16-byte global accesses are aligned and never straddle an extent
+  // Output row blocks ("destinations"): rows [dest_k0[d], dest_k0[d+1]) form their own contiguous tensor
+  // (outer, rows_d, inner) starting at z + dest_off[d].  One destination = the plain layout; several = the
+  // destination-major partial product a reduce-scatter over a split mode sends out (one chunk per peer).
+  int n_dest;
+  int dest_k0[kMaxTtmDest + 1];
+  long long dest_off[kMaxTtmDest];
 };
 
-// One CTA: rows [kb*8*KT, +8*KT) of the output mode, n-tiles [blockIdx.x*TILE_N, +TILE_N).
+// Persistent CTA: K block blockIdx.y; tile groups blockIdx.x, blockIdx.x + gridDim.x, ... of TILE_N n-tiles each.
 template <int KT, int NT, int KC, int STAGES, bool LAST>
 __global__ void __launch_bounds__(kThreads, (KT * NT <= 20) ? 2 : 1) ttm_dmma_kernel(const TtmParams p) {
   constexpr int TILE_N = kWarps * NT;
   constexpr int XS = TILE_N * KC * 8;     // doubles per stage of X
   constexpr int MS = (KC / 4) * KT * 32;  // doubles per stage of factor fragments
+  constexpr int RING = 8;                 // tile tables alive at once (the loader runs < STAGES tiles ahead)
   static_assert((TILE_N & (TILE_N - 1)) == 0, "TILE_N must be a power of two");
   static_assert(KC % 16 == 0, "swizzle assumes 16-double rows");
+  static_assert(STAGES + 1 <= RING, "tile-table ring too small");
 
   extern __shared__ __align__(16) double smem[];
   double* const xs = smem;
   double* const ms = smem + STAGES * XS;
-  __shared__ long long tile_base[TILE_N];
-  __shared__ int tile_lim[TILE_N];
+  __shared__ long long tile_base[RING][TILE_N];  // element offset of the n-tile's first column at l = 0
+  __shared__ long long tile_slab[RING][TILE_N];  // !LAST: slab index a of the n-tile
+  __shared__ int tile_b0[RING][TILE_N];          // !LAST: first column b of the n-tile
+  __shared__ int tile_lim[RING][TILE_N];         // valid columns (rows of X for LAST) in the n-tile, 0..8
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kb = blockIdx.y;
-  const long long tile0 = static_cast<long long>(blockIdx.x) * TILE_N;
+  const long long n_groups = (p.n_tiles + TILE_N - 1) / TILE_N;
+  const long long my_tiles = blockIdx.x < n_groups ? (n_groups - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const long long total_items = my_tiles * p.n_chunks;
 
-  if (tid < TILE_N) {
-    const long long g = tile0 + tid;
-    long long base = 0;
-    int lim = 0;
-    if (g < p.n_tiles) {
-      if (LAST) {
-        base = g * 8 * p.len;
-        lim = static_cast<int>(min(8LL, p.outer - g * 8));
-      } else {
-        const long long a = g / p.tiles_per_slab;
-        const long long b0 = (g - a * p.tiles_per_slab) * 8;
-        base = a * p.len * p.inner + b0;
-        lim = static_cast<int>(min(8LL, p.inner - b0));
+  // first n-tile of this CTA's j-th tile
+  auto tile_first = [&](long long j) { return (static_cast<long long>(blockIdx.x) + j * gridDim.x) * TILE_N; };
+
+  auto prep_table = [&](long long j) {
+    if (tid < TILE_N) {
+      const long long g = tile_first(j) + tid;
+      long long base = 0, slab = 0;
+      int lim = 0, b0 = 0;
+      if (g < p.n_tiles) {
+        if (LAST) {
+          base = g * 8 * p.len;
+          lim = static_cast<int>(min(8LL, p.outer - g * 8));
+        } else {
+          // n_tiles < 2^31 (checked by the launcher): 32-bit division
+          const unsigned a = static_cast<unsigned>(g) / static_cast<unsigned>(p.tiles_per_slab);
+          b0 = static_cast<int>(static_cast<unsigned>(g) - a * static_cast<unsigned>(p.tiles_per_slab)) * 8;
+          slab = a;
+          base = slab * p.len * p.inner + b0;
+          lim = static_cast<int>(min(8LL, p.inner - b0));
+        }
       }
+      tile_base[j % RING][tid] = base;
+      tile_slab[j % RING][tid] = slab;
+      tile_b0[j % RING][tid] = b0;
+      tile_lim[j % RING][tid] = lim;
     }
-    tile_base[tid] = base;
-    tile_lim[tid] = lim;
-  }
-  __syncthreads();
+  };
 
   const double* const mfrag_kb = p.mfrag + static_cast<long long>(kb) * p.n_chunks * MS;
 
-  auto issue_chunk = [&](int chunk, int stage) {
+  // ---- loader.  With 256 threads and 16-byte copies every thread owns a fixed (n-tile, 16-byte column) pair and
+  // walks the contraction rows, so its global address is a running pointer and its shared address a constant.
+  constexpr int R = TILE_N / 4;       // 16-byte copies per thread per chunk (TILE_N * KC * 8 doubles / 2 / 256)
+  constexpr int LSTEP = 64 / TILE_N;  // !LAST: rows between a thread's consecutive copies
+  // !LAST: column pair ld_c of n-tile ld_t, rows ld_l + r * LSTEP
+  const int ld_c = tid & 3, ld_t = (tid >> 2) & (TILE_N - 1), ld_l = (tid >> 2) / TILE_N;
+  // LAST: 16-byte piece ld_c8 of row ld_row of n-tiles ld_t0 + 4 r
+  const int ld_c8 = tid & 7, ld_row = (tid >> 3) & 7, ld_t0 = tid >> 6;
+  const int dst_first = LAST ? ld_t0 * (8 * KC) + ld_row * KC + ((2 * ld_c8) ^ ((ld_row & 3) << 2))
+                             : ld_t * (KC * 8) + ld_l * 8;
+  const int swz0 = (ld_l >> 1) & 1;
+  const double* ld_src = p.x;  // row 0 of the current load tile for this thread
+  bool ld_ok = false;          // !LAST: the thread's column pair exists in its n-tile
+  long long ld_a = 0;          // LAST: X row of the thread's first copy
+
+  auto begin_load_tile = [&](long long j) {
+    if (LAST) {
+      ld_a = tile_first(j) * 8 + ld_t0 * 8 + ld_row;
+      ld_src = p.x + ld_a * p.len + 2 * ld_c8;
+    } else {
+      ld_ok = 2 * ld_c < tile_lim[j % RING][ld_t];
+      ld_src = p.x + tile_base[j % RING][ld_t] + 2 * ld_c + ld_l * p.inner;
+    }
+  };
+
+  auto issue_chunk = [&](long long j, int chunk, int stage) {
     double* const xd = xs + stage * XS;
     const long long l0 = static_cast<long long>(chunk) * KC;
-    if (!LAST) {
-      if (p.vec) {
-#pragma unroll 2
-        for (int idx = tid; idx < TILE_N * KC * 4; idx += kThreads) {
-          const int c = idx & 3, t = (idx >> 2) & (TILE_N - 1), l = idx / (4 * TILE_N);
-          const bool ok = (l0 + l < p.len) && (2 * c < tile_lim[t]);
-          const double* src = ok ? p.x + tile_base[t] + (l0 + l) * p.inner + 2 * c : p.x;
-          cp_async16(xd + t * (KC * 8) + l * 8 + ((2 * c) ^ (((l >> 1) & 1) << 2)), src, ok);
+    if (p.vec) {
+      if (chunk == 0) begin_load_tile(j);
+      if (!LAST) {
+        const double* src = ld_src + l0 * p.inner;
+        const long long rows_left = p.len - l0 - ld_l;  // copy r is inside the extent iff r * LSTEP < rows_left
+        const long long step = static_cast<long long>(LSTEP) * p.inner;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const bool ok = ld_ok && (r * LSTEP < rows_left);
+          const int swz = (swz0 ^ ((r * LSTEP / 2) & 1)) << 2;
+          cp_async16(xd + dst_first + r * (LSTEP * 8) + ((2 * ld_c) ^ swz), ok ? src : p.x, ok);
+          src += step;
         }
       } else {
-        for (int idx = tid; idx < TILE_N * KC * 8; idx += kThreads) {
-          const int b = idx & 7, t = (idx >> 3) & (TILE_N - 1), l = idx / (8 * TILE_N);
-          const bool ok = (l0 + l < p.len) && (b < tile_lim[t]);
-          const double* src = ok ? p.x + tile_base[t] + (l0 + l) * p.inner + b : p.x;
-          cp_async8(xd + t * (KC * 8) + l * 8 + (b ^ (((l >> 1) & 1) << 2)), src, ok);
+        const double* src = ld_src + l0;
+        const bool col_ok = l0 + 2 * ld_c8 < p.len;
+        const long long step = 32 * p.len;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const bool ok = col_ok && (ld_a + 32 * r < p.outer);
+          cp_async16(xd + dst_first + r * (4 * 8 * KC), ok ? src : p.x, ok);
+          src += step;
         }
       }
     } else {
-      if (p.vec) {
-#pragma unroll 2
-        for (int idx = tid; idx < TILE_N * 8 * (KC / 2); idx += kThreads) {
-          const int c = idx % (KC / 2), r = (idx / (KC / 2)) & 7, t = idx / (4 * KC);
-          const bool ok = (r < tile_lim[t]) && (l0 + 2 * c < p.len);
-          const double* src = ok ? p.x + tile_base[t] + r * p.len + l0 + 2 * c : p.x;
-          cp_async16(xd + t * (8 * KC) + r * KC + ((2 * c) ^ ((r & 3) << 2)), src, ok);
+      // unaligned / odd extents: element-wise 8-byte copies (rare shapes; correctness path)
+      const long long* const base = tile_base[j % RING];
+      const int* const lim = tile_lim[j % RING];
+      if (!LAST) {
+        for (int idx = tid; idx < TILE_N * KC * 8; idx += kThreads) {
+          const int b = idx & 7, t = (idx >> 3) & (TILE_N - 1), l = idx / (8 * TILE_N);
+          const bool ok = (l0 + l < p.len) && (b < lim[t]);
+          const double* src = ok ? p.x + base[t] + (l0 + l) * p.inner + b : p.x;
+          cp_async8(xd + t * (KC * 8) + l * 8 + (b ^ (((l >> 1) & 1) << 2)), src, ok);
         }
       } else {
         for (int idx = tid; idx < TILE_N * 8 * KC; idx += kThreads) {
           const int l = idx % KC, r = (idx / KC) & 7, t = idx / (8 * KC);
-          const bool ok = (r < tile_lim[t]) && (l0 + l < p.len);
-          const double* src = ok ? p.x + tile_base[t] + r * p.len + l0 + l : p.x;
+          const bool ok = (r < lim[t]) && (l0 + l < p.len);
+          const double* src = ok ? p.x + base[t] + r * p.len + l0 + l : p.x;
           cp_async8(xd + t * (8 * KC) + r * KC + (l ^ ((r & 3) << 2)), src, ok);
         }
       }
     }
     const double* msrc = mfrag_kb + static_cast<long long>(chunk) * MS;
     double* const md = ms + stage * MS;
+#pragma unroll
     for (int idx = tid; idx < MS / 2; idx += kThreads) cp_async16(md + 2 * idx, msrc + 2 * idx, true);
   };
 
@@ -157,23 +216,80 @@ __global__ void __launch_bounds__(kThreads, (KT * NT <= 20) ? 2 : 1) ttm_dmma_ke
 #pragma unroll
     for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
+  // Epilogue of one tile: a lane holds rows k = 8 i + lane/4 and columns 2 (lane%4), +1 of each of its n-tiles.
+  auto store_tile = [&](long long j) {
+    const int col = 2 * (lane & 3);
+    const long long first = tile_first(j);
+#pragma unroll
+    for (int jj = 0; jj < NT; ++jj) {
+      const int t = warp * NT + jj;
+      const int lim = tile_lim[j % RING][t];
+      if (lim == 0) continue;
+      const long long g = first + t;
+#pragma unroll
+      for (int i = 0; i < KT; ++i) {
+        const long long k_abs = static_cast<long long>(kb) * (8 * KT) + 8 * i + (lane >> 2);
+        if (k_abs >= p.new_len) continue;
+        int d = 0;
+        while (d + 1 < p.n_dest && k_abs >= p.dest_k0[d + 1]) ++d;
+        const long long k = k_abs - p.dest_k0[d];
+        const long long rows_d = p.dest_k0[d + 1] - p.dest_k0[d];
+        double* const zd = p.z + p.dest_off[d];
+        if (LAST) {
+          const long long a = g * 8 + col;
+          if (col < lim) zd[a * rows_d + k] = acc[i][jj][0];
+          if (col + 1 < lim) zd[(a + 1) * rows_d + k] = acc[i][jj][1];
+        } else {
+          const long long a = tile_slab[j % RING][t];
+          const long long b = tile_b0[j % RING][t] + col;
+          double* dst = zd + (a * rows_d + k) * p.inner + b;
+          if (p.vec) {
+            if (col < lim) *reinterpret_cast<double2*>(dst) = make_double2(acc[i][jj][0], acc[i][jj][1]);
+          } else {
+            if (col < lim) dst[0] = acc[i][jj][0];
+            if (col + 1 < lim) dst[1] = acc[i][jj][1];
+          }
+        }
+      }
+    }
+  };
+
+  // ---- prologue: tables for the first STAGES tiles, then STAGES-1 chunks in flight
+  long long prepped = min(my_tiles, static_cast<long long>(STAGES));
+  for (long long j = 0; j < prepped; ++j) prep_table(j);
+  __syncthreads();
+  long long load_j = 0, cons_j = 0;
+  int load_c = 0, cons_c = 0;
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < p.n_chunks) issue_chunk(s, s);
+    if (load_j < my_tiles) {
+      issue_chunk(load_j, load_c, s);
+      if (++load_c == p.n_chunks) {
+        load_c = 0;
+        ++load_j;
+      }
+    }
     cp_async_commit();
   }
+  int load_stage = STAGES - 1, cons_stage = 0;
 
   const int frag_k = lane & 3, frag_n = lane >> 2;
-  for (int chunk = 0; chunk < p.n_chunks; ++chunk) {
+  for (long long it = 0; it < total_items; ++it) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
-    {
-      const int next = chunk + STAGES - 1;
-      if (next < p.n_chunks) issue_chunk(next, next % STAGES);
-      cp_async_commit();
+    if (load_j < my_tiles) {
+      issue_chunk(load_j, load_c, load_stage);
+      if (++load_c == p.n_chunks) {
+        load_c = 0;
+        ++load_j;
+      }
     }
-    const double* const xd = xs + (chunk % STAGES) * XS + (warp * NT) * (KC * 8);
-    const double* const md = ms + (chunk % STAGES) * MS + lane;
+    cp_async_commit();
+    load_stage = (load_stage + 1 == STAGES) ? 0 : load_stage + 1;
+
+    const double* const xd = xs + cons_stage * XS + (warp * NT) * (KC * 8);
+    const double* const md = ms + cons_stage * MS + lane;
+    cons_stage = (cons_stage + 1 == STAGES) ? 0 : cons_stage + 1;
 #pragma unroll
     for (int s = 0; s < KC / 4; ++s) {
       double a[KT];
@@ -191,38 +307,22 @@ __global__ void __launch_bounds__(kThreads, (KT * NT <= 20) ? 2 : 1) ttm_dmma_ke
         for (int i = 0; i < KT; ++i) dmma884(acc[i][j][0], acc[i][j][1], a[i], b);
       }
     }
-  }
-  cp_async_wait<0>();
-
-  // Epilogue: lane holds rows k = 8 i + lane/4 and columns 2 (lane%4), 2 (lane%4) + 1 of each of its n-tiles.
-  const int col = 2 * (lane & 3);
+    if (++cons_c == p.n_chunks) {
+      store_tile(cons_j);
 #pragma unroll
-  for (int j = 0; j < NT; ++j) {
-    const int t = warp * NT + j;
-    const int lim = tile_lim[t];
-    if (lim == 0) continue;
-    const long long g = tile0 + t;
+      for (int i = 0; i < KT; ++i)
 #pragma unroll
-    for (int i = 0; i < KT; ++i) {
-      const long long k = static_cast<long long>(kb) * (8 * KT) + 8 * i + (lane >> 2);
-      if (k >= p.new_len) continue;
-      if (LAST) {
-        const long long a = g * 8 + col;
-        if (col < lim) p.z[a * p.new_len + k] = acc[i][j][0];
-        if (col + 1 < lim) p.z[(a + 1) * p.new_len + k] = acc[i][j][1];
-      } else {
-        const long long a = g / p.tiles_per_slab;
-        const long long b = (g - a * p.tiles_per_slab) * 8 + col;
-        double* dst = p.z + (a * p.new_len + k) * p.inner + b;
-        if (p.vec) {
-          if (col < lim) *reinterpret_cast<double2*>(dst) = make_double2(acc[i][j][0], acc[i][j][1]);
-        } else {
-          if (col < lim) dst[0] = acc[i][j][0];
-          if (col + 1 < lim) dst[1] = acc[i][j][1];
-        }
-      }
+        for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      cons_c = 0;
+      ++cons_j;
+    }
+    // table of the tile the loader enters next; visible after the barrier at the top of the next iteration
+    if (prepped <= load_j && load_j < my_tiles) {
+      prep_table(prepped);
+      ++prepped;
     }
   }
+  cp_async_wait<0>();
 }
 
 // factor (rows new_len x cols len, element (k,l) at m[k*row_stride + l*col_stride]) -> fragment order:
@@ -243,28 +343,40 @@ __global__ void prep_fragments_kernel(const double* __restrict__ m, long long ro
 }
 
 template <int KT, int NT, int KC, int STAGES, bool LAST>
-cudaError_t launch_one(cudaStream_t stream, const TtmParams& p, int k_blocks) {
+cudaError_t launch_one(cudaStream_t stream, const TtmParams& p, int k_blocks, int sm_count) {
   constexpr int TILE_N = kWarps * NT;
   constexpr size_t smem = sizeof(double) * STAGES * (TILE_N * KC * 8 + (KC / 4) * KT * 32);
   auto kernel = ttm_dmma_kernel<KT, NT, KC, STAGES, LAST>;
-  static bool configured = false;  // per instantiation
-  if (!configured) {
+  static int ctas_per_sm = 0;  // per instantiation
+  if (ctas_per_sm == 0) {
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    configured = true;
+    int occ = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, smem);
+    if (e != cudaSuccess) return e;
+    ctas_per_sm = occ < 1 ? 1 : occ;
   }
-  const long long ctas = (p.n_tiles + TILE_N - 1) / TILE_N;
-  dim3 grid(static_cast<unsigned>(ctas), static_cast<unsigned>(k_blocks));
+  const long long groups = (p.n_tiles + TILE_N - 1) / TILE_N;
+  const long long resident = std::max(1LL, static_cast<long long>(sm_count) * ctas_per_sm / k_blocks);
+  dim3 grid(static_cast<unsigned>(std::min(groups, resident)), static_cast<unsigned>(k_blocks));
   kernel<<<grid, kThreads, smem, stream>>>(p);
   return cudaGetLastError();
 }
 
-template <int KT, int NT>
-cudaError_t launch_kt(cudaStream_t stream, const TtmParams& p, int k_blocks, bool last) {
+// NT (n-tiles per warp) trades register reuse of the factor fragments against the number of CTA tiles: wide
+// tiles when the problem has plenty of columns, narrow ones when it would not otherwise cover the SMs.
+template <int KT>
+cudaError_t launch_kt(cudaStream_t stream, const TtmParams& p, int k_blocks, bool last, int sm_count) {
   constexpr int KC = 16;
-  constexpr int STAGES = (KT * NT <= 20) ? 3 : 4;
-  return last ? launch_one<KT, NT, KC, STAGES, true>(stream, p, k_blocks)
-              : launch_one<KT, NT, KC, STAGES, false>(stream, p, k_blocks);
+  constexpr int WIDE = (KT <= 5) ? 4 : 2;
+  constexpr int STAGES_WIDE = (KT * WIDE <= 20) ? 3 : 4;
+  const long long wide_groups = (p.n_tiles + kWarps * WIDE - 1) / (kWarps * WIDE);
+  if (wide_groups * k_blocks >= sm_count) {
+    return last ? launch_one<KT, WIDE, KC, STAGES_WIDE, true>(stream, p, k_blocks, sm_count)
+                : launch_one<KT, WIDE, KC, STAGES_WIDE, false>(stream, p, k_blocks, sm_count);
+  }
+  return last ? launch_one<KT, 1, KC, 4, true>(stream, p, k_blocks, sm_count)
+              : launch_one<KT, 1, KC, 4, false>(stream, p, k_blocks, sm_count);
 }
 
 }  // namespace
@@ -299,8 +411,25 @@ cudaError_t prep_factor_fragments(cudaStream_t stream, const double* m, long lon
 }
 
 cudaError_t launch_ttm(cudaStream_t stream, const double* x, long long outer, long long len, long long inner,
-                       const double* mfrag, const TtmFragmentLayout& f, long long new_len, double* z) {
+                       const double* mfrag, const TtmFragmentLayout& f, long long new_len, double* z, int sm_count,
+                       int n_dest, const long long* dest_cuts) {
   TtmParams p;
+  if (n_dest < 1 || n_dest > kMaxTtmDest) return cudaErrorInvalidValue;
+  p.n_dest = n_dest;
+  bool dest_aligned = true;
+  {
+    long long off = 0;
+    for (int d = 0; d < n_dest; ++d) {
+      const long long k0 = dest_cuts ? dest_cuts[d] : 0, k1 = dest_cuts ? dest_cuts[d + 1] : new_len;
+      p.dest_k0[d] = static_cast<int>(k0);
+      p.dest_k0[d + 1] = static_cast<int>(k1);
+      p.dest_off[d] = off;
+      dest_aligned = dest_aligned && (off % 2 == 0);
+      off += outer * (k1 - k0) * inner;
+    }
+    for (int d = n_dest + 1; d <= kMaxTtmDest; ++d) p.dest_k0[d] = p.dest_k0[n_dest];
+    for (int d = n_dest; d < kMaxTtmDest; ++d) p.dest_off[d] = 0;
+  }
   p.x = x;
   p.z = z;
   p.mfrag = mfrag;
@@ -310,7 +439,8 @@ cudaError_t launch_ttm(cudaStream_t stream, const double* x, long long outer, lo
   p.new_len = new_len;
   p.n_chunks = f.n_chunks;
   const bool last = inner == 1;
-  const bool base_aligned = (reinterpret_cast<uintptr_t>(x) % 16 == 0) && (reinterpret_cast<uintptr_t>(z) % 16 == 0);
+  const bool base_aligned =
+      (reinterpret_cast<uintptr_t>(x) % 16 == 0) && (reinterpret_cast<uintptr_t>(z) % 16 == 0) && dest_aligned;
   if (last) {
     p.tiles_per_slab = 1;
     p.n_tiles = (outer + 7) / 8;
@@ -320,16 +450,17 @@ cudaError_t launch_ttm(cudaStream_t stream, const double* x, long long outer, lo
     p.n_tiles = outer * p.tiles_per_slab;
     p.vec = base_aligned && (inner % 2 == 0);
   }
+  if (p.n_tiles >= (1LL << 31)) return cudaErrorInvalidValue;  // 2^34 columns: beyond any tensor that fits in HBM
   switch (f.kt) {
-    case 1: return launch_kt<1, 4>(stream, p, f.k_blocks, last);
-    case 2: return launch_kt<2, 4>(stream, p, f.k_blocks, last);
-    case 3: return launch_kt<3, 4>(stream, p, f.k_blocks, last);
-    case 4: return launch_kt<4, 4>(stream, p, f.k_blocks, last);
-    case 5: return launch_kt<5, 4>(stream, p, f.k_blocks, last);
-    case 6: return launch_kt<6, 2>(stream, p, f.k_blocks, last);
-    case 8: return launch_kt<8, 2>(stream, p, f.k_blocks, last);
-    case 10: return launch_kt<10, 2>(stream, p, f.k_blocks, last);
-    case 13: return launch_kt<13, 2>(stream, p, f.k_blocks, last);
+    case 1: return launch_kt<1>(stream, p, f.k_blocks, last, sm_count);
+    case 2: return launch_kt<2>(stream, p, f.k_blocks, last, sm_count);
+    case 3: return launch_kt<3>(stream, p, f.k_blocks, last, sm_count);
+    case 4: return launch_kt<4>(stream, p, f.k_blocks, last, sm_count);
+    case 5: return launch_kt<5>(stream, p, f.k_blocks, last, sm_count);
+    case 6: return launch_kt<6>(stream, p, f.k_blocks, last, sm_count);
+    case 8: return launch_kt<8>(stream, p, f.k_blocks, last, sm_count);
+    case 10: return launch_kt<10>(stream, p, f.k_blocks, last, sm_count);
+    case 13: return launch_kt<13>(stream, p, f.k_blocks, last, sm_count);
   }
   return cudaErrorInvalidValue;
 }

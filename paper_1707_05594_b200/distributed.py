@@ -1,0 +1,515 @@
+"""HOOI on a Cartesian processor grid: one process per GPU, tensors block-distributed, factors replicated.
+
+This is the paper's distribution scheme executed for real — the reference only
+*simulates* it (simulate.hpp) and charges (q_n - 1)|Out_u| elements per TTM (grid_volume.hpp:41):
+
+  * grid q (prod q = P), normally `optimal_static_grid(tree, spec, P)`; rank = row-major rank of the block
+    coordinates (simulate.hpp:69-73); every tensor of the sweep is cut along mode n at floor(b * ext_n / q_n)
+    (grid.hpp:114-119) with its own extent (L_n before the mode is multiplied, K_n after);
+  * TTM along mode n: each rank multiplies its block by its row slice of the replicated factor.  If q_n = 1 that
+    is the whole story (no communication).  If q_n > 1 the products are partial sums over the split mode: the
+    kernel writes them destination-major, the q_n ranks of the mode-n process group exchange the chunks
+    (send/recv, each rank ships (q_n - 1)/q_n of its partial product = the reference's volume) and every rank adds
+    the q_n contributions to its K-slice in rank order — a reduce-scatter with a fixed, deterministic summation order;
+  * leaf n: Gram of the local block (after gathering the mode-n slices to the group's first rank when q_n > 1),
+    all-reduced over all ranks, then the same eigen-solve on every rank (bit-identical input, so the replicated
+    factors stay consistent without a broadcast);
+  * core: the same distributed TTM chain with the new factors.
+
+The rank program is a generator that *yields* its communication requests.  `run_rank` executes them with
+torch.distributed (NCCL on GPUs, gloo in the CPU tests); `run_virtual` steps P rank programs in lock-step inside
+one process and moves the data itself — that is how the multi-rank path is exercised on a single GPU.
+Local arithmetic goes through a backend: `GpuOps` (the CUDA library, device pointers of torch tensors — torch is
+only the allocator and the collective plumbing) or a NumPy backend that lives with the tests.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from typing import Callable, Dict, Generator, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import planner as P
+from ._lib import check, dbl_p, lib, size_array
+
+
+# ----------------------------------------------------------------------------------------------- layout
+class GridLayout:
+    """Block distribution induced by one grid (grid.hpp:23-45, 114-125; simulate.hpp:69-73)."""
+
+    def __init__(self, q: Sequence[int]):
+        self.q = [int(v) for v in q]
+        self.n = len(self.q)
+        self.procs = int(np.prod(self.q, dtype=np.int64))
+
+    def coords(self, rank: int) -> List[int]:
+        c = [0] * self.n
+        for m in range(self.n - 1, -1, -1):
+            c[m] = rank % self.q[m]
+            rank //= self.q[m]
+        return c
+
+    def rank_of(self, coords: Sequence[int]) -> int:
+        r = 0
+        for m in range(self.n):
+            r = r * self.q[m] + int(coords[m])
+        return r
+
+    def cuts(self, ext: int, mode: int) -> List[int]:
+        return P.block_bounds(int(ext), self.q[mode])
+
+    def local_range(self, rank: int, mode: int, ext: int) -> Tuple[int, int]:
+        c = self.coords(rank)[mode]
+        cuts = self.cuts(ext, mode)
+        return cuts[c], cuts[c + 1]
+
+    def local_dims(self, rank: int, ext: Sequence[int]) -> List[int]:
+        return [hi - lo for lo, hi in (self.local_range(rank, m, e) for m, e in enumerate(ext))]
+
+    def slices(self, rank: int, ext: Sequence[int]):
+        return tuple(slice(*self.local_range(rank, m, e)) for m, e in enumerate(ext))
+
+    def mode_group(self, rank: int, mode: int) -> List[int]:
+        """Ranks that share every coordinate but `mode`, ordered by their mode coordinate."""
+        c = self.coords(rank)
+        out = []
+        for v in range(self.q[mode]):
+            c2 = list(c)
+            c2[mode] = v
+            out.append(self.rank_of(c2))
+        return out
+
+
+# ----------------------------------------------------------------------------------------------- requests
+@dataclass
+class Exchange:      # point-to-point batch: sends [(peer, tensor)], recvs [(peer, tensor)]
+    sends: list
+    recvs: list
+
+
+@dataclass
+class AllReduce:     # sum over all ranks, in place
+    tensor: object
+
+
+@dataclass
+class Volume:        # bookkeeping: elements this rank shipped for a TTM node (checked against the reference model)
+    node: int
+    elements: int
+
+
+# ----------------------------------------------------------------------------------------------- backends
+class GpuOps:
+    """Local kernels on one B200 through the C ABI; buffers are torch CUDA tensors (allocator + NCCL plumbing)."""
+
+    def __init__(self, ctx, device_index: int = 0):
+        import torch
+        self.torch = torch
+        self.ctx = ctx
+        self.device = torch.device("cuda", device_index)
+        self.stream = torch.cuda.ExternalStream(ctx.stream, device=self.device)
+
+    def _ptr(self, t):
+        return ctypes.cast(t.data_ptr(), dbl_p)
+
+    def empty(self, count: int):
+        with self.torch.cuda.stream(self.stream):
+            return self.torch.empty(max(int(count), 1), dtype=self.torch.float64, device=self.device)[:int(count)]
+
+    def zeros(self, count: int):
+        with self.torch.cuda.stream(self.stream):
+            return self.torch.zeros(max(int(count), 1), dtype=self.torch.float64, device=self.device)[:int(count)]
+
+    def from_host(self, array: np.ndarray):
+        with self.torch.cuda.stream(self.stream):
+            return self.torch.from_numpy(np.ascontiguousarray(array, dtype=np.float64).reshape(-1)).to(
+                self.device, non_blocking=False)
+
+    def to_host(self, t) -> np.ndarray:
+        with self.torch.cuda.stream(self.stream):
+            out = t.cpu()
+        return out.numpy()
+
+    def ttm_partial(self, x, dims, mode, factor, l_full, l0, k, dest_cuts):
+        count = int(np.prod([d if i != mode else k for i, d in enumerate(dims)], dtype=np.int64))
+        z = self.empty(count)
+        cuts = size_array(dest_cuts)
+        check(lib.tp_dev_ttm_partial(self.ctx._h, self._ptr(x), len(dims), size_array(dims), int(mode),
+                                     self._ptr(factor), ctypes.c_size_t(l_full), ctypes.c_size_t(l0),
+                                     ctypes.c_size_t(k), len(dest_cuts) - 1, cuts, self._ptr(z)))
+        return z
+
+    def reduce_slots(self, slots, count):
+        out = self.empty(count)
+        ptrs = (dbl_p * len(slots))(*[self._ptr(s) for s in slots])
+        check(lib.tp_dev_reduce_slots(self.ctx._h, self._ptr(out), ptrs, len(slots), ctypes.c_size_t(count)))
+        return out
+
+    def assemble(self, dst, outer, full_len, inner, src, l0, count):
+        check(lib.tp_dev_assemble_mode(self.ctx._h, self._ptr(dst), ctypes.c_size_t(outer), ctypes.c_size_t(full_len),
+                                       ctypes.c_size_t(inner), self._ptr(src), ctypes.c_size_t(l0),
+                                       ctypes.c_size_t(count)))
+
+    def gram(self, y, outer, rows, inner):
+        g = self.empty(rows * rows)
+        check(lib.tp_dev_gram(self.ctx._h, self._ptr(y), ctypes.c_size_t(outer), ctypes.c_size_t(rows),
+                              ctypes.c_size_t(inner), self._ptr(g)))
+        return g
+
+    def leaf_solve(self, gram, rows, k):
+        factor = self.empty(rows * k)
+        with self.torch.cuda.stream(self.stream):
+            status = self.torch.zeros(2, dtype=self.torch.int32, device=self.device)
+        flag = ctypes.cast(status.data_ptr(), ctypes.POINTER(ctypes.c_int))
+        info = ctypes.cast(status.data_ptr() + 4, ctypes.POINTER(ctypes.c_int))
+        check(lib.tp_dev_leaf_solve(self.ctx._h, self._ptr(gram), ctypes.c_size_t(rows), int(k), self._ptr(factor),
+                                    flag, info))
+        return factor, status
+
+    def sum_squares(self, x, count):
+        out = self.empty(1)
+        check(lib.tp_dev_sum_squares(self.ctx._h, self._ptr(x), ctypes.c_size_t(count), self._ptr(out)))
+        return out
+
+    def status_to_host(self, status):
+        flag, info = (int(v) for v in self.to_host_int(status))
+        return flag, info
+
+    def to_host_int(self, t):
+        with self.torch.cuda.stream(self.stream):
+            return t.cpu().tolist()
+
+    def synchronize(self):
+        self.ctx.synchronize()
+
+
+# ----------------------------------------------------------------------------------------------- rank program
+@dataclass
+class SweepResult:
+    tree_macs: int = 0
+    core_macs: int = 0
+    peak_live: int = 0
+    degenerate: bool = False
+    volume_sent: Dict[int, int] = field(default_factory=dict)   # tree node -> elements this rank shipped
+
+
+class DistributedHooi:
+    """One rank's share of Jacobi HOOI sweeps (hooi.hpp:189-229) on a static grid."""
+
+    def __init__(self, ops, spec: P.ProblemSpec, tree: P.TtmTree, q: Sequence[int], rank: int):
+        self.ops, self.spec, self.tree, self.rank = ops, spec, tree, int(rank)
+        self.layout = GridLayout(q)
+        self.n = spec.n_modes()
+        P.validate_tree(tree, spec)
+        P.validate_grid(self.layout.q, spec, self.layout.procs)
+        if not 0 <= self.rank < self.layout.procs:
+            raise ValueError("rank outside the grid")
+        self.cost = P.tree_cost(tree, spec)
+        self.factors: List[object] = [None] * self.n      # replicated, L_n x K_n column-major flat buffers
+        self.core = None                                   # local core block, flat
+        self.core_ldims: List[int] = []
+        self.tensor = None                                 # local block of T, flat
+        self.tensor_ldims = self.layout.local_dims(self.rank, spec.L)
+        self.core_order = _cheapest_chain_order(spec)
+        self.events: Optional[Callable[[str, int], None]] = None   # timing hook: ("begin"/"end" + phase, node)
+
+    # -- state ------------------------------------------------------------------------------------
+    def set_local_tensor(self, block: np.ndarray):
+        if list(block.shape) != self.tensor_ldims:
+            raise ValueError("local block has shape %s, expected %s" % (block.shape, self.tensor_ldims))
+        self.tensor = self.ops.from_host(block)
+
+    def set_local_tensor_buffer(self, buf):
+        self.tensor = buf
+
+    def set_factors(self, factors: Sequence[np.ndarray]):
+        self.factors = [self.ops.from_host(np.asfortranarray(f).reshape(-1, order="F")) for f in factors]
+
+    def get_factors(self) -> List[np.ndarray]:
+        return [self.ops.to_host(f).reshape((l, k), order="F").copy()
+                for f, l, k in zip(self.factors, self.spec.L, self.spec.K)]
+
+    def get_local_core(self) -> np.ndarray:
+        return self.ops.to_host(self.core).reshape(self.core_ldims).copy()
+
+    def _mark(self, what: str, node: int = -1):
+        if self.events:
+            self.events(what, node)
+
+    # -- distributed mode product -------------------------------------------------------------------
+    def _ttm(self, x, ext, ldims, mode, factor, node, result: SweepResult):
+        """x: local block with global extents ext / local dims ldims; returns (z, new_ext, new_ldims)."""
+        lay, q_n = self.layout, self.layout.q[mode]
+        k, l_full = self.spec.K[mode], self.spec.L[mode]
+        l0, _ = lay.local_range(self.rank, mode, ext[mode])
+        new_ext = list(ext)
+        new_ext[mode] = k
+        new_ldims = list(ldims)
+        if q_n == 1:
+            z = self.ops.ttm_partial(x, ldims, mode, factor, l_full, l0, k, [0, k])
+            new_ldims[mode] = k
+            return z, new_ext, new_ldims
+        kcuts = lay.cuts(k, mode)
+        group = lay.mode_group(self.rank, mode)
+        me = lay.coords(self.rank)[mode]
+        part = self.ops.ttm_partial(x, ldims, mode, factor, l_full, l0, k, kcuts)
+        per_row = int(np.prod(ldims, dtype=np.int64)) // ldims[mode]      # outer_loc * inner_loc
+        offs = [per_row * c for c in kcuts]
+        mine = offs[me + 1] - offs[me]
+        slots, sends, recvs = [], [], []
+        for d, peer in enumerate(group):
+            if d == me:
+                slots.append(part[offs[me]:offs[me + 1]])
+            else:
+                sends.append((peer, part[offs[d]:offs[d + 1]]))
+                buf = self.ops.empty(mine)
+                recvs.append((peer, buf))
+                slots.append(buf)
+        if node >= 0:
+            result.volume_sent[node] = result.volume_sent.get(node, 0) + (offs[-1] - mine)
+        yield Exchange(sends, recvs)
+        z = self.ops.reduce_slots(slots, mine)
+        new_ldims[mode] = kcuts[me + 1] - kcuts[me]
+        return z, new_ext, new_ldims
+
+    # -- leaf: Gram (all ranks) + eigen-solve -------------------------------------------------------
+    def _leaf(self, y, ext, ldims, mode, result: SweepResult, statuses: list):
+        lay, q_n = self.layout, self.layout.q[mode]
+        rows, k = self.spec.L[mode], self.spec.K[mode]
+        outer = int(np.prod(ldims[:mode], dtype=np.int64)) if mode else 1
+        inner = int(np.prod(ldims[mode + 1:], dtype=np.int64)) if mode + 1 < self.n else 1
+        if q_n == 1:
+            gram = self.ops.gram(y, outer, rows, inner)
+        else:
+            # the unfolding's rows are split over the mode-n group: bring the slices to the group's first rank,
+            # which then owns these columns of the unfolding; the other ranks add nothing to the Gram sum
+            group = lay.mode_group(self.rank, mode)
+            me = lay.coords(self.rank)[mode]
+            cuts = lay.cuts(rows, mode)
+            if me == 0:
+                full = self.ops.empty(outer * rows * inner)
+                recvs, pieces = [], []
+                for d, peer in enumerate(group):
+                    count = cuts[d + 1] - cuts[d]
+                    if d == 0:
+                        pieces.append((y, cuts[d], count))
+                    else:
+                        buf = self.ops.empty(outer * count * inner)
+                        recvs.append((peer, buf))
+                        pieces.append((buf, cuts[d], count))
+                yield Exchange([], recvs)
+                for buf, lo, count in pieces:
+                    self.ops.assemble(full, outer, rows, inner, buf, lo, count)
+                gram = self.ops.gram(full, outer, rows, inner)
+            else:
+                yield Exchange([(group[0], y)], [])
+                gram = self.ops.zeros(rows * rows)
+        yield AllReduce(gram)
+        factor, status = self.ops.leaf_solve(gram, rows, k)
+        statuses.append(status)
+        return factor
+
+    # -- one sweep ------------------------------------------------------------------------------------
+    def sweep(self) -> Generator:
+        """Generator: yields Exchange / AllReduce requests, returns a SweepResult."""
+        res = SweepResult(tree_macs=self.cost.total_macs, peak_live=self.cost.depth + 1)
+        statuses: list = []
+        fresh: List[object] = [None] * self.n
+        tree = self.tree
+
+        def walk(node, x, ext, ldims):
+            for c in tree.children[node]:
+                mode = tree.mode[c]
+                if tree.kind[c] == P.LEAF:
+                    self._mark("begin_leaf", c)
+                    fresh[mode] = yield from self._leaf(x, ext, ldims, mode, res, statuses)
+                    self._mark("end_leaf", c)
+                else:
+                    self._mark("begin_ttm", c)
+                    z, e2, l2 = yield from self._ttm(x, ext, ldims, mode, self.factors[mode], c, res)
+                    self._mark("end_ttm", c)
+                    yield from walk(c, z, e2, l2)
+
+        self._mark("begin_tree")
+        yield from walk(0, self.tensor, list(self.spec.L), list(self.tensor_ldims))
+        self._mark("end_tree")
+        # core_from_factors (hooi.hpp:93-100) in the cheapest order, with the new factors
+        self._mark("begin_core")
+        x, ext, ldims = self.tensor, list(self.spec.L), list(self.tensor_ldims)
+        card = int(np.prod(self.spec.L, dtype=object))
+        core_macs = 0
+        for m in range(self.n):                      # the ledger keeps the reference's mode order
+            core_macs += self.spec.K[m] * card
+            card = card * self.spec.K[m] // self.spec.L[m]
+        for m in self.core_order:
+            x, ext, ldims = yield from self._ttm(x, ext, ldims, m, fresh[m], -1, res)
+        self._mark("end_core")
+        self.core, self.core_ldims = x, ldims
+        self.factors = fresh
+        res.core_macs = core_macs
+        for status in statuses:
+            flag, info = self.ops.status_to_host(status)
+            if info != 0:
+                from ._lib import Errc, TuckerplanError
+                raise TuckerplanError(int(Errc.too_large), "eigensolver did not converge")
+            res.degenerate = res.degenerate or bool(flag)
+        return res
+
+    def norm_squared(self, buf, count) -> Generator:
+        s = self.ops.sum_squares(buf, count)
+        yield AllReduce(s)
+        return float(self.ops.to_host(s)[0])
+
+    def fit_from_norms(self) -> Generator:
+        """sqrt(||T||^2 - ||G||^2) / ||T|| (orthonormal factors)."""
+        t2 = yield from self.norm_squared(self.tensor, int(np.prod(self.tensor_ldims, dtype=np.int64)))
+        g2 = yield from self.norm_squared(self.core, int(np.prod(self.core_ldims, dtype=np.int64)))
+        return float(np.sqrt(max(t2 - g2, 0.0) / t2)), float(np.sqrt(g2))
+
+
+def _cheapest_chain_order(spec: P.ProblemSpec) -> List[int]:
+    """Same DP as the engine's core chain (engine.cu cheapest_chain_order): fewest MACs, ties to the smaller mode."""
+    n = spec.n_modes()
+    full = (1 << n) - 1
+    best = {0: (0, [])}
+    for done in range(full):
+        if done not in best:
+            continue
+        cost, order = best[done]
+        card = 1
+        for m in range(n):
+            card *= spec.K[m] if (done >> m) & 1 else spec.L[m]
+        for m in range(n):
+            if (done >> m) & 1:
+                continue
+            nxt = done | (1 << m)
+            c = cost + spec.K[m] * card
+            if nxt not in best or c < best[nxt][0]:
+                best[nxt] = (c, order + [m])
+    return best[full][1]
+
+
+# ----------------------------------------------------------------------------------------------- runners
+def run_rank(gen: Generator, dist, to_tensor=lambda b: b):
+    """Drive one rank program with torch.distributed (`dist`); buffers must be torch tensors of the right device."""
+    try:
+        req = next(gen)
+        while True:
+            if isinstance(req, Exchange):
+                ops = [dist.P2POp(dist.isend, to_tensor(t), peer) for peer, t in req.sends]
+                ops += [dist.P2POp(dist.irecv, to_tensor(t), peer) for peer, t in req.recvs]
+                if ops:
+                    for work in dist.batch_isend_irecv(ops):
+                        work.wait()
+            elif isinstance(req, AllReduce):
+                dist.all_reduce(to_tensor(req.tensor))
+            else:
+                raise TypeError("unknown request %r" % (req,))
+            req = gen.send(None)
+    except StopIteration as stop:
+        return stop.value
+
+
+def run_virtual(gens: Sequence[Generator], copy=lambda dst, src: dst.copy_(src), add=lambda dst, src: dst.add_(src)):
+    """Step P rank programs in lock-step inside one process and perform their requests by direct copies.
+
+    All ranks must issue the same kind of request at each step (they do: the program is SPMD and data-independent).
+    AllReduce sums in rank order into a scratch copy and hands every rank the same bits, as NCCL/gloo would."""
+    n = len(gens)
+    results = [None] * n
+    reqs = []
+    live = [True] * n
+    for r, g in enumerate(gens):
+        try:
+            reqs.append(next(g))
+        except StopIteration as stop:
+            reqs.append(None)
+            live[r] = False
+            results[r] = stop.value
+    while any(live):
+        kinds = {type(reqs[r]) for r in range(n) if live[r]}
+        if len(kinds) != 1 or not all(live):
+            raise RuntimeError("rank programs diverged: %s" % kinds)
+        kind = kinds.pop()
+        if kind is Exchange:
+            posted = {}
+            for r in range(n):
+                for peer, t in reqs[r].sends:
+                    posted.setdefault((r, peer), []).append(t)
+            for r in range(n):
+                for peer, t in reqs[r].recvs:
+                    queue = posted.get((peer, r))
+                    if not queue:
+                        raise RuntimeError("rank %d expects a message from %d that was never sent" % (r, peer))
+                    copy(t, queue.pop(0))
+            if any(v for v in posted.values()):
+                raise RuntimeError("unmatched sends")
+        elif kind is AllReduce:
+            total = reqs[0].tensor.clone()
+            for r in range(1, n):
+                add(total, reqs[r].tensor)
+            for r in range(n):
+                copy(reqs[r].tensor, total)
+        else:
+            raise TypeError("unknown request %r" % (kind,))
+        for r, g in enumerate(gens):
+            try:
+                reqs[r] = g.send(None)
+            except StopIteration as stop:
+                live[r] = False
+                results[r] = stop.value
+    return results
+
+
+# ----------------------------------------------------------------------------------------------- regrid
+def regrid_plan(ext: Sequence[int], src: GridLayout, dst: GridLayout, rank: int):
+    """Who sends what when a tensor with extents `ext` moves from layout `src` to layout `dst` (the paper's regrid,
+    PAPER.md:767; counted by simulate.hpp:97-113).  Returns (sends, recvs): lists of (peer, global slices)."""
+    def overlap(a, b):
+        out = []
+        for (alo, ahi), (blo, bhi) in zip(a, b):
+            lo, hi = max(alo, blo), min(ahi, bhi)
+            if lo >= hi:
+                return None
+            out.append((lo, hi))
+        return out
+
+    def box(layout, r):
+        return [layout.local_range(r, m, e) for m, e in enumerate(ext)]
+
+    mine_src, mine_dst = box(src, rank), box(dst, rank)
+    sends = [(p, o) for p in range(dst.procs) if (o := overlap(mine_src, box(dst, p)))]
+    recvs = [(p, o) for p in range(src.procs) if (o := overlap(box(src, p), mine_dst))]
+    return sends, recvs
+
+
+def regrid(block, ext: Sequence[int], src: GridLayout, dst: GridLayout, rank: int, empty) -> Generator:
+    """Generator: moves this rank's block (torch tensor shaped like its `src` block) to the `dst` layout."""
+    sends, recvs = regrid_plan(ext, src, dst, rank)
+    src_lo = [src.local_range(rank, m, e)[0] for m, e in enumerate(ext)]
+    dst_lo = [dst.local_range(rank, m, e)[0] for m, e in enumerate(ext)]
+    dst_dims = dst.local_dims(rank, ext)
+    out = empty(int(np.prod(dst_dims, dtype=np.int64))).view(dst_dims)
+    send_list, recv_list, local = [], [], None
+    for peer, o in sends:
+        piece = block[tuple(slice(lo - s, hi - s) for (lo, hi), s in zip(o, src_lo))]
+        if peer == rank:
+            local = (o, piece)
+        else:
+            send_list.append((peer, piece.contiguous().view(-1)))
+    pending = []
+    for peer, o in recvs:
+        if peer == rank:
+            continue
+        shape = [hi - lo for lo, hi in o]
+        buf = empty(int(np.prod(shape, dtype=np.int64)))
+        recv_list.append((peer, buf))
+        pending.append((o, buf, shape))
+    yield Exchange(send_list, recv_list)
+    if local is not None:
+        o, piece = local
+        out[tuple(slice(lo - s, hi - s) for (lo, hi), s in zip(o, dst_lo))].copy_(piece)
+    for o, buf, shape in pending:
+        out[tuple(slice(lo - s, hi - s) for (lo, hi), s in zip(o, dst_lo))].copy_(buf.view(shape))
+    return out

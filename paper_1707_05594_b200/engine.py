@@ -210,6 +210,10 @@ class HooiPlan:
         nn, kind_a, mode_a, parent_a = tree._c()
         check(lib.tp_plan_create(ctx._h, n, L, K, nn, kind_a, mode_a, parent_a, _KINDS[kind], ctypes.byref(self._h)))
 
+    def set_overlap_evd(self, on: bool):
+        """Jacobi only: eigen-solves on side streams beside the tree (default) or everything serial on one stream."""
+        check(lib.tp_plan_set_option(self.ctx._h, self._h, 1, 1 if on else 0))
+
     def _factor_ptrs(self, arrays):
         return (dbl_p * len(arrays))(*[a.ctypes.data_as(dbl_p) for a in arrays])
 

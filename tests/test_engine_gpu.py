@@ -299,4 +299,6 @@ def test_sweep_parity_config1_full(ctx):
         assert r["angle"] < 1e-9 and r["core_rel"] < 1e-10
         assert abs(r["fit_gpu"] - r["fit_oracle"]) <= 1e-10 * max(r["fit_oracle"], 1e-3)
     assert abs(err_gpu - err_oracle) <= 1e-10 * max(err_oracle, 1e-3)
-    assert err_gpu < 2e-3                             # the noise floor: sigma * sqrt(|T|) / ||T||
+    # converged to the noise floor sigma sqrt(|T|) / ||T|| (||X|| = ||G|| ~ sqrt(prod K))
+    floor = cfg.sigma * np.sqrt(np.prod(cfg.L)) / np.sqrt(np.prod(cfg.K) + cfg.sigma ** 2 * np.prod(cfg.L))
+    assert err_gpu < 1.05 * floor
