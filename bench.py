@@ -220,7 +220,7 @@ def run_b200(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if world > 1 or args.distributed:
         from paper_1707_05594_b200 import distributed as D
         return D.run_bench_rank(args, rank, world, local_rank)
 
@@ -399,6 +399,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--distributed", action="store_true", help="force the grid executor at N=1 (run under torchrun)")
+    ap.add_argument("--grid", default=None, help="override the optimal static grid, e.g. 2x2x2")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

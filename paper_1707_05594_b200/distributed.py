@@ -183,6 +183,10 @@ class GpuOps:
     def synchronize(self):
         self.ctx.synchronize()
 
+    def stream_context(self):
+        """torch ops issued by the runners (copies, NCCL calls) must queue on the engine's stream."""
+        return self.torch.cuda.stream(self.stream)
+
 
 # ----------------------------------------------------------------------------------------------- rank program
 @dataclass
@@ -391,8 +395,19 @@ def _cheapest_chain_order(spec: P.ProblemSpec) -> List[int]:
 
 
 # ----------------------------------------------------------------------------------------------- runners
-def run_rank(gen: Generator, dist, to_tensor=lambda b: b):
-    """Drive one rank program with torch.distributed (`dist`); buffers must be torch tensors of the right device."""
+def _stream_of(ops):
+    import contextlib
+    return ops.stream_context() if ops is not None and hasattr(ops, "stream_context") else contextlib.nullcontext()
+
+
+def run_rank(gen: Generator, dist, ops=None, to_tensor=lambda b: b):
+    """Drive one rank program with torch.distributed (`dist`); buffers must be torch tensors of the right device.
+    Pass the rank's `ops` so that the collectives queue on the engine's stream."""
+    with _stream_of(ops):
+        return _run_rank(gen, dist, to_tensor)
+
+
+def _run_rank(gen: Generator, dist, to_tensor):
     try:
         req = next(gen)
         while True:
@@ -411,11 +426,18 @@ def run_rank(gen: Generator, dist, to_tensor=lambda b: b):
         return stop.value
 
 
-def run_virtual(gens: Sequence[Generator], copy=lambda dst, src: dst.copy_(src), add=lambda dst, src: dst.add_(src)):
+def run_virtual(gens: Sequence[Generator], ops=None, copy=lambda dst, src: dst.copy_(src),
+                add=lambda dst, src: dst.add_(src)):
     """Step P rank programs in lock-step inside one process and perform their requests by direct copies.
+    Pass the (shared) `ops` so that those copies queue on the engine's stream.
 
     All ranks must issue the same kind of request at each step (they do: the program is SPMD and data-independent).
     AllReduce sums in rank order into a scratch copy and hands every rank the same bits, as NCCL/gloo would."""
+    with _stream_of(ops):
+        return _run_virtual(gens, copy, add)
+
+
+def _run_virtual(gens, copy, add):
     n = len(gens)
     results = [None] * n
     reqs = []
@@ -513,3 +535,223 @@ def regrid(block, ext: Sequence[int], src: GridLayout, dst: GridLayout, rank: in
     for o, buf, shape in pending:
         out[tuple(slice(lo - s, hi - s) for (lo, hi), s in zip(o, dst_lo))].copy_(buf.view(shape))
     return out
+
+
+# ----------------------------------------------------------------------------------------------- bench driver
+class _DevicePointerView:
+    """Zero-copy torch view of a library-owned device buffer (via __cuda_array_interface__)."""
+
+    def __init__(self, ptr: int, count: int):
+        self.__cuda_array_interface__ = {"shape": (int(count),), "typestr": "<f8", "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+def build_local_block(ctx, ops, cfg, layout: GridLayout, rank: int, dist, threads: int):
+    """This rank's block of T = X + sigma E under `layout`.  Every rank generates a mode-0 slab range of the noise
+    (the slab-parallel stream of workloads.py, or its slice of the single stream), assembles the matching rows of X
+    on its GPU, and the ranks regrid from that mode-0 layout to the target grid (send/recv)."""
+    import torch
+    from . import engine as E, hostgen, workloads as W
+    world = layout.procs
+    gen_q = [world] + [1] * (layout.n - 1)
+    if cfg.L[0] < world:
+        raise ValueError("mode 0 is shorter than the process count")
+    gen = GridLayout(gen_q)
+    i0, i1 = gen.local_range(rank, 0, cfg.L[0])
+    rest = list(cfg.L[1:])
+    noise = np.empty([i1 - i0] + rest, dtype=np.float64)
+    seed = 1000 * cfg.index + 3
+    if cfg.slab_noise:
+        from concurrent.futures import ThreadPoolExecutor
+        flat = noise.reshape(i1 - i0, -1)
+        with ThreadPoolExecutor(max_workers=max(1, threads)) as pool:
+            list(pool.map(lambda i: hostgen.random_tensor(rest, seed + i0 + i, flat[i]), range(i1 - i0)))
+    else:
+        full = hostgen.random_tensor(cfg.L, seed)      # one sequential stream: generate, keep the slab range
+        noise[...] = full[i0:i1]
+        del full
+    block = E.DeviceTensor.upload(ctx, noise)
+    del noise
+    x = E.DeviceTensor.upload(ctx, W.generating_core(cfg))
+    for n, a in enumerate(W.generating_factors(cfg)):
+        nxt = x.ttm(a[i0:i1] if n == 0 else a, n)
+        x.free()
+        x = nxt
+    block.axpby(cfg.sigma, 1.0, x)
+    x.free()
+    ctx.synchronize()
+    with torch.cuda.stream(ops.stream):
+        view = torch.as_tensor(_DevicePointerView(block.device_ptr, block.size), device=ops.device).view(
+            [i1 - i0] + rest)
+        gen_dist = regrid(view, cfg.L, gen, layout, rank, ops.empty)
+        local = run_rank(gen_dist, dist, ops) if dist is not None else run_virtual([gen_dist], ops)[0]
+        local = local.contiguous().view(-1).clone()
+    ctx.synchronize()
+    block.free()
+    return local
+
+
+def run_bench_rank(args, rank: int, world: int, local_rank: int):
+    """bench.py for N >= 1 ranks under torchrun: one process per GPU, NCCL over NVLink."""
+    import json
+    import os
+    import time
+    import torch
+    import torch.distributed as dist
+    from . import engine as E, workloads as W
+    import bench as B
+
+    torch.cuda.set_device(local_rank)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    cfg = W.CONFIGS[args.config]
+    spec = cfg.spec
+    tree = P.optimal_tree(spec).tree
+    cost = P.tree_cost(tree, spec)
+    grid = P.optimal_static_grid(tree, spec, world)
+    q = grid.grid if not getattr(args, "grid", None) else [int(v) for v in args.grid.split("x")]
+    layout = GridLayout(q)
+    hbm_gbs, hbm_src = B.read_peaks()
+    p_fp64, fp64_src = B.measure_fp64_peak(torch)
+    ctx = E.Context(local_rank)
+    ops = GpuOps(ctx, local_rank)
+    cores = max(1, (os.cpu_count() or 1) // world)
+    t0 = time.perf_counter()
+    local = build_local_block(ctx, ops, cfg, layout, rank, dist, cores)
+    build_s = time.perf_counter() - t0
+    dh = DistributedHooi(ops, spec, tree, q, rank)
+    dh.set_local_tensor_buffer(local)
+    f0 = W.start_factors(cfg)
+
+    spans = {}
+    marks = []
+
+    def hook(what, node):
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(ops.stream)
+        marks.append((what, node, ev))
+
+    def one_sweep():
+        return run_rank(dh.sweep(), dist, ops)
+
+    dh.set_factors(f0)
+    for _ in range(max(args.warmup, 0)):
+        one_sweep()
+    dh.set_factors(f0)
+    ctx.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    k0, _ = ctx.launch_counts()
+    sampler = B.ClockSampler(local_rank) if rank == 0 else None
+    if sampler:
+        sampler.start()
+    dh.events = hook
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(ops.stream)
+    res = None
+    for _ in range(args.steps):
+        res = one_sweep()
+    e1.record(ops.stream)
+    e1.synchronize()
+    ctx.synchronize()
+    dist.barrier()
+    dh.events = None
+    clocks = sampler.stop() if sampler else None
+    k1, lib_calls = ctx.launch_counts()
+    total_ms = e0.elapsed_time(e1)
+    # per-node TTM spans (kernel + exchange + reduction), summed over the K steps
+    open_ev = {}
+    node_ms, tree_ms, core_ms = {}, 0.0, 0.0
+    for what, node, ev in marks:
+        if what.startswith("begin_"):
+            open_ev[(what[6:], node)] = ev
+        else:
+            key = (what[4:], node)
+            ms = open_ev.pop(key).elapsed_time(ev)
+            if key[0] == "ttm":
+                node_ms[node] = node_ms.get(node, 0.0) + ms
+            elif key[0] == "tree":
+                tree_ms += ms
+            elif key[0] == "core":
+                core_ms += ms
+    nodes = sorted(node_ms)
+    stats = torch.tensor([total_ms, tree_ms, core_ms] + [node_ms[n] for n in nodes], dtype=torch.float64,
+                         device=ops.device)
+    dist.all_reduce(stats, op=dist.ReduceOp.MAX)       # device time, max over ranks
+    stats = (stats / args.steps).tolist()
+    ms_per_step, tree_phase_ms, core_ms = stats[0], stats[1], stats[2]
+    node_ms = dict(zip(nodes, stats[3:]))
+    fit, core_norm = run_rank(dh.fit_from_norms(), dist, ops)
+
+    # e2e: per step the local block comes from pinned host memory and the result goes back to the host
+    e2e = None
+    if not args.no_e2e:
+        host_block = torch.empty(local.numel(), dtype=torch.float64, pin_memory=True)
+        with torch.cuda.stream(ops.stream):
+            host_block.copy_(local)
+        ctx.synchronize()
+        dh.set_factors(f0)
+        dist.barrier()
+        w0 = time.perf_counter()
+        for _ in range(args.steps):
+            with torch.cuda.stream(ops.stream):
+                local.copy_(host_block, non_blocking=True)
+            dh.set_factors(dh.get_factors() if dh.core is not None else f0)
+            one_sweep()
+            dh.get_factors()
+            dh.get_local_core()
+        ctx.synchronize()
+        dist.barrier()
+        secs = torch.tensor([(time.perf_counter() - w0) / args.steps], dtype=torch.float64, device=ops.device)
+        dist.all_reduce(secs, op=dist.ReduceOp.MAX)
+        fbytes = 8 * sum(l * k for l, k in zip(spec.L, spec.K))
+        e2e = {"value": float(secs.item()), "unit": "s/iter", "h2d_bytes_per_step": int(local.numel() * 8 + fbytes) * world,
+               "d2h_bytes_per_step": int(fbytes * world + 8 * int(np.prod(spec.K))), "host_memory": "pinned"}
+
+    if rank == 0:
+        # per-TTM roofline on P GPUs (SURVEY §8d): flops / P, local bytes 8 (|In| + q_n |Out|) / P, plus the
+        # reduce-scatter bytes 8 (q_n - 1) |Out| / P over NVLink when the grid splits the contracted mode
+        rows, t_roof, flops_total = [], 0.0, 0
+        for node, kind in enumerate(tree.kind):
+            if kind != P.MODE:
+                continue
+            n = tree.mode[node]
+            flops = 2 * spec.K[n] * cost.card_in[node]
+            local_bytes = 8 * (cost.card_in[node] + q[n] * cost.card_out[node]) / world + 8 * spec.K[n] * spec.L[n]
+            link_bytes = 8 * (q[n] - 1) * cost.card_out[node] / world
+            t = max(flops / world / (p_fp64 * 1e12), local_bytes / (hbm_gbs * 1e9)) + link_bytes / (B.NVLINK_GBS * 1e9)
+            t_roof += t
+            flops_total += flops
+            ms = node_ms.get(node, 0.0)
+            rows.append({"node": node, "mode": n, "ms": ms, "roofline_ms": t * 1e3, "frac": t * 1e3 / ms if ms else None,
+                         "nvlink_bytes_per_gpu": link_bytes})
+        ttm_ms = sum(r["ms"] for r in rows)
+        dom = max(rows, key=lambda r: r["ms"])
+        dom_flops = 2 * spec.K[dom["mode"]] * cost.card_in[dom["node"]]
+        achieved = dom_flops / (dom["ms"] * 1e-3) / 1e12 if dom["ms"] else None
+        line = {
+            "metric": "hooi_s_per_iter", "value": ms_per_step * 1e-3, "unit": "s/iter", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name, "iterations": cfg.iterations, "schedule": "jacobi on optimal_tree",
+                       "tree": tree.label(), "grid": list(q), "grid_volume_elements": P.static_volume(tree, spec, q, world).total,
+                       "l2": "inputs_larger_than_L2", "noise": "slab-parallel" if cfg.slab_noise else "sequential",
+                       "evd": "replicated on every rank"},
+            "ttm_tree": {"tflops": flops_total / (ttm_ms * 1e-3) / 1e12 if ttm_ms else None,
+                         "roofline_frac": t_roof * 1e3 / ttm_ms if ttm_ms else None, "measured_ms": ttm_ms,
+                         "roofline_ms": t_roof * 1e3, "flops": flops_total, "p_fp64_tflops": p_fp64,
+                         "p_fp64_source": fp64_src, "hbm_gbs": hbm_gbs, "hbm_source": hbm_src,
+                         "nvlink_gbs": B.NVLINK_GBS, "per_node": rows,
+                         "note": "per-node time = local kernel + chunk exchange + ordered reduction, max over ranks"},
+            "phases_ms": {"tree_phase_incl_leaves": tree_phase_ms, "core_ms": core_ms},
+            "relative_fit": fit, "core_norm": core_norm, "build_s": build_s,
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": p_fp64 * world, "unit": "TFLOP/s",
+                         "frac": achieved / (p_fp64 * world) if achieved else None, "traffic": None,
+                         "kernel": "ttm_dmma_kernel (tree node %d, mode %d) across %d GPUs" % (dom["node"], dom["mode"] + 1, world),
+                         "peak_source": fp64_src},
+            "cpu_baseline": None, "e2e": e2e, "gpu_launches": int(k1 - k0), "library_calls": int(lib_calls),
+            "clocks": clocks, "degenerate": bool(res.degenerate),
+            "volume_sent_rank0": {str(k): v for k, v in res.volume_sent.items()},
+        }
+        print(json.dumps(line))
+    dist.destroy_process_group()
+    return 0

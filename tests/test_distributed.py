@@ -1,0 +1,251 @@
+"""The Cartesian-grid executor (paper_1707_05594_b200/distributed.py) against the single-process oracle.
+
+CPU: virtual ranks for many grids, and real torch.distributed runs with the gloo backend (world_size 2 and 4),
+both on the NumPy local-ops backend — this covers partitioning, the exchange pattern, the reduction order and the
+schedule.  GPU (-m gpu): the same rank programs as virtual ranks on one B200 with the CUDA kernels."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import hooi_oracle as ho
+from paper_1707_05594_b200 import distributed as D
+from paper_1707_05594_b200 import hostgen, planner as P, workloads as W
+from tests.numpy_ops import NumpyOps
+
+
+def otree(t):
+    return ho.Tree(t.n_modes, t.kind, t.mode, t.parent)
+
+
+def assemble_core(layout, spec, blocks):
+    core = np.zeros(spec.K)
+    for r, b in enumerate(blocks):
+        core[layout.slices(r, spec.K)] = b
+    return core
+
+
+def check_against_oracle(spec, tree, q, t, f0, factors, core, results, sweeps):
+    of = [f.copy() for f in f0]
+    ocore = None
+    for _ in range(sweeps):
+        ost = ho.SweepStats()
+        ocore, of = ho.hooi_sweep(t, spec.L, spec.K, of, otree(tree), "jacobi", ost)
+    for a, b in zip(factors, of):
+        assert ho.sin_largest_principal_angle(a, b) < 1e-9
+        assert np.max(np.abs(np.abs(a) - np.abs(b))) < 1e-8          # same vectors up to sign
+    on = np.sqrt(np.sum(ocore * ocore))
+    assert abs(np.sqrt(np.sum(core * core)) - on) <= 1e-10 * on
+    assert np.max(np.abs(np.abs(core) - np.abs(ocore))) <= 1e-9 * np.max(np.abs(ocore))
+    res = results[0]
+    assert (res.tree_macs, res.core_macs, res.peak_live) == (ost.tree_macs, ost.core_macs, ost.peak_live)
+    # shipped elements per TTM node, summed over ranks, equal the reference's static volume (q_n - 1)|Out_u|
+    vol = P.static_volume(tree, spec, q, int(np.prod(q)))
+    for node, want in enumerate(vol.per_node):
+        got = sum(r.volume_sent.get(node, 0) for r in results)
+        assert got == want, (node, got, want)
+
+
+def run_virtual_case(ops, L, K, q, sweeps=2, seed=5):
+    spec = P.ProblemSpec(list(L), list(K))
+    tree = P.optimal_tree(spec).tree
+    cfg = W.Config(1, list(L), list(K), 1e-2, sweeps)
+    t = W.build_tensor_host(cfg)
+    f0 = W.start_factors(cfg)
+    layout = D.GridLayout(q)
+    ranks = [D.DistributedHooi(ops, spec, tree, q, r) for r in range(layout.procs)]
+    for r, dh in enumerate(ranks):
+        dh.set_local_tensor(np.ascontiguousarray(t[layout.slices(r, spec.L)]))
+        dh.set_factors(f0)
+    results = None
+    for _ in range(sweeps):
+        results = D.run_virtual([dh.sweep() for dh in ranks], ops)
+    fits = D.run_virtual([dh.fit_from_norms() for dh in ranks], ops)
+    factors = ranks[0].get_factors()
+    for dh in ranks[1:]:                      # replicated factors stay bit-identical on every rank
+        for a, b in zip(factors, dh.get_factors()):
+            assert np.array_equal(a, b)
+    core = assemble_core(layout, spec, [dh.get_local_core() for dh in ranks])
+    check_against_oracle(spec, tree, q, t, f0, factors, core, results, sweeps)
+    tn = ho.frobenius_norm(t)
+    want_fit = np.sqrt(max(tn ** 2 - np.sum(core * core), 0.0)) / tn
+    assert all(abs(f[0] - want_fit) <= 1e-9 * max(want_fit, 1e-3) for f in fits)
+
+
+VIRTUAL_CASES = [
+    ((12, 10, 8), (4, 3, 2), (1, 1, 1)),
+    ((12, 10, 8), (4, 3, 2), (2, 1, 1)), ((12, 10, 8), (4, 3, 2), (1, 3, 1)), ((12, 10, 8), (4, 3, 2), (1, 1, 2)),
+    ((12, 10, 8), (4, 3, 2), (2, 2, 2)), ((12, 10, 8), (4, 3, 2), (4, 1, 2)), ((13, 11, 7), (5, 3, 3), (3, 1, 2)),
+    ((9, 8, 7, 6), (3, 3, 2, 2), (1, 2, 1, 2)), ((9, 8, 7, 6), (3, 3, 2, 2), (3, 1, 2, 1)),
+    ((6, 6, 5, 5, 4), (2, 2, 2, 2, 2), (2, 1, 2, 1, 2)), ((17, 9), (4, 4), (4, 2)),
+]
+
+
+@pytest.mark.parametrize("L,K,q", VIRTUAL_CASES)
+def test_virtual_ranks_numpy(L, K, q):
+    run_virtual_case(NumpyOps(), L, K, q)
+
+
+def test_optimal_grids_of_scaled_configs():
+    """The grids the planner actually picks (tests/golden via test_planner) drive the executor end to end."""
+    for L, K, procs in [((24, 24, 24), (8, 8, 8), 8), ((16, 16, 16, 16), (4, 4, 4, 4), 8),
+                        ((40, 10, 10, 5), (8, 2, 4, 1), 8), ((8, 8, 8, 8, 8), (2, 2, 2, 2, 2), 2)]:
+        spec = P.ProblemSpec(list(L), list(K))
+        q = P.optimal_static_grid(P.optimal_tree(spec).tree, spec, procs).grid
+        run_virtual_case(NumpyOps(), L, K, q, sweeps=1)
+
+
+def test_regrid_roundtrip_and_counts():
+    ext = (7, 6, 5)
+    full = hostgen.random_tensor(ext, 3)
+    src, dst = D.GridLayout((4, 1, 1)), D.GridLayout((1, 2, 2))
+    ops = NumpyOps()
+    blocks = [torch.from_numpy(np.ascontiguousarray(full[src.slices(r, ext)])) for r in range(4)]
+    outs = D.run_virtual([D.regrid(blocks[r], ext, src, dst, r, ops.empty) for r in range(4)])
+    moved = 0
+    for r in range(4):
+        assert np.array_equal(outs[r].numpy(), full[dst.slices(r, ext)])
+        sends, _ = D.regrid_plan(ext, src, dst, r)
+        moved += sum(int(np.prod([hi - lo for lo, hi in o])) for p, o in sends if p != r)
+    # elements whose owner changes, counted the reference's way (simulate.hpp:97-113): walk every element
+    want = 0
+    for idx in np.ndindex(*ext):
+        a = src.rank_of([P.block_of(c, e, q) for c, e, q in zip(idx, ext, src.q)])
+        b = dst.rank_of([P.block_of(c, e, q) for c, e, q in zip(idx, ext, dst.q)])
+        want += a != b
+    assert moved == want
+    back = D.run_virtual([D.regrid(outs[r], ext, dst, src, r, ops.empty) for r in range(4)])
+    for r in range(4):
+        assert np.array_equal(back[r].numpy(), blocks[r].numpy())
+
+
+def test_layout_matches_reference_owner_rank():
+    lay = D.GridLayout((2, 3, 2))
+    assert [lay.rank_of(lay.coords(r)) for r in range(12)] == list(range(12))
+    assert lay.coords(7) == [1, 0, 1]                      # row-major, simulate.hpp:69-73
+    assert lay.mode_group(7, 1) == [lay.rank_of([1, b, 1]) for b in range(3)]
+    assert lay.local_dims(0, (100, 100, 100)) == [50, 33, 50]
+    assert lay.local_range(lay.rank_of([0, 2, 0]), 1, 100) == (66, 100)
+
+
+# ----------------------------------------------------------------------------- real process groups (gloo, CPU)
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _gloo_worker(rank, world, port, L, K, q, sweeps, out_dir):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        spec = P.ProblemSpec(list(L), list(K))
+        tree = P.optimal_tree(spec).tree
+        cfg = W.Config(1, list(L), list(K), 1e-2, sweeps)
+        t = W.build_tensor_host(cfg, threads=1)
+        f0 = W.start_factors(cfg)
+        layout = D.GridLayout(q)
+        dh = D.DistributedHooi(NumpyOps(), spec, tree, q, rank)
+        dh.set_local_tensor(np.ascontiguousarray(t[layout.slices(rank, spec.L)]))
+        dh.set_factors(f0)
+        res = None
+        for _ in range(sweeps):
+            res = D.run_rank(dh.sweep(), dist)
+        fit, core_norm = D.run_rank(dh.fit_from_norms(), dist)
+        np.savez(os.path.join(out_dir, "rank%d.npz" % rank), core=dh.get_local_core(), fit=fit,
+                 volume_nodes=np.array(sorted(res.volume_sent), dtype=np.int64),
+                 volume=np.array([res.volume_sent[k] for k in sorted(res.volume_sent)], dtype=np.int64),
+                 stats=np.array([res.tree_macs, res.core_macs, res.peak_live], dtype=np.int64),
+                 **{"f%d" % i: f for i, f in enumerate(dh.get_factors())})
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("L,K,q", [((12, 10, 8), (4, 3, 2), (1, 1, 2)), ((12, 10, 8), (4, 3, 2), (2, 1, 1)),
+                                   ((13, 11, 7), (5, 3, 3), (2, 1, 2))])
+def test_gloo_process_group(tmp_path, L, K, q):
+    import torch.multiprocessing as mp
+    world = int(np.prod(q))
+    sweeps = 2
+    mp.spawn(_gloo_worker, args=(world, _free_port(), L, K, q, sweeps, str(tmp_path)), nprocs=world, join=True)
+    spec = P.ProblemSpec(list(L), list(K))
+    tree = P.optimal_tree(spec).tree
+    cfg = W.Config(1, list(L), list(K), 1e-2, sweeps)
+    t = W.build_tensor_host(cfg, threads=1)
+    f0 = W.start_factors(cfg)
+    layout = D.GridLayout(q)
+    data = [np.load(os.path.join(str(tmp_path), "rank%d.npz" % r)) for r in range(world)]
+    factors = [data[0]["f%d" % i] for i in range(len(L))]
+    for d in data[1:]:
+        for i in range(len(L)):
+            assert np.array_equal(d["f%d" % i], factors[i])
+    core = assemble_core(layout, spec, [d["core"] for d in data])
+
+    class R:  # adapt the saved arrays to what check_against_oracle reads
+        def __init__(self, d):
+            self.tree_macs, self.core_macs, self.peak_live = (int(v) for v in d["stats"])
+            self.volume_sent = {int(k): int(v) for k, v in zip(d["volume_nodes"], d["volume"])}
+
+    check_against_oracle(spec, tree, q, t, f0, factors, core, [R(d) for d in data], sweeps)
+
+
+# ----------------------------------------------------------------------------- one B200, virtual ranks, CUDA kernels
+GPU_CASES = [((48, 40, 36), (8, 6, 5), (1, 1, 4)), ((48, 40, 36), (8, 6, 5), (2, 2, 2)),
+             ((33, 26, 24, 10), (5, 4, 6, 3), (1, 2, 1, 2)), ((40, 30, 50), (13, 9, 12), (8, 1, 1)),
+             ((64, 64, 64), (12, 12, 12), (1, 1, 8)), ((20, 12, 10, 9, 8), (4, 3, 3, 2, 2), (2, 1, 1, 1, 2))]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("L,K,q", GPU_CASES)
+def test_virtual_ranks_gpu(L, K, q):
+    from paper_1707_05594_b200 import engine as E
+    ctx = E.Context(0)
+    try:
+        run_virtual_case(D.GpuOps(ctx), L, K, q)
+    finally:
+        ctx.close()
+
+
+@pytest.mark.gpu
+def test_gpu_ops_match_numpy_ops():
+    """Every local building block of the grid executor: CUDA (tp_dev_*) against the NumPy stand-in."""
+    from paper_1707_05594_b200 import engine as E
+    ctx = E.Context(0)
+    g, n = D.GpuOps(ctx), NumpyOps()
+    try:
+        cases = [((6, 9, 7), 2, 11, 3, 5, [0, 1, 2, 3, 5]), ((6, 9, 8), 1, 20, 4, 6, [0, 3, 6]),
+                 ((5, 36), 1, 36, 0, 5, [0, 1, 2, 3, 5]), ((48, 40, 9), 2, 36, 9, 5, [0, 1, 2, 3, 5]),
+                 ((48, 40, 9), 2, 36, 27, 5, [0, 5]), ((10, 7, 12), 0, 33, 5, 13, [0, 6, 13]),
+                 ((4, 50, 6), 1, 64, 14, 20, [0, 2, 5, 7, 10, 12, 15, 17, 20]), ((300, 16), 1, 16, 0, 3, [0, 1, 3])]
+        for dims, mode, l_full, l0, k, cuts in cases:
+            x = hostgen.random_tensor(dims, 7)
+            f = np.asfortranarray(hostgen.random_tensor([k, l_full], 8).T)          # L x K column-major
+            fbuf = f.reshape(-1, order="F")
+            got = g.to_host(g.ttm_partial(g.from_host(x), list(dims), mode, g.from_host(fbuf), l_full, l0, k, cuts))
+            want = n.to_host(n.ttm_partial(n.from_host(x), list(dims), mode, n.from_host(fbuf), l_full, l0, k, cuts))
+            assert got.shape == want.shape
+            assert np.max(np.abs(got - want)) < 1e-12 * dims[mode], (dims, mode, cuts)
+        slots = [hostgen.random_tensor([1000], s) for s in range(5)]
+        got = g.to_host(g.reduce_slots([g.from_host(s) for s in slots], 1000))
+        assert np.array_equal(got, ((((slots[0] + slots[1]) + slots[2]) + slots[3]) + slots[4]))
+        dst_g, dst_n = g.zeros(4 * 9 * 5), n.zeros(4 * 9 * 5)
+        piece = hostgen.random_tensor([4, 3, 5], 2)
+        g.assemble(dst_g, 4, 9, 5, g.from_host(piece), 2, 3)
+        n.assemble(dst_n, 4, 9, 5, n.from_host(piece), 2, 3)
+        assert np.array_equal(g.to_host(dst_g), n.to_host(dst_n))
+        y = hostgen.random_tensor([6, 36, 5], 4)
+        gg = g.to_host(g.gram(g.from_host(y), 6, 36, 5))
+        gn = n.to_host(n.gram(n.from_host(y), 6, 36, 5))
+        assert np.max(np.abs(gg - gn)) < 1e-11
+        fg, sg = g.leaf_solve(g.from_host(gn), 36, 5)
+        fn, sn = n.leaf_solve(n.from_host(gn), 36, 5)
+        assert np.max(np.abs(g.to_host(fg) - n.to_host(fn))) < 1e-9
+        assert g.status_to_host(sg) == n.status_to_host(sn)
+        v = hostgen.random_tensor([12345], 1)
+        assert abs(g.to_host(g.sum_squares(g.from_host(v), 12345))[0] - float(np.dot(v, v))) < 1e-9
+    finally:
+        ctx.close()
