@@ -1,0 +1,86 @@
+// A caller written against the reference's API (names as in reference tools/tuckerplan_cli.cpp:376-445 and
+// tests/test_engine.cpp), compiled against include/tuckerplan/ of THIS repo and linked to libtuckerplan_b200.so.
+//   dropin planner  -> planner selections for the cube / pinned specs (no GPU needed)
+//   dropin hooi     -> the README transcript: 12x10x8 seed 7, K = 4,3,2, Gauss-Seidel on the chain-input tree
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "tuckerplan/tuckerplan.hpp"
+
+namespace tp = tuckerplan;
+
+static std::string label(const tp::TtmTree& t, int id = 0) {
+  const tp::TreeNode& n = t.nodes[id];
+  std::string s = n.kind == tp::NodeKind::root ? "T" : (n.kind == tp::NodeKind::mode ? "M" : "F");
+  if (n.kind != tp::NodeKind::root) s += std::to_string(n.mode + 1);
+  if (!n.children.empty()) {
+    s += "(";
+    for (std::size_t i = 0; i < n.children.size(); ++i) s += (i ? ", " : "") + label(t, n.children[i]);
+    s += ")";
+  }
+  return s;
+}
+
+int main(int argc, char** argv) {
+  const std::string cmd = argc > 1 ? argv[1] : "planner";
+  try {
+    if (cmd == "planner") {
+      const tp::ProblemSpec cube{{4, 4, 4}, {2, 2, 2}};
+      std::printf("chain %llu\n", (unsigned long long)tp::tree_cost(tp::chain_tree(cube), cube).total_macs);
+      std::printf("opt %llu\n", (unsigned long long)tp::optimal_tree(cube).total_macs);
+      const tp::StaticGridResult g = tp::optimal_static_grid(tp::chain_tree(cube), cube, 4);
+      std::printf("grid %llux%llux%llu vol %llu\n", (unsigned long long)g.grid.q[0], (unsigned long long)g.grid.q[1],
+                  (unsigned long long)g.grid.q[2], (unsigned long long)g.report.total);
+      const tp::ProblemSpec c3{{400, 100, 100, 50}, {40, 10, 20, 5}};
+      std::printf("tree %s\n", label(tp::optimal_tree(c3).tree).c_str());
+      std::printf("canonical %d depth %d\n", tp::is_canonical(tp::canonicalize(tp::chain_tree(cube))) ? 1 : 0,
+                  tp::tree_depth(tp::optimal_tree(c3).tree));
+      try {
+        tp::validate_spec(tp::ProblemSpec{{3, 3}, {1, 4}});
+      } catch (const tp::Error& e) {
+        std::printf("error %d mode %d\n", static_cast<int>(e.code()), e.mode());
+      }
+      try {
+        tp::optimal_static_grid(tp::chain_tree(cube), cube, 7);
+      } catch (const tp::Error& e) {
+        std::printf("error %d\n", static_cast<int>(e.code()));
+      }
+      const tp::DenseTensor t = tp::random_tensor({3, 4, 2}, 5);
+      const tp::DenseTensor back = tp::fold(tp::unfold(t, 1), t.dims, 1);
+      std::printf("fold %d first %.17g\n", back.data == t.data ? 1 : 0, t.data[0]);
+      return 0;
+    }
+    if (cmd == "hooi") {
+      const tp::DenseTensor t = tp::random_tensor({12, 10, 8}, 7);
+      tp::ProblemSpec s;
+      for (std::size_t d : t.dims) s.L.push_back(d);
+      s.K = {4, 3, 2};
+      const tp::TtmTree tree = tp::build_tree(s, tp::TreeStrategy::chain_input);
+      tp::Decomposition d = tp::random_decomposition(t, s, 0);
+      std::printf("start: error %.12f\n", tp::reconstruction_error(t, d));
+      for (int i = 0; i < 2; ++i) {
+        tp::SweepStats stats;
+        d = tp::hooi_sweep(t, s, d, tree, tp::SweepKind::gauss_seidel, &stats);
+        std::printf("sweep %d: error %.12f, tree macs %llu, peak live %d\n", i + 1, tp::reconstruction_error(t, d),
+                    (unsigned long long)stats.tree_macs, stats.peak_live);
+      }
+      // the resident form gives the same numbers
+      tp::DeviceHooi resident(t, s, tp::optimal_tree(s).tree, tp::SweepKind::jacobi);
+      resident.set_factors(tp::random_decomposition(t, s, 0).factors);
+      const tp::SweepStats st = resident.sweep();
+      std::printf("resident jacobi: error %.12f, tree macs %llu\n", resident.reconstruction_error(),
+                  (unsigned long long)st.tree_macs);
+      try {
+        tp::hooi_sweep(t, s, d, tp::balanced_tree(s), tp::SweepKind::gauss_seidel);
+      } catch (const tp::Error& e) {
+        std::printf("error %d\n", static_cast<int>(e.code()));
+      }
+      return 0;
+    }
+  } catch (const tp::Error& e) {
+    std::printf("tuckerplan::Error %d: %s\n", static_cast<int>(e.code()), e.what());
+    return 1;
+  }
+  return 2;
+}

@@ -1,0 +1,40 @@
+"""A C++ caller written against the reference's header API, compiled against include/tuckerplan/ of this repo."""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+LIBDIR = os.path.join(ROOT, "paper_1707_05594_b200", "lib")
+
+
+@pytest.fixture(scope="module")
+def dropin():
+    exe = os.path.join(ROOT, "build", "dropin")
+    os.makedirs(os.path.dirname(exe), exist_ok=True)
+    subprocess.check_call(["g++", "-std=c++20", "-O2", "-Wall", "-Wextra", "-I" + os.path.join(ROOT, "include"),
+                           os.path.join(ROOT, "tests", "cpp", "dropin.cpp"), "-o", exe, "-L" + LIBDIR,
+                           "-ltuckerplan_b200", "-Wl,-rpath," + LIBDIR])
+    return exe
+
+
+def test_planner_through_cpp_headers(dropin):
+    out = subprocess.check_output([dropin, "planner"]).decode().splitlines()
+    assert out[0] == "chain 576" and out[1] == "opt 448"                      # test_trees.cpp:60-70, test_tree_search.cpp:80-88
+    assert out[2] == "grid 1x2x2 vol 80"                                       # test_grids.cpp:117-124
+    assert out[3] == "tree T(M2(M3(M4(F1), M1(F4)), M4(M1(F3))), M4(M3(M1(F2))))"
+    assert out[4] == "canonical 1 depth 3"
+    assert out[5] == "error 1 mode 1"                                          # Errc::k_too_large at mode 1
+    assert out[6] == "error 7"                                                 # Errc::no_valid_grid
+    assert out[7].startswith("fold 1 ")
+
+
+@pytest.mark.gpu
+def test_readme_transcript_through_cpp_headers(dropin, readme_kat):
+    out = subprocess.check_output([dropin, "hooi"]).decode().splitlines()
+    assert out[0] == "start: error " + readme_kat["start_error"]
+    assert out[1] == "sweep 1: error %s, tree macs %d, peak live %d" % (
+        readme_kat["sweep1_error"], readme_kat["tree_macs"], readme_kat["peak_live"])
+    assert out[2].startswith("sweep 2: error 0.918925317677")
+    assert out[3].startswith("resident jacobi: error ")
+    assert out[4] == "error 11"                                                # Errc::needs_chain_tree
