@@ -287,6 +287,7 @@ def run_b200(args):
     node_ms = [v / steps for v in node_ms_sum]
     fit = plan.fit_from_norms(dt)
     final_factors = plan.get_factors()
+    evd_info = plan.evd_info()
 
     # The per-TTM numbers come from a second pass of the same K iterations with the eigen-solves serialised behind
     # the tree instead of beside it: in the overlapped schedule above a TTM's event span also contains whatever
@@ -372,7 +373,7 @@ def run_b200(args):
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg.name, "iterations": cfg.iterations, "schedule": "jacobi on optimal_tree",
-                   "tree": tree.label(), "grid": [1] * spec.n_modes(), "evd": "overlapped on side streams",
+                   "tree": tree.label(), "grid": [1] * spec.n_modes(), "evd": "top-k subspace iteration where certified, else full syevd; on side streams",
                    "l2": "flushed_between_steps" if small else "inputs_larger_than_L2",
                    "noise": "slab-parallel" if cfg.slab_noise else "sequential"},
         "ttm_tree": {"schedule": "serial pass (eigen-solves not overlapped), same K iterations",
@@ -382,6 +383,7 @@ def run_b200(args):
                      "per_node": [{k: r[k] for k in ("node", "mode", "bound", "ms", "tflops", "frac")} for r in rows]},
         "ttm_tree_overlapped_ms": sum(overlapped_node_ms[r["node"]] for r in rows),
         "serial_schedule": {"ms_per_step": float(np.mean(serial_ms)), "phases_ms": serial_phases},
+        "evd": {"fast_path_leaves": evd_info[0], "redone_with_full_solve_last_sweep": evd_info[1]},
         "phases_ms": phases, "relative_fit": fit, "wall_s_timed_region": wall, "build_s": t_build,
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(k1 - k0),
         "library_calls": int(lib_calls), "clocks": clocks,

@@ -213,8 +213,14 @@ int tp_plan_destroy(tp_ctx* ctx, tp_plan* plan);
 /* Execution options (results are identical either way).  TP_OPT_OVERLAP_EVD (default 1): in a Jacobi sweep run each
  * leaf's eigen-solve on a side stream beside the remaining tree TTMs; 0 serialises everything on one stream, which is
  * what per-kernel timing and profiling want. */
-enum { TP_OPT_OVERLAP_EVD = 1 };
+enum { TP_OPT_OVERLAP_EVD = 1, TP_OPT_FAST_EVD = 2 };
 int tp_plan_set_option(tp_ctx* ctx, tp_plan* plan, int option, int value);
+/* TP_OPT_FAST_EVD (default 1): Jacobi leaves with L_n >= 256 and 2 (K_n + 8) <= L_n compute only the K_n leading
+ * eigenvectors by warm-started block subspace iteration + Rayleigh-Ritz; every kept Ritz pair must satisfy
+ * ||G x - theta x|| <= 1e-13 theta_max, otherwise (or when the gap estimate says "degenerate") the leaf is redone
+ * with the full eigen-solve, so the factors are the reference's (hooi.hpp:55-69) to rounding either way.
+ * tp_plan_last_evd_info: leaves eligible for the fast path, and how many of them the last sweep had to redo. */
+int tp_plan_last_evd_info(tp_ctx* ctx, tp_plan* plan, int* fast_eligible, int* rejected);
 /* Decomposition::factors (hooi.hpp:78-81) <-> device: factors[n] is L_n x K_n column-major on the host */
 int tp_plan_set_factors(tp_ctx* ctx, tp_plan* plan, const double* const* factors);
 int tp_plan_get_factors(tp_ctx* ctx, tp_plan* plan, double* const* factors_out);

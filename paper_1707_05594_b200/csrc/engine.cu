@@ -12,6 +12,7 @@
 // (depth-first execution frees in tree order, so depth d has one live tensor),
 // sized from the planner's node cardinalities.
 #include <cuda_runtime.h>
+#include <cublas_v2.h>
 #include <cusolverDn.h>
 
 #include <algorithm>
@@ -33,6 +34,12 @@ namespace tpb {
   do {                                               \
     cudaError_t tpb_e_ = (expr);                     \
     if (tpb_e_ != cudaSuccess) cuda_fail(tpb_e_, #expr); \
+  } while (0)
+#define TPB_BLAS(expr)                                                                          \
+  do {                                                                                          \
+    cublasStatus_t tpb_b_ = (expr);                                                             \
+    if (tpb_b_ != CUBLAS_STATUS_SUCCESS)                                                        \
+      raise(TP_ERR_CUDA, std::string(#expr) + ": cublas status " + std::to_string(static_cast<int>(tpb_b_))); \
   } while (0)
 #define TPB_SOLVER(expr)                                                                        \
   do {                                                                                          \
@@ -61,6 +68,8 @@ struct tp_ctx {
   static constexpr int kAux = 4;
   cudaStream_t aux[kAux] = {nullptr, nullptr, nullptr, nullptr};
   cusolverDnHandle_t aux_solver[kAux] = {nullptr, nullptr, nullptr, nullptr};
+  cublasHandle_t blas = nullptr;     // small dense products inside the eigen-solve (off the hot path)
+  cublasHandle_t aux_blas[kAux] = {nullptr, nullptr, nullptr, nullptr};
 };
 
 struct tp_tensor {
@@ -174,8 +183,27 @@ struct LeafScratch {
   int lwork = 0;
   int* info = nullptr;
   int* flag = nullptr;         // degenerate flag, OR-ed by leaves
+  // warm-started subspace iteration (top-k only): block basis / products, small Rayleigh-Ritz problem
+  int block = 0;               // columns of the iteration block (k + oversampling), 0 = fast path not set up
+  double* q = nullptr;         // rows x block
+  double* z = nullptr;         // rows x block
+  double* x = nullptr;         // rows x block (Ritz vectors, ascending)
+  double* h = nullptr;         // block x block
+  double* theta = nullptr;     // block
+  double* small_work = nullptr;
+  int small_lwork = 0;
+  int* verdict = nullptr;      // [0] |= 1: a kept Ritz pair missed the residual bound; [1]: potrf/syevd info
+  int failures = 0;            // consecutive sweeps in which the fast path was rejected
+  bool fast_used = false;      // this sweep's factor came from the fast path (verdict still to be checked)
 
   void release() {
+    cudaFree(q);
+    cudaFree(z);
+    cudaFree(x);
+    cudaFree(h);
+    cudaFree(theta);
+    cudaFree(small_work);
+    cudaFree(verdict);
     cudaFree(gram);
     cudaFree(gram_ws);
     cudaFree(w);
@@ -209,6 +237,7 @@ void leaf_scratch_reserve(tp_ctx* ctx, LeafScratch& s, long long rows, size_t gr
     TPB_CUDA(cudaMalloc(&s.info, sizeof(int)));
     TPB_CUDA(cudaMalloc(&s.flag, sizeof(int)));
     TPB_CUDA(cudaMemsetAsync(s.flag, 0, sizeof(int), ctx->stream));
+    TPB_CUDA(cudaMemsetAsync(s.info, 0, sizeof(int), ctx->stream));
   }
 }
 
@@ -239,8 +268,103 @@ void leaf_solve(tp_ctx* ctx, LeafScratch& s, long long rows, int k, double* fact
   TPB_SOLVER(cusolverDnDsyevd(solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, static_cast<int>(rows),
                               s.gram, static_cast<int>(rows), s.w, s.work, s.lwork, s.info));
   ctx->library_calls += 1;
-  TPB_CUDA(launch_select_basis(stream, s.gram, s.w, static_cast<int>(rows), k, factor_out, s.flag));
+  TPB_CUDA(launch_select_basis(stream, s.gram, s.w, static_cast<int>(rows), static_cast<int>(rows), k, factor_out,
+                               s.flag));
   ctx->own_kernels += 1;
+}
+
+// ---- top-k eigen-solve by warm-started block subspace iteration --------------------------------------------
+// The leaves only need the K_n leading eigenvectors of an L_n x L_n Gram matrix whose spectrum, for the tensors
+// HOOI is run on, drops sharply after K_n, and the previous factor is an excellent start.  Orthogonal iteration
+// on a block of K_n + p columns (p = oversampling) with a Rayleigh-Ritz step converges like
+// (lambda_{K+p+1} / lambda_K)^steps.  The schedule is fixed (no host decisions inside the sweep): 2 rounds of
+// [3 x (Z = G Q; Q = CholQR2(Z))] + Rayleigh-Ritz; a device flag records whether every kept Ritz pair satisfies
+// ||G x - theta x|| <= 1e-13 theta_max and whether the gap estimate is safe.  The sweep checks the flags once at
+// its end; a rejected leaf is redone with the full eigen-solve (the Gram matrix is left intact here), so the
+// result is always the reference's: eigenvectors of the Gram matrix to rounding (hooi.hpp:55-69).
+constexpr int kSubspaceOversample = 8;
+constexpr int kSubspaceRounds = 2;
+constexpr int kSubspacePowerSteps = 3;
+constexpr double kSubspaceTol = 1e-13;
+
+bool subspace_eligible(long long rows, int k) {
+  // below ~700 rows the full eigen-solve is as fast as the ~70 small launches of the iteration
+  return rows >= 704 && 2LL * (k + kSubspaceOversample) <= rows;
+}
+
+void subspace_reserve(tp_ctx* ctx, LeafScratch& s, long long rows, int k) {
+  const int b = k + kSubspaceOversample;
+  if (s.block == b) return;
+  const size_t nb = static_cast<size_t>(rows) * b;
+  s.q = device_alloc(nb);
+  s.z = device_alloc(nb);
+  s.x = device_alloc(nb);
+  s.h = device_alloc(static_cast<size_t>(b) * b);
+  s.theta = device_alloc(static_cast<size_t>(b));
+  int l1 = 0, l2 = 0;
+  TPB_SOLVER(cusolverDnDsyevd_bufferSize(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, b, s.h, b,
+                                         s.theta, &l1));
+  TPB_SOLVER(cusolverDnDpotrf_bufferSize(ctx->solver, CUBLAS_FILL_MODE_LOWER, b, s.h, b, &l2));
+  s.small_lwork = std::max(l1, l2);
+  s.small_work = device_alloc(static_cast<size_t>(s.small_lwork));
+  TPB_CUDA(cudaMalloc(&s.verdict, 2 * sizeof(int)));
+  TPB_CUDA(cudaMemsetAsync(s.verdict, 0, 2 * sizeof(int), ctx->stream));
+  s.block = b;
+}
+
+// Q (rows x b, column-major) <- orthonormal basis of span(Z) by Cholesky QR, applied twice.  Z is overwritten.
+void cholqr2(cublasHandle_t blas, cusolverDnHandle_t solver, LeafScratch& s, int rows, int b, double* zbuf) {
+  const double one = 1.0, zero = 0.0;
+  for (int pass = 0; pass < 2; ++pass) {
+    TPB_BLAS(cublasDgemm(blas, CUBLAS_OP_T, CUBLAS_OP_N, b, b, rows, &one, zbuf, rows, zbuf, rows, &zero, s.h, b));
+    TPB_SOLVER(cusolverDnDpotrf(solver, CUBLAS_FILL_MODE_LOWER, b, s.h, b, s.small_work, s.small_lwork,
+                                s.verdict + 1));
+    // Z <- Z L^{-T}
+    TPB_BLAS(cublasDtrsm(blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, rows, b,
+                         &one, s.h, b, zbuf, rows));
+  }
+}
+
+// Enqueues the whole fast solve on the leaf's stream; the verdict is read by the caller at the end of the sweep.
+void leaf_solve_subspace(tp_ctx* ctx, LeafScratch& s, long long rows_ll, int k, const double* start,
+                         double* factor_out, int aux) {
+  cusolverDnHandle_t solver = aux < 0 ? ctx->solver : ctx->aux_solver[aux];
+  cublasHandle_t blas = aux < 0 ? ctx->blas : ctx->aux_blas[aux];
+  cudaStream_t stream = aux < 0 ? ctx->stream : ctx->aux[aux];
+  const int rows = static_cast<int>(rows_ll), b = s.block;
+  const double one = 1.0, zero = 0.0;
+  TPB_CUDA(cudaMemsetAsync(s.verdict, 0, 2 * sizeof(int), stream));
+  // start block: previous factor, then deterministic filler for the oversampling columns
+  TPB_CUDA(cudaMemcpyAsync(s.q, start, sizeof(double) * rows * k, cudaMemcpyDeviceToDevice, stream));
+  TPB_CUDA(launch_fill_pseudo_random(stream, s.q + static_cast<size_t>(rows) * k,
+                                     static_cast<size_t>(rows) * (b - k), 0x7461636bull));
+  cholqr2(blas, solver, s, rows, b, s.q);
+  for (int round = 0; round < kSubspaceRounds; ++round) {
+    for (int step = 0; step < kSubspacePowerSteps; ++step) {
+      TPB_BLAS(cublasDgemm(blas, CUBLAS_OP_N, CUBLAS_OP_N, rows, b, rows, &one, s.gram, rows, s.q, rows, &zero, s.z,
+                           rows));
+      std::swap(s.q, s.z);
+      cholqr2(blas, solver, s, rows, b, s.q);
+    }
+    // Rayleigh-Ritz on span(Q): H = Q^T G Q, H = V Theta V^T (ascending), X = Q V
+    TPB_BLAS(cublasDgemm(blas, CUBLAS_OP_N, CUBLAS_OP_N, rows, b, rows, &one, s.gram, rows, s.q, rows, &zero, s.z,
+                         rows));
+    TPB_BLAS(cublasDgemm(blas, CUBLAS_OP_T, CUBLAS_OP_N, b, b, rows, &one, s.q, rows, s.z, rows, &zero, s.h, b));
+    TPB_SOLVER(cusolverDnDsyevd(solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, b, s.h, b, s.theta,
+                                s.small_work, s.small_lwork, s.verdict + 1));
+    TPB_BLAS(cublasDgemm(blas, CUBLAS_OP_N, CUBLAS_OP_N, rows, b, b, &one, s.q, rows, s.h, b, &zero, s.x, rows));
+    if (round + 1 < kSubspaceRounds) {
+      std::swap(s.q, s.x);  // Ritz vectors (orthonormal) seed the next round
+    } else {
+      // residuals of the kept pairs: (Z V)_j - theta_j X_j with Z = G Q
+      TPB_BLAS(cublasDgemm(blas, CUBLAS_OP_N, CUBLAS_OP_N, rows, b, b, &one, s.z, rows, s.h, b, &zero, s.q, rows));
+      TPB_CUDA(launch_ritz_residuals(stream, s.q, s.x, s.theta, rows, b, k, kSubspaceTol, s.verdict));
+    }
+  }
+  ctx->library_calls += 2 + kSubspaceRounds * (kSubspacePowerSteps * 7 + 4) + 1;
+  TPB_CUDA(launch_select_basis(stream, s.x, s.theta, rows, b, k, factor_out, s.flag));
+  ctx->own_kernels += 3;
+  s.fast_used = true;
 }
 
 void leaf_update(tp_ctx* ctx, LeafScratch& s, const double* y, const std::vector<size_t>& dims, int mode, int k,
@@ -258,6 +382,9 @@ int read_and_clear_flag(tp_ctx* ctx, LeafScratch& s) {
   if (host[1] != 0) raise(TP_ERR_TOO_LARGE, "eigensolver did not converge");  // hooi.hpp:56-57
   return host[0];
 }
+
+// Reads the certificates of the leaves that took the fast path this sweep; returns the modes to redo.
+std::vector<int> verify_fast_leaves(tp_ctx* ctx, tp_plan* p);
 
 int read_and_clear_flags(tp_ctx* ctx, std::vector<LeafScratch>& slots) {
   std::vector<int> host(2 * slots.size(), 0);
@@ -299,6 +426,16 @@ struct tp_plan {
   std::vector<LeafScratch> leaf;              // one Gram / eigen-solve scratch per mode (leaves run concurrently)
   std::vector<cudaEvent_t> gram_ready, factor_ready;
   bool overlap_evd = true;                    // Jacobi: eigen-solves on side streams beside the tree TTMs
+  bool fast_evd = true;                       // top-k subspace iteration where eligible, verified, full solve otherwise
+  int fast_rejected = 0;
+  std::vector<std::vector<int>> visit_order;  // per node: children in execution order (see plan_visit_order)
+  std::vector<int> leaf_rank;                 // per mode: position of its leaf in the execution order
+  int spare_sms = 6;                          // SMs left to the side streams while eigen-solves are in flight
+  int leaves_in_flight = 0;
+  struct PendingLeaf {
+    int mode, node;
+  };
+  std::vector<PendingLeaf> pending;           // leaves whose eigen-solve still has to be queued                      // leaves of the last sweep that had to be redone with the full solve
   tp_sweep_stats model{};   // analytic SweepStats (tree_macs, core_macs, peak_live)
   tp_sweep_timing timing{};
   // event pool for phase timing: triples (phase, begin, end)
@@ -342,40 +479,125 @@ void plan_refresh_fragments(tp_ctx* ctx, tp_plan* p, int mode, const double* fac
   ctx->own_kernels += 1;
 }
 
-void plan_ttm(tp_ctx* ctx, tp_plan* p, const double* x, const std::vector<size_t>& dims, int mode, double* out) {
+// `spare_sms`: SMs the persistent TTM grid leaves free so that eigen-solve kernels queued on the side streams can
+// run beside it (the TTM CTAs are register-heavy and would otherwise hold every SM until the kernel ends).
+void plan_ttm(tp_ctx* ctx, tp_plan* p, const double* x, const std::vector<size_t>& dims, int mode, double* out,
+              int spare_sms = 0) {
   long long outer, inner;
   mode_extents(dims, mode, outer, inner);
   TPB_CUDA(launch_ttm(ctx->stream, x, outer, static_cast<long long>(dims[mode]), inner, p->frag[mode],
-                      p->frag_layout[mode], static_cast<long long>(p->spec.K[mode]), out, ctx->sm_count));
+                      p->frag_layout[mode], static_cast<long long>(p->spec.K[mode]), out,
+                      std::max(1, ctx->sm_count - spare_sms)));
   ctx->own_kernels += 1;
 }
 
 // Leaf update.  The Gram kernels stay on the main stream (the intermediate they read lives in a per-depth buffer the
 // next sibling TTM overwrites); with `overlap` the eigen-solve moves to a side stream and the main stream carries on
 // with the tree, joining again before the core chain needs the new factors.
-void plan_leaf(tp_ctx* ctx, tp_plan* p, const double* y, const std::vector<size_t>& dims, int mode, double* dst,
-               int node, bool overlap) {
+void plan_leaf_solve(tp_ctx* ctx, tp_plan* p, int mode, int node, double* dst, bool overlap) {
   const int k = static_cast<int>(p->spec.K[mode]);
-  Span gram(ctx, p, kGram, node);
-  const long long rows = leaf_gram(ctx, p->leaf[mode], y, dims, mode, k);
-  gram.close();
+  const long long rows = static_cast<long long>(p->spec.L[mode]);
   const int aux = overlap ? mode % tp_ctx::kAux : -1;
-  if (overlap) {
-    TPB_CUDA(cudaEventRecord(p->gram_ready[mode], ctx->stream));
-    TPB_CUDA(cudaStreamWaitEvent(ctx->aux[aux], p->gram_ready[mode], 0));
-  }
+  if (overlap) TPB_CUDA(cudaStreamWaitEvent(ctx->aux[aux], p->gram_ready[mode], 0));
   Span evd(ctx, p, kEvd, node, aux);
-  leaf_solve(ctx, p->leaf[mode], rows, k, dst, aux);
+  LeafScratch& slot = p->leaf[mode];
+  slot.fast_used = false;
+  if (p->fast_evd && p->sweep_kind == TP_SWEEP_JACOBI && slot.failures < 2 && subspace_eligible(rows, k)) {
+    subspace_reserve(ctx, slot, rows, k);
+    leaf_solve_subspace(ctx, slot, rows, k, p->cur[mode], dst, aux);
+  } else {
+    leaf_solve(ctx, slot, rows, k, dst, aux);
+  }
   evd.close();
   if (overlap) TPB_CUDA(cudaEventRecord(p->factor_ready[mode], ctx->aux[aux]));
 }
 
-void plan_join_leaves(tp_ctx* ctx, tp_plan* p) {
-  for (int m = 0; m < p->n; ++m) TPB_CUDA(cudaStreamWaitEvent(ctx->stream, p->factor_ready[m], 0));
+// Eigen-solves whose Gram matrix is queued but whose own (many, partly host-blocking) library calls are not yet:
+// they are issued right after the NEXT product has been queued on the main stream, so the GPU is never left
+// without work while the host walks through a solver's call sequence.
+void plan_flush_pending(tp_ctx* ctx, tp_plan* p) {
+  for (const tp_plan::PendingLeaf& job : p->pending) plan_leaf_solve(ctx, p, job.mode, job.node, p->fresh[job.mode], true);
+  p->pending.clear();
+}
+
+void plan_leaf(tp_ctx* ctx, tp_plan* p, const double* y, const std::vector<size_t>& dims, int mode, double* dst,
+               int node, bool overlap) {
+  const int k = static_cast<int>(p->spec.K[mode]);
+  Span gram(ctx, p, kGram, node);
+  leaf_gram(ctx, p->leaf[mode], y, dims, mode, k);
+  gram.close();
+  if (overlap) {
+    TPB_CUDA(cudaEventRecord(p->gram_ready[mode], ctx->stream));
+    p->pending.push_back(tp_plan::PendingLeaf{mode, node});
+    ++p->leaves_in_flight;
+  } else {
+    plan_leaf_solve(ctx, p, mode, node, dst, false);
+  }
+}
+
+std::vector<int> verify_fast_leaves(tp_ctx* ctx, tp_plan* p) {
+  std::vector<int> host(3 * p->n, 0);
+  bool any = false;
+  for (int m = 0; m < p->n; ++m) {
+    LeafScratch& s = p->leaf[m];
+    if (!s.fast_used) continue;
+    any = true;
+    TPB_CUDA(cudaMemcpyAsync(&host[3 * m], s.verdict, 2 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    TPB_CUDA(cudaMemcpyAsync(&host[3 * m + 2], s.flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  }
+  std::vector<int> rejected;
+  if (!any) return rejected;
+  TPB_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (int m = 0; m < p->n; ++m) {
+    LeafScratch& s = p->leaf[m];
+    if (!s.fast_used) continue;
+    // residual bound missed, a factorisation inside failed, or the gap estimate says "degenerate" (then the exact
+    // spectrum decides)
+    const bool bad = host[3 * m] != 0 || host[3 * m + 1] != 0 || host[3 * m + 2] != 0;
+    if (bad) {
+      rejected.push_back(m);
+      ++s.failures;
+      TPB_CUDA(cudaMemsetAsync(s.flag, 0, sizeof(int), ctx->stream));
+    } else {
+      s.failures = 0;
+    }
+    s.fast_used = false;
+  }
+  return rejected;
+}
+
+// Execution order of siblings.  A Jacobi sweep gives the same factors in any order (every product uses the
+// start-of-sweep factors, hooi.hpp:9-12), so children are visited leaves-first and then by descending leaf count of
+// their subtrees (stable): eigen-solves start as early as possible and the remaining big products hide them.
+void plan_visit_order(tp_plan* p) {
+  const Tree& t = p->tree;
+  std::vector<int> leaves(t.size(), 0);
+  for (int id = t.size() - 1; id >= 0; --id) {
+    if (t.leaf(id)) leaves[id] = 1;
+    if (t.parent[id] >= 0) leaves[t.parent[id]] += leaves[id];
+  }
+  p->visit_order.assign(t.size(), {});
+  for (int id = 0; id < t.size(); ++id) {
+    std::vector<int> order = t.kids[id];
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+      if (t.leaf(a) != t.leaf(b)) return t.leaf(a);
+      return leaves[a] > leaves[b];
+    });
+    p->visit_order[id] = std::move(order);
+  }
+  p->leaf_rank.assign(p->n, 0);
+  int next = 0;
+  std::vector<int> stack{0};
+  while (!stack.empty()) {
+    const int id = stack.back();
+    stack.pop_back();
+    if (t.leaf(id)) p->leaf_rank[t.mode[id]] = next++;
+    for (auto it = p->visit_order[id].rbegin(); it != p->visit_order[id].rend(); ++it) stack.push_back(*it);
+  }
 }
 
 void jacobi_walk(tp_ctx* ctx, tp_plan* p, int node, const double* tensor, std::vector<size_t>& dims, int depth) {
-  for (int c : p->tree.kids[node]) {
+  for (int c : p->visit_order[node]) {
     const int mode = p->tree.mode[c];
     if (p->tree.kind[c] == TP_NODE_LEAF) {
       plan_leaf(ctx, p, tensor, dims, mode, p->fresh[mode], c, p->overlap_evd);
@@ -383,8 +605,9 @@ void jacobi_walk(tp_ctx* ctx, tp_plan* p, int node, const double* tensor, std::v
       double* out = p->depth_buf[depth];
       {
         Span s(ctx, p, kTree, c);
-        plan_ttm(ctx, p, tensor, dims, mode, out);
+        plan_ttm(ctx, p, tensor, dims, mode, out, (p->overlap_evd && p->leaves_in_flight > 0) ? p->spare_sms : 0);
         s.close();
+        plan_flush_pending(ctx, p);
       }
       const size_t saved = dims[mode];
       dims[mode] = static_cast<size_t>(p->spec.K[mode]);
@@ -397,15 +620,26 @@ void jacobi_walk(tp_ctx* ctx, tp_plan* p, int node, const double* tensor, std::v
 // core_from_factors (hooi.hpp:93-100): T x_0 F_0^T ... x_{N-1} F_{N-1}^T.  Mode products along different modes
 // commute, so the chain runs in the cheapest order (plan->core_order) instead of the reference's fixed 0..N-1; the
 // result differs from the reference's only by rounding.  Ping-pong buffers, the last product lands in `core`.
-void plan_core(tp_ctx* ctx, tp_plan* p, const double* tensor, const std::vector<double*>& factors) {
+void plan_core(tp_ctx* ctx, tp_plan* p, const double* tensor, const std::vector<double*>& factors,
+               bool wait_for_leaves = false) {
   Span s(ctx, p, kCore);
   std::vector<size_t> dims(p->spec.L.begin(), p->spec.L.end());
   const double* src = tensor;
   for (int i = 0; i < p->n; ++i) {
     const int m = p->core_order[i];
+    if (wait_for_leaves) {
+      // a factor whose eigen-solve is still unqueued must be queued before the chain can wait for it
+      for (const tp_plan::PendingLeaf& job : p->pending)
+        if (job.mode == m) {
+          plan_flush_pending(ctx, p);
+          break;
+        }
+      TPB_CUDA(cudaStreamWaitEvent(ctx->stream, p->factor_ready[m], 0));
+    }
     plan_refresh_fragments(ctx, p, m, factors[m]);
     double* dst = (i == p->n - 1) ? p->core : p->core_tmp[i & 1];
-    plan_ttm(ctx, p, src, dims, m, dst);
+    plan_ttm(ctx, p, src, dims, m, dst, (wait_for_leaves && i == 0 && !p->pending.empty()) ? p->spare_sms : 0);
+    if (wait_for_leaves) plan_flush_pending(ctx, p);
     dims[m] = static_cast<size_t>(p->spec.K[m]);
     src = dst;
   }
@@ -414,33 +648,41 @@ void plan_core(tp_ctx* ctx, tp_plan* p, const double* tensor, const std::vector<
 
 // Cheapest order of the core chain: forward DP over the set of already-multiplied modes; ties keep the smaller mode
 // first (strict improvement only, modes scanned ascending), so the reference order wins whenever it is optimal.
-std::vector<int> cheapest_chain_order(const Spec& s, u64* macs_out) {
+// Among equally cheap orders the mode whose new factor is finished first (`rank`, smaller = earlier) goes first, so
+// the chain's first — largest — product can start while later eigen-solves are still running.
+std::vector<int> cheapest_chain_order(const Spec& s, const std::vector<int>& rank, u64* macs_out) {
   const int n = s.n();
   const std::uint32_t full = (n >= 32) ? ~0u : ((1u << n) - 1);
-  std::vector<u64> best(static_cast<size_t>(full) + 1, kSat);
-  std::vector<signed char> last(static_cast<size_t>(full) + 1, -1);
-  best[0] = 0;
-  for (std::uint32_t done = 0; done < full; ++done) {
-    if (best[done] == kSat) continue;
+  auto card_of = [&](std::uint32_t done) {
     u64 card = 1;
     for (int m = 0; m < n; ++m) card = mul_sat(card, ((done >> m) & 1u) ? s.K[m] : s.L[m]);
+    return card;
+  };
+  // togo[S] = fewest MACs to finish from the state where the modes of S are already multiplied
+  std::vector<u64> togo(static_cast<size_t>(full) + 1, kSat);
+  togo[full] = 0;
+  for (std::uint32_t done = full; done-- > 0;) {
+    const u64 card = card_of(done);
     for (int m = 0; m < n; ++m) {
       if ((done >> m) & 1u) continue;
-      const u64 c = add_sat(best[done], mul_sat(s.K[m], card));
-      const std::uint32_t next = done | (1u << m);
-      if (c < best[next]) {
-        best[next] = c;
-        last[next] = static_cast<signed char>(m);
-      }
+      const u64 c = add_sat(mul_sat(s.K[m], card), togo[done | (1u << m)]);
+      if (c < togo[done]) togo[done] = c;
     }
   }
-  std::vector<int> order(n);
-  std::uint32_t at = full;
-  for (int i = n - 1; i >= 0; --i) {
-    order[i] = last[at];
-    at &= ~(1u << last[at]);
+  std::vector<int> order;
+  std::uint32_t done = 0;
+  while (done != full) {
+    const u64 card = card_of(done);
+    int pick = -1;
+    for (int m = 0; m < n; ++m) {
+      if ((done >> m) & 1u) continue;
+      if (add_sat(mul_sat(s.K[m], card), togo[done | (1u << m)]) != togo[done]) continue;
+      if (pick < 0 || rank[m] < rank[pick]) pick = m;
+    }
+    order.push_back(pick);
+    done |= 1u << pick;
   }
-  if (macs_out) *macs_out = best[full];
+  if (macs_out) *macs_out = togo[0];
   return order;
 }
 
@@ -503,10 +745,14 @@ int tp_ctx_create(int device, tp_ctx** out) {
       TPB_SOLVER(cusolverDnCreate(&ctx->solver));
       TPB_SOLVER(cusolverDnSetStream(ctx->solver, ctx->stream));
       ctx->reduce_scratch = device_alloc(reduce_scratch_doubles() + 1);
+      TPB_BLAS(cublasCreate(&ctx->blas));
+      TPB_BLAS(cublasSetStream(ctx->blas, ctx->stream));
       for (int a = 0; a < tp_ctx::kAux; ++a) {
         TPB_CUDA(cudaStreamCreateWithPriority(&ctx->aux[a], cudaStreamNonBlocking, prio_low));
         TPB_SOLVER(cusolverDnCreate(&ctx->aux_solver[a]));
         TPB_SOLVER(cusolverDnSetStream(ctx->aux_solver[a], ctx->aux[a]));
+        TPB_BLAS(cublasCreate(&ctx->aux_blas[a]));
+        TPB_BLAS(cublasSetStream(ctx->aux_blas[a], ctx->aux[a]));
       }
     } catch (...) {
       delete ctx;
@@ -522,9 +768,11 @@ int tp_ctx_destroy(tp_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     if (ctx->solver) cusolverDnDestroy(ctx->solver);
+    if (ctx->blas) cublasDestroy(ctx->blas);
     for (int a = 0; a < tp_ctx::kAux; ++a) {
       if (ctx->aux[a]) cudaStreamSynchronize(ctx->aux[a]);
       if (ctx->aux_solver[a]) cusolverDnDestroy(ctx->aux_solver[a]);
+      if (ctx->aux_blas[a]) cublasDestroy(ctx->aux_blas[a]);
       if (ctx->aux[a]) cudaStreamDestroy(ctx->aux[a]);
     }
     cudaFree(ctx->reduce_scratch);
@@ -821,7 +1069,8 @@ int tp_plan_create(tp_ctx* ctx, int n_modes, const tp_u64* L, const tp_u64* K, i
       for (size_t d = 0; d < p->depth_cap.size(); ++d) p->depth_buf[d] = device_alloc(p->depth_cap[d]);
 
       // core chain in its cheapest order; ping-pong buffers hold its largest partial product
-      p->core_order = cheapest_chain_order(p->spec, &p->core_macs_executed);
+      plan_visit_order(p);
+      p->core_order = cheapest_chain_order(p->spec, p->leaf_rank, &p->core_macs_executed);
       card = partial_cardinality(p->spec, 0);
       for (int i = 0; i + 1 < n_modes; ++i) {
         const int m = p->core_order[i];
@@ -971,9 +1220,23 @@ int tp_plan_sweep(tp_ctx* ctx, tp_plan* p, const tp_tensor* t, tp_sweep_stats* s
         for (int m = 0; m < p->n; ++m) plan_refresh_fragments(ctx, p, m, p->cur[m]);
         s.close();
       }
+      p->leaves_in_flight = 0;
+      p->pending.clear();
       jacobi_walk(ctx, p, 0, t->data, dims, 0);
-      if (p->overlap_evd) plan_join_leaves(ctx, p);
-      plan_core(ctx, p, t->data, p->fresh);
+      plan_core(ctx, p, t->data, p->fresh, p->overlap_evd);  // waits for each new factor just before using it
+      // leaves solved by subspace iteration are accepted only with their residual certificate; a rejected leaf is
+      // redone with the full eigen-solve on its (intact) Gram matrix, and the core with it
+      const std::vector<int> rejected = verify_fast_leaves(ctx, p);
+      p->fast_rejected = static_cast<int>(rejected.size());
+      if (!rejected.empty()) {
+        for (int m : rejected) {
+          Span evd(ctx, p, kEvd, -1);
+          leaf_solve(ctx, p->leaf[m], static_cast<long long>(p->spec.L[m]), static_cast<int>(p->spec.K[m]),
+                     p->fresh[m], -1);
+          evd.close();
+        }
+        plan_core(ctx, p, t->data, p->fresh);
+      }
       std::swap(p->cur, p->fresh);
     } else {
       {
@@ -1017,8 +1280,24 @@ int tp_plan_set_option(tp_ctx* ctx, tp_plan* p, int option, int value) {
     if (!p) raise(TP_ERR_BAD_ARGUMENT, "null plan");
     if (option == TP_OPT_OVERLAP_EVD)
       p->overlap_evd = value != 0;
+    else if (option == TP_OPT_FAST_EVD)
+      p->fast_evd = value != 0;
     else
       raise(TP_ERR_BAD_ARGUMENT, "unknown plan option");
+  });
+}
+
+int tp_plan_last_evd_info(tp_ctx* ctx, tp_plan* p, int* fast_eligible, int* rejected) {
+  return guarded([&] {
+    (void)ctx;
+    if (!p) raise(TP_ERR_BAD_ARGUMENT, "null plan");
+    int eligible = 0;
+    for (int m = 0; m < p->n; ++m)
+      if (p->fast_evd && p->sweep_kind == TP_SWEEP_JACOBI && p->leaf[m].failures < 2 &&
+          subspace_eligible(static_cast<long long>(p->spec.L[m]), static_cast<int>(p->spec.K[m])))
+        ++eligible;
+    if (fast_eligible) *fast_eligible = eligible;
+    if (rejected) *rejected = p->fast_rejected;
   });
 }
 
@@ -1240,7 +1519,8 @@ int tp_dev_leaf_solve(tp_ctx* ctx, double* gram, size_t rows, int k, double* fac
     TPB_SOLVER(cusolverDnDsyevd(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, static_cast<int>(rows),
                                 gram, static_cast<int>(rows), s.w, s.work, s.lwork, info));
     ctx->library_calls += 1;
-    TPB_CUDA(launch_select_basis(ctx->stream, gram, s.w, static_cast<int>(rows), k, factor, flag));
+    TPB_CUDA(launch_select_basis(ctx->stream, gram, s.w, static_cast<int>(rows), static_cast<int>(rows), k, factor,
+                                 flag));
     ctx->own_kernels += 1;
   });
 }

@@ -196,7 +196,8 @@ GramLayout gram_layout(long long outer, long long rows, long long inner, int sm_
   g.tiles = static_cast<int>((rows + kTile - 1) / kTile);
   g.chunks = inner == 1 ? (outer + kKC - 1) / kKC : outer * ((inner + kKC - 1) / kKC);
   const long long lower_tiles = static_cast<long long>(g.tiles) * (g.tiles + 1) / 2;
-  long long want = (2LL * sm_count + lower_tiles - 1) / lower_tiles;           // fill the machine twice
+  // two CTAs fit per SM; aim for at least four full waves so that the last, partial wave costs little
+  long long want = (8LL * sm_count + lower_tiles - 1) / lower_tiles;
   want = std::min(want, std::max(1LL, g.chunks / 8));                          // at least 8 chunks per split
   want = std::max(1LL, std::min(want, 512LL));
   const long long per = (g.chunks + want - 1) / want;

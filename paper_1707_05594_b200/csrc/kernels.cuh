@@ -57,9 +57,14 @@ cudaError_t launch_assemble_mode(cudaStream_t stream, double* dst, long long out
                                  long long inner, const double* src, long long l0, long long count);
 // y[i] = beta * y[i] + alpha * x[i]
 cudaError_t launch_axpby(cudaStream_t stream, double* y, double beta, double alpha, const double* x, size_t n);
-// Top-k eigenvectors from an ascending syevd result (vectors column-major rows x rows, eigenvalues w) with the
-// reference's sign rule and degenerate-gap flag (hooi.hpp:60-74).  factor is rows x k column-major; *flag is OR-ed.
-cudaError_t launch_select_basis(cudaStream_t stream, const double* vectors, const double* w, int rows, int k,
-                                double* factor, int* flag);
+// Top-k eigenvectors from an ascending eigen-solve result (vectors column-major rows x ncols, values w[ncols]) with
+// the reference's sign rule and degenerate-gap flag (hooi.hpp:60-74).  factor is rows x k column-major; *flag is OR-ed.
+cudaError_t launch_select_basis(cudaStream_t stream, const double* vectors, const double* w, int rows, int ncols,
+                                int k, double* factor, int* flag);
+// out[i] = deterministic pseudo-random value in [-0.5, 0.5)
+cudaError_t launch_fill_pseudo_random(cudaStream_t stream, double* out, size_t n, unsigned long long salt);
+// *verdict |= 1 unless every one of the k largest Ritz pairs has ||(ZV)_j - theta_j X_j|| <= tol * theta_max
+cudaError_t launch_ritz_residuals(cudaStream_t stream, const double* zv, const double* x, const double* theta,
+                                  int rows, int ncols, int k, double tol, int* verdict);
 
 }  // namespace tpb

@@ -59,10 +59,10 @@ __global__ void __launch_bounds__(kReduceThreads) final_sum(const double* __rest
 // largest-magnitude entry (first on ties) is positive (reference hooi.hpp:60-68).  Block 0 also evaluates the
 // spectral-gap flag (hooi.hpp:70-74).
 __global__ void __launch_bounds__(256) select_basis_kernel(const double* __restrict__ vectors,
-                                                           const double* __restrict__ w, int rows, int k,
+                                                           const double* __restrict__ w, int rows, int ncols, int k,
                                                            double* __restrict__ factor, int* __restrict__ flag) {
   const int j = blockIdx.x;
-  const double* col = vectors + static_cast<long long>(rows - 1 - j) * rows;
+  const double* col = vectors + static_cast<long long>(ncols - 1 - j) * rows;
   __shared__ double best_abs[256];
   __shared__ int best_idx[256];
   double ba = -1.0;
@@ -91,9 +91,9 @@ __global__ void __launch_bounds__(256) select_basis_kernel(const double* __restr
   const double sign = col[best_idx[0]] < 0.0 ? -1.0 : 1.0;
   double* dst = factor + static_cast<long long>(j) * rows;
   for (int i = threadIdx.x; i < rows; i += blockDim.x) dst[i] = sign * col[i];
-  if (j == 0 && threadIdx.x == 0 && k < rows) {
-    const double top = fmax(w[rows - 1], 0.0);
-    const double gap = w[rows - k] - w[rows - 1 - k];
+  if (j == 0 && threadIdx.x == 0 && k < ncols) {
+    const double top = fmax(w[ncols - 1], 0.0);
+    const double gap = w[ncols - k] - w[ncols - 1 - k];
     if (gap <= 1e-10 * fmax(top, 1e-300)) atomicOr(flag, 1);
   }
 }
@@ -103,6 +103,41 @@ __global__ void __launch_bounds__(256) axpby_kernel(double* __restrict__ y, doub
   const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n; i += stride)
     y[i] = fma(alpha, x[i], beta * y[i]);
+}
+
+// Deterministic filler for the oversampling columns of the subspace-iteration start block (splitmix64 hash of the
+// element index; only the span matters and it is re-orthonormalised before use).
+__global__ void __launch_bounds__(256) fill_pseudo_random_kernel(double* __restrict__ out, size_t n,
+                                                                 unsigned long long salt) {
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
+    unsigned long long z = (i + 1) * 0x9E3779B97F4A7C15ull + salt;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    out[i] = static_cast<double>(z >> 11) * (1.0 / 9007199254740992.0) - 0.5;
+  }
+}
+
+// One block per kept Ritz pair j (the j-th largest): r = (Z V)_col - theta * X_col over `rows` entries.
+// verdict[0] |= 1 when ||r|| > tol * theta_max (not converged).  Columns are stored ascending, as syevd returns them.
+__global__ void __launch_bounds__(256) ritz_residual_kernel(const double* __restrict__ zv, const double* __restrict__ x,
+                                                            const double* __restrict__ theta, int rows, int ncols,
+                                                            double tol, int* __restrict__ verdict) {
+  const int c = ncols - 1 - blockIdx.x;
+  const double th = theta[c];
+  const double* a = zv + static_cast<long long>(c) * rows;
+  const double* b = x + static_cast<long long>(c) * rows;
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < rows; i += blockDim.x) {
+    const double r = a[i] - th * b[i];
+    acc = fma(r, r, acc);
+  }
+  const double total = block_sum(acc);
+  if (threadIdx.x == 0) {
+    const double top = fmax(fabs(theta[ncols - 1]), 1e-300);
+    if (!(sqrt(total) <= tol * top)) atomicOr(verdict, 1);
+  }
 }
 
 struct SlotList {
@@ -168,9 +203,20 @@ cudaError_t launch_diff_sum_squares(cudaStream_t stream, const double* x, const 
   return cudaGetLastError();
 }
 
-cudaError_t launch_select_basis(cudaStream_t stream, const double* vectors, const double* w, int rows, int k,
-                                double* factor, int* flag) {
-  select_basis_kernel<<<k, 256, 0, stream>>>(vectors, w, rows, k, factor, flag);
+cudaError_t launch_select_basis(cudaStream_t stream, const double* vectors, const double* w, int rows, int ncols,
+                                int k, double* factor, int* flag) {
+  select_basis_kernel<<<k, 256, 0, stream>>>(vectors, w, rows, ncols, k, factor, flag);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_pseudo_random(cudaStream_t stream, double* out, size_t n, unsigned long long salt) {
+  fill_pseudo_random_kernel<<<kReduceBlocks, 256, 0, stream>>>(out, n, salt);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ritz_residuals(cudaStream_t stream, const double* zv, const double* x, const double* theta,
+                                  int rows, int ncols, int k, double tol, int* verdict) {
+  ritz_residual_kernel<<<k, 256, 0, stream>>>(zv, x, theta, rows, ncols, tol, verdict);
   return cudaGetLastError();
 }
 

@@ -214,6 +214,16 @@ class HooiPlan:
         """Jacobi only: eigen-solves on side streams beside the tree (default) or everything serial on one stream."""
         check(lib.tp_plan_set_option(self.ctx._h, self._h, 1, 1 if on else 0))
 
+    def set_fast_evd(self, on: bool):
+        """Top-k subspace-iteration eigen-solve on eligible Jacobi leaves (verified; full solve otherwise)."""
+        check(lib.tp_plan_set_option(self.ctx._h, self._h, 2, 1 if on else 0))
+
+    def evd_info(self):
+        """(leaves eligible for the fast eigen-solve, leaves the last sweep redid with the full solve)."""
+        a, b = ctypes.c_int(), ctypes.c_int()
+        check(lib.tp_plan_last_evd_info(self.ctx._h, self._h, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
     def _factor_ptrs(self, arrays):
         return (dbl_p * len(arrays))(*[a.ctypes.data_as(dbl_p) for a in arrays])
 

@@ -302,3 +302,64 @@ def test_sweep_parity_config1_full(ctx):
     # converged to the noise floor sigma sqrt(|T|) / ||T|| (||X|| = ||G|| ~ sqrt(prod K))
     floor = cfg.sigma * np.sqrt(np.prod(cfg.L)) / np.sqrt(np.prod(cfg.K) + cfg.sigma ** 2 * np.prod(cfg.L))
     assert err_gpu < 1.05 * floor
+
+
+def test_fast_eigensolve_is_certified_and_matches(ctx):
+    """Leaves with L_n >= 256 take the top-k subspace-iteration path; its residual certificate must hold on the
+    low-rank-plus-noise workload, and the factors must still be the oracle's (full eigen-decomposition)."""
+    cfg = W.scaled_config(5, [768, 720, 704], [24, 20, 16], 3)
+    spec = cfg.spec
+    tree = P.optimal_tree(spec).tree
+    t = W.build_tensor_host(cfg)
+    f0 = W.start_factors(cfg)
+    dt = E.DeviceTensor.upload(ctx, t)
+    plan = E.HooiPlan(ctx, spec, tree, "jacobi")
+    plan.set_factors(f0)
+    of = [f.copy() for f in f0]
+    rejected = []
+    for _ in range(cfg.iterations):
+        st = plan.sweep(dt)
+        ocore, of = ho.hooi_sweep(t, spec.L, spec.K, of, otree(tree), "jacobi")
+        eligible, rej = plan.evd_info()
+        rejected.append(rej)
+        assert not st.degenerate
+        angle = max(ho.sin_largest_principal_angle(a, b) for a, b in zip(plan.get_factors(), of))
+        gn, on = plan.core_norm(), np.sqrt(np.sum(ocore * ocore))
+        assert angle < 1e-9 and abs(gn - on) <= 1e-10 * on
+        # individual vectors too (same sign rule), not just the subspace
+        for a, b in zip(plan.get_factors(), of):
+            assert np.max(np.abs(a - b)) < 1e-7
+    assert eligible == 3
+    assert rejected[-1] == 0                      # warm-started sweeps are served by the fast path
+    # the same sweeps with the fast path off give the same factors to rounding
+    plan.set_fast_evd(False)
+    plan.set_factors(f0)
+    for _ in range(cfg.iterations):
+        plan.sweep(dt)
+    assert plan.evd_info()[0] == 0
+    angle = max(ho.sin_largest_principal_angle(a, b) for a, b in zip(plan.get_factors(), of))
+    assert angle < 1e-9
+    plan.close()
+    dt.free()
+
+
+def test_fast_eigensolve_falls_back_without_a_gap(ctx):
+    """A plain random tensor has no spectral gap: the certificate fails, the full solve takes over, parity holds."""
+    L, K = [800, 24, 20], [12, 5, 4]
+    spec = P.ProblemSpec(L, K)
+    tree = P.optimal_tree(spec).tree
+    t = hostgen.random_tensor(L, 99)
+    f0 = hostgen.random_orthonormal_factors(L, K, 98)
+    dt = E.DeviceTensor.upload(ctx, t)
+    plan = E.HooiPlan(ctx, spec, tree, "jacobi")
+    plan.set_factors(f0)
+    of = [f.copy() for f in f0]
+    for it in range(3):
+        plan.sweep(dt)
+        ocore, of = ho.hooi_sweep(t, spec.L, spec.K, of, otree(tree), "jacobi")
+        angle = max(ho.sin_largest_principal_angle(a, b) for a, b in zip(plan.get_factors(), of))
+        assert angle < 1e-9, (it, angle, plan.evd_info())
+        gn, on = plan.core_norm(), np.sqrt(np.sum(ocore * ocore))
+        assert abs(gn - on) <= 1e-10 * on
+    plan.close()
+    dt.free()
