@@ -17,6 +17,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -463,13 +465,17 @@ cudaEvent_t next_event(tp_plan* p) {
 struct Span {
   tp_plan* plan;
   cudaStream_t stream;
+  cudaEvent_t end;
+  // both events are reserved up front so that spans may nest (an eigen-solve queued inside the core span)
   Span(tp_ctx* c, tp_plan* p, int phase, int node = -1, int aux = -1)
       : plan(p), stream(aux < 0 ? c->stream : c->aux[aux]) {
     plan->event_phase.push_back(phase);
     plan->event_node.push_back(node);
-    TPB_CUDA(cudaEventRecord(next_event(plan), stream));
+    cudaEvent_t begin = next_event(plan);
+    end = next_event(plan);
+    TPB_CUDA(cudaEventRecord(begin, stream));
   }
-  void close() { TPB_CUDA(cudaEventRecord(next_event(plan), stream)); }
+  void close() { TPB_CUDA(cudaEventRecord(end, stream)); }
 };
 
 void plan_refresh_fragments(tp_ctx* ctx, tp_plan* p, int mode, const double* factor) {
@@ -708,8 +714,12 @@ void plan_collect_timing(tp_ctx* ctx, tp_plan* p) {
     if (node >= 0) (p->event_phase[i] == kEvd ? p->node_evd_ms : p->node_ms)[node] += ms;
   }
   if (!p->event_phase.empty()) {
+    // first span's begin to the end of the last main-stream span (the core chain closes every sweep)
+    size_t last = 0;
+    for (size_t i = 0; i < p->event_phase.size(); ++i)
+      if (p->event_phase[i] != kEvd) last = i;
     float ms = 0.f;
-    TPB_CUDA(cudaEventElapsedTime(&ms, p->events[0], p->events[p->events_used - 1]));
+    TPB_CUDA(cudaEventElapsedTime(&ms, p->events[0], p->events[2 * last + 1]));
     t.total_ms = ms;
   }
   p->timing = t;

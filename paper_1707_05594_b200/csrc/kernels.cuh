@@ -13,7 +13,8 @@ struct TtmFragmentLayout {
   int k_blocks = 1;  // ceil(new_len / (8 kt))
   int kc = 16;       // contraction steps per pipeline stage
   int n_chunks = 1;  // ceil(len / kc)
-  size_t doubles = 0;
+  size_t layout_doubles = 0;  // one fragment-ordered copy
+  size_t doubles = 0;         // the buffer: two copies (consecutive-row and interleaved-row k order)
 };
 
 int ttm_pick_kt(long long new_len);
@@ -30,6 +31,14 @@ constexpr int kMaxTtmDest = 16;
 cudaError_t launch_ttm(cudaStream_t stream, const double* x, long long outer, long long len, long long inner,
                        const double* mfrag, const TtmFragmentLayout& f, long long new_len, double* z, int sm_count,
                        int n_dest = 1, const long long* dest_cuts = nullptr);
+
+// Warp-specialised TMA variant (ttm_tma_kernels.cu): used by launch_ttm for 16-byte-aligned, even extents with enough
+// columns to fill the machine.  mfrag must be the copy matching the mode (interleaved rows when inner > 1).
+bool ttm_tma_eligible(const double* x, long long outer, long long len, long long inner, const double* z, int kt,
+                      int k_blocks, int sm_count);
+cudaError_t launch_ttm_tma(cudaStream_t stream, const double* x, long long outer, long long len, long long inner,
+                           const double* mfrag, const TtmFragmentLayout& f, long long new_len, double* z,
+                           int sm_count, int n_dest, const long long* dest_cuts);
 
 // ---- Gram of the mode-n unfolding, read in place (gram_kernels.cu) -----------
 struct GramLayout {

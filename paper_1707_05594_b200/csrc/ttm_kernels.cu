@@ -28,6 +28,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -327,6 +328,9 @@ __global__ void __launch_bounds__(kThreads, (KT * NT <= 20) ? 2 : 1) ttm_dmma_ke
 
 // factor (rows new_len x cols len, element (k,l) at m[k*row_stride + l*col_stride]) -> fragment order:
 // [k block][chunk][step][m-tile i][lane]  holding  M(kb*8KT + 8i + lane/4, chunk*KC + 4 step + lane%4), zero padded.
+// Two copies are written: out[0 .. total) with the k-indices of a step on consecutive rows (l = 4 step + lane%4; the
+// cp.async kernel and the inner == 1 TMA kernel), and out[total .. 2 total) with them interleaved inside 8-row groups
+// (steps 2g / 2g+1 take rows 8g + {0,2,4,6} / {1,3,5,7}; the inner > 1 TMA kernel, see ttm_tma_kernels.cu).
 __global__ void prep_fragments_kernel(const double* __restrict__ m, long long row_stride, long long col_stride,
                                       long long new_len, long long len, int kt, long long steps_padded,
                                       long long total, double* __restrict__ out) {
@@ -340,6 +344,8 @@ __global__ void prep_fragments_kernel(const double* __restrict__ m, long long ro
   const long long k = kb * (8LL * kt) + 8 * i + (lane >> 2);
   const long long l = 4 * step + (lane & 3);
   out[e] = (k < new_len && l < len) ? m[k * row_stride + l * col_stride] : 0.0;
+  const long long li = 8 * (step >> 1) + 2 * (lane & 3) + (step & 1);
+  out[total + e] = (k < new_len && li < len) ? m[k * row_stride + li * col_stride] : 0.0;
 }
 
 template <int KT, int NT, int KC, int STAGES, bool LAST>
@@ -395,13 +401,14 @@ TtmFragmentLayout ttm_fragment_layout(long long new_len, long long len) {
   f.k_blocks = static_cast<int>((new_len + 8LL * f.kt - 1) / (8LL * f.kt));
   f.kc = 16;
   f.n_chunks = static_cast<int>((len + f.kc - 1) / f.kc);
-  f.doubles = static_cast<size_t>(f.k_blocks) * f.n_chunks * (f.kc / 4) * f.kt * 32;
+  f.layout_doubles = static_cast<size_t>(f.k_blocks) * f.n_chunks * (f.kc / 4) * f.kt * 32;
+  f.doubles = 2 * f.layout_doubles;  // consecutive-row copy + interleaved-row copy
   return f;
 }
 
 cudaError_t prep_factor_fragments(cudaStream_t stream, const double* m, long long row_stride, long long col_stride,
                                   long long new_len, long long len, const TtmFragmentLayout& f, double* out) {
-  const long long total = static_cast<long long>(f.doubles);
+  const long long total = static_cast<long long>(f.layout_doubles);
   const long long steps_padded = static_cast<long long>(f.n_chunks) * (f.kc / 4);
   const int threads = 256;
   const unsigned blocks = static_cast<unsigned>((total + threads - 1) / threads);
@@ -413,6 +420,18 @@ cudaError_t prep_factor_fragments(cudaStream_t stream, const double* m, long lon
 cudaError_t launch_ttm(cudaStream_t stream, const double* x, long long outer, long long len, long long inner,
                        const double* mfrag, const TtmFragmentLayout& f, long long new_len, double* z, int sm_count,
                        int n_dest, const long long* dest_cuts) {
+  static const bool tma_off = [] {
+    const char* v = std::getenv("TPB_DISABLE_TMA");
+    return v && v[0] == '1';
+  }();
+  // TPB_DISABLE_TMA=1 (read once) / TPB_DISABLE_TMA_NOW (read per launch): force the cp.async kernel (A/B tests)
+  if (!tma_off && !std::getenv("TPB_DISABLE_TMA_NOW") && ttm_tma_eligible(x, outer, len, inner, z, f.kt, f.k_blocks, sm_count)) {
+    bool chunks_aligned = true;
+    for (int d = 0; dest_cuts && d < n_dest; ++d) chunks_aligned = chunks_aligned && ((outer * dest_cuts[d] * inner) % 2 == 0);
+    if (chunks_aligned)
+      return launch_ttm_tma(stream, x, outer, len, inner, inner == 1 ? mfrag : mfrag + f.layout_doubles, f, new_len, z,
+                            sm_count, n_dest, dest_cuts);
+  }
   TtmParams p;
   if (n_dest < 1 || n_dest > kMaxTtmDest) return cudaErrorInvalidValue;
   p.n_dest = n_dest;

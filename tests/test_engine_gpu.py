@@ -422,3 +422,58 @@ def test_config5_full_size_properties(ctx):
     finally:
         from paper_1707_05594_b200._lib import lib
         lib.tp_host_free(handle)
+
+
+# shapes with enough columns to take the warp-specialised TMA kernel (>= 148 wide tiles), awkward extents included
+TMA_SHAPES = [
+    ((3, 50, 40000), 1, 5), ((50, 40002), 0, 7), ((40010, 50), 1, 20), ((130, 18, 300), 1, 13),
+    ((2, 770, 20000), 1, 24), ((96, 90, 704), 0, 24), ((24, 720, 704), 1, 20), ((24, 20, 704, 60), 2, 16),
+    ((2500, 16, 18), 1, 8), ((38000, 34), 1, 10), ((38001, 34), 1, 33), ((5, 36, 9000), 1, 100),
+    ((3, 40, 8, 1250), 1, 41), ((4, 17, 10000), 1, 104), ((4, 18, 10000), 1, 110), ((60000, 20), 1, 3),
+    # several tiles per persistent CTA
+    ((100000, 64), 1, 16), ((3, 64, 70000), 1, 10), ((200000, 32), 1, 5), ((20, 48, 30000), 1, 13), ((300000, 20), 1, 24),
+    ((7, 33, 50000), 1, 100),
+]
+
+
+@pytest.mark.parametrize("dims,mode,new_len", TMA_SHAPES)
+def test_ttm_tma_path_matches_oracle(ctx, dims, mode, new_len):
+    seed = (sum(dims) * 17 + mode * 5 + new_len) % 10000
+    t = hostgen.random_tensor(dims, seed)
+    m = hostgen.random_tensor([new_len, dims[mode]], seed + 1)
+    got = E.ttm(t, m, mode, ctx=ctx)
+    want = ho.ttm(t, m, mode)
+    bad = np.argwhere(np.abs(got - want) > 64 * EPS * np.sqrt(dims[mode]) * np.max(np.abs(m)) * np.max(np.abs(t)))
+    assert bad.size == 0, (len(bad), bad[:5].tolist(), bad[-3:].tolist())
+
+
+def test_tma_kernel_is_stable_under_concurrent_kernels(ctx):
+    """Regression: the warp-specialised TMA kernel reads its stages with generic-proxy loads; without a
+    fence.proxy.async before a stage is handed back, a TMA refill could overtake those reads as soon as other
+    kernels shared the SMs (stale 128-byte box rows).  Run it beside unrelated fill kernels and compare with the
+    cp.async kernel's result."""
+    import os
+    import torch
+    from paper_1707_05594_b200 import distributed as D
+    ops = D.GpuOps(ctx)
+    big = torch.empty(32 << 20, dtype=torch.float64, device="cuda")
+    side = torch.cuda.Stream()
+    for dims, k in (((276480, 352), 16), ((384, 360, 352), 20)):
+        x = hostgen.random_tensor(dims, 1)
+        f = np.asfortranarray(hostgen.random_tensor([k, dims[1]], 2).T).reshape(-1, order="F")
+        xb, fb = ops.from_host(x), ops.from_host(f)
+        os.environ["TPB_DISABLE_TMA_NOW"] = "1"
+        try:
+            ref = ops.to_host(ops.ttm_partial(xb, list(dims), 1, fb, dims[1], 0, k, [0, k]))
+        finally:
+            del os.environ["TPB_DISABLE_TMA_NOW"]
+        for _ in range(5):
+            ctx.synchronize()
+            torch.cuda.synchronize()
+            z = ops.ttm_partial(xb, list(dims), 1, fb, dims[1], 0, k, [0, k])
+            with torch.cuda.stream(side):
+                for _ in range(30):
+                    big.zero_()
+            got = ops.to_host(z)
+            torch.cuda.synchronize()
+            assert np.max(np.abs(got - ref)) <= 64 * EPS * np.sqrt(dims[1]) * np.max(np.abs(f)) * np.max(np.abs(x))
