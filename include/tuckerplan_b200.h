@@ -269,11 +269,20 @@ int tp_dev_gram(tp_ctx* ctx, const double* y, size_t outer, size_t rows, size_t 
 /* top-k eigenvectors of gram (destroyed) with the reference's sign rule into factor (rows x k column-major);
  * *flag (device int) is OR-ed with the degenerate-gap flag; *info (device int) receives the solver status. */
 int tp_dev_leaf_solve(tp_ctx* ctx, double* gram, size_t rows, int k, double* factor, int* flag, int* info);
+/* Same, warm-started: `start` (rows x k column-major, e.g. the previous factor; may be NULL) seeds the certified top-k
+ * subspace iteration (see TP_OPT_FAST_EVD); the certificate is checked before returning (one stream synchronisation)
+ * and the full eigen-solve takes over when it fails.  gram is left intact by the fast path, destroyed by the fallback.
+ * *used_fast (host, may be NULL) reports which path produced the factor. */
+int tp_dev_leaf_solve_warm(tp_ctx* ctx, double* gram, size_t rows, int k, const double* start, double* factor,
+                           int* flag, int* info, int* used_fast);
 /* *out (device double) = sum x[i]^2 */
 int tp_dev_sum_squares(tp_ctx* ctx, const double* x, size_t count, double* out);
 
 /* By-value hooi_sweep (hooi.hpp:189-191): host tensor + host factors in, host factors + core out; uploads, runs,
  * downloads.  This is the call the reference-facing C++ wrapper makes. */
+/* Consecutive calls with the same shape, ranks, tree and schedule reuse the device tensor, plan and workspaces kept
+ * in the context (tp_ctx_release_cache frees them early; tp_ctx_destroy does too). */
+int tp_ctx_release_cache(tp_ctx* ctx);
 int tp_hooi_sweep_host(tp_ctx* ctx, int n_modes, const size_t* dims, const double* tensor, const tp_u64* K,
                        const double* const* factors_in, int n_nodes, const int* kind, const int* mode,
                        const int* parent, int sweep_kind, double* const* factors_out, double* core_out,

@@ -67,6 +67,11 @@ struct tp_ctx {
   // side streams for the eigen-solves of a Jacobi sweep: the leaves are independent of each other and of the
   // remaining tree TTMs, and an eigen-solve is latency-bound, so it runs beside the TTM kernels
   void* dev_scratch = nullptr;       // LeafScratch of the tp_dev_* entry points
+  // by-value hooi_sweep calls in a loop (the reference CLI's pattern) keep their device tensor and plan between
+  // calls as long as shape, ranks, tree and schedule repeat; only the tensor and factor bytes move again
+  std::vector<long long> host_call_key;
+  tp_plan* host_call_plan = nullptr;
+  tp_tensor* host_call_tensor = nullptr;
   static constexpr int kAux = 4;
   cudaStream_t aux[kAux] = {nullptr, nullptr, nullptr, nullptr};
   cusolverDnHandle_t aux_solver[kAux] = {nullptr, nullptr, nullptr, nullptr};
@@ -195,6 +200,7 @@ struct LeafScratch {
   double* small_work = nullptr;
   int small_lwork = 0;
   int* verdict = nullptr;      // [0] |= 1: a kept Ritz pair missed the residual bound; [1]: potrf/syevd info
+  long long fast_rows = 0;     // rows the iteration buffers were sized for (tp_dev_leaf_solve_warm only)
   int failures = 0;            // consecutive sweeps in which the fast path was rejected
   bool fast_used = false;      // this sweep's factor came from the fast path (verdict still to be checked)
 
@@ -328,8 +334,8 @@ void cholqr2(cublasHandle_t blas, cusolverDnHandle_t solver, LeafScratch& s, int
 }
 
 // Enqueues the whole fast solve on the leaf's stream; the verdict is read by the caller at the end of the sweep.
-void leaf_solve_subspace(tp_ctx* ctx, LeafScratch& s, long long rows_ll, int k, const double* start,
-                         double* factor_out, int aux) {
+void leaf_solve_subspace(tp_ctx* ctx, LeafScratch& s, const double* gram, long long rows_ll, int k,
+                         const double* start, double* factor_out, int aux) {
   cusolverDnHandle_t solver = aux < 0 ? ctx->solver : ctx->aux_solver[aux];
   cublasHandle_t blas = aux < 0 ? ctx->blas : ctx->aux_blas[aux];
   cudaStream_t stream = aux < 0 ? ctx->stream : ctx->aux[aux];
@@ -343,13 +349,13 @@ void leaf_solve_subspace(tp_ctx* ctx, LeafScratch& s, long long rows_ll, int k, 
   cholqr2(blas, solver, s, rows, b, s.q);
   for (int round = 0; round < kSubspaceRounds; ++round) {
     for (int step = 0; step < kSubspacePowerSteps; ++step) {
-      TPB_BLAS(cublasDgemm(blas, CUBLAS_OP_N, CUBLAS_OP_N, rows, b, rows, &one, s.gram, rows, s.q, rows, &zero, s.z,
+      TPB_BLAS(cublasDgemm(blas, CUBLAS_OP_N, CUBLAS_OP_N, rows, b, rows, &one, gram, rows, s.q, rows, &zero, s.z,
                            rows));
       std::swap(s.q, s.z);
       cholqr2(blas, solver, s, rows, b, s.q);
     }
     // Rayleigh-Ritz on span(Q): H = Q^T G Q, H = V Theta V^T (ascending), X = Q V
-    TPB_BLAS(cublasDgemm(blas, CUBLAS_OP_N, CUBLAS_OP_N, rows, b, rows, &one, s.gram, rows, s.q, rows, &zero, s.z,
+    TPB_BLAS(cublasDgemm(blas, CUBLAS_OP_N, CUBLAS_OP_N, rows, b, rows, &one, gram, rows, s.q, rows, &zero, s.z,
                          rows));
     TPB_BLAS(cublasDgemm(blas, CUBLAS_OP_T, CUBLAS_OP_N, b, b, rows, &one, s.q, rows, s.z, rows, &zero, s.h, b));
     TPB_SOLVER(cusolverDnDsyevd(solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, b, s.h, b, s.theta,
@@ -510,7 +516,7 @@ void plan_leaf_solve(tp_ctx* ctx, tp_plan* p, int mode, int node, double* dst, b
   slot.fast_used = false;
   if (p->fast_evd && p->sweep_kind == TP_SWEEP_JACOBI && slot.failures < 2 && subspace_eligible(rows, k)) {
     subspace_reserve(ctx, slot, rows, k);
-    leaf_solve_subspace(ctx, slot, rows, k, p->cur[mode], dst, aux);
+    leaf_solve_subspace(ctx, slot, slot.gram, rows, k, p->cur[mode], dst, aux);
   } else {
     leaf_solve(ctx, slot, rows, k, dst, aux);
   }
@@ -728,6 +734,14 @@ void plan_collect_timing(tp_ctx* ctx, tp_plan* p) {
 }  // namespace
 }  // namespace tpb
 
+static void release_host_call_cache(tp_ctx* ctx) {
+  if (ctx->host_call_plan) tp_plan_destroy(ctx, ctx->host_call_plan);
+  if (ctx->host_call_tensor) tp_tensor_free(ctx, ctx->host_call_tensor);
+  ctx->host_call_plan = nullptr;
+  ctx->host_call_tensor = nullptr;
+  ctx->host_call_key.clear();
+}
+
 extern "C" {
 
 int tp_ctx_create(int device, tp_ctx** out) {
@@ -787,6 +801,7 @@ int tp_ctx_destroy(tp_ctx* ctx) {
     }
     cudaFree(ctx->reduce_scratch);
     cudaFree(ctx->frag_scratch);
+    release_host_call_cache(ctx);
     if (ctx->dev_scratch) {
       static_cast<LeafScratch*>(ctx->dev_scratch)->release();
       delete static_cast<LeafScratch*>(ctx->dev_scratch);
@@ -1535,12 +1550,71 @@ int tp_dev_leaf_solve(tp_ctx* ctx, double* gram, size_t rows, int k, double* fac
   });
 }
 
+int tp_dev_leaf_solve_warm(tp_ctx* ctx, double* gram, size_t rows, int k, const double* start, double* factor,
+                           int* flag, int* info, int* used_fast) {
+  return guarded([&] {
+    bind(ctx);
+    if (!gram || !factor || !flag || !info) raise(TP_ERR_BAD_ARGUMENT, "null pointer");
+    check_leaf_args(static_cast<long long>(rows), 1, k);
+    if (used_fast) *used_fast = 0;
+    LeafScratch& s = dev_scratch(ctx);
+    if (start && subspace_eligible(static_cast<long long>(rows), k)) {
+      leaf_scratch_reserve(ctx, s, 1, 0);
+      if (s.block != k + kSubspaceOversample) {  // a different block size: rebuild the iteration buffers
+        cudaFree(s.q); cudaFree(s.z); cudaFree(s.x); cudaFree(s.h); cudaFree(s.theta); cudaFree(s.small_work);
+        cudaFree(s.verdict);
+        s.q = s.z = s.x = s.h = s.theta = s.small_work = nullptr;
+        s.verdict = nullptr;
+        s.block = 0;
+      }
+      if (s.block == 0 || static_cast<long long>(rows) > s.fast_rows) {
+        if (s.block) {
+          cudaFree(s.q); cudaFree(s.z); cudaFree(s.x); cudaFree(s.h); cudaFree(s.theta); cudaFree(s.small_work);
+          cudaFree(s.verdict);
+          s.block = 0;
+        }
+        subspace_reserve(ctx, s, static_cast<long long>(rows), k);
+        s.fast_rows = static_cast<long long>(rows);
+      }
+      int* const saved_flag = s.flag;
+      s.flag = flag;  // the caller's degenerate flag
+      leaf_solve_subspace(ctx, s, gram, static_cast<long long>(rows), k, start, factor, -1);
+      s.flag = saved_flag;
+      s.fast_used = false;
+      int host[3] = {0, 0, 0};
+      TPB_CUDA(cudaMemcpyAsync(&host[0], s.verdict, 2 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+      TPB_CUDA(cudaMemcpyAsync(&host[2], flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+      TPB_CUDA(cudaStreamSynchronize(ctx->stream));
+      if (host[0] == 0 && host[1] == 0 && host[2] == 0) {
+        TPB_CUDA(cudaMemsetAsync(info, 0, sizeof(int), ctx->stream));
+        if (used_fast) *used_fast = 1;
+        return;
+      }
+      TPB_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));  // let the exact spectrum decide
+    }
+    leaf_scratch_reserve(ctx, s, static_cast<long long>(rows), 0);
+    TPB_SOLVER(cusolverDnDsyevd(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, static_cast<int>(rows),
+                                gram, static_cast<int>(rows), s.w, s.work, s.lwork, info));
+    ctx->library_calls += 1;
+    TPB_CUDA(launch_select_basis(ctx->stream, gram, s.w, static_cast<int>(rows), static_cast<int>(rows), k, factor,
+                                 flag));
+    ctx->own_kernels += 1;
+  });
+}
+
 int tp_dev_sum_squares(tp_ctx* ctx, const double* x, size_t count, double* out) {
   return guarded([&] {
     bind(ctx);
     if (!x || !out) raise(TP_ERR_BAD_ARGUMENT, "null pointer");
     TPB_CUDA(launch_sum_squares(ctx->stream, x, count, ctx->reduce_scratch, out));
     ctx->own_kernels += 2;
+  });
+}
+
+int tp_ctx_release_cache(tp_ctx* ctx) {
+  return guarded([&] {
+    bind(ctx);
+    release_host_call_cache(ctx);
   });
 }
 
@@ -1552,24 +1626,35 @@ int tp_hooi_sweep_host(tp_ctx* ctx, int n_modes, const size_t* dims, const doubl
     bind(ctx);
     if (!dims || !tensor || !K || !factors_in) raise(TP_ERR_BAD_ARGUMENT, "null argument");
     std::vector<u64> L(dims, dims + std::max(n_modes, 0));
-    tp_plan* plan = nullptr;
-    tp_tensor* t = nullptr;
+    std::vector<long long> key{n_modes, n_nodes, sweep_kind};
+    for (int m = 0; m < n_modes; ++m) {
+      key.push_back(static_cast<long long>(dims[m]));
+      key.push_back(static_cast<long long>(K[m]));
+    }
+    for (int i = 0; i < n_nodes && kind && mode && parent; ++i) {
+      key.push_back(kind[i]);
+      key.push_back(mode[i]);
+      key.push_back(parent[i]);
+    }
     auto forward = [&](int status) {
       if (status == TP_OK) return;
       const std::string msg = tp_last_error();
       const int bad = tp_last_error_mode();
-      if (plan) tp_plan_destroy(ctx, plan);
-      if (t) tp_tensor_free(ctx, t);
+      release_host_call_cache(ctx);
       raise(status, msg, bad);
     };
-    forward(tp_plan_create(ctx, n_modes, L.data(), K, n_nodes, kind, mode, parent, sweep_kind, &plan));
-    forward(tp_tensor_upload(ctx, n_modes, dims, tensor, &t));
-    forward(tp_plan_set_factors(ctx, plan, factors_in));
-    forward(tp_plan_sweep(ctx, plan, t, stats));
-    if (factors_out) forward(tp_plan_get_factors(ctx, plan, factors_out));
-    if (core_out) forward(tp_plan_get_core(ctx, plan, core_out));
-    tp_plan_destroy(ctx, plan);
-    tp_tensor_free(ctx, t);
+    if (key != ctx->host_call_key || !ctx->host_call_plan || !ctx->host_call_tensor) {
+      release_host_call_cache(ctx);
+      forward(tp_plan_create(ctx, n_modes, L.data(), K, n_nodes, kind, mode, parent, sweep_kind, &ctx->host_call_plan));
+      forward(tp_tensor_alloc(ctx, n_modes, dims, &ctx->host_call_tensor));
+      ctx->host_call_key = key;
+    }
+    tp_tensor* t = ctx->host_call_tensor;
+    TPB_CUDA(cudaMemcpyAsync(t->data, tensor, t->size * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    forward(tp_plan_set_factors(ctx, ctx->host_call_plan, factors_in));
+    forward(tp_plan_sweep(ctx, ctx->host_call_plan, t, stats));
+    if (factors_out) forward(tp_plan_get_factors(ctx, ctx->host_call_plan, factors_out));
+    if (core_out) forward(tp_plan_get_core(ctx, ctx->host_call_plan, core_out));
   });
 }
 

@@ -556,7 +556,7 @@ struct Volume {
 };
 
 namespace detail {
-inline Volume volume_under(const Tree& t, const Spec& s, const Cards& cards, const Grid& q) {
+inline Volume volume_under(const Tree& t, const Cards& cards, const Grid& q) {
   Volume v;
   v.per_node.assign(t.size(), 0);
   for (int id = 0; id < t.size(); ++id) {
@@ -571,7 +571,7 @@ inline Volume volume_under(const Tree& t, const Spec& s, const Cards& cards, con
 // grid_volume.hpp:32-46: sum over TTM nodes of (q_n - 1) |Out_u|
 inline Volume static_volume(const Tree& t, const Spec& s, const Grid& q, u64 procs) {
   validate_grid(q, s, procs);
-  return detail::volume_under(t, s, node_cardinalities(t, s), q);
+  return detail::volume_under(t, node_cardinalities(t, s), q);
 }
 
 struct StaticGrid {
@@ -586,9 +586,9 @@ inline StaticGrid optimal_static_grid(const Tree& t, const Spec& s, u64 procs, i
   if (grids.empty()) raise(TP_ERR_NO_VALID_GRID, "no grid with prod q = procs fits under K");
   const Cards cards = node_cardinalities(t, s);
   auto scan = [&](std::size_t lo, std::size_t hi) {
-    std::pair<u64, std::size_t> best{detail::volume_under(t, s, cards, grids[lo]).total, lo};
+    std::pair<u64, std::size_t> best{detail::volume_under(t, cards, grids[lo]).total, lo};
     for (std::size_t i = lo + 1; i < hi; ++i) {
-      const u64 v = detail::volume_under(t, s, cards, grids[i]).total;
+      const u64 v = detail::volume_under(t, cards, grids[i]).total;
       if (v < best.first) best = {v, i};
     }
     return best;

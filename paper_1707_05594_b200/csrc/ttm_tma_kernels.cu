@@ -107,8 +107,12 @@ __global__ void __launch_bounds__(kThreads, (KT * NT <= 12) ? 2 : 1)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kb = blockIdx.y;
-  const long long n_groups = (p.n_boxes + BOXES - 1) / BOXES;
-  const long long my_tiles = blockIdx.x < n_groups ? (n_groups - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  // Balanced partition: CTA b owns the contiguous box range [b n / G, (b+1) n / G) and walks it in tiles of BOXES
+  // boxes; boxes of the last tile beyond the range are neither loaded (their TMA coordinates are out of bounds ->
+  // zero fill, no memory traffic) nor stored.
+  const long long cta_begin = static_cast<long long>(blockIdx.x) * p.n_boxes / gridDim.x;
+  const long long cta_end = static_cast<long long>(blockIdx.x + 1) * p.n_boxes / gridDim.x;
+  const long long my_tiles = (cta_end - cta_begin + BOXES - 1) / BOXES;
 
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -122,7 +126,7 @@ __global__ void __launch_bounds__(kThreads, (KT * NT <= 12) ? 2 : 1)
   }
   __syncthreads();
 
-  auto first_box = [&](long long j) { return (static_cast<long long>(blockIdx.x) + j * gridDim.x) * BOXES; };
+  auto first_box = [&](long long j) { return cta_begin + j * BOXES; };
 
   if (warp == 0) {
     // ------------------------------------------------------------------ producer
@@ -136,13 +140,13 @@ __global__ void __launch_bounds__(kThreads, (KT * NT <= 12) ? 2 : 1)
         const long long g0 = first_box(j);
 #pragma unroll
         for (int q = 0; q < BOXES; ++q) {
-          const long long g = g0 + q;
+          const long long g = g0 + q < cta_end ? g0 + q : p.n_boxes;  // past the range -> out of bounds
           if (LAST) {
-            box_c0[q] = static_cast<int>(min(g, p.n_boxes) * 16);  // row; beyond the extent -> all zero fill
+            box_c0[q] = static_cast<int>(g * 16);  // first row; n_boxes * 16 >= outer -> all zero fill
             box_c2[q] = 0;
           } else {
-            const unsigned a = static_cast<unsigned>(min(g, p.n_boxes)) / static_cast<unsigned>(p.boxes_per_slab);
-            box_c0[q] = static_cast<int>(static_cast<unsigned>(min(g, p.n_boxes)) - a * p.boxes_per_slab) * 16;
+            const unsigned a = static_cast<unsigned>(g) / static_cast<unsigned>(p.boxes_per_slab);
+            box_c0[q] = static_cast<int>(static_cast<unsigned>(g) - a * p.boxes_per_slab) * 16;
             box_c2[q] = static_cast<int>(a);  // a == outer for boxes past the end -> zero fill
           }
         }
@@ -236,7 +240,7 @@ __global__ void __launch_bounds__(kThreads, (KT * NT <= 12) ? 2 : 1)
       const int t = cw * NT + jj;
       const long long g = g0 + (t >> 1);
       const int half = t & 1;
-      if (g < p.n_boxes) {
+      if (g < cta_end) {
         long long slab = 0;
         int c0 = 0;
         if (!LAST) {
@@ -309,9 +313,10 @@ cudaError_t launch_tma_one(cudaStream_t stream, const CUtensorMap& map, const Tm
     if (e != cudaSuccess) return e;
     ctas_per_sm = occ < 1 ? 1 : occ;
   }
-  const long long groups = (p.n_boxes + BOXES - 1) / BOXES;
   const long long resident = std::max(1LL, static_cast<long long>(sm_count) * ctas_per_sm / k_blocks);
-  dim3 grid(static_cast<unsigned>(std::min(groups, resident)), static_cast<unsigned>(k_blocks));
+  // every resident CTA gets an equal share of the boxes (at least half a tile each, else fewer CTAs)
+  const long long useful = std::max(1LL, (p.n_boxes * 2 + BOXES - 1) / BOXES);
+  dim3 grid(static_cast<unsigned>(std::min(useful, resident)), static_cast<unsigned>(k_blocks));
   kernel<<<grid, kThreads, smem, stream>>>(map, p);
   return cudaGetLastError();
 }
@@ -339,8 +344,9 @@ bool ttm_tma_eligible(const double* x, long long outer, long long len, long long
   const int tile_n = kConsumerWarps * ((kt <= 5) ? 4 : 2);
   const long long boxes = last ? (outer + 15) / 16 : outer * ((inner + 15) / 16);
   if (boxes >= (1LL << 31)) return false;
-  // wide tiles only: small problems stay with the narrow-tile cp.async kernel
-  return (boxes + tile_n / 2 - 1) / (tile_n / 2) * k_blocks >= sm_count;
+  // at least one full tile per SM; smaller problems are faster on the narrow cp.async kernel (measured: the TMA
+  // pipeline's start-up costs ~5 us more)
+  return boxes * k_blocks >= static_cast<long long>(tile_n / 2) * sm_count;
 }
 
 cudaError_t launch_ttm_tma(cudaStream_t stream, const double* x, long long outer, long long len, long long inner,

@@ -109,6 +109,7 @@ class GpuOps:
         self.ctx = ctx
         self.device = torch.device("cuda", device_index)
         self.stream = torch.cuda.ExternalStream(ctx.stream, device=self.device)
+        self.fast_solves = 0   # leaves served by the certified subspace iteration
 
     def _ptr(self, t):
         return ctypes.cast(t.data_ptr(), dbl_p)
@@ -157,14 +158,18 @@ class GpuOps:
                               ctypes.c_size_t(inner), self._ptr(g)))
         return g
 
-    def leaf_solve(self, gram, rows, k):
+    def leaf_solve(self, gram, rows, k, start=None):
+        """Top-k eigenvectors of gram; `start` (previous factor) enables the certified subspace iteration."""
         factor = self.empty(rows * k)
         with self.torch.cuda.stream(self.stream):
             status = self.torch.zeros(2, dtype=self.torch.int32, device=self.device)
         flag = ctypes.cast(status.data_ptr(), ctypes.POINTER(ctypes.c_int))
         info = ctypes.cast(status.data_ptr() + 4, ctypes.POINTER(ctypes.c_int))
-        check(lib.tp_dev_leaf_solve(self.ctx._h, self._ptr(gram), ctypes.c_size_t(rows), int(k), self._ptr(factor),
-                                    flag, info))
+        used = ctypes.c_int()
+        check(lib.tp_dev_leaf_solve_warm(self.ctx._h, self._ptr(gram), ctypes.c_size_t(rows), int(k),
+                                         self._ptr(start) if start is not None else None, self._ptr(factor), flag,
+                                         info, ctypes.byref(used)))
+        self.fast_solves += used.value
         return factor, status
 
     def sum_squares(self, x, count):
@@ -310,7 +315,7 @@ class DistributedHooi:
                 yield Exchange([(group[0], y)], [])
                 gram = self.ops.zeros(rows * rows)
         yield AllReduce(gram)
-        factor, status = self.ops.leaf_solve(gram, rows, k)
+        factor, status = self.ops.leaf_solve(gram, rows, k, self.factors[mode])
         statuses.append(status)
         return factor
 

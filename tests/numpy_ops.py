@@ -44,7 +44,7 @@ class NumpyOps:
         u = ho.unfold(y.numpy().reshape(outer, rows, inner), 1)
         return torch.from_numpy((u @ u.T).reshape(-1).copy())
 
-    def leaf_solve(self, gram, rows, k):
+    def leaf_solve(self, gram, rows, k, start=None):
         vec, deg = ho.leading_from_gram(gram.numpy().reshape(rows, rows), k)
         factor = torch.from_numpy(np.asfortranarray(vec).reshape(-1, order="F").copy())
         return factor, torch.tensor([int(deg), 0], dtype=torch.int32)

@@ -194,7 +194,7 @@ def test_gloo_process_group(tmp_path, L, K, q):
 
 
 # ----------------------------------------------------------------------------- one B200, virtual ranks, CUDA kernels
-GPU_CASES = [((48, 40, 36), (8, 6, 5), (1, 1, 4)), ((48, 40, 36), (8, 6, 5), (2, 2, 2)),
+GPU_CASES = [((48, 40, 36), (8, 6, 5), (1, 1, 4)), ((768, 36, 30), (12, 6, 5), (1, 2, 2)), ((48, 40, 36), (8, 6, 5), (2, 2, 2)),
              ((33, 26, 24, 10), (5, 4, 6, 3), (1, 2, 1, 2)), ((40, 30, 50), (13, 9, 12), (8, 1, 1)),
              ((64, 64, 64), (12, 12, 12), (1, 1, 8)), ((20, 12, 10, 9, 8), (4, 3, 3, 2, 2), (2, 1, 1, 1, 2))]
 
