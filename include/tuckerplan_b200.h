@@ -278,6 +278,17 @@ int tp_dev_leaf_solve_warm(tp_ctx* ctx, double* gram, size_t rows, int k, const 
 /* *out (device double) = sum x[i]^2 */
 int tp_dev_sum_squares(tp_ctx* ctx, const double* x, size_t count, double* out);
 
+/* Small dense steps of the certified top-k eigen-solve (the part of hooi.hpp:55 `SelfAdjointEigenSolver` this engine
+ * replaces for the leaves); all pointers are device pointers, matrices column-major, block <= 112.
+ *   tp_dev_cholesky      S (block x block, SPD, full storage) -> lower factor L, upper triangle zeroed;
+ *                        *fail |= 1 if a pivot is not positive
+ *   tp_dev_trsm_right_lt Z (rows x block) <- Z L^{-T}, in place
+ *   tp_dev_jacobi_eig    H (block x block, symmetric, full storage) -> eigenvalues ascending in w, eigenvectors as
+ *                        columns of v; fail[0] |= 2 if not converged, fail[1] = max(fail[1], sweeps used) */
+int tp_dev_cholesky(tp_ctx* ctx, const double* s, int block, double* l, int* fail);
+int tp_dev_trsm_right_lt(tp_ctx* ctx, double* z, size_t rows, int block, const double* l);
+int tp_dev_jacobi_eig(tp_ctx* ctx, const double* h, int block, double* w, double* v, int* fail);
+
 /* By-value hooi_sweep (hooi.hpp:189-191): host tensor + host factors in, host factors + core out; uploads, runs,
  * downloads.  This is the call the reference-facing C++ wrapper makes. */
 /* Consecutive calls with the same shape, ranks, tree and schedule reuse the device tensor, plan and workspaces kept

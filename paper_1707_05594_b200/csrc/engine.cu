@@ -77,6 +77,9 @@ struct tp_ctx {
   cusolverDnHandle_t aux_solver[kAux] = {nullptr, nullptr, nullptr, nullptr};
   cublasHandle_t blas = nullptr;     // small dense products inside the eigen-solve (off the hot path)
   cublasHandle_t aux_blas[kAux] = {nullptr, nullptr, nullptr, nullptr};
+  // fixed cuBLAS workspaces (one per handle): recorded CUDA graphs must not depend on cuBLAS' own pool
+  static constexpr size_t kBlasWorkspaceBytes = 32u << 20;
+  void* blas_ws[kAux + 1] = {nullptr, nullptr, nullptr, nullptr, nullptr};
 };
 
 struct tp_tensor {
@@ -197,14 +200,27 @@ struct LeafScratch {
   double* x = nullptr;         // rows x block (Ritz vectors, ascending)
   double* h = nullptr;         // block x block
   double* theta = nullptr;     // block
+  double* chol = nullptr;      // block x block Cholesky factor
+  double* ritz = nullptr;      // block x block Ritz rotation
   double* small_work = nullptr;
   int small_lwork = 0;
-  int* verdict = nullptr;      // [0] |= 1: a kept Ritz pair missed the residual bound; [1]: potrf/syevd info
+  int* verdict = nullptr;      // [0] |= 1: a kept Ritz pair missed the residual bound; [1]: a factorisation failed
+                               // (1 Cholesky pivot, 2 Jacobi not converged, else cuSOLVER info); [2]: Jacobi sweeps used
+  // the iteration is a fixed kernel sequence on fixed buffers: recorded once, replayed as a CUDA graph afterwards
+  cudaGraphExec_t graph = nullptr;
+  const double* graph_gram = nullptr;
+  long long graph_rows = 0;
+  int graph_k = 0;
+  const double* graph_result = nullptr;  // where the recorded sequence leaves the Ritz vectors
+  int graph_state = 0;         // 0: not run yet (first run is eager), 1: eager run done, 2: graph ready, -1: disabled
   long long fast_rows = 0;     // rows the iteration buffers were sized for (tp_dev_leaf_solve_warm only)
   int failures = 0;            // consecutive sweeps in which the fast path was rejected
   bool fast_used = false;      // this sweep's factor came from the fast path (verdict still to be checked)
 
   void release() {
+    if (graph) cudaGraphExecDestroy(graph);
+    cudaFree(chol);
+    cudaFree(ritz);
     cudaFree(q);
     cudaFree(z);
     cudaFree(x);
@@ -244,8 +260,9 @@ void leaf_scratch_reserve(tp_ctx* ctx, LeafScratch& s, long long rows, size_t gr
   if (!s.info) {
     TPB_CUDA(cudaMalloc(&s.info, sizeof(int)));
     TPB_CUDA(cudaMalloc(&s.flag, sizeof(int)));
-    TPB_CUDA(cudaMemsetAsync(s.flag, 0, sizeof(int), ctx->stream));
-    TPB_CUDA(cudaMemsetAsync(s.info, 0, sizeof(int), ctx->stream));
+    // synchronous: the first writers may sit on a side stream that is not ordered after ctx->stream
+    TPB_CUDA(cudaMemset(s.flag, 0, sizeof(int)));
+    TPB_CUDA(cudaMemset(s.info, 0, sizeof(int)));
   }
 }
 
@@ -284,20 +301,26 @@ void leaf_solve(tp_ctx* ctx, LeafScratch& s, long long rows, int k, double* fact
 // ---- top-k eigen-solve by warm-started block subspace iteration --------------------------------------------
 // The leaves only need the K_n leading eigenvectors of an L_n x L_n Gram matrix whose spectrum, for the tensors
 // HOOI is run on, drops sharply after K_n, and the previous factor is an excellent start.  Orthogonal iteration
-// on a block of K_n + p columns (p = oversampling) with a Rayleigh-Ritz step converges like
-// (lambda_{K+p+1} / lambda_K)^steps.  The schedule is fixed (no host decisions inside the sweep): 2 rounds of
-// [3 x (Z = G Q; Q = CholQR2(Z))] + Rayleigh-Ritz; a device flag records whether every kept Ritz pair satisfies
-// ||G x - theta x|| <= 1e-13 theta_max and whether the gap estimate is safe.  The sweep checks the flags once at
-// its end; a rejected leaf is redone with the full eigen-solve (the Gram matrix is left intact here), so the
-// result is always the reference's: eigenvectors of the Gram matrix to rounding (hooi.hpp:55-69).
+// on a block of K_n + p columns (p = oversampling) converges like (lambda_{K+p+1} / lambda_K)^steps.  The schedule
+// is fixed (no host decisions inside the sweep): kSubspacePowerSteps x [Z = G Q; Q = CholQR(Z)] -- one Cholesky-QR
+// pass keeps the block well conditioned, which is all the iteration needs since only span(Q) matters; the last
+// step repeats the pass so that Q is orthonormal to rounding -- then one Rayleigh-Ritz step.  A device flag records
+// whether every kept Ritz pair satisfies ||G x - theta x|| <= 1e-13 theta_max and whether the gap estimate is
+// safe.  The sweep checks the flags once at its end; a rejected leaf is redone with the full eigen-solve (the Gram
+// matrix is left intact here), so the result is always the reference's: eigenvectors of the Gram matrix to
+// rounding (hooi.hpp:55-69).
 constexpr int kSubspaceOversample = 8;
-constexpr int kSubspaceRounds = 2;
-constexpr int kSubspacePowerSteps = 3;
+constexpr int kSubspacePowerSteps = 6;
 constexpr double kSubspaceTol = 1e-13;
 
-bool subspace_eligible(long long rows, int k) {
-  // below ~700 rows the full eigen-solve is as fast as the ~70 small launches of the iteration
-  return rows >= 704 && 2LL * (k + kSubspaceOversample) <= rows;
+// `cols`: columns of the unfolding whose Gram matrix is solved (its rank bound); the iteration block must not exceed
+// it or Z = G Q is rank deficient and the Cholesky-QR breaks down.
+bool subspace_eligible(long long rows, int k, double cols = 1e300) {
+  const long long b = k + kSubspaceOversample;
+  if (2 * b > rows || static_cast<double>(b) > cols) return false;
+  // with the single-launch small steps (evd_kernels.cu) and graph replay the iteration wins at every size; wider
+  // blocks go through cuSOLVER's potrf / syevd, ~70 launches, which only pays against a large full eigen-solve
+  return static_cast<size_t>(b) <= small_evd_max_block() || rows >= 704;
 }
 
 void subspace_reserve(tp_ctx* ctx, LeafScratch& s, long long rows, int k) {
@@ -309,69 +332,148 @@ void subspace_reserve(tp_ctx* ctx, LeafScratch& s, long long rows, int k) {
   s.x = device_alloc(nb);
   s.h = device_alloc(static_cast<size_t>(b) * b);
   s.theta = device_alloc(static_cast<size_t>(b));
+  s.chol = device_alloc(static_cast<size_t>(b) * b);
+  s.ritz = device_alloc(static_cast<size_t>(b) * b);
   int l1 = 0, l2 = 0;
   TPB_SOLVER(cusolverDnDsyevd_bufferSize(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, b, s.h, b,
                                          s.theta, &l1));
   TPB_SOLVER(cusolverDnDpotrf_bufferSize(ctx->solver, CUBLAS_FILL_MODE_LOWER, b, s.h, b, &l2));
   s.small_lwork = std::max(l1, l2);
   s.small_work = device_alloc(static_cast<size_t>(s.small_lwork));
-  TPB_CUDA(cudaMalloc(&s.verdict, 2 * sizeof(int)));
-  TPB_CUDA(cudaMemsetAsync(s.verdict, 0, 2 * sizeof(int), ctx->stream));
+  TPB_CUDA(cudaMalloc(&s.verdict, 4 * sizeof(int)));
+  TPB_CUDA(cudaMemset(s.verdict, 0, 4 * sizeof(int)));
   s.block = b;
 }
 
-// Q (rows x b, column-major) <- orthonormal basis of span(Z) by Cholesky QR, applied twice.  Z is overwritten.
-void cholqr2(cublasHandle_t blas, cusolverDnHandle_t solver, LeafScratch& s, int rows, int b, double* zbuf) {
+struct SubspaceIo {
+  cublasHandle_t blas;
+  cusolverDnHandle_t solver;
+  cudaStream_t stream;
+  bool own_small;  // block fits the single-CTA kernels of evd_kernels.cu (else cuSOLVER potrf / syevd)
+};
+
+// Z (rows x b, column-major) <- Z L^{-T} with L L^T = Z^T Z, `passes` times (2 = orthonormal to rounding).
+void cholqr(tp_ctx* ctx, const SubspaceIo& io, LeafScratch& s, int rows, int b, double* zbuf, int passes) {
   const double one = 1.0, zero = 0.0;
-  for (int pass = 0; pass < 2; ++pass) {
-    TPB_BLAS(cublasDgemm(blas, CUBLAS_OP_T, CUBLAS_OP_N, b, b, rows, &one, zbuf, rows, zbuf, rows, &zero, s.h, b));
-    TPB_SOLVER(cusolverDnDpotrf(solver, CUBLAS_FILL_MODE_LOWER, b, s.h, b, s.small_work, s.small_lwork,
-                                s.verdict + 1));
-    // Z <- Z L^{-T}
-    TPB_BLAS(cublasDtrsm(blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, rows, b,
-                         &one, s.h, b, zbuf, rows));
+  for (int pass = 0; pass < passes; ++pass) {
+    TPB_BLAS(cublasDgemm(io.blas, CUBLAS_OP_T, CUBLAS_OP_N, b, b, rows, &one, zbuf, rows, zbuf, rows, &zero, s.h, b));
+    if (io.own_small) {
+      TPB_CUDA(launch_cholesky(io.stream, s.h, b, s.chol, s.verdict + 1));
+      TPB_CUDA(launch_trsm_right_lt(io.stream, zbuf, rows, b, s.chol));
+      ctx->own_kernels += 2;
+      ctx->library_calls += 1;
+    } else {
+      TPB_SOLVER(cusolverDnDpotrf(io.solver, CUBLAS_FILL_MODE_LOWER, b, s.h, b, s.small_work, s.small_lwork,
+                                  s.verdict + 1));
+      TPB_BLAS(cublasDtrsm(io.blas, CUBLAS_SIDE_RIGHT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_T, CUBLAS_DIAG_NON_UNIT, rows,
+                           b, &one, s.h, b, zbuf, rows));
+      ctx->library_calls += 3;
+    }
   }
+}
+
+// The iteration proper: from the start block in s.q (first k columns filled by the caller) to Ritz vectors
+// (ascending) and values in the returned buffer / s.theta, and the certificate in s.verdict.  Touches only device
+// memory owned by `s` plus `gram` (read), with no host decision inside -- it is what the CUDA graph records.
+const double* subspace_body(tp_ctx* ctx, const SubspaceIo& io, LeafScratch& s, const double* gram, int rows, int k) {
+  const int b = s.block;
+  const double one = 1.0, zero = 0.0;
+  double *q = s.q, *z = s.z, *x = s.x;
+  TPB_CUDA(cudaMemsetAsync(s.verdict, 0, 4 * sizeof(int), io.stream));
+  // deterministic filler for the oversampling columns; the start block needs no orthonormalisation of its own
+  TPB_CUDA(launch_fill_pseudo_random(io.stream, q + static_cast<size_t>(rows) * k, static_cast<size_t>(rows) * (b - k),
+                                     0x7461636bull));
+  ctx->own_kernels += 1;
+  for (int step = 0; step < kSubspacePowerSteps; ++step) {
+    TPB_BLAS(cublasDgemm(io.blas, CUBLAS_OP_N, CUBLAS_OP_N, rows, b, rows, &one, gram, rows, q, rows, &zero, z, rows));
+    std::swap(q, z);
+    cholqr(ctx, io, s, rows, b, q, step + 1 == kSubspacePowerSteps ? 2 : 1);
+  }
+  // Rayleigh-Ritz on span(Q): H = Q^T G Q, H = V Theta V^T (ascending), X = Q V
+  TPB_BLAS(cublasDgemm(io.blas, CUBLAS_OP_N, CUBLAS_OP_N, rows, b, rows, &one, gram, rows, q, rows, &zero, z, rows));
+  TPB_BLAS(cublasDgemm(io.blas, CUBLAS_OP_T, CUBLAS_OP_N, b, b, rows, &one, q, rows, z, rows, &zero, s.h, b));
+  const double* v = s.h;
+  if (io.own_small) {
+    TPB_CUDA(launch_jacobi_eig(io.stream, s.h, b, s.theta, s.ritz, s.verdict + 1));
+    ctx->own_kernels += 1;
+    v = s.ritz;
+  } else {
+    TPB_SOLVER(cusolverDnDsyevd(io.solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, b, s.h, b, s.theta,
+                                s.small_work, s.small_lwork, s.verdict + 1));
+    ctx->library_calls += 1;
+  }
+  TPB_BLAS(cublasDgemm(io.blas, CUBLAS_OP_N, CUBLAS_OP_N, rows, b, b, &one, q, rows, v, b, &zero, x, rows));
+  // residuals of the kept pairs: (Z V)_j - theta_j X_j with Z = G Q
+  TPB_BLAS(cublasDgemm(io.blas, CUBLAS_OP_N, CUBLAS_OP_N, rows, b, b, &one, z, rows, v, b, &zero, q, rows));
+  TPB_CUDA(launch_ritz_residuals(io.stream, q, x, s.theta, rows, b, k, kSubspaceTol, s.verdict));
+  ctx->own_kernels += 1;
+  ctx->library_calls += kSubspacePowerSteps + 4;
+  return x;
 }
 
 // Enqueues the whole fast solve on the leaf's stream; the verdict is read by the caller at the end of the sweep.
 void leaf_solve_subspace(tp_ctx* ctx, LeafScratch& s, const double* gram, long long rows_ll, int k,
                          const double* start, double* factor_out, int aux) {
-  cusolverDnHandle_t solver = aux < 0 ? ctx->solver : ctx->aux_solver[aux];
-  cublasHandle_t blas = aux < 0 ? ctx->blas : ctx->aux_blas[aux];
-  cudaStream_t stream = aux < 0 ? ctx->stream : ctx->aux[aux];
+  SubspaceIo io;
+  io.solver = aux < 0 ? ctx->solver : ctx->aux_solver[aux];
+  io.blas = aux < 0 ? ctx->blas : ctx->aux_blas[aux];
+  io.stream = aux < 0 ? ctx->stream : ctx->aux[aux];
+  io.own_small = static_cast<size_t>(s.block) <= small_evd_max_block();
   const int rows = static_cast<int>(rows_ll), b = s.block;
-  const double one = 1.0, zero = 0.0;
-  TPB_CUDA(cudaMemsetAsync(s.verdict, 0, 2 * sizeof(int), stream));
-  // start block: previous factor, then deterministic filler for the oversampling columns
-  TPB_CUDA(cudaMemcpyAsync(s.q, start, sizeof(double) * rows * k, cudaMemcpyDeviceToDevice, stream));
-  TPB_CUDA(launch_fill_pseudo_random(stream, s.q + static_cast<size_t>(rows) * k,
-                                     static_cast<size_t>(rows) * (b - k), 0x7461636bull));
-  cholqr2(blas, solver, s, rows, b, s.q);
-  for (int round = 0; round < kSubspaceRounds; ++round) {
-    for (int step = 0; step < kSubspacePowerSteps; ++step) {
-      TPB_BLAS(cublasDgemm(blas, CUBLAS_OP_N, CUBLAS_OP_N, rows, b, rows, &one, gram, rows, s.q, rows, &zero, s.z,
-                           rows));
-      std::swap(s.q, s.z);
-      cholqr2(blas, solver, s, rows, b, s.q);
+  static const bool graphs_off = std::getenv("TPB_DISABLE_GRAPH") != nullptr;
+  const bool key_ok = s.graph_gram == gram && s.graph_rows == rows_ll && s.graph_k == k;
+  if (!key_ok && s.graph_state > 0) {  // the slot is being reused for another problem: start over
+    if (s.graph) cudaGraphExecDestroy(s.graph);
+    s.graph = nullptr;
+    s.graph_state = 0;
+  }
+  // start block: previous factor (the filler columns are written inside the body)
+  TPB_CUDA(cudaMemcpyAsync(s.q, start, sizeof(double) * rows * k, cudaMemcpyDeviceToDevice, io.stream));
+  const double* ritz_vectors = nullptr;
+  if (io.own_small && !graphs_off && s.graph_state == 1) {
+    // second run on the same buffers: record the sequence.  Lazy initialisation (kernel attributes, cuBLAS
+    // heuristics) happened during the eager first run.
+    const unsigned long long own0 = ctx->own_kernels, lib0 = ctx->library_calls;
+    cudaGraph_t recorded = nullptr;
+    bool ok = cudaStreamBeginCapture(io.stream, cudaStreamCaptureModeRelaxed) == cudaSuccess;
+    if (ok) {
+      try {
+        ritz_vectors = subspace_body(ctx, io, s, gram, rows, k);
+      } catch (const Failure&) {
+        ok = false;
+      }
+      if (cudaStreamEndCapture(io.stream, &recorded) != cudaSuccess) ok = false;
+      if (ok && cudaGraphInstantiate(&s.graph, recorded, 0) != cudaSuccess) ok = false;
+      if (recorded) cudaGraphDestroy(recorded);
     }
-    // Rayleigh-Ritz on span(Q): H = Q^T G Q, H = V Theta V^T (ascending), X = Q V
-    TPB_BLAS(cublasDgemm(blas, CUBLAS_OP_N, CUBLAS_OP_N, rows, b, rows, &one, gram, rows, s.q, rows, &zero, s.z,
-                         rows));
-    TPB_BLAS(cublasDgemm(blas, CUBLAS_OP_T, CUBLAS_OP_N, b, b, rows, &one, s.q, rows, s.z, rows, &zero, s.h, b));
-    TPB_SOLVER(cusolverDnDsyevd(solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, b, s.h, b, s.theta,
-                                s.small_work, s.small_lwork, s.verdict + 1));
-    TPB_BLAS(cublasDgemm(blas, CUBLAS_OP_N, CUBLAS_OP_N, rows, b, b, &one, s.q, rows, s.h, b, &zero, s.x, rows));
-    if (round + 1 < kSubspaceRounds) {
-      std::swap(s.q, s.x);  // Ritz vectors (orthonormal) seed the next round
+    if (ok) {
+      s.graph_state = 2;
+      s.graph_result = ritz_vectors;
     } else {
-      // residuals of the kept pairs: (Z V)_j - theta_j X_j with Z = G Q
-      TPB_BLAS(cublasDgemm(blas, CUBLAS_OP_N, CUBLAS_OP_N, rows, b, b, &one, s.z, rows, s.h, b, &zero, s.q, rows));
-      TPB_CUDA(launch_ritz_residuals(stream, s.q, s.x, s.theta, rows, b, k, kSubspaceTol, s.verdict));
+      cudaGetLastError();  // recording is an optimisation: fall back to plain launches for this slot
+      s.graph = nullptr;
+      s.graph_state = -1;
+    }
+    ctx->own_kernels = own0;
+    ctx->library_calls = lib0;
+  }
+  if (s.graph_state == 2) {
+    ritz_vectors = s.graph_result;
+    TPB_CUDA(cudaGraphLaunch(s.graph, io.stream));
+    // same work as the eager body, for the launch accounting
+    ctx->own_kernels += 1 + 2 * (kSubspacePowerSteps + 1) + 2;
+    ctx->library_calls += (kSubspacePowerSteps + 1) + kSubspacePowerSteps + 4;
+  } else {
+    ritz_vectors = subspace_body(ctx, io, s, gram, rows, k);
+    if (io.own_small && !graphs_off && s.graph_state == 0) {
+      s.graph_state = 1;
+      s.graph_gram = gram;
+      s.graph_rows = rows_ll;
+      s.graph_k = k;
     }
   }
-  ctx->library_calls += 2 + kSubspaceRounds * (kSubspacePowerSteps * 7 + 4) + 1;
-  TPB_CUDA(launch_select_basis(stream, s.x, s.theta, rows, b, k, factor_out, s.flag));
-  ctx->own_kernels += 3;
+  TPB_CUDA(launch_select_basis(io.stream, ritz_vectors, s.theta, rows, b, k, factor_out, s.flag));
+  ctx->own_kernels += 1;
   s.fast_used = true;
 }
 
@@ -503,6 +605,14 @@ void plan_ttm(tp_ctx* ctx, tp_plan* p, const double* x, const std::vector<size_t
   ctx->own_kernels += 1;
 }
 
+// Columns of the unfolding a leaf's Gram matrix comes from: every other mode is already at its core extent.
+double plan_leaf_columns(const tp_plan* p, int mode) {
+  double cols = 1.0;
+  for (int m = 0; m < p->n; ++m)
+    if (m != mode) cols *= static_cast<double>(p->spec.K[m]);
+  return cols;
+}
+
 // Leaf update.  The Gram kernels stay on the main stream (the intermediate they read lives in a per-depth buffer the
 // next sibling TTM overwrites); with `overlap` the eigen-solve moves to a side stream and the main stream carries on
 // with the tree, joining again before the core chain needs the new factors.
@@ -514,7 +624,8 @@ void plan_leaf_solve(tp_ctx* ctx, tp_plan* p, int mode, int node, double* dst, b
   Span evd(ctx, p, kEvd, node, aux);
   LeafScratch& slot = p->leaf[mode];
   slot.fast_used = false;
-  if (p->fast_evd && p->sweep_kind == TP_SWEEP_JACOBI && slot.failures < 2 && subspace_eligible(rows, k)) {
+  if (p->fast_evd && p->sweep_kind == TP_SWEEP_JACOBI && slot.failures < 2 &&
+      subspace_eligible(rows, k, plan_leaf_columns(p, mode))) {
     subspace_reserve(ctx, slot, rows, k);
     leaf_solve_subspace(ctx, slot, slot.gram, rows, k, p->cur[mode], dst, aux);
   } else {
@@ -548,24 +659,28 @@ void plan_leaf(tp_ctx* ctx, tp_plan* p, const double* y, const std::vector<size_
 }
 
 std::vector<int> verify_fast_leaves(tp_ctx* ctx, tp_plan* p) {
-  std::vector<int> host(3 * p->n, 0);
+  std::vector<int> host(4 * p->n, 0);
   bool any = false;
   for (int m = 0; m < p->n; ++m) {
     LeafScratch& s = p->leaf[m];
     if (!s.fast_used) continue;
     any = true;
-    TPB_CUDA(cudaMemcpyAsync(&host[3 * m], s.verdict, 2 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-    TPB_CUDA(cudaMemcpyAsync(&host[3 * m + 2], s.flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    TPB_CUDA(cudaMemcpyAsync(&host[4 * m], s.verdict, 3 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    TPB_CUDA(cudaMemcpyAsync(&host[4 * m + 3], s.flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   }
   std::vector<int> rejected;
   if (!any) return rejected;
   TPB_CUDA(cudaStreamSynchronize(ctx->stream));
+  static const bool trace = std::getenv("TPB_TRACE_EVD") != nullptr;
   for (int m = 0; m < p->n; ++m) {
     LeafScratch& s = p->leaf[m];
     if (!s.fast_used) continue;
     // residual bound missed, a factorisation inside failed, or the gap estimate says "degenerate" (then the exact
     // spectrum decides)
-    const bool bad = host[3 * m] != 0 || host[3 * m + 1] != 0 || host[3 * m + 2] != 0;
+    const bool bad = host[4 * m] != 0 || host[4 * m + 1] != 0 || host[4 * m + 3] != 0;
+    if (trace)
+      std::fprintf(stderr, "[tpb evd] mode %d block %d: residual_miss=%d factorisation=%d jacobi_sweeps=%d degenerate=%d graph=%d\n",
+                   m, s.block, host[4 * m], host[4 * m + 1], host[4 * m + 2], host[4 * m + 3], s.graph_state);
     if (bad) {
       rejected.push_back(m);
       ++s.failures;
@@ -771,12 +886,16 @@ int tp_ctx_create(int device, tp_ctx** out) {
       ctx->reduce_scratch = device_alloc(reduce_scratch_doubles() + 1);
       TPB_BLAS(cublasCreate(&ctx->blas));
       TPB_BLAS(cublasSetStream(ctx->blas, ctx->stream));
+      TPB_CUDA(cudaMalloc(&ctx->blas_ws[tp_ctx::kAux], tp_ctx::kBlasWorkspaceBytes));
+      TPB_BLAS(cublasSetWorkspace(ctx->blas, ctx->blas_ws[tp_ctx::kAux], tp_ctx::kBlasWorkspaceBytes));
       for (int a = 0; a < tp_ctx::kAux; ++a) {
         TPB_CUDA(cudaStreamCreateWithPriority(&ctx->aux[a], cudaStreamNonBlocking, prio_low));
         TPB_SOLVER(cusolverDnCreate(&ctx->aux_solver[a]));
         TPB_SOLVER(cusolverDnSetStream(ctx->aux_solver[a], ctx->aux[a]));
         TPB_BLAS(cublasCreate(&ctx->aux_blas[a]));
         TPB_BLAS(cublasSetStream(ctx->aux_blas[a], ctx->aux[a]));
+        TPB_CUDA(cudaMalloc(&ctx->blas_ws[a], tp_ctx::kBlasWorkspaceBytes));
+        TPB_BLAS(cublasSetWorkspace(ctx->aux_blas[a], ctx->blas_ws[a], tp_ctx::kBlasWorkspaceBytes));
       }
     } catch (...) {
       delete ctx;
@@ -801,6 +920,7 @@ int tp_ctx_destroy(tp_ctx* ctx) {
     }
     cudaFree(ctx->reduce_scratch);
     cudaFree(ctx->frag_scratch);
+    for (void* ws : ctx->blas_ws) cudaFree(ws);
     release_host_call_cache(ctx);
     if (ctx->dev_scratch) {
       static_cast<LeafScratch*>(ctx->dev_scratch)->release();
@@ -1319,7 +1439,8 @@ int tp_plan_last_evd_info(tp_ctx* ctx, tp_plan* p, int* fast_eligible, int* reje
     int eligible = 0;
     for (int m = 0; m < p->n; ++m)
       if (p->fast_evd && p->sweep_kind == TP_SWEEP_JACOBI && p->leaf[m].failures < 2 &&
-          subspace_eligible(static_cast<long long>(p->spec.L[m]), static_cast<int>(p->spec.K[m])))
+          subspace_eligible(static_cast<long long>(p->spec.L[m]), static_cast<int>(p->spec.K[m]),
+                            plan_leaf_columns(p, m)))
         ++eligible;
     if (fast_eligible) *fast_eligible = eligible;
     if (rejected) *rejected = p->fast_rejected;
@@ -1598,6 +1719,43 @@ int tp_dev_leaf_solve_warm(tp_ctx* ctx, double* gram, size_t rows, int k, const 
     ctx->library_calls += 1;
     TPB_CUDA(launch_select_basis(ctx->stream, gram, s.w, static_cast<int>(rows), static_cast<int>(rows), k, factor,
                                  flag));
+    ctx->own_kernels += 1;
+  });
+}
+
+static void check_block(int block) {
+  if (block < 1 || static_cast<size_t>(block) > small_evd_max_block())
+    raise(TP_ERR_BAD_ARGUMENT, "block size outside 1.." + std::to_string(small_evd_max_block()));
+}
+
+int tp_dev_cholesky(tp_ctx* ctx, const double* s, int block, double* l, int* fail) {
+  return guarded([&] {
+    bind(ctx);
+    if (!s || !l || !fail) raise(TP_ERR_BAD_ARGUMENT, "null pointer");
+    check_block(block);
+    TPB_CUDA(launch_cholesky(ctx->stream, s, block, l, fail));
+    ctx->own_kernels += 1;
+  });
+}
+
+int tp_dev_trsm_right_lt(tp_ctx* ctx, double* z, size_t rows, int block, const double* l) {
+  return guarded([&] {
+    bind(ctx);
+    if (!z || !l) raise(TP_ERR_BAD_ARGUMENT, "null pointer");
+    check_block(block);
+    if (rows == 0) return;
+    if (rows > static_cast<size_t>(TP_MAX_GRAM_ROWS)) raise(TP_ERR_TOO_LARGE, "too many rows");
+    TPB_CUDA(launch_trsm_right_lt(ctx->stream, z, static_cast<int>(rows), block, l));
+    ctx->own_kernels += 1;
+  });
+}
+
+int tp_dev_jacobi_eig(tp_ctx* ctx, const double* h, int block, double* w, double* v, int* fail) {
+  return guarded([&] {
+    bind(ctx);
+    if (!h || !w || !v || !fail) raise(TP_ERR_BAD_ARGUMENT, "null pointer");
+    check_block(block);
+    TPB_CUDA(launch_jacobi_eig(ctx->stream, h, block, w, v, fail));
     ctx->own_kernels += 1;
   });
 }

@@ -1,0 +1,270 @@
+// Small dense building blocks of the top-k eigen-solve (engine.cu: leaf_solve_subspace).  The block subspace
+// iteration needs, besides GEMM-shaped products (cuBLAS), three latency-bound operations on tiny matrices that the
+// vendor libraries serve with dozens of launches each: a b x b Cholesky factorisation, the triangular solve that
+// turns Z into an orthonormal basis, and the eigen-decomposition of the b x b Rayleigh-Ritz matrix (b = K_n + 8).
+// Each is one launch here, so a leaf's whole iteration is a short, fixed kernel sequence that the engine replays as
+// a CUDA graph.  All kernels are deterministic.
+#include <cuda_runtime.h>
+
+#include <cfloat>
+
+#include "kernels.cuh"
+
+namespace tpb {
+namespace {
+
+constexpr int kMaxBlock = 112;  // largest iteration block: 2 b^2 doubles of shared memory must fit in 227 KB
+constexpr int kSmallThreads = 512;
+constexpr int kSmallWarps = kSmallThreads / 32;
+
+// L L^T = S for the symmetric positive definite b x b matrix S (column-major, full storage).  Single CTA, S lives in
+// shared memory; warps own trailing columns, lanes rows.  *fail |= 1 when a pivot is not positive (rank-deficient
+// iteration block -> the caller falls back to the full eigen-solve).
+__global__ void __launch_bounds__(kSmallThreads) cholesky_kernel(const double* __restrict__ s_in, int b,
+                                                                 double* __restrict__ l_out, int* __restrict__ fail) {
+  extern __shared__ double sm[];  // b x b, column-major
+  __shared__ double pivot[kMaxBlock];
+  __shared__ int bad;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int e = tid; e < b * b; e += kSmallThreads) sm[e] = s_in[e];
+  if (tid == 0) bad = 0;
+  __syncthreads();
+  for (int j = 0; j < b; ++j) {
+    const double d = sm[j * b + j];  // final since the previous trailing update; nobody writes it again
+    if (!(d > 0.0)) {                // uniform: every thread reads the same value
+      if (tid == 0) bad = 1;
+      break;
+    }
+    const double piv = sqrt(d);
+    for (int i = j + 1 + tid; i < b; i += kSmallThreads) sm[j * b + i] /= piv;
+    if (tid == 0) pivot[j] = piv;
+    __syncthreads();
+    // trailing update of the lower triangle: S(i, k) -= L(i, j) L(k, j), k > j, i >= k
+    for (int k = j + 1 + warp; k < b; k += kSmallWarps) {
+      const double lkj = sm[j * b + k];
+      for (int i = k + lane; i < b; i += 32) sm[k * b + i] = fma(-sm[j * b + i], lkj, sm[k * b + i]);
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  if (tid == 0 && bad) atomicOr(fail, 1);
+  for (int col = warp; col < b; col += kSmallWarps)
+    for (int row = lane; row < b; row += 32)
+      l_out[col * b + row] = row > col ? sm[col * b + row] : (row == col ? (bad ? 1.0 : pivot[col]) : 0.0);
+}
+
+// Z <- Z L^{-T} (Z: n x b column-major, in place): every row x solves x L^T = z.  A row is spread over 8 lanes, lane
+// l keeping columns l, l + 8, ... in registers; column j is finished by its owner (x_j = z_j / L_jj), broadcast by
+// one shuffle, and eliminated from the columns to its right by all 8 lanes at once (independent FMAs, no reduction).
+// A warp serves 4 rows, a CTA 32.
+constexpr int kTrsmThreads = 256;
+constexpr int kTrsmRows = kTrsmThreads / 8;
+constexpr int kTrsmSlots = kMaxBlock / 8;
+__global__ void __launch_bounds__(kTrsmThreads) trsm_right_lt_kernel(double* __restrict__ z, int n, int b,
+                                                                     const double* __restrict__ l) {
+  extern __shared__ double ls[];  // b x b, column-major lower
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int sub = lane & 7;  // which columns of the row this lane keeps
+  const int row = blockIdx.x * kTrsmRows + (tid >> 5) * 4 + (lane >> 3);
+  for (int e = tid; e < b * b; e += kTrsmThreads) ls[e] = l[e];
+  double x[kTrsmSlots];
+  const bool live = row < n;
+#pragma unroll
+  for (int m = 0; m < kTrsmSlots; ++m) {
+    const int col = sub + 8 * m;
+    x[m] = (live && col < b) ? z[static_cast<long long>(col) * n + row] : 0.0;
+  }
+  __syncthreads();
+  const unsigned group_base = lane & ~7u;
+#pragma unroll
+  for (int mj = 0; mj < kTrsmSlots; ++mj) {
+    if (8 * mj >= b) break;  // uniform
+#pragma unroll
+    for (int lj = 0; lj < 8; ++lj) {
+      const int j = 8 * mj + lj;
+      if (j >= b) break;  // uniform
+      if (sub == lj) x[mj] /= ls[j * b + j];
+      const double xj = __shfl_sync(0xffffffffu, x[mj], group_base | lj);
+#pragma unroll
+      for (int m = mj; m < kTrsmSlots; ++m) {
+        const int i = sub + 8 * m;  // column to the right of j kept by this lane
+        if (i > j && i < b) x[m] = fma(-xj, ls[j * b + i], x[m]);
+      }
+    }
+  }
+  if (live) {
+#pragma unroll
+    for (int m = 0; m < kTrsmSlots; ++m) {
+      const int col = sub + 8 * m;
+      if (col < b) z[static_cast<long long>(col) * n + row] = x[m];
+    }
+  }
+}
+
+// Eigen-decomposition of the symmetric b x b matrix H (column-major, full storage) by the parallel cyclic Jacobi
+// method: round-robin pairing gives b/2 disjoint rotations per step; the step's update H <- J^T H J touches every
+// 2 x 2 block (row pair, column pair) exactly once, so it needs no barrier between the column and the row half.
+// Single CTA; H and the accumulated rotations V live in shared memory (leading dimension m = b rounded up to even:
+// the odd case plays against an all-zero dummy index that is never rotated).  Output: eigenvalues ascending in w,
+// matching eigenvectors as columns of v_out (b x b column-major).
+// *fail |= 2 if the off-diagonal mass has not vanished after kMaxSweeps sweeps; fail[1] = max(fail[1], sweeps used).
+constexpr int kMaxSweeps = 30;
+__global__ void __launch_bounds__(kSmallThreads) jacobi_eig_kernel(const double* __restrict__ h_in, int b,
+                                                                   double* __restrict__ w, double* __restrict__ v_out,
+                                                                   int* __restrict__ fail) {
+  extern __shared__ double sm[];
+  const int m = (b + 1) & ~1;
+  const int half = m / 2;
+  double* const h = sm;          // m x m
+  double* const v = sm + m * m;  // m x m
+  __shared__ double rot_c[kMaxBlock / 2], rot_s[kMaxBlock / 2];
+  __shared__ int rot_p[kMaxBlock / 2], rot_q[kMaxBlock / 2];
+  __shared__ double red[2 * kSmallWarps];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int col = warp; col < m; col += kSmallWarps)
+    for (int row = lane; row < m; row += 32) {
+      h[col * m + row] = (col < b && row < b) ? h_in[col * b + row] : 0.0;
+      v[col * m + row] = (col == row) ? 1.0 : 0.0;
+    }
+  __syncthreads();
+
+  int sweep = 0;
+  for (; sweep < kMaxSweeps; ++sweep) {
+    // off-diagonal mass against the whole: the backward error of a dense symmetric solver is (b eps ||H||_F)
+    double off = 0.0, all = 0.0;
+    for (int col = warp; col < m; col += kSmallWarps)
+      for (int row = lane; row < m; row += 32) {
+        const double x = h[col * m + row] * h[col * m + row];
+        all += x;
+        if (row != col) off += x;
+      }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      off += __shfl_xor_sync(0xffffffffu, off, o);
+      all += __shfl_xor_sync(0xffffffffu, all, o);
+    }
+    if (lane == 0) {
+      red[warp] = off;
+      red[kSmallWarps + warp] = all;
+    }
+    __syncthreads();
+    off = 0.0;
+    all = 0.0;
+    for (int i = 0; i < kSmallWarps; ++i) {
+      off += red[i];
+      all += red[kSmallWarps + i];
+    }
+    __syncthreads();
+    if (off <= (b * DBL_EPSILON) * (b * DBL_EPSILON) * all) break;  // uniform: same sums in every thread
+    if (!(all <= DBL_MAX)) {  // NaN / Inf input (a failed factorisation upstream): nothing to converge to
+      sweep = kMaxSweeps;
+      break;
+    }
+
+    for (int step = 0; step < m - 1; ++step) {
+      if (tid < half) {
+        const int p = (step + tid) % (m - 1);
+        const int q = (tid == 0) ? (m - 1) : (step + m - 1 - tid) % (m - 1);
+        double c = 1.0, s = 0.0;
+        const double hpq = h[q * m + p];
+        if (q < b && hpq != 0.0) {
+          // angle |theta| <= pi/4 with tan(2 theta) = 2 h_pq / (h_qq - h_pp), from cos(2 theta) without tangents
+          const double a = h[q * m + q] - h[p * m + p], b2 = 2.0 * hpq;
+          const double rinv = rsqrt(a * a + b2 * b2);
+          const double c2 = 0.5 + 0.5 * fabs(a) * rinv;  // cos^2(theta)
+          const double cinv = rsqrt(c2);
+          c = c2 * cinv;
+          s = (a >= 0.0 ? 0.5 : -0.5) * b2 * rinv * cinv;
+        }
+        rot_p[tid] = p;
+        rot_q[tid] = q;
+        rot_c[tid] = c;
+        rot_s[tid] = s;
+      }
+      __syncthreads();
+      for (int tj = warp; tj < half; tj += kSmallWarps) {
+        const int pj = rot_p[tj], qj = rot_q[tj];
+        const double cj = rot_c[tj], sj = rot_s[tj];
+        double* const hp = h + pj * m;
+        double* const hq = h + qj * m;
+        for (int ti = lane; ti < half; ti += 32) {
+          const int pi = rot_p[ti], qi = rot_q[ti];
+          const double ci = rot_c[ti], si = rot_s[ti];
+          const double a = hp[pi], bq = hq[pi], cc = hp[qi], d = hq[qi];
+          // columns (H J_j), then rows (J_i^T ...)
+          const double a1 = cj * a - sj * bq, b1 = sj * a + cj * bq;
+          const double c1 = cj * cc - sj * d, d1 = sj * cc + cj * d;
+          const bool diag = ti == tj;
+          hp[pi] = ci * a1 - si * c1;
+          hp[qi] = diag ? 0.0 : si * a1 + ci * c1;
+          hq[pi] = diag ? 0.0 : ci * b1 - si * d1;
+          hq[qi] = si * b1 + ci * d1;
+        }
+        double* const vp = v + pj * m;
+        double* const vq = v + qj * m;
+        for (int r = lane; r < m; r += 32) {
+          const double x = vp[r], y = vq[r];
+          vp[r] = cj * x - sj * y;
+          vq[r] = sj * x + cj * y;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (tid == 0) {
+    if (sweep == kMaxSweeps) atomicOr(fail, 2);
+    atomicMax(fail + 1, sweep);
+  }
+  // ascending order by rank (ties by index); eigenvectors follow their values
+  for (int i = warp; i < b; i += kSmallWarps) {
+    const double li = h[i * m + i];
+    int rank = 0;
+    for (int j = lane; j < b; j += 32) {
+      const double lj = h[j * m + j];
+      rank += (lj < li) || (lj == li && j < i);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
+    if (lane == 0) w[rank] = li;
+    for (int r = lane; r < b; r += 32) v_out[rank * b + r] = v[i * m + r];
+  }
+}
+
+template <typename Kernel>
+cudaError_t allow_shared(Kernel kernel, size_t bytes, bool& configured) {
+  if (configured) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+  if (e == cudaSuccess) configured = true;
+  return e;
+}
+
+}  // namespace
+
+size_t small_evd_max_block() { return kMaxBlock; }
+
+cudaError_t launch_cholesky(cudaStream_t stream, const double* s, int b, double* l, int* fail) {
+  static bool configured = false;
+  cudaError_t e = allow_shared(cholesky_kernel, sizeof(double) * kMaxBlock * kMaxBlock, configured);
+  if (e != cudaSuccess) return e;
+  cholesky_kernel<<<1, kSmallThreads, sizeof(double) * b * b, stream>>>(s, b, l, fail);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_trsm_right_lt(cudaStream_t stream, double* z, int n, int b, const double* l) {
+  static bool configured = false;
+  cudaError_t e = allow_shared(trsm_right_lt_kernel, sizeof(double) * kMaxBlock * kMaxBlock, configured);
+  if (e != cudaSuccess) return e;
+  trsm_right_lt_kernel<<<(n + kTrsmRows - 1) / kTrsmRows, kTrsmThreads, sizeof(double) * b * b, stream>>>(z, n, b, l);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_jacobi_eig(cudaStream_t stream, const double* h, int b, double* w, double* v, int* fail) {
+  static bool configured = false;
+  cudaError_t e = allow_shared(jacobi_eig_kernel, sizeof(double) * 2 * kMaxBlock * kMaxBlock, configured);
+  if (e != cudaSuccess) return e;
+  const int m = (b + 1) & ~1;
+  jacobi_eig_kernel<<<1, kSmallThreads, sizeof(double) * 2 * m * m, stream>>>(h, b, w, v, fail);
+  return cudaGetLastError();
+}
+
+}  // namespace tpb

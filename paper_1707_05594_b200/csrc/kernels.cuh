@@ -73,6 +73,11 @@ cudaError_t launch_select_basis(cudaStream_t stream, const double* vectors, cons
 // out[i] = deterministic pseudo-random value in [-0.5, 0.5)
 cudaError_t launch_fill_pseudo_random(cudaStream_t stream, double* out, size_t n, unsigned long long salt);
 // *verdict |= 1 unless every one of the k largest Ritz pairs has ||(ZV)_j - theta_j X_j|| <= tol * theta_max
+// evd_kernels.cu: single-launch small dense steps of the top-k eigen-solve (block size b <= small_evd_max_block()).
+size_t small_evd_max_block();
+cudaError_t launch_cholesky(cudaStream_t stream, const double* s, int b, double* l, int* fail);         // S = L L^T
+cudaError_t launch_trsm_right_lt(cudaStream_t stream, double* z, int n, int b, const double* l);        // Z <- Z L^-T
+cudaError_t launch_jacobi_eig(cudaStream_t stream, const double* h, int b, double* w, double* v, int* fail);
 cudaError_t launch_ritz_residuals(cudaStream_t stream, const double* zv, const double* x, const double* theta,
                                   int rows, int ncols, int k, double tol, int* verdict);
 

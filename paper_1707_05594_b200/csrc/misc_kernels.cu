@@ -88,7 +88,8 @@ __global__ void __launch_bounds__(256) select_basis_kernel(const double* __restr
     }
     __syncthreads();
   }
-  const double sign = col[best_idx[0]] < 0.0 ? -1.0 : 1.0;
+  // an all-NaN column (a failed iteration whose result the caller discards) leaves no index behind
+  const double sign = (best_idx[0] < rows && col[best_idx[0]] < 0.0) ? -1.0 : 1.0;
   double* dst = factor + static_cast<long long>(j) * rows;
   for (int i = threadIdx.x; i < rows; i += blockDim.x) dst[i] = sign * col[i];
   if (j == 0 && threadIdx.x == 0 && k < ncols) {

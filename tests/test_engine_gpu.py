@@ -343,6 +343,41 @@ def test_fast_eigensolve_is_certified_and_matches(ctx):
     dt.free()
 
 
+@pytest.mark.parametrize("L,K,sweeps", [
+    ([96, 96, 96, 96], [10, 10, 10, 10], 5),      # small leaves: single-launch Cholesky / Jacobi steps, graph replay
+    ([200, 60, 45], [21, 9, 5], 5),               # odd block sizes (29, 17, 13)
+    ([720, 240, 40], [106, 12, 10], 4),           # block 114 > 112: cuSOLVER potrf / syevd variant for mode 0
+])
+def test_fast_eigensolve_small_and_wide_blocks(ctx, L, K, sweeps):
+    """Every eligible leaf takes the certified top-k path; from the third sweep on the recorded CUDA graph is what
+    runs.  Factors must stay the oracle's (full eigen-decomposition) through all of them."""
+    cfg = W.scaled_config(5, L, K, sweeps)
+    spec = cfg.spec
+    tree = P.optimal_tree(spec).tree
+    t = W.build_tensor_host(cfg)
+    f0 = W.start_factors(cfg)
+    dt = E.DeviceTensor.upload(ctx, t)
+    plan = E.HooiPlan(ctx, spec, tree, "jacobi")
+    plan.set_factors(f0)
+    of = [f.copy() for f in f0]
+    rejected = []
+    for it in range(sweeps):
+        st = plan.sweep(dt)
+        ocore, of = ho.hooi_sweep(t, spec.L, spec.K, of, otree(tree), "jacobi")
+        eligible, rej = plan.evd_info()
+        rejected.append(rej)
+        assert not st.degenerate
+        angle = max(ho.sin_largest_principal_angle(a, b) for a, b in zip(plan.get_factors(), of))
+        gn, on = plan.core_norm(), np.sqrt(np.sum(ocore * ocore))
+        assert angle < 1e-9 and abs(gn - on) <= 1e-10 * on, (it, angle, rejected)
+        for a, b in zip(plan.get_factors(), of):
+            assert np.max(np.abs(a - b)) < 1e-7
+    assert eligible == len(L)
+    assert rejected[-1] == 0 and rejected[-2] == 0
+    plan.close()
+    dt.free()
+
+
 def test_fast_eigensolve_falls_back_without_a_gap(ctx):
     """A plain random tensor has no spectral gap: the certificate fails, the full solve takes over, parity holds."""
     L, K = [800, 24, 20], [12, 5, 4]
