@@ -86,7 +86,15 @@ struct tp_tensor {
   std::vector<size_t> dims;
   size_t size = 0;
   double* data = nullptr;
+  // changes whenever the contents may have changed (creation, tp_tensor_axpby, a by-value re-upload, handing out
+  // the raw pointer); plans compare it before reusing products of this tensor kept from the previous sweep
+  tp_u64 stamp = 0;
 };
+
+static tp_u64 next_tensor_stamp() {
+  static tp_u64 counter = 0;
+  return ++counter;
+}
 
 namespace tpb {
 namespace {
@@ -118,6 +126,7 @@ tp_tensor* new_tensor(const std::vector<size_t>& dims) {
   tp_tensor* t = new tp_tensor;
   t->dims = dims;
   t->size = checked_size(static_cast<int>(dims.size()), dims.data());
+  t->stamp = next_tensor_stamp();
   try {
     t->data = device_alloc(t->size);
   } catch (...) {
@@ -212,6 +221,9 @@ struct LeafScratch {
   long long graph_rows = 0;
   int graph_k = 0;
   const double* graph_result = nullptr;  // where the recorded sequence leaves the Ritz vectors
+  // all `block` Ritz vectors of the previous accepted solve on the same (gram, rows, k): the next start block.  With
+  // them the Rayleigh-Ritz matrix starts out nearly diagonal and the Jacobi solver needs few sweeps.
+  const double* last_ritz = nullptr;
   int graph_state = 0;         // 0: not run yet (first run is eager), 1: eager run done, 2: graph ready, -1: disabled
   long long fast_rows = 0;     // rows the iteration buffers were sized for (tp_dev_leaf_solve_warm only)
   int failures = 0;            // consecutive sweeps in which the fast path was rejected
@@ -237,6 +249,15 @@ struct LeafScratch {
     *this = LeafScratch{};
   }
 };
+
+// The iteration buffers are about to change: the recorded graph and the kept Ritz vectors point into them.
+void forget_recorded_solve(LeafScratch& s) {
+  if (s.graph) cudaGraphExecDestroy(s.graph);
+  s.graph = nullptr;
+  if (s.graph_state > 0) s.graph_state = 0;
+  s.graph_gram = nullptr;
+  s.last_ritz = nullptr;
+}
 
 void leaf_scratch_reserve(tp_ctx* ctx, LeafScratch& s, long long rows, size_t gram_ws_doubles) {
   if (rows > s.max_rows) {
@@ -372,7 +393,8 @@ void cholqr(tp_ctx* ctx, const SubspaceIo& io, LeafScratch& s, int rows, int b, 
   }
 }
 
-// The iteration proper: from the start block in s.q (first k columns filled by the caller) to Ritz vectors
+// The iteration proper: from the start block in s.q (filled by the caller; it needs no orthonormalisation of its
+// own, only its span matters) to Ritz vectors
 // (ascending) and values in the returned buffer / s.theta, and the certificate in s.verdict.  Touches only device
 // memory owned by `s` plus `gram` (read), with no host decision inside -- it is what the CUDA graph records.
 const double* subspace_body(tp_ctx* ctx, const SubspaceIo& io, LeafScratch& s, const double* gram, int rows, int k) {
@@ -380,10 +402,6 @@ const double* subspace_body(tp_ctx* ctx, const SubspaceIo& io, LeafScratch& s, c
   const double one = 1.0, zero = 0.0;
   double *q = s.q, *z = s.z, *x = s.x;
   TPB_CUDA(cudaMemsetAsync(s.verdict, 0, 4 * sizeof(int), io.stream));
-  // deterministic filler for the oversampling columns; the start block needs no orthonormalisation of its own
-  TPB_CUDA(launch_fill_pseudo_random(io.stream, q + static_cast<size_t>(rows) * k, static_cast<size_t>(rows) * (b - k),
-                                     0x7461636bull));
-  ctx->own_kernels += 1;
   for (int step = 0; step < kSubspacePowerSteps; ++step) {
     TPB_BLAS(cublasDgemm(io.blas, CUBLAS_OP_N, CUBLAS_OP_N, rows, b, rows, &one, gram, rows, q, rows, &zero, z, rows));
     std::swap(q, z);
@@ -422,13 +440,23 @@ void leaf_solve_subspace(tp_ctx* ctx, LeafScratch& s, const double* gram, long l
   const int rows = static_cast<int>(rows_ll), b = s.block;
   static const bool graphs_off = std::getenv("TPB_DISABLE_GRAPH") != nullptr;
   const bool key_ok = s.graph_gram == gram && s.graph_rows == rows_ll && s.graph_k == k;
-  if (!key_ok && s.graph_state > 0) {  // the slot is being reused for another problem: start over
+  if (!key_ok) {  // the slot is being reused for another problem: start over
     if (s.graph) cudaGraphExecDestroy(s.graph);
     s.graph = nullptr;
-    s.graph_state = 0;
+    if (s.graph_state > 0) s.graph_state = 0;
+    s.last_ritz = nullptr;
   }
-  // start block: previous factor (the filler columns are written inside the body)
-  TPB_CUDA(cudaMemcpyAsync(s.q, start, sizeof(double) * rows * k, cudaMemcpyDeviceToDevice, io.stream));
+  if (s.last_ritz) {
+    // start block: the previous solve's Ritz vectors, dominant first (Cholesky QR orthogonalises in column order)
+    TPB_CUDA(launch_reverse_columns(io.stream, s.q, s.last_ritz, rows, b));
+    ctx->own_kernels += 1;
+  } else {
+    // start block: previous factor + deterministic filler for the oversampling columns
+    TPB_CUDA(cudaMemcpyAsync(s.q, start, sizeof(double) * rows * k, cudaMemcpyDeviceToDevice, io.stream));
+    TPB_CUDA(launch_fill_pseudo_random(io.stream, s.q + static_cast<size_t>(rows) * k,
+                                       static_cast<size_t>(rows) * (b - k), 0x7461636bull));
+    ctx->own_kernels += 1;
+  }
   const double* ritz_vectors = nullptr;
   if (io.own_small && !graphs_off && s.graph_state == 1) {
     // second run on the same buffers: record the sequence.  Lazy initialisation (kernel attributes, cuBLAS
@@ -461,7 +489,7 @@ void leaf_solve_subspace(tp_ctx* ctx, LeafScratch& s, const double* gram, long l
     ritz_vectors = s.graph_result;
     TPB_CUDA(cudaGraphLaunch(s.graph, io.stream));
     // same work as the eager body, for the launch accounting
-    ctx->own_kernels += 1 + 2 * (kSubspacePowerSteps + 1) + 2;
+    ctx->own_kernels += 2 * (kSubspacePowerSteps + 1) + 2;
     ctx->library_calls += (kSubspacePowerSteps + 1) + kSubspacePowerSteps + 4;
   } else {
     ritz_vectors = subspace_body(ctx, io, s, gram, rows, k);
@@ -475,6 +503,7 @@ void leaf_solve_subspace(tp_ctx* ctx, LeafScratch& s, const double* gram, long l
   TPB_CUDA(launch_select_basis(io.stream, ritz_vectors, s.theta, rows, b, k, factor_out, s.flag));
   ctx->own_kernels += 1;
   s.fast_used = true;
+  s.last_ritz = ritz_vectors;  // dropped again by whoever finds the certificate violated
 }
 
 void leaf_update(tp_ctx* ctx, LeafScratch& s, const double* y, const std::vector<size_t>& dims, int mode, int k,
@@ -540,6 +569,19 @@ struct tp_plan {
   int fast_rejected = 0;
   std::vector<std::vector<int>> visit_order;  // per node: children in execution order (see plan_visit_order)
   std::vector<int> leaf_rank;                 // per mode: position of its leaf in the execution order
+  // Carried path (Jacobi): the core chain T x F_new... may contract the modes in any order; run along a root-to-leaf
+  // path of the TTM tree it produces, with the new factors, exactly the intermediates the NEXT sweep's walk needs at
+  // those nodes.  They are kept (own buffers) and the next walk starts from them, so per sweep every tree node is
+  // computed once and the core costs one small extra product instead of a second pass over the tensor.
+  bool carry_enabled = true;
+  std::vector<int> carry_nodes;               // TTM nodes of the path, root child first (empty: no carrying)
+  int carry_leaf_mode = -1;                   // mode of the leaf the path ends in = last product of the core chain
+  std::vector<char> on_carry;                 // per node
+  std::vector<double*> carry_buf;             // one per path node
+  bool carry_valid = false;                   // carry_buf holds products of (carry_tensor @ carry_stamp, cur factors)
+  const tp_tensor* carry_tensor = nullptr;
+  tp_u64 carry_stamp = 0;
+  bool carry_live = false;                    // this sweep's walk starts from the carried products
   int spare_sms = 6;                          // SMs left to the side streams while eigen-solves are in flight
   int leaves_in_flight = 0;
   struct PendingLeaf {
@@ -684,6 +726,7 @@ std::vector<int> verify_fast_leaves(tp_ctx* ctx, tp_plan* p) {
     if (bad) {
       rejected.push_back(m);
       ++s.failures;
+      s.last_ritz = nullptr;
       TPB_CUDA(cudaMemsetAsync(s.flag, 0, sizeof(int), ctx->stream));
     } else {
       s.failures = 0;
@@ -707,6 +750,10 @@ void plan_visit_order(tp_plan* p) {
   for (int id = 0; id < t.size(); ++id) {
     std::vector<int> order = t.kids[id];
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+      const bool ca = !p->on_carry.empty() && p->on_carry[a], cb = !p->on_carry.empty() && p->on_carry[b];
+      // the carried path ends in the mode the core chain contracts last: its leaves are needed last, so they go last
+      // and their eigen-solves overlap the chain's large products
+      if (ca != cb) return cb;
       if (t.leaf(a) != t.leaf(b)) return t.leaf(a);
       return leaves[a] > leaves[b];
     });
@@ -730,7 +777,9 @@ void jacobi_walk(tp_ctx* ctx, tp_plan* p, int node, const double* tensor, std::v
       plan_leaf(ctx, p, tensor, dims, mode, p->fresh[mode], c, p->overlap_evd);
     } else {
       double* out = p->depth_buf[depth];
-      {
+      if (p->carry_live && p->on_carry[c]) {
+        out = p->carry_buf[depth];  // computed by the previous sweep's core chain (path depth == tree depth)
+      } else {
         Span s(ctx, p, kTree, c);
         plan_ttm(ctx, p, tensor, dims, mode, out, (p->overlap_evd && p->leaves_in_flight > 0) ? p->spare_sms : 0);
         s.close();
@@ -749,7 +798,7 @@ void jacobi_walk(tp_ctx* ctx, tp_plan* p, int node, const double* tensor, std::v
 // result differs from the reference's only by rounding.  Ping-pong buffers, the last product lands in `core`.
 void plan_core(tp_ctx* ctx, tp_plan* p, const double* tensor, const std::vector<double*>& factors,
                bool wait_for_leaves = false) {
-  Span s(ctx, p, kCore);
+  const bool carry = p->carry_enabled && !p->carry_nodes.empty();
   std::vector<size_t> dims(p->spec.L.begin(), p->spec.L.end());
   const double* src = tensor;
   for (int i = 0; i < p->n; ++i) {
@@ -763,14 +812,58 @@ void plan_core(tp_ctx* ctx, tp_plan* p, const double* tensor, const std::vector<
         }
       TPB_CUDA(cudaStreamWaitEvent(ctx->stream, p->factor_ready[m], 0));
     }
+    const bool last = i == p->n - 1;
+    // along a carried path the partial products are next sweep's tree nodes: timed as such, kept in their buffers
+    Span s = (carry && !last) ? Span(ctx, p, kTree, p->carry_nodes[i]) : Span(ctx, p, kCore);
     plan_refresh_fragments(ctx, p, m, factors[m]);
-    double* dst = (i == p->n - 1) ? p->core : p->core_tmp[i & 1];
+    double* dst = last ? p->core : (carry ? p->carry_buf[i] : p->core_tmp[i & 1]);
     plan_ttm(ctx, p, src, dims, m, dst, (wait_for_leaves && i == 0 && !p->pending.empty()) ? p->spare_sms : 0);
+    s.close();
     if (wait_for_leaves) plan_flush_pending(ctx, p);
     dims[m] = static_cast<size_t>(p->spec.K[m]);
     src = dst;
   }
-  s.close();
+}
+
+// Picks the path the core chain follows (see tp_plan::carry_nodes) and fixes the order of the chain accordingly.
+// Any root-to-leaf path works and all cost the same in steady state (tree + one product onto the core), so the choice
+// goes by scheduling: the chain's first product needs the new factor of the path's first mode, whose leaf lies in
+// another subtree -- take the path for which that leaf (then the second mode's, ...) comes earliest in the walk.
+void plan_choose_carry(tp_plan* p) {
+  const Tree& t = p->tree;
+  p->carry_nodes.clear();
+  p->carry_leaf_mode = -1;
+  p->on_carry.assign(t.size(), 0);
+  if (p->sweep_kind != TP_SWEEP_JACOBI || p->n < 2) {
+    plan_visit_order(p);
+    return;
+  }
+  std::vector<int> best_nodes, best_key;
+  int best_leaf = -1;
+  for (int leaf = 0; leaf < t.size(); ++leaf) {
+    if (!t.leaf(leaf)) continue;
+    std::vector<int> nodes;
+    for (int id = t.parent[leaf]; id > 0; id = t.parent[id]) nodes.push_back(id);
+    std::reverse(nodes.begin(), nodes.end());
+    if (static_cast<int>(nodes.size()) != p->n - 1) continue;  // (always n - 1 TTM nodes above a leaf)
+    p->on_carry.assign(t.size(), 0);
+    for (int id : nodes) p->on_carry[id] = 1;
+    plan_visit_order(p);
+    std::vector<int> key;
+    for (int id : nodes) key.push_back(p->leaf_rank[t.mode[id]]);
+    if (best_leaf < 0 || key < best_key) {
+      best_key = key;
+      best_nodes = nodes;
+      best_leaf = leaf;
+    }
+  }
+  p->on_carry.assign(t.size(), 0);
+  if (best_leaf >= 0) {
+    for (int id : best_nodes) p->on_carry[id] = 1;
+    p->carry_nodes = best_nodes;
+    p->carry_leaf_mode = t.mode[best_leaf];
+  }
+  plan_visit_order(p);
 }
 
 // Cheapest order of the core chain: forward DP over the set of already-multiplied modes; ties keep the smaller mode
@@ -811,6 +904,14 @@ std::vector<int> cheapest_chain_order(const Spec& s, const std::vector<int>& ran
   }
   if (macs_out) *macs_out = togo[0];
   return order;
+}
+
+// The chain just run left the path products of (t, current factors) in the carry buffers.
+void plan_mark_carried(tp_plan* p, const tp_tensor* t) {
+  if (!p->carry_enabled || p->carry_nodes.empty()) return;
+  p->carry_valid = true;
+  p->carry_tensor = t;
+  p->carry_stamp = t->stamp;
 }
 
 void check_tensor_matches(const tp_plan* p, const tp_tensor* t) {  // hooi.hpp:85-91
@@ -1018,7 +1119,11 @@ int tp_tensor_dims(const tp_tensor* t, int* n_modes, size_t* dims) {
   });
 }
 
-void* tp_tensor_device_ptr(const tp_tensor* t) { return t ? t->data : nullptr; }
+void* tp_tensor_device_ptr(const tp_tensor* t) {
+  if (!t) return nullptr;
+  const_cast<tp_tensor*>(t)->stamp = next_tensor_stamp();  // the caller may write through the pointer
+  return t->data;
+}
 
 int tp_tensor_norm(tp_ctx* ctx, const tp_tensor* t, double* out) {
   return guarded([&] {
@@ -1214,8 +1319,24 @@ int tp_plan_create(tp_ctx* ctx, int n_modes, const tp_u64* L, const tp_u64* K, i
       for (size_t d = 0; d < p->depth_cap.size(); ++d) p->depth_buf[d] = device_alloc(p->depth_cap[d]);
 
       // core chain in its cheapest order; ping-pong buffers hold its largest partial product
-      plan_visit_order(p);
-      p->core_order = cheapest_chain_order(p->spec, p->leaf_rank, &p->core_macs_executed);
+      plan_choose_carry(p);
+      if (p->carry_nodes.empty()) {
+        p->core_order = cheapest_chain_order(p->spec, p->leaf_rank, &p->core_macs_executed);
+      } else {
+        p->core_order.clear();
+        p->core_macs_executed = 0;
+        u64 at = partial_cardinality(p->spec, 0);
+        for (int id : p->carry_nodes) {
+          const int m = p->tree.mode[id];
+          p->core_order.push_back(m);
+          p->core_macs_executed = add_or_throw(p->core_macs_executed, mul_or_throw(p->spec.K[m], at));
+          at = scale_exact(at, p->spec.K[m], p->spec.L[m]);
+          p->carry_buf.push_back(device_alloc(static_cast<size_t>(cards.out[id])));
+        }
+        p->core_order.push_back(p->carry_leaf_mode);
+        p->core_macs_executed =
+            add_or_throw(p->core_macs_executed, mul_or_throw(p->spec.K[p->carry_leaf_mode], at));
+      }
       card = partial_cardinality(p->spec, 0);
       for (int i = 0; i + 1 < n_modes; ++i) {
         const int m = p->core_order[i];
@@ -1281,6 +1402,7 @@ int tp_plan_destroy(tp_ctx* ctx, tp_plan* p) {
     for (double* d : p->fresh) cudaFree(d);
     for (double* d : p->frag) cudaFree(d);
     for (double* d : p->depth_buf) cudaFree(d);
+    for (double* d : p->carry_buf) cudaFree(d);
     cudaFree(p->core);
     cudaFree(p->core_tmp[0]);
     cudaFree(p->core_tmp[1]);
@@ -1304,6 +1426,8 @@ int tp_plan_set_factors(tp_ctx* ctx, tp_plan* p, const double* const* factors) {
       TPB_CUDA(cudaMemcpyAsync(p->cur[m], factors[m], sizeof(double) * p->spec.L[m] * p->spec.K[m],
                                cudaMemcpyHostToDevice, ctx->stream));
     }
+    p->carry_valid = false;
+    for (LeafScratch& slot : p->leaf) slot.last_ritz = nullptr;  // the caller's factors are the start, not ours
     TPB_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }
@@ -1344,7 +1468,9 @@ int tp_plan_compute_core(tp_ctx* ctx, tp_plan* p, const tp_tensor* t) {
     p->events_used = 0;
     p->event_phase.clear();
     p->event_node.clear();
+    p->carry_valid = false;
     plan_core(ctx, p, t->data, p->cur);
+    plan_mark_carried(p, t);
     plan_collect_timing(ctx, p);
   });
 }
@@ -1367,6 +1493,8 @@ int tp_plan_sweep(tp_ctx* ctx, tp_plan* p, const tp_tensor* t, tp_sweep_stats* s
       }
       p->leaves_in_flight = 0;
       p->pending.clear();
+      p->carry_live = p->carry_enabled && p->carry_valid && p->carry_tensor == t && p->carry_stamp == t->stamp;
+      p->carry_valid = false;  // the chain at the end of this sweep overwrites the carried products
       jacobi_walk(ctx, p, 0, t->data, dims, 0);
       plan_core(ctx, p, t->data, p->fresh, p->overlap_evd);  // waits for each new factor just before using it
       // leaves solved by subspace iteration are accepted only with their residual certificate; a rejected leaf is
@@ -1383,6 +1511,7 @@ int tp_plan_sweep(tp_ctx* ctx, tp_plan* p, const tp_tensor* t, tp_sweep_stats* s
         plan_core(ctx, p, t->data, p->fresh);
       }
       std::swap(p->cur, p->fresh);
+      plan_mark_carried(p, t);
     } else {
       {
         Span s(ctx, p, kTree);
@@ -1427,6 +1556,10 @@ int tp_plan_set_option(tp_ctx* ctx, tp_plan* p, int option, int value) {
       p->overlap_evd = value != 0;
     else if (option == TP_OPT_FAST_EVD)
       p->fast_evd = value != 0;
+    else if (option == TP_OPT_CARRY_PATH) {
+      p->carry_enabled = value != 0;
+      p->carry_valid = false;
+    }
     else
       raise(TP_ERR_BAD_ARGUMENT, "unknown plan option");
   });
@@ -1465,6 +1598,7 @@ int tp_tensor_axpby(tp_ctx* ctx, tp_tensor* y, double beta, double alpha, const 
     if (!y || !x) raise(TP_ERR_BAD_ARGUMENT, "null tensor");
     if (y->dims != x->dims) raise(TP_ERR_SHAPE_MISMATCH, "tensor shapes differ");
     TPB_CUDA(launch_axpby(ctx->stream, y->data, beta, alpha, x->data, y->size));
+    y->stamp = next_tensor_stamp();
     ctx->own_kernels += 1;
   });
 }
@@ -1683,22 +1817,26 @@ int tp_dev_leaf_solve_warm(tp_ctx* ctx, double* gram, size_t rows, int k, const 
       leaf_scratch_reserve(ctx, s, 1, 0);
       if (s.block != k + kSubspaceOversample) {  // a different block size: rebuild the iteration buffers
         cudaFree(s.q); cudaFree(s.z); cudaFree(s.x); cudaFree(s.h); cudaFree(s.theta); cudaFree(s.small_work);
-        cudaFree(s.verdict);
-        s.q = s.z = s.x = s.h = s.theta = s.small_work = nullptr;
+        cudaFree(s.verdict); cudaFree(s.chol); cudaFree(s.ritz);
+        s.q = s.z = s.x = s.h = s.theta = s.small_work = s.chol = s.ritz = nullptr;
         s.verdict = nullptr;
         s.block = 0;
+        forget_recorded_solve(s);
       }
       if (s.block == 0 || static_cast<long long>(rows) > s.fast_rows) {
         if (s.block) {
           cudaFree(s.q); cudaFree(s.z); cudaFree(s.x); cudaFree(s.h); cudaFree(s.theta); cudaFree(s.small_work);
-          cudaFree(s.verdict);
+          cudaFree(s.verdict); cudaFree(s.chol); cudaFree(s.ritz);
+          s.chol = s.ritz = nullptr;
           s.block = 0;
+          forget_recorded_solve(s);
         }
         subspace_reserve(ctx, s, static_cast<long long>(rows), k);
         s.fast_rows = static_cast<long long>(rows);
       }
       int* const saved_flag = s.flag;
       s.flag = flag;  // the caller's degenerate flag
+      s.last_ritz = nullptr;  // the result of this entry point depends on its arguments only (replicas stay identical)
       leaf_solve_subspace(ctx, s, gram, static_cast<long long>(rows), k, start, factor, -1);
       s.flag = saved_flag;
       s.fast_used = false;
@@ -1711,6 +1849,7 @@ int tp_dev_leaf_solve_warm(tp_ctx* ctx, double* gram, size_t rows, int k, const 
         if (used_fast) *used_fast = 1;
         return;
       }
+      s.last_ritz = nullptr;
       TPB_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));  // let the exact spectrum decide
     }
     leaf_scratch_reserve(ctx, s, static_cast<long long>(rows), 0);
@@ -1809,6 +1948,7 @@ int tp_hooi_sweep_host(tp_ctx* ctx, int n_modes, const size_t* dims, const doubl
     }
     tp_tensor* t = ctx->host_call_tensor;
     TPB_CUDA(cudaMemcpyAsync(t->data, tensor, t->size * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    t->stamp = next_tensor_stamp();
     forward(tp_plan_set_factors(ctx, ctx->host_call_plan, factors_in));
     forward(tp_plan_sweep(ctx, ctx->host_call_plan, t, stats));
     if (factors_out) forward(tp_plan_get_factors(ctx, ctx->host_call_plan, factors_out));

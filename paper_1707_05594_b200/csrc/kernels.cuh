@@ -78,6 +78,7 @@ size_t small_evd_max_block();
 cudaError_t launch_cholesky(cudaStream_t stream, const double* s, int b, double* l, int* fail);         // S = L L^T
 cudaError_t launch_trsm_right_lt(cudaStream_t stream, double* z, int n, int b, const double* l);        // Z <- Z L^-T
 cudaError_t launch_jacobi_eig(cudaStream_t stream, const double* h, int b, double* w, double* v, int* fail);
+cudaError_t launch_reverse_columns(cudaStream_t stream, double* dst, const double* src, int rows, int ncols);
 cudaError_t launch_ritz_residuals(cudaStream_t stream, const double* zv, const double* x, const double* theta,
                                   int rows, int ncols, int k, double tol, int* verdict);
 

@@ -122,6 +122,17 @@ __global__ void __launch_bounds__(256) fill_pseudo_random_kernel(double* __restr
 
 // One block per kept Ritz pair j (the j-th largest): r = (Z V)_col - theta * X_col over `rows` entries.
 // verdict[0] |= 1 when ||r|| > tol * theta_max (not converged).  Columns are stored ascending, as syevd returns them.
+// dst[:, j] = src[:, ncols - 1 - j] (rows x ncols, column-major): ascending Ritz vectors -> dominant direction first.
+__global__ void __launch_bounds__(256) reverse_columns_kernel(double* __restrict__ dst, const double* __restrict__ src,
+                                                              int rows, int ncols) {
+  const size_t n = static_cast<size_t>(rows) * ncols;
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
+    const size_t col = i / rows, row = i - col * rows;
+    dst[i] = src[(ncols - 1 - col) * static_cast<size_t>(rows) + row];
+  }
+}
+
 __global__ void __launch_bounds__(256) ritz_residual_kernel(const double* __restrict__ zv, const double* __restrict__ x,
                                                             const double* __restrict__ theta, int rows, int ncols,
                                                             double tol, int* __restrict__ verdict) {
@@ -207,6 +218,13 @@ cudaError_t launch_diff_sum_squares(cudaStream_t stream, const double* x, const 
 cudaError_t launch_select_basis(cudaStream_t stream, const double* vectors, const double* w, int rows, int ncols,
                                 int k, double* factor, int* flag) {
   select_basis_kernel<<<k, 256, 0, stream>>>(vectors, w, rows, ncols, k, factor, flag);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reverse_columns(cudaStream_t stream, double* dst, const double* src, int rows, int ncols) {
+  const size_t n = static_cast<size_t>(rows) * ncols;
+  const int blocks = static_cast<int>(std::min<size_t>((n + 255) / 256, kReduceBlocks));
+  reverse_columns_kernel<<<std::max(blocks, 1), 256, 0, stream>>>(dst, src, rows, ncols);
   return cudaGetLastError();
 }
 

@@ -218,6 +218,10 @@ class HooiPlan:
         """Top-k subspace-iteration eigen-solve on eligible Jacobi leaves (verified; full solve otherwise)."""
         check(lib.tp_plan_set_option(self.ctx._h, self._h, 2, 1 if on else 0))
 
+    def set_carry_path(self, on: bool):
+        """Keep the core chain's partial products (they are next sweep's tree nodes along one path) between sweeps."""
+        check(lib.tp_plan_set_option(self.ctx._h, self._h, 3, 1 if on else 0))
+
     def evd_info(self):
         """(leaves eligible for the fast eigen-solve, leaves the last sweep redid with the full solve)."""
         a, b = ctypes.c_int(), ctypes.c_int()

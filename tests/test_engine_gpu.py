@@ -400,6 +400,71 @@ def test_fast_eigensolve_falls_back_without_a_gap(ctx):
     dt.free()
 
 
+CARRY_CASES = [
+    ([40, 36, 30], [6, 5, 4]),
+    ([20, 18, 16, 14], [4, 3, 3, 2]),
+    ([12, 10, 9, 8, 7], [3, 2, 2, 2, 2]),
+    ([300, 8], [3, 3]),
+]
+
+
+@pytest.mark.parametrize("L,K", CARRY_CASES, ids=lambda v: "x".join(map(str, v)))
+@pytest.mark.parametrize("tree_kind", ["optimal", "chain", "balanced"])
+def test_carried_path_is_bit_identical_and_invalidates(ctx, L, K, tree_kind):
+    """TP_OPT_CARRY_PATH only removes recomputation: with it on (default) or off, sweeps give the same bits; changing
+    the tensor or the factors between sweeps drops the carried products."""
+    cfg = W.scaled_config(1, L, K, 4)
+    spec = cfg.spec
+    tree = {"optimal": lambda: P.optimal_tree(spec).tree, "chain": lambda: P.chain_tree(spec),
+            "balanced": lambda: P.balanced_tree(spec)}[tree_kind]()
+    t = W.build_tensor_host(cfg)
+    f0 = W.start_factors(cfg)
+    dt = E.DeviceTensor.upload(ctx, t)
+
+    def run(carry, fast):
+        plan = E.HooiPlan(ctx, spec, tree, "jacobi")
+        plan.set_carry_path(carry)
+        plan.set_fast_evd(fast)
+        plan.set_factors(f0)
+        out = []
+        for _ in range(4):
+            plan.sweep(dt)
+            out.append((plan.get_factors(), plan.get_core()))
+        plan.close()
+        return out
+
+    for fast in (False, True):
+        on, off = run(True, fast), run(False, fast)
+        for (fa, ca), (fb, cb) in zip(on, off):
+            assert all(np.array_equal(a, b) for a, b in zip(fa, fb))
+            assert np.array_equal(ca, cb)
+
+    # against the oracle through a change of tensor and a reset of the factors in mid-run
+    plan = E.HooiPlan(ctx, spec, tree, "jacobi")
+    plan.set_factors(f0)
+    of = [f.copy() for f in f0]
+    t2 = t.copy()
+    noise = hostgen.random_tensor(L, 4242)
+    for it in range(6):
+        if it == 2:                                  # T <- T + 0.05 E on the device and on the host
+            dn = E.DeviceTensor.upload(ctx, noise)
+            dt.axpby(1.0, 0.05, dn)
+            dn.free()
+            t2 = t2 + 0.05 * noise
+        if it == 4:
+            plan.set_factors(f0)
+            of = [f.copy() for f in f0]
+        plan.sweep(dt)
+        ocore, of = ho.hooi_sweep(t2, spec.L, spec.K, of, otree(tree), "jacobi")
+        angle = max(ho.sin_largest_principal_angle(a, b) for a, b in zip(plan.get_factors(), of))
+        gn, on_ = plan.core_norm(), np.sqrt(np.sum(ocore * ocore))
+        assert angle < 1e-9 and abs(gn - on_) <= 1e-10 * on_, (it, angle)
+        err = plan.reconstruction_error(dt)
+        assert abs(err - ho.reconstruction_error(t2, ocore, of)) <= 1e-10 * max(err, 1e-3)
+    plan.close()
+    dt.free()
+
+
 @pytest.mark.parametrize("index", [2, 3, 4])
 def test_sweep_parity_full_size_configs(ctx, index):
     """BASELINE.json configs[1..3] at full size, two Jacobi iterations on the optimal tree, against the oracle."""
