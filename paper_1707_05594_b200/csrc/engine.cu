@@ -226,7 +226,9 @@ struct LeafScratch {
   const double* last_ritz = nullptr;
   int graph_state = 0;         // 0: not run yet (first run is eager), 1: eager run done, 2: graph ready, -1: disabled
   long long fast_rows = 0;     // rows the iteration buffers were sized for (tp_dev_leaf_solve_warm only)
-  int failures = 0;            // consecutive sweeps in which the fast path was rejected
+  int failures = 0;            // consecutive warm sweeps in which the fast path was rejected
+  bool was_cold = false;       // this sweep's solve started from the caller's factors
+  bool cold_rejected = false;  // a cold start missed its certificate before: later cold starts take the full solve
   bool fast_used = false;      // this sweep's factor came from the fast path (verdict still to be checked)
 
   void release() {
@@ -397,15 +399,16 @@ void cholqr(tp_ctx* ctx, const SubspaceIo& io, LeafScratch& s, int rows, int b, 
 // own, only its span matters) to Ritz vectors
 // (ascending) and values in the returned buffer / s.theta, and the certificate in s.verdict.  Touches only device
 // memory owned by `s` plus `gram` (read), with no host decision inside -- it is what the CUDA graph records.
-const double* subspace_body(tp_ctx* ctx, const SubspaceIo& io, LeafScratch& s, const double* gram, int rows, int k) {
+const double* subspace_body(tp_ctx* ctx, const SubspaceIo& io, LeafScratch& s, const double* gram, int rows, int k,
+                            int power_steps = kSubspacePowerSteps) {
   const int b = s.block;
   const double one = 1.0, zero = 0.0;
   double *q = s.q, *z = s.z, *x = s.x;
   TPB_CUDA(cudaMemsetAsync(s.verdict, 0, 4 * sizeof(int), io.stream));
-  for (int step = 0; step < kSubspacePowerSteps; ++step) {
+  for (int step = 0; step < power_steps; ++step) {
     TPB_BLAS(cublasDgemm(io.blas, CUBLAS_OP_N, CUBLAS_OP_N, rows, b, rows, &one, gram, rows, q, rows, &zero, z, rows));
     std::swap(q, z);
-    cholqr(ctx, io, s, rows, b, q, step + 1 == kSubspacePowerSteps ? 2 : 1);
+    cholqr(ctx, io, s, rows, b, q, step + 1 == power_steps ? 2 : 1);
   }
   // Rayleigh-Ritz on span(Q): H = Q^T G Q, H = V Theta V^T (ascending), X = Q V
   TPB_BLAS(cublasDgemm(io.blas, CUBLAS_OP_N, CUBLAS_OP_N, rows, b, rows, &one, gram, rows, q, rows, &zero, z, rows));
@@ -425,7 +428,7 @@ const double* subspace_body(tp_ctx* ctx, const SubspaceIo& io, LeafScratch& s, c
   TPB_BLAS(cublasDgemm(io.blas, CUBLAS_OP_N, CUBLAS_OP_N, rows, b, b, &one, z, rows, v, b, &zero, q, rows));
   TPB_CUDA(launch_ritz_residuals(io.stream, q, x, s.theta, rows, b, k, kSubspaceTol, s.verdict));
   ctx->own_kernels += 1;
-  ctx->library_calls += kSubspacePowerSteps + 4;
+  ctx->library_calls += power_steps + 4;
   return x;
 }
 
@@ -573,6 +576,7 @@ struct tp_plan {
   // path of the TTM tree it produces, with the new factors, exactly the intermediates the NEXT sweep's walk needs at
   // those nodes.  They are kept (own buffers) and the next walk starts from them, so per sweep every tree node is
   // computed once and the core costs one small extra product instead of a second pass over the tensor.
+  bool factors_from_caller = true;            // no sweep has run since the factors were set
   bool carry_enabled = true;
   std::vector<int> carry_nodes;               // TTM nodes of the path, root child first (empty: no carrying)
   int carry_leaf_mode = -1;                   // mode of the leaf the path ends in = last product of the core chain
@@ -666,9 +670,12 @@ void plan_leaf_solve(tp_ctx* ctx, tp_plan* p, int mode, int node, double* dst, b
   Span evd(ctx, p, kEvd, node, aux);
   LeafScratch& slot = p->leaf[mode];
   slot.fast_used = false;
-  if (p->fast_evd && p->sweep_kind == TP_SWEEP_JACOBI && slot.failures < 2 &&
+  // cold: the start factors are the caller's (plan creation / tp_plan_set_factors), not a previous sweep's result
+  const bool cold = p->factors_from_caller;
+  if (p->fast_evd && p->sweep_kind == TP_SWEEP_JACOBI && slot.failures < 2 && !(cold && slot.cold_rejected) &&
       subspace_eligible(rows, k, plan_leaf_columns(p, mode))) {
     subspace_reserve(ctx, slot, rows, k);
+    slot.was_cold = cold;
     leaf_solve_subspace(ctx, slot, slot.gram, rows, k, p->cur[mode], dst, aux);
   } else {
     leaf_solve(ctx, slot, rows, k, dst, aux);
@@ -725,7 +732,10 @@ std::vector<int> verify_fast_leaves(tp_ctx* ctx, tp_plan* p) {
                    m, s.block, host[4 * m], host[4 * m + 1], host[4 * m + 2], host[4 * m + 3], s.graph_state);
     if (bad) {
       rejected.push_back(m);
-      ++s.failures;
+      if (s.was_cold)
+        s.cold_rejected = true;  // arbitrary start factors need more than the fixed schedule on this problem
+      else
+        ++s.failures;
       s.last_ritz = nullptr;
       TPB_CUDA(cudaMemsetAsync(s.flag, 0, sizeof(int), ctx->stream));
     } else {
@@ -1427,6 +1437,7 @@ int tp_plan_set_factors(tp_ctx* ctx, tp_plan* p, const double* const* factors) {
                                cudaMemcpyHostToDevice, ctx->stream));
     }
     p->carry_valid = false;
+    p->factors_from_caller = true;
     for (LeafScratch& slot : p->leaf) slot.last_ritz = nullptr;  // the caller's factors are the start, not ours
     TPB_CUDA(cudaStreamSynchronize(ctx->stream));
   });
@@ -1511,6 +1522,7 @@ int tp_plan_sweep(tp_ctx* ctx, tp_plan* p, const tp_tensor* t, tp_sweep_stats* s
         plan_core(ctx, p, t->data, p->fresh);
       }
       std::swap(p->cur, p->fresh);
+      p->factors_from_caller = false;
       plan_mark_carried(p, t);
     } else {
       {

@@ -18,39 +18,58 @@ constexpr int kSmallThreads = 512;
 constexpr int kSmallWarps = kSmallThreads / 32;
 
 // L L^T = S for the symmetric positive definite b x b matrix S (column-major, full storage).  Single CTA, S lives in
-// shared memory; warps own trailing columns, lanes rows.  *fail |= 1 when a pivot is not positive (rank-deficient
-// iteration block -> the caller falls back to the full eigen-solve).
+// shared memory; warps own trailing columns, lanes rows.  The trailing update works on the unscaled column,
+// S(i,k) -= S(i,j) S(k,j) / d_j, so a step needs one barrier; the columns are scaled by 1/sqrt(d_j) on the way out.
+// *fail |= 1 when a pivot is not positive (rank-deficient iteration block -> the caller falls back to the full
+// eigen-solve).
 __global__ void __launch_bounds__(kSmallThreads) cholesky_kernel(const double* __restrict__ s_in, int b,
                                                                  double* __restrict__ l_out, int* __restrict__ fail) {
   extern __shared__ double sm[];  // b x b, column-major
   __shared__ double pivot[kMaxBlock];
-  __shared__ int bad;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int e = tid; e < b * b; e += kSmallThreads) sm[e] = s_in[e];
-  if (tid == 0) bad = 0;
+  for (int e = tid; e < kMaxBlock; e += kSmallThreads) pivot[e] = 1.0;
   __syncthreads();
+  bool bad = false;
   for (int j = 0; j < b; ++j) {
-    const double d = sm[j * b + j];  // final since the previous trailing update; nobody writes it again
+    const double d = sm[j * b + j];  // final since the previous step's barrier; nobody writes it again
     if (!(d > 0.0)) {                // uniform: every thread reads the same value
-      if (tid == 0) bad = 1;
+      bad = true;
       break;
     }
-    const double piv = sqrt(d);
-    for (int i = j + 1 + tid; i < b; i += kSmallThreads) sm[j * b + i] /= piv;
-    if (tid == 0) pivot[j] = piv;
-    __syncthreads();
-    // trailing update of the lower triangle: S(i, k) -= L(i, j) L(k, j), k > j, i >= k
+    if (tid == 0) pivot[j] = sqrt(d);
+    const double dinv = 1.0 / d;
+    // this lane's rows of column j, shared by every trailing column the warp updates (b <= 112: four row passes)
+    constexpr int kPasses = (kMaxBlock + 31) / 32;
+    double cj[kPasses];
+#pragma unroll
+    for (int r = 0; r < kPasses; ++r) {
+      const int i = lane + 32 * r;
+      cj[r] = (i > j && i < b) ? sm[j * b + i] : 0.0;
+    }
     for (int k = j + 1 + warp; k < b; k += kSmallWarps) {
-      const double lkj = sm[j * b + k];
-      for (int i = k + lane; i < b; i += 32) sm[k * b + i] = fma(-sm[j * b + i], lkj, sm[k * b + i]);
+      const double skj = sm[j * b + k] * dinv;
+      double v[kPasses];
+#pragma unroll
+      for (int r = 0; r < kPasses; ++r) {
+        const int i = lane + 32 * r;
+        v[r] = (i >= k && i < b) ? sm[k * b + i] : 0.0;
+      }
+#pragma unroll
+      for (int r = 0; r < kPasses; ++r) {
+        const int i = lane + 32 * r;
+        if (i >= k && i < b) sm[k * b + i] = fma(-cj[r], skj, v[r]);
+      }
     }
     __syncthreads();
   }
   __syncthreads();
   if (tid == 0 && bad) atomicOr(fail, 1);
-  for (int col = warp; col < b; col += kSmallWarps)
+  for (int col = warp; col < b; col += kSmallWarps) {
+    const double piv = pivot[col];
     for (int row = lane; row < b; row += 32)
-      l_out[col * b + row] = row > col ? sm[col * b + row] : (row == col ? (bad ? 1.0 : pivot[col]) : 0.0);
+      l_out[col * b + row] = row > col ? sm[col * b + row] / piv : (row == col ? piv : 0.0);
+  }
 }
 
 // Z <- Z L^{-T} (Z: n x b column-major, in place): every row x solves x L^T = z.  A row is spread over 8 lanes, lane
@@ -109,7 +128,10 @@ __global__ void __launch_bounds__(kTrsmThreads) trsm_right_lt_kernel(double* __r
 // matching eigenvectors as columns of v_out (b x b column-major).
 // *fail |= 2 if the off-diagonal mass has not vanished after kMaxSweeps sweeps; fail[1] = max(fail[1], sweeps used).
 constexpr int kMaxSweeps = 30;
-__global__ void __launch_bounds__(kSmallThreads) jacobi_eig_kernel(const double* __restrict__ h_in, int b,
+// Instantiated per block-size class: (512 threads, b <= 32), (1024, b <= 64: latency-bound, one round of column
+// pairs per step), (512, b <= 112: shared-memory-bandwidth-bound, the batched loads want the registers).
+template <int kJacobiThreads, int kBlockCap>
+__global__ void __launch_bounds__(kJacobiThreads) jacobi_eig_kernel(const double* __restrict__ h_in, int b,
                                                                    double* __restrict__ w, double* __restrict__ v_out,
                                                                    int* __restrict__ fail) {
   extern __shared__ double sm[];
@@ -119,9 +141,10 @@ __global__ void __launch_bounds__(kSmallThreads) jacobi_eig_kernel(const double*
   double* const v = sm + m * m;  // m x m
   __shared__ double rot_c[kMaxBlock / 2], rot_s[kMaxBlock / 2];
   __shared__ int rot_p[kMaxBlock / 2], rot_q[kMaxBlock / 2];
-  __shared__ double red[2 * kSmallWarps];
+  constexpr int kJacobiWarps = kJacobiThreads / 32;
+  __shared__ double red[2 * kJacobiWarps];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int col = warp; col < m; col += kSmallWarps)
+  for (int col = warp; col < m; col += kJacobiWarps)
     for (int row = lane; row < m; row += 32) {
       h[col * m + row] = (col < b && row < b) ? h_in[col * b + row] : 0.0;
       v[col * m + row] = (col == row) ? 1.0 : 0.0;
@@ -132,7 +155,7 @@ __global__ void __launch_bounds__(kSmallThreads) jacobi_eig_kernel(const double*
   for (; sweep < kMaxSweeps; ++sweep) {
     // off-diagonal mass against the whole: the backward error of a dense symmetric solver is (b eps ||H||_F)
     double off = 0.0, all = 0.0;
-    for (int col = warp; col < m; col += kSmallWarps)
+    for (int col = warp; col < m; col += kJacobiWarps)
       for (int row = lane; row < m; row += 32) {
         const double x = h[col * m + row] * h[col * m + row];
         all += x;
@@ -145,14 +168,14 @@ __global__ void __launch_bounds__(kSmallThreads) jacobi_eig_kernel(const double*
     }
     if (lane == 0) {
       red[warp] = off;
-      red[kSmallWarps + warp] = all;
+      red[kJacobiWarps + warp] = all;
     }
     __syncthreads();
     off = 0.0;
     all = 0.0;
-    for (int i = 0; i < kSmallWarps; ++i) {
+    for (int i = 0; i < kJacobiWarps; ++i) {
       off += red[i];
-      all += red[kSmallWarps + i];
+      all += red[kJacobiWarps + i];
     }
     __syncthreads();
     if (off <= (b * DBL_EPSILON) * (b * DBL_EPSILON) * all) break;  // uniform: same sums in every thread
@@ -182,30 +205,64 @@ __global__ void __launch_bounds__(kSmallThreads) jacobi_eig_kernel(const double*
         rot_s[tid] = s;
       }
       __syncthreads();
-      for (int tj = warp; tj < half; tj += kSmallWarps) {
+      // this lane's row pairs and its rows of V (as many 32-lane passes as the block cap needs) stay the same for
+      // every column pair the warp visits in this step
+      constexpr int kPairPasses = (kBlockCap / 2 + 31) / 32;
+      constexpr int kRowPasses = (kBlockCap + 31) / 32;
+      int pi[kPairPasses], qi[kPairPasses];
+      double ci[kPairPasses], si[kPairPasses];
+#pragma unroll
+      for (int a = 0; a < kPairPasses; ++a) {
+        const int ti = lane + 32 * a;
+        const bool on = ti < half;
+        pi[a] = on ? rot_p[ti] : 0;
+        qi[a] = on ? rot_q[ti] : 0;
+        ci[a] = on ? rot_c[ti] : 1.0;
+        si[a] = on ? rot_s[ti] : 0.0;
+      }
+      for (int tj = warp; tj < half; tj += kJacobiWarps) {
         const int pj = rot_p[tj], qj = rot_q[tj];
         const double cj = rot_c[tj], sj = rot_s[tj];
         double* const hp = h + pj * m;
         double* const hq = h + qj * m;
-        for (int ti = lane; ti < half; ti += 32) {
-          const int pi = rot_p[ti], qi = rot_q[ti];
-          const double ci = rot_c[ti], si = rot_s[ti];
-          const double a = hp[pi], bq = hq[pi], cc = hp[qi], d = hq[qi];
-          // columns (H J_j), then rows (J_i^T ...)
-          const double a1 = cj * a - sj * bq, b1 = sj * a + cj * bq;
-          const double c1 = cj * cc - sj * d, d1 = sj * cc + cj * d;
-          const bool diag = ti == tj;
-          hp[pi] = ci * a1 - si * c1;
-          hp[qi] = diag ? 0.0 : si * a1 + ci * c1;
-          hq[pi] = diag ? 0.0 : ci * b1 - si * d1;
-          hq[qi] = si * b1 + ci * d1;
-        }
         double* const vp = v + pj * m;
         double* const vq = v + qj * m;
-        for (int r = lane; r < m; r += 32) {
-          const double x = vp[r], y = vq[r];
-          vp[r] = cj * x - sj * y;
-          vq[r] = sj * x + cj * y;
+        // all loads of the column pair first, then the arithmetic, then the stores: the blocks are disjoint
+        double ha[kPairPasses], hb[kPairPasses], hc[kPairPasses], hd[kPairPasses];
+        double vx[kRowPasses], vy[kRowPasses];
+#pragma unroll
+        for (int a = 0; a < kPairPasses; ++a) {
+          ha[a] = hp[pi[a]];
+          hb[a] = hq[pi[a]];
+          hc[a] = hp[qi[a]];
+          hd[a] = hq[qi[a]];
+        }
+#pragma unroll
+        for (int r = 0; r < kRowPasses; ++r) {
+          const int row = lane + 32 * r;
+          vx[r] = row < m ? vp[row] : 0.0;
+          vy[r] = row < m ? vq[row] : 0.0;
+        }
+#pragma unroll
+        for (int a = 0; a < kPairPasses; ++a) {
+          const int ti = lane + 32 * a;
+          if (ti >= half) continue;
+          // columns (H J_j), then rows (J_i^T ...)
+          const double a1 = cj * ha[a] - sj * hb[a], b1 = sj * ha[a] + cj * hb[a];
+          const double c1 = cj * hc[a] - sj * hd[a], d1 = sj * hc[a] + cj * hd[a];
+          const bool diag = ti == tj;
+          hp[pi[a]] = ci[a] * a1 - si[a] * c1;
+          hp[qi[a]] = diag ? 0.0 : si[a] * a1 + ci[a] * c1;
+          hq[pi[a]] = diag ? 0.0 : ci[a] * b1 - si[a] * d1;
+          hq[qi[a]] = si[a] * b1 + ci[a] * d1;
+        }
+#pragma unroll
+        for (int r = 0; r < kRowPasses; ++r) {
+          const int row = lane + 32 * r;
+          if (row < m) {
+            vp[row] = cj * vx[r] - sj * vy[r];
+            vq[row] = sj * vx[r] + cj * vy[r];
+          }
         }
       }
       __syncthreads();
@@ -216,7 +273,7 @@ __global__ void __launch_bounds__(kSmallThreads) jacobi_eig_kernel(const double*
     atomicMax(fail + 1, sweep);
   }
   // ascending order by rank (ties by index); eigenvectors follow their values
-  for (int i = warp; i < b; i += kSmallWarps) {
+  for (int i = warp; i < b; i += kJacobiWarps) {
     const double li = h[i * m + i];
     int rank = 0;
     for (int j = lane; j < b; j += 32) {
@@ -259,11 +316,23 @@ cudaError_t launch_trsm_right_lt(cudaStream_t stream, double* z, int n, int b, c
 }
 
 cudaError_t launch_jacobi_eig(cudaStream_t stream, const double* h, int b, double* w, double* v, int* fail) {
-  static bool configured = false;
-  cudaError_t e = allow_shared(jacobi_eig_kernel, sizeof(double) * 2 * kMaxBlock * kMaxBlock, configured);
-  if (e != cudaSuccess) return e;
+  static bool configured[3] = {false, false, false};
   const int m = (b + 1) & ~1;
-  jacobi_eig_kernel<<<1, kSmallThreads, sizeof(double) * 2 * m * m, stream>>>(h, b, w, v, fail);
+  const size_t smem = sizeof(double) * 2 * m * m;
+  cudaError_t e;
+  if (b <= 32) {
+    e = allow_shared(jacobi_eig_kernel<512, 32>, sizeof(double) * 2 * 32 * 32, configured[0]);
+    if (e != cudaSuccess) return e;
+    jacobi_eig_kernel<512, 32><<<1, 512, smem, stream>>>(h, b, w, v, fail);
+  } else if (b <= 64) {
+    e = allow_shared(jacobi_eig_kernel<1024, 64>, sizeof(double) * 2 * 64 * 64, configured[1]);
+    if (e != cudaSuccess) return e;
+    jacobi_eig_kernel<1024, 64><<<1, 1024, smem, stream>>>(h, b, w, v, fail);
+  } else {
+    e = allow_shared(jacobi_eig_kernel<512, kMaxBlock>, sizeof(double) * 2 * kMaxBlock * kMaxBlock, configured[2]);
+    if (e != cudaSuccess) return e;
+    jacobi_eig_kernel<512, kMaxBlock><<<1, 512, smem, stream>>>(h, b, w, v, fail);
+  }
   return cudaGetLastError();
 }
 
