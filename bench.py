@@ -419,7 +419,8 @@ def main():
     ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--distributed", action="store_true", help="force the grid executor at N=1 (run under torchrun)")
-    ap.add_argument("--grid", default=None, help="override the optimal static grid, e.g. 2x2x2")
+    ap.add_argument("--grid", default=None,
+                    help="override the optimal static grid, e.g. 2x2x2; 'dynamic' = per-node grids (optimal_dynamic_scheme)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

@@ -129,6 +129,23 @@ int tp_optimal_static_grid(int n_modes, const tp_u64* L, const tp_u64* K, int n_
                            const int* mode, const int* parent, tp_u64 procs, int threads, tp_u64* q_out,
                            tp_u64* total, tp_u64* per_node_ttm);
 
+/* Per-node grids — grid_dynamic.hpp.  A scheme = the root's anchor grid + one grid per TTM node; node_grids is
+ * n_nodes x n_modes row-major, rows of the root and of leaves are ignored on input and zero on output.
+ * scheme_volume — grid_dynamic.hpp:37-62: per node (q_n - 1)|Out_u| plus |In_u| where the grid differs from the
+ * parent's; per_node_ttm / per_node_regrid have n_nodes entries and may be NULL. */
+int tp_scheme_volume(int n_modes, const tp_u64* L, const tp_u64* K, int n_nodes, const int* kind, const int* mode,
+                     const int* parent, const tp_u64* root_grid, const tp_u64* node_grids, tp_u64 procs,
+                     tp_u64* total, tp_u64* per_node_ttm, tp_u64* per_node_regrid);
+/* optimal_dynamic_scheme — grid_dynamic.hpp:141-167 (ties: keep the parent's grid; first regrid target in
+ * enumeration order); legacy_target != 0 = DynamicOptions::legacy_regrid_target (grid_dynamic.hpp:64-66). */
+int tp_optimal_dynamic_scheme(int n_modes, const tp_u64* L, const tp_u64* K, int n_nodes, const int* kind,
+                              const int* mode, const int* parent, tp_u64 procs, int legacy_target,
+                              tp_u64* root_grid_out, tp_u64* node_grids_out, tp_u64* total, tp_u64* per_node_ttm,
+                              tp_u64* per_node_regrid);
+/* count_moved — simulate.hpp:104-121: elements of a tensor with extents ext whose owner rank differs between the
+ * two grids (what a regrid ships, summed over ranks). */
+int tp_count_moved(int n_modes, const tp_u64* ext, const tp_u64* from_grid, const tp_u64* to_grid, tp_u64* out);
+
 /* --------------------------------------------------------- seeded host data
  * libstdc++ mt19937_64 + ONE normal_distribution<double>(0,1) object. */
 

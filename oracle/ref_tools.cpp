@@ -14,6 +14,8 @@
 //               itself needs Eigen and cannot be compiled here)
 //   blocks    — block_bounds / block_of                  (grid.hpp:114-125)
 //   psi       — grid_count                                (grid.hpp:49-70)
+//   dynamic   — optimal_dynamic_scheme (both objectives) / scheme_volume / simulate_distribution in trace mode
+//               where its guards allow (grid_dynamic.hpp:141-167, simulate.hpp:123-178)
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -122,6 +124,63 @@ static int cmd_plan(int argc, char** argv) {
   return 0;
 }
 
+static tp::TtmTree tree_by_name(const std::string& name, const tp::ProblemSpec& s) {
+  if (name == "opt") return tp::optimal_tree(s).tree;
+  if (name == "chain") return tp::chain_tree(s, tp::ChainOrder::input);
+  if (name == "chain_by_cost") return tp::chain_tree(s, tp::ChainOrder::by_cost);
+  if (name == "balanced") return tp::balanced_tree(s);
+  throw tp::Error(tp::Errc::bad_argument, "unknown tree name");
+}
+
+static std::string scheme_json(const tp::TtmTree& t, const tp::ProblemSpec& s, const tp::DynamicSchemeResult& r,
+                               u64 procs) {
+  std::string out = "{\"root\":" + arr(r.scheme.root.q) + ",\"total\":" + std::to_string(r.report.total);
+  std::vector<int> ids;
+  std::vector<u64> ttm, regrid;
+  std::string grids = "[";
+  for (const auto& nv : r.report.per_node) {
+    if (!ids.empty()) grids += ",";
+    ids.push_back(nv.node);
+    ttm.push_back(nv.ttm);
+    regrid.push_back(nv.regrid);
+    grids += arr(r.scheme.node_grids.at(nv.node).q);
+  }
+  out += ",\"nodes\":" + arr(ids) + ",\"node_grids\":" + grids + "]";
+  out += ",\"ttm\":" + arr(ttm) + ",\"regrid\":" + arr(regrid);
+  if (tp::input_cardinality(s) <= tp::kTraceMaxElements && procs <= tp::kTraceMaxProcs) {
+    const tp::SimLedger led = tp::simulate_distribution(t, s, r.scheme, procs, true);
+    std::vector<u64> mt, mr;
+    for (const auto& nt : led.nodes) {
+      mt.push_back(nt.measured_ttm);
+      mr.push_back(nt.measured_regrid);
+    }
+    out += ",\"traced_ttm\":" + arr(mt) + ",\"traced_regrid\":" + arr(mr);
+  }
+  return out + "}";
+}
+
+static int cmd_dynamic(int argc, char** argv) {
+  if (argc < 6) return 2;
+  tp::ProblemSpec s{parse_list(argv[2]), parse_list(argv[3])};
+  const u64 procs = std::strtoull(argv[4], nullptr, 10);
+  const std::string name = argv[5];
+  try {
+    const tp::TtmTree t = tree_by_name(name, s);
+    std::string out = "{\"L\":" + arr(s.L) + ",\"K\":" + arr(s.K) + ",\"procs\":" + std::to_string(procs);
+    out += ",\"tree_name\":\"" + name + "\",\"tree\":" + tree_json(t, s);
+    tp::DynamicOptions legacy;
+    legacy.legacy_regrid_target = true;
+    out += ",\"scheme\":" + scheme_json(t, s, tp::optimal_dynamic_scheme(t, s, procs), procs);
+    out += ",\"legacy\":" + scheme_json(t, s, tp::optimal_dynamic_scheme(t, s, procs, legacy), procs);
+    out += ",\"static_total\":" + std::to_string(tp::optimal_static_grid(t, s, procs).report.total);
+    std::puts((out + "}").c_str());
+  } catch (const tp::Error& e) {
+    std::printf("{\"L\":%s,\"K\":%s,\"procs\":%llu,\"tree_name\":\"%s\",\"error\":%d}\n", arr(s.L).c_str(),
+                arr(s.K).c_str(), (unsigned long long)procs, name.c_str(), static_cast<int>(e.code()));
+  }
+  return 0;
+}
+
 static int write_raw(const char* path, const std::vector<double>& v) {
   FILE* f = std::fopen(path, "wb");
   if (!f) return 1;
@@ -134,6 +193,7 @@ int main(int argc, char** argv) {
   if (argc < 2) return 2;
   const std::string cmd = argv[1];
   if (cmd == "plan") return cmd_plan(argc, argv);
+  if (cmd == "dynamic") return cmd_dynamic(argc, argv);
   if (cmd == "tensor" && argc == 5) {
     const std::vector<u64> d = parse_list(argv[2]);
     const tp::DenseTensor t =

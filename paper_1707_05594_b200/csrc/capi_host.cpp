@@ -177,6 +177,56 @@ int tp_optimal_static_grid(int n, const tp_u64* L, const tp_u64* K, int n_nodes,
   });
 }
 
+static Scheme scheme_from_arrays(const Tree& t, int n, const tp_u64* root_grid, const tp_u64* node_grids) {
+  if (!root_grid || !node_grids) raise(TP_ERR_BAD_ARGUMENT, "null grid array");
+  Scheme sc;
+  sc.root.assign(root_grid, root_grid + n);
+  sc.node.assign(t.size(), Grid{});
+  for (int id = 0; id < t.size(); ++id)
+    if (t.internal(id)) sc.node[id].assign(node_grids + static_cast<size_t>(id) * n, node_grids + static_cast<size_t>(id + 1) * n);
+  return sc;
+}
+
+static void scheme_volume_out(const SchemeVolume& v, tp_u64* total, tp_u64* per_node_ttm, tp_u64* per_node_regrid) {
+  if (total) *total = v.total;
+  if (per_node_ttm) std::memcpy(per_node_ttm, v.ttm.data(), v.ttm.size() * sizeof(u64));
+  if (per_node_regrid) std::memcpy(per_node_regrid, v.regrid.data(), v.regrid.size() * sizeof(u64));
+}
+
+int tp_scheme_volume(int n, const tp_u64* L, const tp_u64* K, int n_nodes, const int* kind, const int* mode,
+                     const int* parent, const tp_u64* root_grid, const tp_u64* node_grids, tp_u64 procs,
+                     tp_u64* total, tp_u64* per_node_ttm, tp_u64* per_node_regrid) {
+  return guarded([&] {
+    const Tree t = tree_from_arrays(n, n_nodes, kind, mode, parent);
+    const Scheme sc = scheme_from_arrays(t, n, root_grid, node_grids);
+    scheme_volume_out(scheme_volume(t, make_spec(n, L, K), sc, procs), total, per_node_ttm, per_node_regrid);
+  });
+}
+
+int tp_optimal_dynamic_scheme(int n, const tp_u64* L, const tp_u64* K, int n_nodes, const int* kind, const int* mode,
+                              const int* parent, tp_u64 procs, int legacy_target, tp_u64* root_grid_out,
+                              tp_u64* node_grids_out, tp_u64* total, tp_u64* per_node_ttm, tp_u64* per_node_regrid) {
+  return guarded([&] {
+    if (!root_grid_out || !node_grids_out) raise(TP_ERR_BAD_ARGUMENT, "null grid array");
+    const Tree t = tree_from_arrays(n, n_nodes, kind, mode, parent);
+    const DynamicScheme r = optimal_dynamic_scheme(t, make_spec(n, L, K), procs, legacy_target != 0);
+    for (int m = 0; m < n; ++m) root_grid_out[m] = r.scheme.root[m];
+    for (int id = 0; id < t.size(); ++id)
+      for (int m = 0; m < n; ++m)
+        node_grids_out[static_cast<size_t>(id) * n + m] = r.scheme.node[id].empty() ? 0 : r.scheme.node[id][m];
+    scheme_volume_out(r.volume, total, per_node_ttm, per_node_regrid);
+  });
+}
+
+int tp_count_moved(int n, const tp_u64* ext, const tp_u64* from_grid, const tp_u64* to_grid, tp_u64* out) {
+  return guarded([&] {
+    if (n <= 0 || !ext || !from_grid || !to_grid || !out) raise(TP_ERR_BAD_ARGUMENT, "null argument");
+    for (int m = 0; m < n; ++m)
+      if (ext[m] == 0 || from_grid[m] == 0 || to_grid[m] == 0) raise(TP_ERR_INVALID_GRID, "zero extent", m);
+    *out = count_moved(std::vector<u64>(ext, ext + n), Grid(from_grid, from_grid + n), Grid(to_grid, to_grid + n));
+  });
+}
+
 int tp_random_tensor(int n_modes, const size_t* dims, tp_u64 seed, double* out) {
   return guarded([&] {
     if (n_modes <= 0 || !dims) raise(TP_ERR_BAD_DIMS, "tensor needs at least one mode");

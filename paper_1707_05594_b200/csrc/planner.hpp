@@ -11,6 +11,7 @@
 //   grid.hpp:36-125, grid_volume.hpp:32-110.
 #pragma once
 
+#include <array>
 #include <algorithm>
 #include <future>
 #include <numeric>
@@ -612,6 +613,149 @@ inline StaticGrid optimal_static_grid(const Tree& t, const Spec& s, u64 procs, i
     }
   }
   return StaticGrid{grids[best.second], static_volume(t, s, grids[best.second], procs)};
+}
+
+// ---- per-node grids (grid_dynamic.hpp) -------------------------------------------------------------------
+// A scheme gives the root an anchor grid and every TTM node its own; a node whose grid differs from its parent's
+// first redistributes its whole input (|In_u| elements), then multiplies and pays (q_n - 1)|Out_u| as before.
+struct Scheme {
+  Grid root;
+  std::vector<Grid> node;  // indexed by node id; empty for the root and the leaves
+};
+
+struct SchemeVolume {
+  u64 total = 0;
+  std::vector<u64> ttm, regrid;  // indexed by node id
+};
+
+inline const Grid& scheme_parent_grid(const Tree& t, const Scheme& sc, int id) {
+  const int up = t.parent[id];
+  return t.kind[up] == TP_NODE_ROOT ? sc.root : sc.node[up];
+}
+
+// grid_dynamic.hpp:37-62
+inline SchemeVolume scheme_volume(const Tree& t, const Spec& s, const Scheme& sc, u64 procs) {
+  validate_grid(sc.root, s, procs);
+  const Cards cards = node_cardinalities(t, s);
+  SchemeVolume v;
+  v.ttm.assign(t.size(), 0);
+  v.regrid.assign(t.size(), 0);
+  for (int id = 0; id < t.size(); ++id) {
+    if (!t.internal(id)) continue;
+    if (id >= static_cast<int>(sc.node.size()) || sc.node[id].empty())
+      raise(TP_ERR_MISSING_ASSIGNMENT, "no grid for internal node " + std::to_string(id));
+    validate_grid(sc.node[id], s, procs);
+    if (sc.node[id] != scheme_parent_grid(t, sc, id)) v.regrid[id] = cards.in[id];
+    v.ttm[id] = mul_or_throw(sc.node[id][t.mode[id]] - 1, cards.out[id]);
+    v.total = add_or_throw(v.total, add_or_throw(v.ttm[id], v.regrid[id]));
+  }
+  return v;
+}
+
+struct DynamicScheme {
+  Scheme scheme;
+  SchemeVolume volume;
+};
+
+// grid_dynamic.hpp:141-167.  below[u][g] = least volume of the subtree at TTM node u when its parent hands it grid
+// g: either keep g, or pay |In_u| and switch to the node's best grid (found once per node: it does not depend on g).
+// Ties keep the parent's grid, and among switch targets the first in enumeration order.  `legacy_target` ranks the
+// switch targets by the children's volume alone (grid_dynamic.hpp:64-66, 107-109).
+// Node ids grow from parent to child (ttm_tree.hpp:111-112), so one descending pass fills the table bottom-up and
+// one ascending pass reads the choices back.
+inline DynamicScheme optimal_dynamic_scheme(const Tree& t, const Spec& s, u64 procs, bool legacy_target = false) {
+  const std::vector<Grid> grids = enumerate_grids(procs, s);
+  if (grids.empty()) raise(TP_ERR_NO_VALID_GRID, "no grid with prod q = procs fits under K");
+  const Cards cards = node_cardinalities(t, s);
+  const std::size_t ng = grids.size();
+  std::vector<std::vector<u64>> below(t.size());
+  std::vector<u64> switch_cost(t.size(), 0);        // |In_u| + volume under the node's best grid
+  std::vector<std::size_t> switch_to(t.size(), 0);
+  auto kids_sum = [&](int id, std::size_t g) {
+    u64 sum = 0;
+    for (int c : t.kids[id])
+      if (t.internal(c)) sum = add_or_throw(sum, below[c][g]);
+    return sum;
+  };
+  auto own = [&](int id, std::size_t g) { return mul_or_throw(grids[g][t.mode[id]] - 1, cards.out[id]); };
+  for (int id = t.size() - 1; id > 0; --id) {
+    if (!t.internal(id)) continue;
+    std::vector<u64> keep(ng);
+    u64 best_rank = kSat;
+    std::size_t arg = 0;
+    for (std::size_t g = 0; g < ng; ++g) {
+      const u64 kids = kids_sum(id, g);
+      keep[g] = add_or_throw(own(id, g), kids);
+      const u64 rank = legacy_target ? kids : keep[g];
+      if (rank < best_rank) {
+        best_rank = rank;
+        arg = g;
+      }
+    }
+    switch_to[id] = arg;
+    switch_cost[id] = add_or_throw(cards.in[id], keep[arg]);
+    below[id].resize(ng);
+    for (std::size_t g = 0; g < ng; ++g) below[id][g] = std::min(keep[g], switch_cost[id]);
+  }
+  // the root's grid is free: it only anchors its children
+  std::size_t root_g = 0;
+  u64 best = kSat;
+  for (std::size_t g = 0; g < ng; ++g) {
+    const u64 v = kids_sum(0, g);
+    if (v < best) {
+      best = v;
+      root_g = g;
+    }
+  }
+  DynamicScheme out;
+  out.scheme.root = grids[root_g];
+  out.scheme.node.assign(t.size(), Grid{});
+  std::vector<std::size_t> chosen(t.size(), root_g);
+  for (int id = 1; id < t.size(); ++id) {
+    if (!t.internal(id)) continue;
+    const std::size_t from = chosen[t.parent[id]];
+    const u64 keep = add_or_throw(own(id, from), kids_sum(id, from));
+    chosen[id] = keep <= switch_cost[id] ? from : switch_to[id];
+    out.scheme.node[id] = grids[chosen[id]];
+  }
+  out.volume = scheme_volume(t, s, out.scheme, procs);
+  return out;
+}
+
+// simulate.hpp:104-121: elements of a tensor with extents `ext` whose owner rank changes between two grids.
+// Counted per mode-wise overlap of the two block partitions instead of element by element.
+inline u64 count_moved(const std::vector<u64>& ext, const Grid& from, const Grid& to) {
+  const int n = static_cast<int>(ext.size());
+  // stay[m][(a, b)] = coordinates of mode m that lie in block a of `from` and block b of `to`
+  std::vector<std::vector<std::array<u64, 3>>> pieces(n);
+  for (int m = 0; m < n; ++m) {
+    const std::vector<u64> ca = block_bounds(ext[m], from[m]), cb = block_bounds(ext[m], to[m]);
+    for (u64 a = 0; a < from[m]; ++a)
+      for (u64 b = 0; b < to[m]; ++b) {
+        const u64 lo = std::max(ca[a], cb[b]), hi = std::min(ca[a + 1], cb[b + 1]);
+        if (hi > lo) pieces[m].push_back({a, b, hi - lo});
+      }
+  }
+  u64 total = 1, same = 0;
+  for (int m = 0; m < n; ++m) total = mul_or_throw(total, ext[m]);
+  // walk the product of the per-mode pieces, accumulating both ranks
+  std::vector<std::size_t> at(n, 0);
+  for (int m = 0; m < n; ++m)
+    if (pieces[m].empty()) return 0;
+  while (true) {
+    u64 ra = 0, rb = 0, elems = 1;
+    for (int m = 0; m < n; ++m) {
+      const auto& pc = pieces[m][at[m]];
+      ra = ra * from[m] + pc[0];
+      rb = rb * to[m] + pc[1];
+      elems *= pc[2];
+    }
+    if (ra == rb) same += elems;
+    int carry = n;
+    while (carry > 0 && ++at[carry - 1] == pieces[carry - 1].size()) at[--carry] = 0;
+    if (carry == 0) break;
+  }
+  return total - same;
 }
 
 }  // namespace tpb

@@ -200,18 +200,25 @@ class SweepResult:
     core_macs: int = 0
     peak_live: int = 0
     degenerate: bool = False
-    volume_sent: Dict[int, int] = field(default_factory=dict)   # tree node -> elements this rank shipped
+    volume_sent: Dict[int, int] = field(default_factory=dict)   # tree node -> elements this rank shipped (TTM)
+    regrid_sent: Dict[int, int] = field(default_factory=dict)   # tree node -> elements this rank shipped (regrid)
 
 
 class DistributedHooi:
-    """One rank's share of Jacobi HOOI sweeps (hooi.hpp:189-229) on a static grid."""
+    """One rank's share of Jacobi HOOI sweeps (hooi.hpp:189-229) on a static grid, or on a per-node scheme
+    (grid_dynamic.hpp: `q` may be a planner.DynamicGridScheme; the tensor and the core live on its root grid, a node
+    whose grid differs from its parent's first redistributes its input)."""
 
-    def __init__(self, ops, spec: P.ProblemSpec, tree: P.TtmTree, q: Sequence[int], rank: int):
+    def __init__(self, ops, spec: P.ProblemSpec, tree: P.TtmTree, q, rank: int):
         self.ops, self.spec, self.tree, self.rank = ops, spec, tree, int(rank)
-        self.layout = GridLayout(q)
+        scheme = q if isinstance(q, P.DynamicGridScheme) else P.uniform_scheme(tree, q)
+        self.scheme = scheme
+        self.layout = GridLayout(scheme.root)
         self.n = spec.n_modes()
         P.validate_tree(tree, spec)
-        P.validate_grid(self.layout.q, spec, self.layout.procs)
+        P.scheme_volume(tree, spec, scheme, self.layout.procs)      # validates every grid, missing_assignment
+        self.node_layout = {node: (self.layout if list(g) == list(self.layout.q) else GridLayout(g))
+                            for node, g in scheme.node_grids.items()}
         if not 0 <= self.rank < self.layout.procs:
             raise ValueError("rank outside the grid")
         self.cost = P.tree_cost(tree, spec)
@@ -247,9 +254,10 @@ class DistributedHooi:
             self.events(what, node)
 
     # -- distributed mode product -------------------------------------------------------------------
-    def _ttm(self, x, ext, ldims, mode, factor, node, result: SweepResult):
+    def _ttm(self, x, ext, ldims, mode, factor, node, result: SweepResult, lay: Optional[GridLayout] = None):
         """x: local block with global extents ext / local dims ldims; returns (z, new_ext, new_ldims)."""
-        lay, q_n = self.layout, self.layout.q[mode]
+        lay = lay or self.layout
+        q_n = lay.q[mode]
         k, l_full = self.spec.K[mode], self.spec.L[mode]
         l0, _ = lay.local_range(self.rank, mode, ext[mode])
         new_ext = list(ext)
@@ -283,8 +291,9 @@ class DistributedHooi:
         return z, new_ext, new_ldims
 
     # -- leaf: Gram (all ranks) + eigen-solve -------------------------------------------------------
-    def _leaf(self, y, ext, ldims, mode, result: SweepResult, statuses: list):
-        lay, q_n = self.layout, self.layout.q[mode]
+    def _leaf(self, y, ext, ldims, mode, result: SweepResult, statuses: list, lay: Optional[GridLayout] = None):
+        lay = lay or self.layout
+        q_n = lay.q[mode]
         rows, k = self.spec.L[mode], self.spec.K[mode]
         outer = int(np.prod(ldims[:mode], dtype=np.int64)) if mode else 1
         inner = int(np.prod(ldims[mode + 1:], dtype=np.int64)) if mode + 1 < self.n else 1
@@ -327,21 +336,32 @@ class DistributedHooi:
         fresh: List[object] = [None] * self.n
         tree = self.tree
 
-        def walk(node, x, ext, ldims):
+        def walk(node, x, ext, ldims, lay):
             for c in tree.children[node]:
                 mode = tree.mode[c]
                 if tree.kind[c] == P.LEAF:
                     self._mark("begin_leaf", c)
-                    fresh[mode] = yield from self._leaf(x, ext, ldims, mode, res, statuses)
+                    fresh[mode] = yield from self._leaf(x, ext, ldims, mode, res, statuses, lay)
                     self._mark("end_leaf", c)
                 else:
+                    xin, lin, target = x, ldims, self.node_layout[c]
+                    if target.q != lay.q:
+                        # the node runs on its own grid: redistribute its input first (the paper's regrid)
+                        self._mark("begin_regrid", c)
+                        sends, _ = regrid_plan(ext, lay, target, self.rank)
+                        res.regrid_sent[c] = sum(int(np.prod([hi - lo for lo, hi in o], dtype=np.int64))
+                                                 for peer, o in sends if peer != self.rank)
+                        moved = yield from regrid(x.view(ldims), ext, lay, target, self.rank, self.ops.empty)
+                        lin = target.local_dims(self.rank, ext)
+                        xin = moved.reshape(-1)
+                        self._mark("end_regrid", c)
                     self._mark("begin_ttm", c)
-                    z, e2, l2 = yield from self._ttm(x, ext, ldims, mode, self.factors[mode], c, res)
+                    z, e2, l2 = yield from self._ttm(xin, ext, lin, mode, self.factors[mode], c, res, target)
                     self._mark("end_ttm", c)
-                    yield from walk(c, z, e2, l2)
+                    yield from walk(c, z, e2, l2, target)
 
         self._mark("begin_tree")
-        yield from walk(0, self.tensor, list(self.spec.L), list(self.tensor_ldims))
+        yield from walk(0, self.tensor, list(self.spec.L), list(self.tensor_ldims), self.layout)
         self._mark("end_tree")
         # core_from_factors (hooi.hpp:93-100) in the cheapest order, with the new factors
         self._mark("begin_core")
@@ -613,7 +633,13 @@ def run_bench_rank(args, rank: int, world: int, local_rank: int):
     tree = P.optimal_tree(spec).tree
     cost = P.tree_cost(tree, spec)
     grid = P.optimal_static_grid(tree, spec, world)
-    q = grid.grid if not getattr(args, "grid", None) else [int(v) for v in args.grid.split("x")]
+    scheme = None
+    if getattr(args, "grid", None) == "dynamic":       # per-node grids (grid_dynamic.hpp): regrid where it pays
+        scheme = P.optimal_dynamic_scheme(tree, spec, world).scheme
+        q = list(scheme.root)
+    else:
+        q = grid.grid if not getattr(args, "grid", None) else [int(v) for v in args.grid.split("x")]
+    node_q = (lambda node: scheme.node_grids[node]) if scheme else (lambda node: q)
     layout = GridLayout(q)
     hbm_gbs, hbm_src = B.read_peaks()
     p_fp64, fp64_src = B.measure_fp64_peak(torch)
@@ -623,7 +649,7 @@ def run_bench_rank(args, rank: int, world: int, local_rank: int):
     t0 = time.perf_counter()
     local = build_local_block(ctx, ops, cfg, layout, rank, dist, cores)
     build_s = time.perf_counter() - t0
-    dh = DistributedHooi(ops, spec, tree, q, rank)
+    dh = DistributedHooi(ops, spec, tree, scheme or q, rank)
     dh.set_local_tensor_buffer(local)
     f0 = W.start_factors(cfg)
 
@@ -672,7 +698,7 @@ def run_bench_rank(args, rank: int, world: int, local_rank: int):
         else:
             key = (what[4:], node)
             ms = open_ev.pop(key).elapsed_time(ev)
-            if key[0] == "ttm":
+            if key[0] in ("ttm", "regrid"):
                 node_ms[node] = node_ms.get(node, 0.0) + ms
             elif key[0] == "tree":
                 tree_ms += ms
@@ -721,8 +747,13 @@ def run_bench_rank(args, rank: int, world: int, local_rank: int):
                 continue
             n = tree.mode[node]
             flops = 2 * spec.K[n] * cost.card_in[node]
-            local_bytes = 8 * (cost.card_in[node] + q[n] * cost.card_out[node]) / world + 8 * spec.K[n] * spec.L[n]
-            link_bytes = 8 * (q[n] - 1) * cost.card_out[node] / world
+            qn = node_q(node)[n]
+            local_bytes = 8 * (cost.card_in[node] + qn * cost.card_out[node]) / world + 8 * spec.K[n] * spec.L[n]
+            link_bytes = 8 * (qn - 1) * cost.card_out[node] / world
+            if scheme:
+                up = tree.parent[node]
+                if list(node_q(node)) != list(q if tree.kind[up] == P.ROOT else node_q(up)):
+                    link_bytes += 8 * cost.card_in[node] / world        # regrid: the model ships the whole input
             t = max(flops / world / (p_fp64 * 1e12), local_bytes / (hbm_gbs * 1e9)) + link_bytes / (B.NVLINK_GBS * 1e9)
             t_roof += t
             flops_total += flops
@@ -738,7 +769,10 @@ def run_bench_rank(args, rank: int, world: int, local_rank: int):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg.name, "iterations": cfg.iterations, "schedule": "jacobi on optimal_tree",
-                       "tree": tree.label(), "grid": list(q), "grid_volume_elements": P.static_volume(tree, spec, q, world).total,
+                       "tree": tree.label(), "grid": list(q),
+                       "node_grids": {str(k): list(v) for k, v in scheme.node_grids.items()} if scheme else None,
+                       "grid_volume_elements": (P.scheme_volume(tree, spec, scheme, world).total if scheme
+                                                else P.static_volume(tree, spec, q, world).total),
                        "l2": "inputs_larger_than_L2", "noise": "slab-parallel" if cfg.slab_noise else "sequential",
                        "evd": "replicated on every rank"},
             "ttm_tree": {"tflops": flops_total / (ttm_ms * 1e-3) / 1e12 if ttm_ms else None,
@@ -746,7 +780,7 @@ def run_bench_rank(args, rank: int, world: int, local_rank: int):
                          "roofline_ms": t_roof * 1e3, "flops": flops_total, "p_fp64_tflops": p_fp64,
                          "p_fp64_source": fp64_src, "hbm_gbs": hbm_gbs, "hbm_source": hbm_src,
                          "nvlink_gbs": B.NVLINK_GBS, "per_node": rows,
-                         "note": "per-node time = local kernel + chunk exchange + ordered reduction, max over ranks"},
+                         "note": "per-node time = (regrid +) local kernel + chunk exchange + ordered reduction, max over ranks"},
             "phases_ms": {"tree_phase_incl_leaves": tree_phase_ms, "core_ms": core_ms},
             "relative_fit": fit, "core_norm": core_norm, "build_s": build_s,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": p_fp64 * world, "unit": "TFLOP/s",
@@ -756,6 +790,7 @@ def run_bench_rank(args, rank: int, world: int, local_rank: int):
             "cpu_baseline": None, "e2e": e2e, "gpu_launches": int(k1 - k0), "library_calls": int(lib_calls),
             "clocks": clocks, "degenerate": bool(res.degenerate),
             "volume_sent_rank0": {str(k): v for k, v in res.volume_sent.items()},
+            "regrid_sent_rank0": {str(k): v for k, v in res.regrid_sent.items()},
         }
         print(json.dumps(line))
     dist.destroy_process_group()

@@ -241,3 +241,79 @@ def optimal_static_grid(t: TtmTree, s: ProblemSpec, procs: int, threads: int = 1
     check(lib.tp_optimal_static_grid(n, L, K, nn, kind, mode, parent, u64(procs), threads, q, ctypes.byref(total),
                                      per))
     return StaticGridResult(list(q), VolumeReport(total.value, list(per)))
+
+
+# ---- per-node grids (grid_dynamic.hpp) ---------------------------------------------------------------------
+@dataclass
+class DynamicGridScheme:
+    """grid_dynamic.hpp:32-35: the root's anchor grid + one grid per TTM node (node id -> grid)."""
+    root: List[int]
+    node_grids: dict
+
+
+@dataclass
+class SchemeVolumeReport:
+    total: int
+    per_node_ttm: List[int]      # indexed by node id, 0 for root / leaves
+    per_node_regrid: List[int]
+
+
+@dataclass
+class DynamicSchemeResult:
+    scheme: DynamicGridScheme
+    report: SchemeVolumeReport
+
+
+def uniform_scheme(t: TtmTree, q: Sequence[int]) -> DynamicGridScheme:
+    """simulate.hpp:53-61: one grid everywhere."""
+    return DynamicGridScheme(list(q), {i: list(q) for i in range(len(t.kind)) if t.kind[i] == MODE})
+
+
+def _scheme_arrays(t: TtmTree, n: int, scheme: DynamicGridScheme):
+    nn = len(t.kind)
+    flat = (u64 * (nn * n))()
+    for node, grid in scheme.node_grids.items():
+        if not 0 <= node < nn or len(grid) != n:
+            raise ValueError("scheme entry does not fit the tree")
+        for m in range(n):
+            flat[node * n + m] = int(grid[m])
+    return (u64 * n)(*[int(v) for v in scheme.root]), flat
+
+
+def scheme_volume(t: TtmTree, s: ProblemSpec, scheme: DynamicGridScheme, procs: int) -> SchemeVolumeReport:
+    """grid_dynamic.hpp:37-62."""
+    n, L, K = s._c()
+    nn, kind, mode, parent = t._c()
+    if len(scheme.root) != n:
+        raise ValueError("root grid does not fit the spec")
+    for node in range(nn):
+        if t.kind[node] == MODE and node not in scheme.node_grids:
+            raise TuckerplanError(int(Errc.missing_assignment), "no grid for internal node %d" % node)
+    root, flat = _scheme_arrays(t, n, scheme)
+    total, ttm, regrid = u64(), (u64 * nn)(), (u64 * nn)()
+    check(lib.tp_scheme_volume(n, L, K, nn, kind, mode, parent, root, flat, u64(procs), ctypes.byref(total), ttm,
+                               regrid))
+    return SchemeVolumeReport(total.value, list(ttm), list(regrid))
+
+
+def optimal_dynamic_scheme(t: TtmTree, s: ProblemSpec, procs: int, legacy_regrid_target: bool = False
+                           ) -> DynamicSchemeResult:
+    """grid_dynamic.hpp:141-167."""
+    n, L, K = s._c()
+    nn, kind, mode, parent = t._c()
+    root, flat = (u64 * n)(), (u64 * (nn * n))()
+    total, ttm, regrid = u64(), (u64 * nn)(), (u64 * nn)()
+    check(lib.tp_optimal_dynamic_scheme(n, L, K, nn, kind, mode, parent, u64(procs), 1 if legacy_regrid_target else 0,
+                                        root, flat, ctypes.byref(total), ttm, regrid))
+    grids = {i: [flat[i * n + m] for m in range(n)] for i in range(nn) if t.kind[i] == MODE}
+    return DynamicSchemeResult(DynamicGridScheme(list(root), grids),
+                               SchemeVolumeReport(total.value, list(ttm), list(regrid)))
+
+
+def count_moved(ext: Sequence[int], from_grid: Sequence[int], to_grid: Sequence[int]) -> int:
+    """simulate.hpp:104-121: elements whose owner rank differs between the two grids."""
+    n = len(ext)
+    out = u64()
+    check(lib.tp_count_moved(n, (u64 * n)(*map(int, ext)), (u64 * n)(*map(int, from_grid)),
+                             (u64 * n)(*map(int, to_grid)), ctypes.byref(out)))
+    return out.value

@@ -49,6 +49,22 @@ int main(int argc, char** argv) {
       const tp::DenseTensor t = tp::random_tensor({3, 4, 2}, 5);
       const tp::DenseTensor back = tp::fold(tp::unfold(t, 1), t.dims, 1);
       std::printf("fold %d first %.17g\n", back.data == t.data ? 1 : 0, t.data[0]);
+      // per-node grids (grid_dynamic.hpp): C4 at P = 8 is where regridding pays
+      const tp::ProblemSpec c4{{48, 48, 48, 48, 48}, {8, 8, 8, 8, 8}};
+      const tp::TtmTree t4 = tp::optimal_tree(c4).tree;
+      const tp::DynamicSchemeResult dyn = tp::optimal_dynamic_scheme(t4, c4, 8);
+      int regrids = 0;
+      for (const tp::NodeVolume& nv : dyn.report.per_node) regrids += nv.regrid ? 1 : 0;
+      std::printf("dynamic %llu regrids %d static %llu again %llu\n", (unsigned long long)dyn.report.total, regrids,
+                  (unsigned long long)tp::optimal_static_grid(t4, c4, 8).report.total,
+                  (unsigned long long)tp::scheme_volume(t4, c4, dyn.scheme, 8).total);
+      tp::DynamicGridScheme holes = dyn.scheme;
+      holes.node_grids.erase(holes.node_grids.begin());
+      try {
+        tp::scheme_volume(t4, c4, holes, 8);
+      } catch (const tp::Error& e) {
+        std::printf("error %d\n", static_cast<int>(e.code()));
+      }
       return 0;
     }
     if (cmd == "hooi") {

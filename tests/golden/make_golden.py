@@ -69,6 +69,28 @@ def main():
     with open(os.path.join(HERE, "planner_golden.json"), "w") as f:
         json.dump({"cases": cases, "psi": psi, "blocks": blocks}, f, separators=(",", ":"))
 
+    # per-node grids: optimal_dynamic_scheme (both objectives), scheme volumes, traced reduce-scatter / regrid counts
+    def dynamic(L, K, procs, tree):
+        return json.loads(run("dynamic", ",".join(map(str, L)), ",".join(map(str, K)), procs, tree))
+    dyn = []
+    for L, K in [([200] * 3, [20] * 3), ([96] * 4, [10] * 4), ([400, 100, 100, 50], [40, 10, 20, 5]),
+                 ([48] * 5, [8] * 5), ([1600] * 3, [100] * 3)]:
+        for procs in (2, 4, 8, 16, 32):
+            for tree in ("opt", "chain", "balanced"):
+                dyn.append(dynamic(L, K, procs, tree))
+    dyn.append(dynamic([672, 672, 627, 16], [279, 279, 153, 14], 32, "opt"))
+    dyn.append(dynamic([4, 4], [5, 2], 2, "opt"))          # invalid spec keeps its code
+    dyn.append(dynamic([5, 4, 3], [1, 1, 1], 2, "opt"))    # no valid grid
+    rng = random.Random(554)
+    for _ in range(140):   # small enough for the reference's trace mode (<= 1e6 elements, <= 64 procs)
+        n = rng.randint(2, 5)
+        L = [rng.randint(2, 14) for _ in range(n)]
+        K = [rng.randint(1, l) for l in L]
+        procs = rng.choice([2, 3, 4, 6, 8, 12, 16])
+        dyn.append(dynamic(L, K, procs, rng.choice(["opt", "chain", "chain_by_cost", "balanced"])))
+    with open(os.path.join(HERE, "dynamic_golden.json"), "w") as f:
+        json.dump(dyn, f, separators=(",", ":"))
+
     # seeded streams: reference random_tensor + the gaussian stream random_decomposition consumes
     streams = {}
     tmp = "/tmp/_tp_golden.bin"
@@ -86,7 +108,7 @@ def main():
         json.dump({"dims": [12, 10, 8], "tensor_seed": 7, "K": [4, 3, 2], "init_seed": 0, "scheme": "gauss_seidel",
                    "tree": "chain-input", "start_error": "0.986423815729", "sweep1_error": "0.940526801758",
                    "tree_macs": 12736, "peak_live": 3, "source": "proj/README.md:122-126"}, f, indent=1)
-    print("wrote", len(cases), "planner cases")
+    print("wrote", len(cases), "planner cases,", len(dyn), "dynamic-grid cases")
 
 
 if __name__ == "__main__":

@@ -27,6 +27,8 @@ def test_planner_through_cpp_headers(dropin):
     assert out[5] == "error 1 mode 1"                                          # Errc::k_too_large at mode 1
     assert out[6] == "error 7"                                                 # Errc::no_valid_grid
     assert out[7].startswith("fold 1 ")
+    assert out[8] == "dynamic 9437184 regrids 3 static 11010048 again 9437184"   # SURVEY §8d, grid_dynamic.hpp
+    assert out[9] == "error 8"                                                 # Errc::missing_assignment
 
 
 @pytest.mark.gpu

@@ -97,6 +97,149 @@ def test_optimal_grids_of_scaled_configs():
         run_virtual_case(NumpyOps(), L, K, q, sweeps=1)
 
 
+def node_input_extents(tree, spec, node):
+    ext = list(spec.L)
+    at = tree.parent[node]
+    while at > 0:
+        ext[tree.mode[at]] = spec.K[tree.mode[at]]
+        at = tree.parent[at]
+    return ext
+
+
+def run_scheme_case(ops, L, K, scheme, tree=None, sweeps=2):
+    """Per-node grids (grid_dynamic.hpp): same parity bar as the static grid, and the elements every node ships --
+    reduce-scatter and regrid -- summed over ranks equal the reference's traced counts (simulate.hpp:84-121)."""
+    spec = P.ProblemSpec(list(L), list(K))
+    tree = tree or P.optimal_tree(spec).tree
+    cfg = W.Config(1, list(L), list(K), 1e-2, sweeps)
+    t = W.build_tensor_host(cfg)
+    f0 = W.start_factors(cfg)
+    layout = D.GridLayout(scheme.root)
+    procs = layout.procs
+    ranks = [D.DistributedHooi(ops, spec, tree, scheme, r) for r in range(procs)]
+    for r, dh in enumerate(ranks):
+        dh.set_local_tensor(np.ascontiguousarray(t[layout.slices(r, spec.L)]))
+        dh.set_factors(f0)
+    results = None
+    for _ in range(sweeps):
+        results = D.run_virtual([dh.sweep() for dh in ranks], ops)
+    factors = ranks[0].get_factors()
+    for dh in ranks[1:]:
+        for a, b in zip(factors, dh.get_factors()):
+            assert np.array_equal(a, b)
+    core = assemble_core(layout, spec, [dh.get_local_core() for dh in ranks])
+    of = [f.copy() for f in f0]
+    for _ in range(sweeps):
+        ocore, of = ho.hooi_sweep(t, spec.L, spec.K, of, otree(tree), "jacobi")
+    for a, b in zip(factors, of):
+        assert ho.sin_largest_principal_angle(a, b) < 1e-9
+    on = np.sqrt(np.sum(ocore * ocore))
+    assert abs(np.sqrt(np.sum(core * core)) - on) <= 1e-10 * on
+    assert np.max(np.abs(np.abs(core) - np.abs(ocore))) <= 1e-9 * np.max(np.abs(ocore))
+    report = P.scheme_volume(tree, spec, scheme, procs)
+    regrids = 0
+    for node in range(len(tree.kind)):
+        if tree.kind[node] != P.MODE:
+            continue
+        grid = scheme.node_grids[node]
+        up = tree.parent[node]
+        parent_grid = scheme.root if tree.kind[up] == P.ROOT else scheme.node_grids[up]
+        assert sum(r.volume_sent.get(node, 0) for r in results) == report.per_node_ttm[node]
+        shipped = sum(r.regrid_sent.get(node, 0) for r in results)
+        if list(grid) != list(parent_grid):
+            regrids += 1
+            assert shipped == P.count_moved(node_input_extents(tree, spec, node), parent_grid, grid)
+            assert shipped <= report.per_node_regrid[node]          # the model charges the whole input
+        else:
+            assert shipped == 0
+    return regrids
+
+
+def hand_scheme(tree, root, overrides):
+    """Uniform scheme on `root` with the grids of the given nodes (and their subtrees) replaced."""
+    scheme = P.uniform_scheme(tree, root)
+    for node, grid in overrides.items():
+        stack = [node]
+        while stack:
+            at = stack.pop()
+            if tree.kind[at] == P.MODE:
+                scheme.node_grids[at] = list(grid)
+            stack.extend(tree.children[at])
+    return scheme
+
+
+def test_dynamic_scheme_virtual_ranks_numpy():
+    """Schemes the planner picks (some regrid, some do not) and hand-made ones that regrid at several depths."""
+    total_regrids = 0
+    for L, K, procs in [((8, 8, 8, 8, 8), (2, 2, 2, 2, 2), 2), ((12, 10, 8), (4, 3, 2), 4), ((9, 8, 7, 6), (3, 3, 2, 2), 4),
+                        ((6, 14, 5, 9), (2, 7, 1, 3), 6)]:
+        spec = P.ProblemSpec(list(L), list(K))
+        tree = P.optimal_tree(spec).tree
+        for legacy in (False, True):
+            total_regrids += run_scheme_case(NumpyOps(), L, K, P.optimal_dynamic_scheme(tree, spec, procs, legacy).scheme,
+                                             sweeps=1)
+    spec = P.ProblemSpec([12, 10, 8], [4, 3, 2])
+    tree = P.optimal_tree(spec).tree
+    kids = [c for c in tree.children[0]]
+    grand = [c for k in kids for c in tree.children[k] if tree.kind[c] == P.MODE]
+    total_regrids += run_scheme_case(NumpyOps(), (12, 10, 8), (4, 3, 2), hand_scheme(tree, [2, 1, 2], {kids[0]: [1, 2, 2]}))
+    total_regrids += run_scheme_case(NumpyOps(), (12, 10, 8), (4, 3, 2),
+                                     hand_scheme(tree, [2, 2, 1], {kids[-1]: [1, 2, 2], grand[0]: [4, 1, 1]}))
+    chain = P.chain_tree(spec)
+    first = chain.children[0][0]
+    total_regrids += run_scheme_case(NumpyOps(), (12, 10, 8), (4, 3, 2), hand_scheme(chain, [2, 2, 1], {first: [1, 2, 2]}),
+                                     tree=chain)
+    assert total_regrids >= 4
+
+
+def _gloo_scheme_worker(rank, world, port, out_dir):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        L, K = (12, 10, 8), (4, 3, 2)
+        spec = P.ProblemSpec(list(L), list(K))
+        tree = P.optimal_tree(spec).tree
+        scheme = hand_scheme(tree, [2, 1, 1], {tree.children[0][0]: [1, 1, 2]})
+        cfg = W.Config(1, list(L), list(K), 1e-2, 2)
+        t = W.build_tensor_host(cfg, threads=1)
+        layout = D.GridLayout(scheme.root)
+        dh = D.DistributedHooi(NumpyOps(), spec, tree, scheme, rank)
+        dh.set_local_tensor(np.ascontiguousarray(t[layout.slices(rank, spec.L)]))
+        dh.set_factors(W.start_factors(cfg))
+        res = None
+        for _ in range(2):
+            res = D.run_rank(dh.sweep(), dist)
+        np.savez(os.path.join(out_dir, "rank%d.npz" % rank), core=dh.get_local_core(),
+                 regrid=np.array([sum(res.regrid_sent.values())], dtype=np.int64),
+                 **{"f%d" % i: f for i, f in enumerate(dh.get_factors())})
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_process_group_with_regrid(tmp_path):
+    """world_size 2 over gloo with a scheme that regrids under the first root child."""
+    import torch.multiprocessing as mp
+    mp.spawn(_gloo_scheme_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    L, K = (12, 10, 8), (4, 3, 2)
+    spec = P.ProblemSpec(list(L), list(K))
+    tree = P.optimal_tree(spec).tree
+    cfg = W.Config(1, list(L), list(K), 1e-2, 2)
+    t = W.build_tensor_host(cfg, threads=1)
+    of = W.start_factors(cfg)
+    for _ in range(2):
+        ocore, of = ho.hooi_sweep(t, spec.L, spec.K, of, otree(tree), "jacobi")
+    data = [np.load(os.path.join(str(tmp_path), "rank%d.npz" % r)) for r in range(2)]
+    for i in range(3):
+        assert np.array_equal(data[0]["f%d" % i], data[1]["f%d" % i])
+        assert ho.sin_largest_principal_angle(data[0]["f%d" % i], of[i]) < 1e-9
+    core = assemble_core(D.GridLayout([2, 1, 1]), spec, [d["core"] for d in data])
+    assert abs(np.linalg.norm(core) - np.linalg.norm(ocore)) <= 1e-10 * np.linalg.norm(ocore)
+    first = tree.children[0][0]
+    assert sum(int(d["regrid"][0]) for d in data) == P.count_moved(node_input_extents(tree, spec, first), [2, 1, 1], [1, 1, 2])
+
+
 def test_regrid_roundtrip_and_counts():
     ext = (7, 6, 5)
     full = hostgen.random_tensor(ext, 3)
@@ -206,6 +349,22 @@ def test_virtual_ranks_gpu(L, K, q):
     ctx = E.Context(0)
     try:
         run_virtual_case(D.GpuOps(ctx), L, K, q)
+    finally:
+        ctx.close()
+
+
+@pytest.mark.gpu
+def test_dynamic_scheme_virtual_ranks_gpu():
+    from paper_1707_05594_b200 import engine as E
+    ctx = E.Context(0)
+    try:
+        ops = D.GpuOps(ctx)
+        spec = P.ProblemSpec([48, 40, 36], [8, 6, 5])
+        tree = P.optimal_tree(spec).tree
+        kids = tree.children[0]
+        assert run_scheme_case(ops, (48, 40, 36), (8, 6, 5), hand_scheme(tree, [2, 1, 2], {kids[0]: [1, 2, 2]})) >= 1
+        c4 = P.ProblemSpec([16] * 5, [4] * 5)
+        run_scheme_case(ops, [16] * 5, [4] * 5, P.optimal_dynamic_scheme(P.optimal_tree(c4).tree, c4, 4).scheme, sweeps=1)
     finally:
         ctx.close()
 

@@ -1,6 +1,9 @@
 """Planner parity: every selection (tree shape and node ids, MAC ledger, grids, volumes, cut points) must be
 bit-identical to the reference's, as recorded in tests/golden/planner_golden.json by the reference itself
 (tests/golden/make_golden.py -> oracle/_ref/ref_tools)."""
+import json
+import os
+
 import pytest
 
 from paper_1707_05594_b200 import Errc, TuckerplanError
@@ -174,3 +177,96 @@ def test_spec_and_tree_error_codes():
     assert code(lambda: P.optimal_static_grid(good, s, 16)) == Errc.no_valid_grid
     assert code(lambda: P.grid_count(0, 3)) == Errc.bad_argument
     assert code(lambda: P.build_tree(s, 9)) == Errc.bad_argument
+
+
+# ---- per-node grids (grid_dynamic.hpp / simulate.hpp), pinned to the reference through tests/golden/dynamic_golden.json
+def _dynamic_cases():
+    with open(os.path.join(os.path.dirname(__file__), "golden", "dynamic_golden.json")) as f:
+        return json.load(f)
+
+
+def _tree_by_name(name, spec):
+    return {"opt": lambda: P.optimal_tree(spec).tree, "chain": lambda: P.chain_tree(spec),
+            "chain_by_cost": lambda: P.chain_tree(spec, P.CHAIN_BY_COST), "balanced": lambda: P.balanced_tree(spec)}[name]()
+
+
+def test_dynamic_schemes_match_reference():
+    cases = _dynamic_cases()
+    assert len(cases) >= 200
+    regridding = 0
+    for c in cases:
+        spec = P.ProblemSpec(c["L"], c["K"])
+        if "error" in c:
+            with pytest.raises(TuckerplanError) as e:
+                P.optimal_dynamic_scheme(_tree_by_name(c["tree_name"], spec), spec, c["procs"])
+            assert int(e.value.code) == c["error"] + 1          # C status = Errc ordinal + 1
+            continue
+        tree = _tree_by_name(c["tree_name"], spec)
+        assert (tree.kind, tree.mode, tree.parent) == (c["tree"]["kind"], c["tree"]["mode"], c["tree"]["parent"])
+        for key, legacy in (("scheme", False), ("legacy", True)):
+            want = c[key]
+            got = P.optimal_dynamic_scheme(tree, spec, c["procs"], legacy)
+            assert got.scheme.root == want["root"], (c["L"], c["K"], c["procs"], key)
+            assert [got.scheme.node_grids[i] for i in want["nodes"]] == want["node_grids"]
+            assert sorted(got.scheme.node_grids) == want["nodes"]
+            assert got.report.total == want["total"]
+            assert [got.report.per_node_ttm[i] for i in want["nodes"]] == want["ttm"]
+            assert [got.report.per_node_regrid[i] for i in want["nodes"]] == want["regrid"]
+            # scheme_volume of the returned scheme reproduces the report
+            again = P.scheme_volume(tree, spec, got.scheme, c["procs"])
+            assert (again.total, again.per_node_ttm, again.per_node_regrid) == \
+                   (got.report.total, got.report.per_node_ttm, got.report.per_node_regrid)
+            if "traced_regrid" in want:   # the reference's element-by-element owner comparison (simulate.hpp:104-121)
+                cards_in = c["tree"]["card_in"]
+                for node, traced in zip(want["nodes"], want["traced_regrid"]):
+                    parent = tree.parent[node]
+                    pg = got.scheme.root if tree.kind[parent] == P.ROOT else got.scheme.node_grids[parent]
+                    ext = list(spec.L)
+                    at = parent
+                    while at > 0:
+                        ext[tree.mode[at]] = spec.K[tree.mode[at]]
+                        at = tree.parent[at]
+                    if got.scheme.node_grids[node] != pg:
+                        assert P.count_moved(ext, pg, got.scheme.node_grids[node]) == traced
+                        assert traced <= cards_in[node]
+                        regridding += 1
+                    else:
+                        assert traced == 0
+        # a uniform scheme on the best static grid costs what static_volume says
+        best = P.optimal_static_grid(tree, spec, c["procs"])
+        assert best.report.total == c["static_total"]
+        uni = P.scheme_volume(tree, spec, P.uniform_scheme(tree, best.grid), c["procs"])
+        assert uni.total == c["static_total"] and not any(uni.per_node_regrid)
+        assert c["scheme"]["total"] <= c["static_total"]
+    assert regridding >= 20
+
+
+def test_config4_dynamic_scheme_of_the_survey():
+    """C4 at P = 8 is the one configuration where regridding pays: 9 437 184 elements with 3 regrids
+    against 11 010 048 on the best static grid."""
+    spec = P.ProblemSpec([48] * 5, [8] * 5)
+    tree = P.optimal_tree(spec).tree
+    r = P.optimal_dynamic_scheme(tree, spec, 8)
+    assert r.report.total == 9437184
+    assert sum(1 for v in r.report.per_node_regrid if v) == 3
+    assert P.optimal_static_grid(tree, spec, 8).report.total == 11010048
+
+
+def test_scheme_volume_error_codes():
+    spec = P.ProblemSpec([6, 5, 4], [3, 2, 2])
+    tree = P.optimal_tree(spec).tree
+    scheme = P.uniform_scheme(tree, [2, 2, 1])
+    del scheme.node_grids[max(scheme.node_grids)]
+    with pytest.raises(TuckerplanError) as e:
+        P.scheme_volume(tree, spec, scheme, 4)
+    assert e.value.code == Errc.missing_assignment             # grid_dynamic.hpp:46-48
+    bad = P.uniform_scheme(tree, [2, 2, 1])
+    bad.node_grids[min(bad.node_grids)] = [4, 1, 1]            # q_0 = 4 > K_0 = 3
+    with pytest.raises(TuckerplanError) as e:
+        P.scheme_volume(tree, spec, bad, 4)
+    assert e.value.code == Errc.invalid_grid
+    with pytest.raises(TuckerplanError) as e:
+        P.optimal_dynamic_scheme(tree, P.ProblemSpec([5, 4, 3], [1, 1, 1]), 2)
+    assert e.value.code == Errc.no_valid_grid
+    assert P.count_moved([6, 5, 4], [2, 2, 1], [2, 2, 1]) == 0
+    assert P.count_moved([6, 5, 4], [2, 2, 1], [1, 2, 2]) > 0
