@@ -213,6 +213,12 @@ def measure_fp64_peak(torch):
         return FP64_FALLBACK_TFLOPS, "fallback (profiles/r01_fp64_peaks.jsonl): %s" % exc
 
 
+def sin_principal_angle(a, b):
+    """sin of the largest principal angle between the column spaces of two orthonormal bases."""
+    r = b - a @ (a.T @ b)                       # component of b outside span(a): accurate for tiny angles
+    return float(np.linalg.svd(r, compute_uv=False).max())
+
+
 def run_b200(args):
     import torch
     from paper_1707_05594_b200 import engine as E, planner as P, workloads as W
@@ -259,10 +265,12 @@ def run_b200(args):
         e1.synchronize()
         return e0.elapsed_time(e1), st
 
+    # One HOOI run from the random orthonormal start: W untimed warm-up iterations, then the K timed ones continue
+    # it ("mean over the config's iterations after one warm-up").  The first iteration of a run is cold
+    # (no carried path yet); it is timed separately below and reported in `carried_path`.
     plan.set_factors(f0)
     for _ in range(max(args.warmup, 0)):
         one_step(False)
-    plan.set_factors(f0)  # the timed K iterations are the config's iterations from the random orthonormal start
     ctx.synchronize()
     torch.cuda.synchronize()
     k0, _ = ctx.launch_counts()
@@ -312,8 +320,15 @@ def run_b200(args):
     plan.set_carry_path(False)
     plan.set_factors(f0)
     nocarry_ms = [one_step(True)[0] for _ in range(steps)]
-    nocarry_same = all(np.array_equal(a, b) for a, b in zip(plan.get_factors(), final_factors))
+    factors_after_k = plan.get_factors()          # K iterations from the start factors
     plan.set_carry_path(True)
+    plan.set_factors(f0)
+    cold_ms = None
+    for i in range(steps):
+        ms, _ = one_step(False)
+        if i == 0:
+            cold_ms = ms                           # first iteration of a run: no carried path yet
+    nocarry_same = all(np.array_equal(a, b) for a, b in zip(plan.get_factors(), factors_after_k))
 
     # TTM-tree phase vs its per-TTM roofline
     rows = tree_roofline(spec, tree, cost, p_fp64, hbm_gbs)
@@ -356,10 +371,12 @@ def run_b200(args):
             d = E.hooi_sweep(host_t, spec, d, tree, "jacobi", ctx=ctx)
         e2e_s = (time.perf_counter() - w0) / e2e_steps
         fbytes = 8 * sum(l * k for l, k in zip(spec.L, spec.K))
-        same = all(np.array_equal(a, b) for a, b in zip(d.factors, final_factors)) if e2e_steps == steps else None
+        # the by-value call starts every eigen-solve from the caller's factors, the resident run from its own Ritz
+        # vectors: same subspaces to rounding, not the same bits
+        agree = max(sin_principal_angle(a, b) for a, b in zip(d.factors, factors_after_k)) if e2e_steps == steps else None
         e2e = {"value": e2e_s, "unit": "s/iter", "h2d_bytes_per_step": total * 8 + fbytes,
                "d2h_bytes_per_step": fbytes + 8 * int(np.prod(spec.K)), "host_memory": "pinned",
-               "bit_identical_to_resident_run": same}
+               "max_sin_principal_angle_vs_resident_run": agree}
 
     # CPU baseline: the oracle port on the same host tensor, all cores, a bounded sample (one iteration)
     cpu = None
@@ -382,6 +399,7 @@ def run_b200(args):
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg.name, "iterations": cfg.iterations, "schedule": "jacobi on optimal_tree",
+                   "timed_steps": "iterations W+1..W+K of one HOOI run from the random orthonormal start",
                    "tree": tree.label(), "grid": [1] * spec.n_modes(), "evd": "top-k subspace iteration where certified, else full syevd; on side streams",
                    "core": "chain along a tree path, partial products carried into the next sweep",
                    "l2": "flushed_between_steps" if small else "inputs_larger_than_L2",
@@ -394,12 +412,13 @@ def run_b200(args):
         "ttm_tree_overlapped_ms": sum(overlapped_node_ms[r["node"]] for r in rows),
         "serial_schedule": {"ms_per_step": float(np.mean(serial_ms)), "phases_ms": serial_phases,
                             "note": "steady state: one cold sweep from the start factors precedes the K timed ones"},
-        "carried_path": {"enabled": True, "ms_first_step_cold": step_ms[0],
-                         "ms_per_step_steady": float(np.mean(step_ms[1:])) if steps > 1 else None,
+        "carried_path": {"enabled": True, "ms_first_iteration_cold": cold_ms,
                          "ms_per_step_disabled": float(np.mean(nocarry_ms)),
                          "factors_bit_identical_when_disabled": bool(nocarry_same),
                          "note": "the core chain runs along a tree path; its partial products are the next sweep's "
-                                 "tree nodes and are not recomputed. step 1 of the timed K starts cold."},
+                                 "tree nodes and are not recomputed. The first iteration of a run (first warm-up step "
+                                 "here) is cold: tree + whole chain. ms_per_step_disabled: same K iterations from "
+                                 "the start factors with the option off (the reference's schedule)."},
         "evd": {"fast_path_leaves": evd_info[0], "redone_with_full_solve_last_sweep": evd_info[1]},
         "phases_ms": phases, "relative_fit": fit, "wall_s_timed_region": wall, "build_s": t_build,
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(k1 - k0),

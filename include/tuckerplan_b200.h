@@ -232,14 +232,14 @@ int tp_plan_destroy(tp_ctx* ctx, tp_plan* plan);
  * what per-kernel timing and profiling want. */
 enum { TP_OPT_OVERLAP_EVD = 1, TP_OPT_FAST_EVD = 2, TP_OPT_CARRY_PATH = 3 };
 int tp_plan_set_option(tp_ctx* ctx, tp_plan* plan, int option, int value);
-/* TP_OPT_CARRY_PATH (default 1, Jacobi plans): the core chain core_from_factors (hooi.hpp:93-100) contracts the modes
+/* TP_OPT_CARRY_PATH (default 1; Gauss-Seidel plans carry the first leaf's chain): the core chain core_from_factors (hooi.hpp:93-100) contracts the modes
  * along one root-to-leaf path of the TTM tree; with the new factors its partial products are exactly the
  * intermediates the next sweep's tree needs at those nodes, so they are kept on the device and the next tp_plan_sweep
  * on the same, unchanged tensor starts from them: per sweep every tree node is computed once and the core costs one
  * small product instead of a second pass over the tensor.  The carried products are dropped by tp_plan_set_factors,
  * by a sweep on another tensor, and whenever the tensor may have changed (tp_tensor_axpby, tp_tensor_device_ptr --
  * take the pointer again after writing through it).  SweepStats stay the analytic (reference) counts.
- * TP_OPT_FAST_EVD (default 1): Jacobi leaves with 2 (K_n + 8) <= L_n (and K_n + 8 <= 112 or L_n >= 704) compute only
+ * TP_OPT_FAST_EVD (default 1): leaves with 2 (K_n + 8) <= L_n (and K_n + 8 <= 112 or L_n >= 704) compute only
  * the K_n leading eigenvectors by warm-started block subspace iteration + Rayleigh-Ritz; every kept Ritz pair must satisfy
  * ||G x - theta x|| <= 1e-13 theta_max, otherwise (or when the gap estimate says "degenerate") the leaf is redone
  * with the full eigen-solve, so the factors are the reference's (hooi.hpp:55-69) to rounding either way.

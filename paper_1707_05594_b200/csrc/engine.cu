@@ -672,7 +672,7 @@ void plan_leaf_solve(tp_ctx* ctx, tp_plan* p, int mode, int node, double* dst, b
   slot.fast_used = false;
   // cold: the start factors are the caller's (plan creation / tp_plan_set_factors), not a previous sweep's result
   const bool cold = p->factors_from_caller;
-  if (p->fast_evd && p->sweep_kind == TP_SWEEP_JACOBI && slot.failures < 2 && !(cold && slot.cold_rejected) &&
+  if (p->fast_evd && slot.failures < 2 && !(cold && slot.cold_rejected) &&
       subspace_eligible(rows, k, plan_leaf_columns(p, mode))) {
     subspace_reserve(ctx, slot, rows, k);
     slot.was_cold = cold;
@@ -844,7 +844,21 @@ void plan_choose_carry(tp_plan* p) {
   p->carry_nodes.clear();
   p->carry_leaf_mode = -1;
   p->on_carry.assign(t.size(), 0);
-  if (p->sweep_kind != TP_SWEEP_JACOBI || p->n < 2) {
+  if (p->n < 2) {
+    plan_visit_order(p);
+    return;
+  }
+  if (p->sweep_kind != TP_SWEEP_JACOBI) {
+    // Gauss-Seidel (chain trees): the first chain of a sweep multiplies by F_1 .. F_{N-1} as they stand at the end
+    // of the previous sweep -- the factors the core chain uses.  Carry that chain; the core closes it with F_0.
+    for (int leaf = 0; leaf < t.size(); ++leaf) {
+      if (!t.leaf(leaf) || t.mode[leaf] != 0) continue;
+      for (int id = t.parent[leaf]; id > 0; id = t.parent[id]) p->carry_nodes.push_back(id);
+      std::reverse(p->carry_nodes.begin(), p->carry_nodes.end());
+      for (int id : p->carry_nodes) p->on_carry[id] = 1;
+      p->carry_leaf_mode = 0;
+      break;
+    }
     plan_visit_order(p);
     return;
   }
@@ -1530,26 +1544,47 @@ int tp_plan_sweep(tp_ctx* ctx, tp_plan* p, const tp_tensor* t, tp_sweep_stats* s
         for (int m = 0; m < p->n; ++m) plan_refresh_fragments(ctx, p, m, p->cur[m]);
         s.close();
       }
+      p->carry_live = p->carry_enabled && p->carry_valid && p->carry_tensor == t && p->carry_stamp == t->stamp &&
+                      !p->carry_nodes.empty();
+      p->carry_valid = false;
+      p->fast_rejected = 0;
       for (int leaf = 0; leaf < p->n; ++leaf) {  // hooi.hpp:206-224
         const double* at = t->data;
         std::vector<size_t> d = dims;
         size_t step = 0;
-        for (int m : p->gs_paths[leaf]) {
-          Span s(ctx, p, kTree);
-          double* out = p->depth_buf[step];
-          plan_ttm(ctx, p, at, d, m, out);
-          s.close();
-          d[m] = static_cast<size_t>(p->spec.K[m]);
-          at = out;
-          ++step;
+        if (leaf == 0 && p->carry_live) {
+          // this chain was computed by the previous sweep's core chain (same tensor, same F_1 .. F_{N-1})
+          at = p->carry_buf.back();
+          for (int m : p->gs_paths[leaf]) d[m] = static_cast<size_t>(p->spec.K[m]);
+        } else {
+          for (int m : p->gs_paths[leaf]) {
+            Span s(ctx, p, kTree);
+            double* out = p->depth_buf[step];
+            plan_ttm(ctx, p, at, d, m, out);
+            s.close();
+            d[m] = static_cast<size_t>(p->spec.K[m]);
+            at = out;
+            ++step;
+          }
         }
         plan_leaf(ctx, p, at, d, leaf, p->fresh[leaf], -1, false);
+        // the next chain multiplies by this factor: a certified top-k solve is checked now, not at the end
+        const std::vector<int> rejected = verify_fast_leaves(ctx, p);
+        if (!rejected.empty()) {
+          ++p->fast_rejected;
+          Span evd(ctx, p, kEvd, -1);
+          leaf_solve(ctx, p->leaf[leaf], static_cast<long long>(p->spec.L[leaf]), static_cast<int>(p->spec.K[leaf]),
+                     p->fresh[leaf], -1);
+          evd.close();
+        }
         std::swap(p->cur[leaf], p->fresh[leaf]);  // later chains see the fresh factor
         Span s(ctx, p, kTree);
         plan_refresh_fragments(ctx, p, leaf, p->cur[leaf]);
         s.close();
       }
       plan_core(ctx, p, t->data, p->cur);
+      p->factors_from_caller = false;
+      plan_mark_carried(p, t);
     }
     const int flag = read_and_clear_flags(ctx, p->leaf);
     plan_collect_timing(ctx, p);
@@ -1583,7 +1618,7 @@ int tp_plan_last_evd_info(tp_ctx* ctx, tp_plan* p, int* fast_eligible, int* reje
     if (!p) raise(TP_ERR_BAD_ARGUMENT, "null plan");
     int eligible = 0;
     for (int m = 0; m < p->n; ++m)
-      if (p->fast_evd && p->sweep_kind == TP_SWEEP_JACOBI && p->leaf[m].failures < 2 &&
+      if (p->fast_evd && p->leaf[m].failures < 2 &&
           subspace_eligible(static_cast<long long>(p->spec.L[m]), static_cast<int>(p->spec.K[m]),
                             plan_leaf_columns(p, m)))
         ++eligible;

@@ -465,6 +465,63 @@ def test_carried_path_is_bit_identical_and_invalidates(ctx, L, K, tree_kind):
     dt.free()
 
 
+@pytest.mark.parametrize("L,K", [([96, 80, 64], [10, 8, 6]), ([40, 36, 30, 24], [5, 4, 4, 3]), ([300, 8], [3, 3]), ([50], [1])],
+                         ids=lambda v: "x".join(map(str, v)))
+def test_gauss_seidel_with_carried_chain_and_certified_solve(ctx, L, K):
+    """Gauss-Seidel (hooi.hpp:206-225) takes the same two shortcuts as Jacobi: the first chain of a sweep is the one
+    the previous sweep's core chain computed, and eligible leaves use the certified top-k solve (checked right after
+    each leaf, because the next chain multiplies by the new factor).  Bits do not depend on the carried chain; the
+    factors stay the oracle's."""
+    cfg = W.scaled_config(1, L, K, 4)
+    spec = cfg.spec
+    tree = P.chain_tree(spec)
+    t = W.build_tensor_host(cfg)
+    f0 = W.start_factors(cfg)
+    dt = E.DeviceTensor.upload(ctx, t)
+
+    def run(carry):
+        plan = E.HooiPlan(ctx, spec, tree, "gauss_seidel")
+        plan.set_carry_path(carry)
+        plan.set_factors(f0)
+        out = []
+        for _ in range(4):
+            st = plan.sweep(dt)
+            out.append((plan.get_factors(), plan.get_core(), st, plan.evd_info()))
+        plan.close()
+        return out
+
+    on, off = run(True), run(False)
+    of = [f.copy() for f in f0]
+    for (fa, ca, st, info), (fb, cb, _, _) in zip(on, off):
+        assert all(np.array_equal(a, b) for a, b in zip(fa, fb)) and np.array_equal(ca, cb)
+        ost = ho.SweepStats()
+        ocore, of = ho.hooi_sweep(t, spec.L, spec.K, of, otree(tree), "gauss_seidel", ost)
+        assert (st.tree_macs, st.core_macs, st.peak_live, st.degenerate) == \
+               (ost.tree_macs, ost.core_macs, ost.peak_live, ost.degenerate)
+        angle = max(ho.sin_largest_principal_angle(a, b) for a, b in zip(fa, of))
+        gn, on_ = np.sqrt(np.sum(ca * ca)), np.sqrt(np.sum(ocore * ocore))
+        assert angle < 1e-9 and abs(gn - on_) <= 1e-10 * on_
+    if L == [96, 80, 64]:
+        assert on[-1][3] == (3, 0)                 # all three leaves eligible, none redone in the last sweep
+    # a change of the tensor between sweeps drops the carried chain
+    plan = E.HooiPlan(ctx, spec, tree, "gauss_seidel")
+    plan.set_factors(f0)
+    plan.sweep(dt)
+    noise = hostgen.random_tensor(L, 77)
+    dn = E.DeviceTensor.upload(ctx, noise)
+    dt.axpby(1.0, 0.1, dn)
+    dn.free()
+    plan.sweep(dt)
+    t2 = t + 0.1 * noise
+    of = [f.copy() for f in f0]
+    _, of = ho.hooi_sweep(t, spec.L, spec.K, of, otree(tree), "gauss_seidel")
+    ocore, of = ho.hooi_sweep(t2, spec.L, spec.K, of, otree(tree), "gauss_seidel")
+    assert max(ho.sin_largest_principal_angle(a, b) for a, b in zip(plan.get_factors(), of)) < 1e-9
+    assert abs(plan.core_norm() - np.sqrt(np.sum(ocore * ocore))) <= 1e-10 * np.sqrt(np.sum(ocore * ocore))
+    plan.close()
+    dt.free()
+
+
 @pytest.mark.parametrize("index", [2, 3, 4])
 def test_sweep_parity_full_size_configs(ctx, index):
     """BASELINE.json configs[1..3] at full size, two Jacobi iterations on the optimal tree, against the oracle."""
