@@ -20,6 +20,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -77,6 +78,10 @@ struct tp_ctx {
   cusolverDnHandle_t aux_solver[kAux] = {nullptr, nullptr, nullptr, nullptr};
   cublasHandle_t blas = nullptr;     // small dense products inside the eigen-solve (off the hot path)
   cublasHandle_t aux_blas[kAux] = {nullptr, nullptr, nullptr, nullptr};
+  // by-value calls upload the tensor in slabs on their own stream so that the root products can start on the
+  // slabs that have arrived (tp_hooi_sweep_host)
+  cudaStream_t copy_stream = nullptr;
+  std::vector<cudaEvent_t> arrival_events;
   // fixed cuBLAS workspaces (one per handle): recorded CUDA graphs must not depend on cuBLAS' own pool
   static constexpr size_t kBlasWorkspaceBytes = 32u << 20;
   void* blas_ws[kAux + 1] = {nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -576,6 +581,18 @@ struct tp_plan {
   // path of the TTM tree it produces, with the new factors, exactly the intermediates the NEXT sweep's walk needs at
   // those nodes.  They are kept (own buffers) and the next walk starts from them, so per sweep every tree node is
   // computed once and the core costs one small extra product instead of a second pass over the tensor.
+  // Streamed first pass (by-value calls): the tensor is still arriving from the host in slabs of its first mode.
+  // issue(c) queues the upload of slab c (idempotent), ready[c] fires when it is on the device.
+  struct Arrival {
+    std::vector<size_t> row_end;               // slab c = rows [row_end[c-1], row_end[c]) of mode 0
+    std::vector<cudaEvent_t> ready;
+    std::function<void(int)> issue;
+  };
+  Arrival* arrival = nullptr;                  // set for the duration of one sweep
+  std::vector<double*> arrival_slots;          // per-slab partial products of the root node that contracts mode 0
+  size_t arrival_slot_doubles = 0;
+  std::vector<double*> arrival_frag;           // fragment-ordered row slices of F_0, one per slab
+  std::vector<size_t> arrival_frag_doubles;
   bool factors_from_caller = true;            // no sweep has run since the factors were set
   bool carry_enabled = true;
   std::vector<int> carry_nodes;               // TTM nodes of the path, root child first (empty: no carrying)
@@ -799,6 +816,127 @@ void jacobi_walk(tp_ctx* ctx, tp_plan* p, int node, const double* tensor, std::v
       dims[mode] = static_cast<size_t>(p->spec.K[mode]);
       jacobi_walk(ctx, p, c, out, dims, depth + 1);
       dims[mode] = saved;
+    }
+  }
+}
+
+// Root level of a Jacobi walk while the tensor is still arriving (plan->arrival): slab by slab, the first root
+// child that contracts a mode other than 0 multiplies its slab (slabs of mode 0 are independent there), and the
+// root child that contracts mode 0 forms the slab's partial product into its own slot; the slots are summed in slab
+// order once all have arrived.  Everything below the root, and any further root children, run as usual afterwards.
+void jacobi_walk_streamed_root(tp_ctx* ctx, tp_plan* p, const double* tensor, std::vector<size_t>& dims) {
+  tp_plan::Arrival& arr = *p->arrival;
+  const Tree& t = p->tree;
+  const int chunks = static_cast<int>(arr.row_end.size());
+  int slab_child = -1, sum_child = -1;
+  for (int c : p->visit_order[0]) {
+    if (!t.internal(c)) continue;
+    if (t.mode[c] == 0 && sum_child < 0) sum_child = c;
+    if (t.mode[c] != 0 && slab_child < 0) slab_child = c;
+  }
+  const long long L0 = static_cast<long long>(dims[0]);
+  long long per_row = 1;  // elements of one mode-0 row of the tensor
+  for (size_t m = 1; m < dims.size(); ++m) per_row *= static_cast<long long>(dims[m]);
+  // the mode-0 child needs one slot per slab; give up on streaming it when that would not fit comfortably
+  size_t sum_out = 0;
+  if (sum_child >= 0) {
+    sum_out = static_cast<size_t>(p->spec.K[0]) * static_cast<size_t>(per_row);
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    const bool have = p->arrival_slot_doubles >= sum_out && static_cast<int>(p->arrival_slots.size()) >= chunks;
+    if (!have && static_cast<double>(sum_out) * 8.0 * chunks > 0.5 * static_cast<double>(free_b)) {
+      sum_child = -1;
+    } else if (!have) {
+      for (double* d : p->arrival_slots) cudaFree(d);
+      p->arrival_slots.assign(chunks, nullptr);
+      for (int c = 0; c < chunks; ++c) p->arrival_slots[c] = device_alloc(sum_out);
+      p->arrival_slot_doubles = sum_out;
+    }
+  }
+  if (sum_child >= 0 && static_cast<int>(p->arrival_frag.size()) < chunks) {
+    p->arrival_frag.resize(chunks, nullptr);
+    p->arrival_frag_doubles.resize(chunks, 0);
+  }
+  double* const slab_out = p->depth_buf[0];
+  cudaEvent_t slab_begin = nullptr, slab_end = nullptr, sum_begin = nullptr, sum_end = nullptr;
+  for (int c = 0; c < chunks; ++c) {
+    arr.issue(c);
+    if (c + 1 < chunks) arr.issue(c + 1);  // keep the link busy while this slab is multiplied
+    TPB_CUDA(cudaStreamWaitEvent(ctx->stream, arr.ready[c], 0));
+    const long long r0 = c ? static_cast<long long>(arr.row_end[c - 1]) : 0, r1 = static_cast<long long>(arr.row_end[c]);
+    if (slab_child >= 0) {
+      const int mode = t.mode[slab_child];
+      long long outer, inner;
+      mode_extents(dims, mode, outer, inner);
+      const long long rest = outer / L0;  // product of the extents between mode 0 and `mode`
+      const long long len = static_cast<long long>(dims[mode]), K = static_cast<long long>(p->spec.K[mode]);
+      if (c == 0) {
+        p->event_phase.push_back(kTree);
+        p->event_node.push_back(slab_child);
+        slab_begin = next_event(p);
+        slab_end = next_event(p);
+        TPB_CUDA(cudaEventRecord(slab_begin, ctx->stream));
+      }
+      TPB_CUDA(launch_ttm(ctx->stream, tensor + r0 * rest * len * inner, (r1 - r0) * rest, len, inner, p->frag[mode],
+                          p->frag_layout[mode], K, slab_out + r0 * rest * K * inner, ctx->sm_count));
+      ctx->own_kernels += 1;
+      if (c + 1 == chunks) TPB_CUDA(cudaEventRecord(slab_end, ctx->stream));
+    }
+    if (sum_child >= 0) {
+      const long long K = static_cast<long long>(p->spec.K[0]);
+      const TtmFragmentLayout f = ttm_fragment_layout(K, r1 - r0);
+      if (p->arrival_frag_doubles[c] < f.doubles) {
+        cudaFree(p->arrival_frag[c]);
+        p->arrival_frag[c] = device_alloc(f.doubles);
+        p->arrival_frag_doubles[c] = f.doubles;
+      }
+      if (c == 0) {
+        p->event_phase.push_back(kTree);
+        p->event_node.push_back(sum_child);
+        sum_begin = next_event(p);
+        sum_end = next_event(p);
+        TPB_CUDA(cudaEventRecord(sum_begin, ctx->stream));
+      }
+      // M = F_0^T restricted to the slab's rows: M(k, l) = F_0[k * L_0 + r0 + l]
+      TPB_CUDA(prep_factor_fragments(ctx->stream, p->cur[0] + r0, L0, 1, K, r1 - r0, f, p->arrival_frag[c]));
+      TPB_CUDA(launch_ttm(ctx->stream, tensor + r0 * per_row, 1, r1 - r0, per_row, p->arrival_frag[c], f, K,
+                          p->arrival_slots[c], ctx->sm_count));
+      ctx->own_kernels += 2;
+    }
+  }
+  // main stream is now ordered after every slab: the rest of the sweep may read the whole tensor
+  auto descend = [&](int c, double* out) {
+    const int mode = t.mode[c];
+    const size_t saved = dims[mode];
+    dims[mode] = static_cast<size_t>(p->spec.K[mode]);
+    jacobi_walk(ctx, p, c, out, dims, 1);
+    dims[mode] = saved;
+  };
+  // the slab child first: its product sits in the depth-0 buffer the other root children reuse
+  std::vector<int> order;
+  if (slab_child >= 0) order.push_back(slab_child);
+  for (int c : p->visit_order[0])
+    if (c != slab_child) order.push_back(c);
+  for (int c : order) {
+    const int mode = t.mode[c];
+    if (t.kind[c] == TP_NODE_LEAF) {
+      plan_leaf(ctx, p, tensor, dims, mode, p->fresh[mode], c, p->overlap_evd);
+    } else if (c == slab_child) {
+      descend(c, slab_out);
+    } else if (c == sum_child) {
+      std::vector<const double*> slots(p->arrival_slots.begin(), p->arrival_slots.begin() + chunks);
+      TPB_CUDA(launch_reduce_slots(ctx->stream, p->depth_buf[0], slots.data(), chunks, sum_out));
+      TPB_CUDA(cudaEventRecord(sum_end, ctx->stream));
+      ctx->own_kernels += 1;
+      plan_flush_pending(ctx, p);
+      descend(c, p->depth_buf[0]);
+    } else {
+      double* out = p->depth_buf[0];
+      Span s(ctx, p, kTree, c);
+      plan_ttm(ctx, p, tensor, dims, mode, out, (p->overlap_evd && p->leaves_in_flight > 0) ? p->spare_sms : 0);
+      s.close();
+      plan_flush_pending(ctx, p);
+      descend(c, out);
     }
   }
 }
@@ -1045,6 +1183,8 @@ int tp_ctx_destroy(tp_ctx* ctx) {
     }
     cudaFree(ctx->reduce_scratch);
     cudaFree(ctx->frag_scratch);
+    for (cudaEvent_t e : ctx->arrival_events) cudaEventDestroy(e);
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     for (void* ws : ctx->blas_ws) cudaFree(ws);
     release_host_call_cache(ctx);
     if (ctx->dev_scratch) {
@@ -1427,6 +1567,8 @@ int tp_plan_destroy(tp_ctx* ctx, tp_plan* p) {
     for (double* d : p->frag) cudaFree(d);
     for (double* d : p->depth_buf) cudaFree(d);
     for (double* d : p->carry_buf) cudaFree(d);
+    for (double* d : p->arrival_slots) cudaFree(d);
+    for (double* d : p->arrival_frag) cudaFree(d);
     cudaFree(p->core);
     cudaFree(p->core_tmp[0]);
     cudaFree(p->core_tmp[1]);
@@ -1520,7 +1662,10 @@ int tp_plan_sweep(tp_ctx* ctx, tp_plan* p, const tp_tensor* t, tp_sweep_stats* s
       p->pending.clear();
       p->carry_live = p->carry_enabled && p->carry_valid && p->carry_tensor == t && p->carry_stamp == t->stamp;
       p->carry_valid = false;  // the chain at the end of this sweep overwrites the carried products
-      jacobi_walk(ctx, p, 0, t->data, dims, 0);
+      if (p->arrival && p->arrival->row_end.size() > 1 && p->n > 1)
+        jacobi_walk_streamed_root(ctx, p, t->data, dims);
+      else
+        jacobi_walk(ctx, p, 0, t->data, dims, 0);
       plan_core(ctx, p, t->data, p->fresh, p->overlap_evd);  // waits for each new factor just before using it
       // leaves solved by subspace iteration are accepted only with their residual certificate; a rejected leaf is
       // redone with the full eigen-solve on its (intact) Gram matrix, and the core with it
@@ -1544,6 +1689,11 @@ int tp_plan_sweep(tp_ctx* ctx, tp_plan* p, const tp_tensor* t, tp_sweep_stats* s
         for (int m = 0; m < p->n; ++m) plan_refresh_fragments(ctx, p, m, p->cur[m]);
         s.close();
       }
+      if (p->arrival)  // a by-value call is still uploading: the chains read the whole tensor
+        for (size_t c = 0; c < p->arrival->row_end.size(); ++c) {
+          p->arrival->issue(static_cast<int>(c));
+          TPB_CUDA(cudaStreamWaitEvent(ctx->stream, p->arrival->ready[c], 0));
+        }
       p->carry_live = p->carry_enabled && p->carry_valid && p->carry_tensor == t && p->carry_stamp == t->stamp &&
                       !p->carry_nodes.empty();
       p->carry_valid = false;
@@ -1994,10 +2144,52 @@ int tp_hooi_sweep_host(tp_ctx* ctx, int n_modes, const size_t* dims, const doubl
       ctx->host_call_key = key;
     }
     tp_tensor* t = ctx->host_call_tensor;
-    TPB_CUDA(cudaMemcpyAsync(t->data, tensor, t->size * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    tp_plan* plan = ctx->host_call_plan;
     t->stamp = next_tensor_stamp();
-    forward(tp_plan_set_factors(ctx, ctx->host_call_plan, factors_in));
-    forward(tp_plan_sweep(ctx, ctx->host_call_plan, t, stats));
+    forward(tp_plan_set_factors(ctx, plan, factors_in));
+    // Large tensors go up in slabs of the first mode on a copy stream; the sweep starts on the slabs that have
+    // arrived (jacobi_walk_streamed_root) instead of idling through the whole PCIe transfer.
+    const size_t rows = dims[0];
+    const size_t per_row = t->size / rows;
+    int chunks = 1;
+    size_t min_bytes = size_t{256} << 20;  // below this the transfer is too short to be worth splitting
+    if (const char* env = std::getenv("TPB_STREAMED_UPLOAD_MIN_BYTES")) min_bytes = std::strtoull(env, nullptr, 10);
+    if (n_modes > 1 && t->size * sizeof(double) >= min_bytes && rows >= 32)
+      chunks = static_cast<int>(std::min<size_t>(8, rows / 16));
+    if (chunks == 1) {
+      TPB_CUDA(cudaMemcpyAsync(t->data, tensor, t->size * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+      forward(tp_plan_sweep(ctx, plan, t, stats));
+    } else {
+      if (!ctx->copy_stream) TPB_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+      while (static_cast<int>(ctx->arrival_events.size()) < chunks) {
+        cudaEvent_t e;
+        TPB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        ctx->arrival_events.push_back(e);
+      }
+      tp_plan::Arrival arrival;
+      const size_t step = ((rows + chunks - 1) / chunks + 15) / 16 * 16;  // whole contraction chunks per slab
+      for (size_t r = step; r < rows; r += step) arrival.row_end.push_back(r);
+      arrival.row_end.push_back(rows);
+      arrival.ready.assign(ctx->arrival_events.begin(), ctx->arrival_events.begin() + arrival.row_end.size());
+      int issued = 0;
+      arrival.issue = [&](int c) {
+        for (; issued <= c; ++issued) {
+          const size_t r0 = issued ? arrival.row_end[issued - 1] : 0, r1 = arrival.row_end[issued];
+          TPB_CUDA(cudaMemcpyAsync(t->data + r0 * per_row, tensor + r0 * per_row, (r1 - r0) * per_row * sizeof(double),
+                                   cudaMemcpyHostToDevice, ctx->copy_stream));
+          TPB_CUDA(cudaEventRecord(arrival.ready[issued], ctx->copy_stream));
+        }
+      };
+      plan->arrival = &arrival;
+      const int status = tp_plan_sweep(ctx, plan, t, stats);
+      plan->arrival = nullptr;
+      if (status != TP_OK) {
+        cudaStreamSynchronize(ctx->copy_stream);  // `tensor` must not be read after this call returns
+        forward(status);
+      }
+      arrival.issue(static_cast<int>(arrival.row_end.size()) - 1);
+      TPB_CUDA(cudaStreamSynchronize(ctx->copy_stream));
+    }
     if (factors_out) forward(tp_plan_get_factors(ctx, ctx->host_call_plan, factors_out));
     if (core_out) forward(tp_plan_get_core(ctx, ctx->host_call_plan, core_out));
   });

@@ -522,6 +522,57 @@ def test_gauss_seidel_with_carried_chain_and_certified_solve(ctx, L, K):
     dt.free()
 
 
+STREAM_CASES = [
+    ([160, 24, 20], [6, 5, 4], "optimal"),          # 3 modes: one root child contracts mode 0, one does not
+    ([130, 12, 10, 8], [5, 3, 3, 2], "optimal"),    # ragged last slab (130 rows in slabs of 32)
+    ([96, 20, 18], [5, 4, 3], "chain"),             # chain tree: N root children, the first non-mode-0 one streams
+    ([64, 30], [4, 4], "optimal"),
+    ([200, 16, 14], [7, 4, 3], "balanced"),
+]
+
+
+@pytest.mark.parametrize("L,K,tree_kind", STREAM_CASES, ids=lambda v: v if isinstance(v, str) else "x".join(map(str, v)))
+@pytest.mark.parametrize("kind", ["jacobi", "gauss_seidel"])
+def test_by_value_call_with_streamed_upload(ctx, monkeypatch, L, K, tree_kind, kind):
+    """tp_hooi_sweep_host uploads large tensors in slabs of the first mode and starts the root products on the slabs
+    that have arrived.  Forced on here for small tensors; results must be the oracle's, and equal to rounding to the
+    whole-tensor upload (the mode-0 root product is then a sum of per-slab partial products)."""
+    if kind == "gauss_seidel" and tree_kind != "chain":
+        pytest.skip("Gauss-Seidel needs a chain tree")
+    cfg = W.scaled_config(1, L, K, 2)
+    spec = cfg.spec
+    tree = {"optimal": lambda: P.optimal_tree(spec).tree, "chain": lambda: P.chain_tree(spec),
+            "balanced": lambda: P.balanced_tree(spec)}[tree_kind]()
+    t = W.build_tensor_host(cfg)
+    f0 = W.start_factors(cfg)
+
+    def run(min_bytes):
+        monkeypatch.setenv("TPB_STREAMED_UPLOAD_MIN_BYTES", str(min_bytes))
+        d = E.Decomposition(None, [f.copy() for f in f0])
+        stats = E.SweepStats()
+        for _ in range(2):
+            d = E.hooi_sweep(t, spec, d, tree, kind, stats, ctx=ctx)
+        return d, stats
+
+    streamed, st = run(0)
+    whole, _ = run(1 << 60)
+    of = [f.copy() for f in f0]
+    for _ in range(2):
+        ost = ho.SweepStats()
+        ocore, of = ho.hooi_sweep(t, spec.L, spec.K, of, otree(tree), kind, ost)
+    assert (st.tree_macs, st.core_macs, st.peak_live, st.degenerate) == \
+           (ost.tree_macs, ost.core_macs, ost.peak_live, ost.degenerate)
+    for d in (streamed, whole):
+        assert max(ho.sin_largest_principal_angle(a, b) for a, b in zip(d.factors, of)) < 1e-9
+        gn, on = np.sqrt(np.sum(d.core * d.core)), np.sqrt(np.sum(ocore * ocore))
+        assert abs(gn - on) <= 1e-10 * on
+        assert abs(E.reconstruction_error(t, d, ctx=ctx) - ho.reconstruction_error(t, ocore, of)) <= 1e-10
+    for a, b in zip(streamed.factors, whole.factors):
+        assert np.max(np.abs(a - b)) < 1e-10
+    if kind == "gauss_seidel":                      # nothing is streamed there: same bits
+        assert all(np.array_equal(a, b) for a, b in zip(streamed.factors, whole.factors))
+
+
 @pytest.mark.parametrize("index", [2, 3, 4])
 def test_sweep_parity_full_size_configs(ctx, index):
     """BASELINE.json configs[1..3] at full size, two Jacobi iterations on the optimal tree, against the oracle."""
