@@ -229,18 +229,42 @@ class DistributedHooi:
         self.tensor_ldims = self.layout.local_dims(self.rank, spec.L)
         self.core_order = _cheapest_chain_order(spec)
         self.events: Optional[Callable[[str, int], None]] = None   # timing hook: ("begin"/"end" + phase, node)
+        # Carried path (as in the single-GPU plan): the core chain contracts along one root-to-leaf
+        # path of the tree with the new factors, on the grids of those nodes; its partial products are the next
+        # sweep's intermediates at those nodes and are kept instead of recomputed.
+        self.carry_enabled = self.n >= 2
+        self._carry_path, self._carry_leaf_mode = self._first_leaf_path()
+        self._carried: Dict[int, tuple] = {}
 
     # -- state ------------------------------------------------------------------------------------
     def set_local_tensor(self, block: np.ndarray):
         if list(block.shape) != self.tensor_ldims:
             raise ValueError("local block has shape %s, expected %s" % (block.shape, self.tensor_ldims))
         self.tensor = self.ops.from_host(block)
+        self._carried = {}
 
     def set_local_tensor_buffer(self, buf):
         self.tensor = buf
+        self._carried = {}
 
     def set_factors(self, factors: Sequence[np.ndarray]):
         self.factors = [self.ops.from_host(np.asfortranarray(f).reshape(-1, order="F")) for f in factors]
+        self._carried = {}
+
+    def invalidate(self):
+        """Call after changing the local tensor block in place: drops the products carried from the last sweep."""
+        self._carried = {}
+
+    def _first_leaf_path(self):
+        """TTM nodes from the root down to the first leaf in execution order, and that leaf's mode."""
+        node, path = 0, []
+        while True:
+            kids = self.tree.children[node]
+            leaf = next((c for c in kids if self.tree.kind[c] == P.LEAF), None)
+            if leaf is not None:
+                return path, self.tree.mode[leaf]
+            node = kids[0]
+            path.append(node)
 
     def get_factors(self) -> List[np.ndarray]:
         return [self.ops.to_host(f).reshape((l, k), order="F").copy()
@@ -343,6 +367,14 @@ class DistributedHooi:
                     self._mark("begin_leaf", c)
                     fresh[mode] = yield from self._leaf(x, ext, ldims, mode, res, statuses, lay)
                     self._mark("end_leaf", c)
+                elif c in self._carried:
+                    # computed by the previous sweep's core chain with the factors this sweep starts from
+                    z, e2, l2, sent, moved = self._carried[c]
+                    if sent:
+                        res.volume_sent[c] = sent
+                    if moved:
+                        res.regrid_sent[c] = moved
+                    yield from walk(c, z, e2, l2, self.node_layout[c])
                 else:
                     xin, lin, target = x, ldims, self.node_layout[c]
                     if target.q != lay.q:
@@ -371,8 +403,31 @@ class DistributedHooi:
         for m in range(self.n):                      # the ledger keeps the reference's mode order
             core_macs += self.spec.K[m] * card
             card = card * self.spec.K[m] // self.spec.L[m]
-        for m in self.core_order:
-            x, ext, ldims = yield from self._ttm(x, ext, ldims, m, fresh[m], -1, res)
+        if self.carry_enabled and self._carry_path:
+            lay, carried = self.layout, {}
+            for c in self._carry_path:
+                mode, target, ledger = tree.mode[c], self.node_layout[c], SweepResult()
+                if target.q != lay.q:
+                    sends, _ = regrid_plan(ext, lay, target, self.rank)
+                    ledger.regrid_sent[c] = sum(int(np.prod([hi - lo for lo, hi in o], dtype=np.int64))
+                                                for peer, o in sends if peer != self.rank)
+                    moved = yield from regrid(x.view(ldims), ext, lay, target, self.rank, self.ops.empty)
+                    x, ldims = moved.reshape(-1), target.local_dims(self.rank, ext)
+                self._mark("begin_ttm", c)
+                x, ext, ldims = yield from self._ttm(x, ext, ldims, mode, fresh[mode], c, ledger, target)
+                self._mark("end_ttm", c)
+                carried[c] = (x, list(ext), list(ldims), ledger.volume_sent.get(c, 0), ledger.regrid_sent.get(c, 0))
+                lay = target
+            m = self._carry_leaf_mode
+            x, ext, ldims = yield from self._ttm(x, ext, ldims, m, fresh[m], -1, res, lay)
+            if lay.q != self.layout.q:      # the core lives on the root grid
+                moved = yield from regrid(x.view(ldims), ext, lay, self.layout, self.rank, self.ops.empty)
+                x, ldims = moved.reshape(-1), self.layout.local_dims(self.rank, ext)
+            self._carried = carried
+        else:
+            self._carried = {}
+            for m in self.core_order:
+                x, ext, ldims = yield from self._ttm(x, ext, ldims, m, fresh[m], -1, res)
         self._mark("end_core")
         self.core, self.core_ldims = x, ldims
         self.factors = fresh
@@ -664,10 +719,10 @@ def run_bench_rank(args, rank: int, world: int, local_rank: int):
     def one_sweep():
         return run_rank(dh.sweep(), dist, ops)
 
+    # one HOOI run from the random orthonormal start: W warm-up iterations, then the K timed ones continue it
     dh.set_factors(f0)
     for _ in range(max(args.warmup, 0)):
         one_sweep()
-    dh.set_factors(f0)
     ctx.synchronize()
     dist.barrier()
     torch.cuda.synchronize()
@@ -769,6 +824,8 @@ def run_bench_rank(args, rank: int, world: int, local_rank: int):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg.name, "iterations": cfg.iterations, "schedule": "jacobi on optimal_tree",
+                       "timed_steps": "iterations W+1..W+K of one HOOI run from the random orthonormal start",
+                       "core": "chain along a tree path, partial products carried into the next sweep",
                        "tree": tree.label(), "grid": list(q),
                        "node_grids": {str(k): list(v) for k, v in scheme.node_grids.items()} if scheme else None,
                        "grid_volume_elements": (P.scheme_volume(tree, spec, scheme, world).total if scheme

@@ -240,6 +240,42 @@ def test_gloo_process_group_with_regrid(tmp_path):
     assert sum(int(d["regrid"][0]) for d in data) == P.count_moved(node_input_extents(tree, spec, first), [2, 1, 1], [1, 1, 2])
 
 
+@pytest.mark.parametrize("L,K,q", [((12, 10, 8), (4, 3, 2), (2, 1, 2)), ((9, 8, 7, 6), (3, 3, 2, 2), (1, 2, 1, 2)),
+                                   ((17, 9), (4, 4), (4, 2))])
+def test_carried_path_in_the_grid_executor(L, K, q):
+    """The grid executor carries the core chain's partial products into the next sweep like the single-GPU plan:
+    same bits with it on or off, and every sweep -- cold or warm -- ships exactly the model's volume per node."""
+    spec = P.ProblemSpec(list(L), list(K))
+    tree = P.optimal_tree(spec).tree
+    cfg = W.Config(1, list(L), list(K), 1e-2, 3)
+    t = W.build_tensor_host(cfg)
+    f0 = W.start_factors(cfg)
+    layout = D.GridLayout(q)
+    vol = P.static_volume(tree, spec, q, layout.procs)
+
+    def run(carry):
+        ops = NumpyOps()
+        ranks = [D.DistributedHooi(ops, spec, tree, q, r) for r in range(layout.procs)]
+        for r, dh in enumerate(ranks):
+            dh.carry_enabled = carry
+            dh.set_local_tensor(np.ascontiguousarray(t[layout.slices(r, spec.L)]))
+            dh.set_factors(f0)
+        out = []
+        for sweep in range(3):
+            results = D.run_virtual([dh.sweep() for dh in ranks], ops)
+            for node, want in enumerate(vol.per_node):
+                assert sum(r.volume_sent.get(node, 0) for r in results) == want, (carry, sweep, node)
+            out.append((ranks[0].get_factors(), assemble_core(layout, spec, [dh.get_local_core() for dh in ranks])))
+            assert bool(ranks[0]._carried) == carry
+        ranks[0].invalidate()
+        assert not ranks[0]._carried
+        return out
+
+    for (fa, ca), (fb, cb) in zip(run(True), run(False)):
+        assert all(np.array_equal(a, b) for a, b in zip(fa, fb))
+        assert np.max(np.abs(ca - cb)) <= 1e-12 * np.max(np.abs(cb))    # the chain order differs: rounding only
+
+
 def test_regrid_roundtrip_and_counts():
     ext = (7, 6, 5)
     full = hostgen.random_tensor(ext, 3)
