@@ -283,6 +283,14 @@ int tp_reconstruction_error(tp_ctx* ctx, const tp_tensor* t, const size_t* core_
  * paper's scheme needs exactly when the grid splits the contracted mode (grid_volume.hpp:41). */
 int tp_dev_ttm_partial(tp_ctx* ctx, const double* x, int n_modes, const size_t* dims, int mode, const double* factor,
                        size_t L_full, size_t l0, size_t K, int n_dest, const size_t* dest_cuts, double* z);
+/* Same product, scattered: chunk d (output rows dest_cuts[d]..dest_cuts[d+1], a contiguous (outer, rows_d, inner)
+ * tensor) is written to dest_ptrs[d], which may be any device-accessible address -- in particular a receive slot in a
+ * peer GPU's memory mapped over NVLink, so that the kernel's epilogue is the send of the reduce-scatter and no copy or
+ * collective call follows (the receivers then add their slots in rank order with tp_dev_reduce_slots).  Entries of
+ * empty chunks are ignored. */
+int tp_dev_ttm_scatter(tp_ctx* ctx, const double* x, int n_modes, const size_t* dims, int mode, const double* factor,
+                       size_t L_full, size_t l0, size_t K, int n_dest, const size_t* dest_cuts,
+                       double* const* dest_ptrs);
 /* out[i] = slots[0][i] + ... + slots[n_slots-1][i], i < count, summed in slot order (deterministic). */
 int tp_dev_reduce_slots(tp_ctx* ctx, double* out, const double* const* slots_host, int n_slots, size_t count);
 /* dst(a, l0+l, b) = src(a, l, b): places a peer's mode slice (outer, count, inner) into (outer, full_len, inner). */

@@ -1947,6 +1947,49 @@ int tp_dev_ttm_partial(tp_ctx* ctx, const double* x, int n_modes, const size_t* 
   });
 }
 
+int tp_dev_ttm_scatter(tp_ctx* ctx, const double* x, int n_modes, const size_t* dims, int mode, const double* factor,
+                       size_t L_full, size_t l0, size_t K, int n_dest, const size_t* dest_cuts,
+                       double* const* dest_ptrs) {
+  return guarded([&] {
+    bind(ctx);
+    if (!x || !factor || !dest_ptrs || !dest_cuts) raise(TP_ERR_BAD_ARGUMENT, "null pointer");
+    checked_size(n_modes, dims);
+    std::vector<size_t> d(dims, dims + n_modes);
+    long long outer, inner;
+    mode_extents(d, mode, outer, inner);
+    const long long len = static_cast<long long>(d[mode]);
+    if (l0 + d[mode] > L_full) raise(TP_ERR_SHAPE_MISMATCH, "factor rows do not cover the block's mode slice");
+    if (K == 0) raise(TP_ERR_SHAPE_MISMATCH, "empty matrix");
+    if (n_dest < 1 || n_dest > kMaxTtmDest) raise(TP_ERR_BAD_ARGUMENT, "between 1 and 16 destinations");
+    std::vector<long long> cuts(n_dest + 1), offsets(n_dest, 0);
+    for (int i = 0; i <= n_dest; ++i) cuts[i] = static_cast<long long>(dest_cuts[i]);
+    if (cuts[0] != 0 || cuts[n_dest] != static_cast<long long>(K)) raise(TP_ERR_BAD_ARGUMENT, "destination cuts must span [0, K]");
+    // the kernels address chunk d as z + dest_off[d]: anchor at the first non-empty chunk's buffer and express the
+    // others (possibly peer-mapped memory) as element distances from it
+    int anchor = -1;
+    for (int i = 0; i < n_dest; ++i) {
+      if (cuts[i + 1] < cuts[i]) raise(TP_ERR_BAD_ARGUMENT, "destination cuts must ascend");
+      if (cuts[i + 1] == cuts[i]) continue;
+      if (!dest_ptrs[i]) raise(TP_ERR_BAD_ARGUMENT, "null destination for a non-empty chunk");
+      if (reinterpret_cast<uintptr_t>(dest_ptrs[i]) % sizeof(double)) raise(TP_ERR_BAD_ARGUMENT, "misaligned destination");
+      if (anchor < 0) anchor = i;
+    }
+    if (anchor < 0) return;
+    double* const z = dest_ptrs[anchor];
+    for (int i = 0; i < n_dest; ++i)
+      if (cuts[i + 1] > cuts[i])
+        offsets[i] = static_cast<long long>((reinterpret_cast<intptr_t>(dest_ptrs[i]) - reinterpret_cast<intptr_t>(z)) /
+                                            static_cast<intptr_t>(sizeof(double)));
+    const TtmFragmentLayout f = ttm_fragment_layout(static_cast<long long>(K), len);
+    double* frag = ensure_frag_scratch(ctx, f.doubles);
+    TPB_CUDA(prep_factor_fragments(ctx->stream, factor + l0, static_cast<long long>(L_full), 1,
+                                   static_cast<long long>(K), len, f, frag));
+    TPB_CUDA(launch_ttm(ctx->stream, x, outer, len, inner, frag, f, static_cast<long long>(K), z, ctx->sm_count,
+                        n_dest, cuts.data(), offsets.data()));
+    ctx->own_kernels += 2;
+  });
+}
+
 int tp_dev_reduce_slots(tp_ctx* ctx, double* out, const double* const* slots_host, int n_slots, size_t count) {
   return guarded([&] {
     bind(ctx);

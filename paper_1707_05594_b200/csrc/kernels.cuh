@@ -28,9 +28,11 @@ constexpr int kMaxTtmDest = 16;
 // Z(a,k,b) = sum_l M(k,l) X(a,l,b); x is (outer, len, inner) row-major, z is (outer, new_len, inner).
 // With n_dest > 1 the output rows are split at dest_cuts[0..n_dest] (dest_cuts[0] = 0, dest_cuts[n_dest] = new_len)
 // and written destination-major: chunk d is the contiguous tensor (outer, dest_cuts[d+1]-dest_cuts[d], inner).
+// dest_offsets (optional, n_dest entries, in elements relative to z): where each chunk starts instead of the packed
+// destination-major layout -- e.g. the distance to a peer GPU's receive slot, so that the stores go straight there.
 cudaError_t launch_ttm(cudaStream_t stream, const double* x, long long outer, long long len, long long inner,
                        const double* mfrag, const TtmFragmentLayout& f, long long new_len, double* z, int sm_count,
-                       int n_dest = 1, const long long* dest_cuts = nullptr);
+                       int n_dest = 1, const long long* dest_cuts = nullptr, const long long* dest_offsets = nullptr);
 
 // Warp-specialised TMA variant (ttm_tma_kernels.cu): used by launch_ttm for 16-byte-aligned, even extents with enough
 // columns to fill the machine.  mfrag must be the copy matching the mode (interleaved rows when inner > 1).
@@ -38,7 +40,7 @@ bool ttm_tma_eligible(const double* x, long long outer, long long len, long long
                       int k_blocks, int sm_count);
 cudaError_t launch_ttm_tma(cudaStream_t stream, const double* x, long long outer, long long len, long long inner,
                            const double* mfrag, const TtmFragmentLayout& f, long long new_len, double* z,
-                           int sm_count, int n_dest, const long long* dest_cuts);
+                           int sm_count, int n_dest, const long long* dest_cuts, const long long* dest_offsets = nullptr);
 
 // ---- Gram of the mode-n unfolding, read in place (gram_kernels.cu) -----------
 struct GramLayout {

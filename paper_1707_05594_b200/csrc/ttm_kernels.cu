@@ -419,7 +419,7 @@ cudaError_t prep_factor_fragments(cudaStream_t stream, const double* m, long lon
 
 cudaError_t launch_ttm(cudaStream_t stream, const double* x, long long outer, long long len, long long inner,
                        const double* mfrag, const TtmFragmentLayout& f, long long new_len, double* z, int sm_count,
-                       int n_dest, const long long* dest_cuts) {
+                       int n_dest, const long long* dest_cuts, const long long* dest_offsets) {
   static const bool tma_off = [] {
     const char* v = std::getenv("TPB_DISABLE_TMA");
     return v && v[0] == '1';
@@ -427,10 +427,11 @@ cudaError_t launch_ttm(cudaStream_t stream, const double* x, long long outer, lo
   // TPB_DISABLE_TMA=1 (read once) / TPB_DISABLE_TMA_NOW (read per launch): force the cp.async kernel (A/B tests)
   if (!tma_off && !std::getenv("TPB_DISABLE_TMA_NOW") && ttm_tma_eligible(x, outer, len, inner, z, f.kt, f.k_blocks, sm_count)) {
     bool chunks_aligned = true;
-    for (int d = 0; dest_cuts && d < n_dest; ++d) chunks_aligned = chunks_aligned && ((outer * dest_cuts[d] * inner) % 2 == 0);
+    for (int d = 0; dest_cuts && d < n_dest; ++d)
+      chunks_aligned = chunks_aligned && ((dest_offsets ? dest_offsets[d] : outer * dest_cuts[d] * inner) % 2 == 0);
     if (chunks_aligned)
       return launch_ttm_tma(stream, x, outer, len, inner, inner == 1 ? mfrag : mfrag + f.layout_doubles, f, new_len, z,
-                            sm_count, n_dest, dest_cuts);
+                            sm_count, n_dest, dest_cuts, dest_offsets);
   }
   TtmParams p;
   if (n_dest < 1 || n_dest > kMaxTtmDest) return cudaErrorInvalidValue;
@@ -442,8 +443,8 @@ cudaError_t launch_ttm(cudaStream_t stream, const double* x, long long outer, lo
       const long long k0 = dest_cuts ? dest_cuts[d] : 0, k1 = dest_cuts ? dest_cuts[d + 1] : new_len;
       p.dest_k0[d] = static_cast<int>(k0);
       p.dest_k0[d + 1] = static_cast<int>(k1);
-      p.dest_off[d] = off;
-      dest_aligned = dest_aligned && (off % 2 == 0);
+      p.dest_off[d] = dest_offsets ? dest_offsets[d] : off;
+      dest_aligned = dest_aligned && (p.dest_off[d] % 2 == 0);
       off += outer * (k1 - k0) * inner;
     }
     for (int d = n_dest + 1; d <= kMaxTtmDest; ++d) p.dest_k0[d] = p.dest_k0[n_dest];

@@ -351,7 +351,7 @@ bool ttm_tma_eligible(const double* x, long long outer, long long len, long long
 
 cudaError_t launch_ttm_tma(cudaStream_t stream, const double* x, long long outer, long long len, long long inner,
                            const double* mfrag, const TtmFragmentLayout& f, long long new_len, double* z,
-                           int sm_count, int n_dest, const long long* dest_cuts) {
+                           int sm_count, int n_dest, const long long* dest_cuts, const long long* dest_offsets) {
   const bool last = inner == 1;
   TmaParams p;
   p.z = z;
@@ -370,8 +370,8 @@ cudaError_t launch_ttm_tma(cudaStream_t stream, const double* x, long long outer
     const long long k0 = dest_cuts ? dest_cuts[d] : 0, k1 = dest_cuts ? dest_cuts[d + 1] : new_len;
     p.dest_k0[d] = static_cast<int>(k0);
     p.dest_k0[d + 1] = static_cast<int>(k1);
-    p.dest_off[d] = off;
-    if (off % 2) return cudaErrorInvalidValue;  // caller checks eligibility; chunks must stay 16-byte aligned
+    p.dest_off[d] = dest_offsets ? dest_offsets[d] : off;
+    if (p.dest_off[d] % 2) return cudaErrorInvalidValue;  // caller checks eligibility; chunks must stay 16-byte aligned
     off += outer * (k1 - k0) * inner;
   }
   for (int d = n_dest + 1; d <= kMaxTtmDest; ++d) p.dest_k0[d] = p.dest_k0[n_dest];

@@ -94,6 +94,25 @@ class AllReduce:     # sum over all ranks, in place
 
 
 @dataclass
+class PeerSlots:     # ask the runner for peer-addressable receive slots of one reduce-scatter (fused scatter epilogue)
+    key: object      # stable per call site, so that runners can keep the buffers between sweeps
+    group: list      # ranks of the mode group in slot order
+    me: int          # this rank's position in the group
+    count: int       # elements of this rank's chunk = size of each of its receive slots
+
+
+@dataclass
+class PeerSlotsReply:
+    my_slots: list   # len(group) local buffers of `count` elements; slot s is written by group[s]
+    targets: list    # len(group) buffers: targets[d] is group[d]'s slot number `me` (its memory, its size)
+
+
+@dataclass
+class GroupBarrier:  # every group member's stores into peer slots are complete and visible
+    group: list
+
+
+@dataclass
 class Volume:        # bookkeeping: elements this rank shipped for a TTM node (checked against the reference model)
     node: int
     elements: int
@@ -140,6 +159,13 @@ class GpuOps:
                                      self._ptr(factor), ctypes.c_size_t(l_full), ctypes.c_size_t(l0),
                                      ctypes.c_size_t(k), len(dest_cuts) - 1, cuts, self._ptr(z)))
         return z
+
+    def ttm_scatter(self, x, dims, mode, factor, l_full, l0, k, dest_cuts, targets):
+        """Partial product whose chunk d is stored straight into targets[d] (own or peer memory)."""
+        ptrs = (dbl_p * len(targets))(*[self._ptr(t) if t is not None and t.numel() else None for t in targets])
+        check(lib.tp_dev_ttm_scatter(self.ctx._h, self._ptr(x), len(dims), size_array(dims), int(mode),
+                                     self._ptr(factor), ctypes.c_size_t(l_full), ctypes.c_size_t(l0),
+                                     ctypes.c_size_t(k), len(dest_cuts) - 1, size_array(dest_cuts), ptrs))
 
     def reduce_slots(self, slots, count):
         out = self.empty(count)
@@ -232,6 +258,8 @@ class DistributedHooi:
         # Carried path (as in the single-GPU plan): the core chain contracts along one root-to-leaf
         # path of the tree with the new factors, on the grids of those nodes; its partial products are the next
         # sweep's intermediates at those nodes and are kept instead of recomputed.
+        self.peer_scatter = True      # use peer-slot stores for reduce-scatters where the runner offers them
+        self.scatter_launches = 0
         self.carry_enabled = self.n >= 2
         self._carry_path, self._carry_leaf_mode = self._first_leaf_path()
         self._carried: Dict[int, tuple] = {}
@@ -294,10 +322,22 @@ class DistributedHooi:
         kcuts = lay.cuts(k, mode)
         group = lay.mode_group(self.rank, mode)
         me = lay.coords(self.rank)[mode]
-        part = self.ops.ttm_partial(x, ldims, mode, factor, l_full, l0, k, kcuts)
         per_row = int(np.prod(ldims, dtype=np.int64)) // ldims[mode]      # outer_loc * inner_loc
         offs = [per_row * c for c in kcuts]
         mine = offs[me + 1] - offs[me]
+        new_ldims[mode] = kcuts[me + 1] - kcuts[me]
+        if self.peer_scatter and hasattr(self.ops, "ttm_scatter"):
+            # fused form: the kernel's epilogue stores every chunk into its owner's receive slot (peer memory over
+            # NVLink); what remains of the reduce-scatter is a barrier and the ordered sum of the local slots
+            reply = yield PeerSlots(("ttm", node, mode, tuple(ldims)), group, me, mine)
+            if reply is not None:
+                self.ops.ttm_scatter(x, ldims, mode, factor, l_full, l0, k, kcuts, reply.targets)
+                self.scatter_launches += 1
+                if node >= 0:
+                    result.volume_sent[node] = result.volume_sent.get(node, 0) + (offs[-1] - mine)
+                yield GroupBarrier(group)
+                return self.ops.reduce_slots(reply.my_slots, mine), new_ext, new_ldims
+        part = self.ops.ttm_partial(x, ldims, mode, factor, l_full, l0, k, kcuts)
         slots, sends, recvs = [], [], []
         for d, peer in enumerate(group):
             if d == me:
@@ -499,6 +539,13 @@ def _run_rank(gen: Generator, dist, to_tensor):
                         work.wait()
             elif isinstance(req, AllReduce):
                 dist.all_reduce(to_tensor(req.tensor))
+            elif isinstance(req, PeerSlots):
+                # process groups reach each other through send/recv here; peer-mapped slots (symmetric memory over
+                # NVLink) are the runner-side half of the fused scatter that still needs multi-GPU hardware to build
+                req = gen.send(None)
+                continue
+            elif isinstance(req, GroupBarrier):
+                dist.barrier()
             else:
                 raise TypeError("unknown request %r" % (req,))
             req = gen.send(None)
@@ -514,10 +561,13 @@ def run_virtual(gens: Sequence[Generator], ops=None, copy=lambda dst, src: dst.c
     All ranks must issue the same kind of request at each step (they do: the program is SPMD and data-independent).
     AllReduce sums in rank order into a scratch copy and hands every rank the same bits, as NCCL/gloo would."""
     with _stream_of(ops):
-        return _run_virtual(gens, copy, add)
+        return _run_virtual(gens, copy, add, ops.empty if ops is not None and hasattr(ops, "empty") else None)
 
 
-def _run_virtual(gens, copy, add):
+def _run_virtual(gens, copy, add, alloc=None):
+    if alloc is None:
+        import torch
+        alloc = lambda count: torch.empty(int(count), dtype=torch.float64)
     n = len(gens)
     results = [None] * n
     reqs = []
@@ -553,11 +603,17 @@ def _run_virtual(gens, copy, add):
                 add(total, reqs[r].tensor)
             for r in range(n):
                 copy(reqs[r].tensor, total)
+        elif kind is PeerSlots:
+            # one address space: a "peer" slot is simply the other rank program's buffer
+            slots = [[alloc(reqs[r].count) for _ in reqs[r].group] for r in range(n)]
+            replies = [PeerSlotsReply(slots[r], [slots[peer][reqs[r].me] for peer in reqs[r].group]) for r in range(n)]
+        elif kind is GroupBarrier:
+            pass                      # lock-step: every rank program has issued its stores
         else:
             raise TypeError("unknown request %r" % (kind,))
         for r, g in enumerate(gens):
             try:
-                reqs[r] = g.send(None)
+                reqs[r] = g.send(replies[r] if kind is PeerSlots else None)
             except StopIteration as stop:
                 live[r] = False
                 results[r] = stop.value

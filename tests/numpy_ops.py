@@ -31,6 +31,14 @@ class NumpyOps:
             chunks.append(np.ascontiguousarray(z[tuple(sl)]).reshape(-1))
         return torch.from_numpy(np.concatenate(chunks))
 
+    def ttm_scatter(self, x, dims, mode, factor, l_full, l0, k, dest_cuts, targets):
+        part = self.ttm_partial(x, dims, mode, factor, l_full, l0, k, dest_cuts)
+        per_row = int(np.prod(dims, dtype=np.int64)) // dims[mode]
+        for d, target in enumerate(targets):
+            lo, hi = per_row * dest_cuts[d], per_row * dest_cuts[d + 1]
+            if hi > lo:
+                target.copy_(part[lo:hi])
+
     def reduce_slots(self, slots, count):
         out = slots[0].clone()
         for s in slots[1:]:

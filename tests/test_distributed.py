@@ -48,7 +48,7 @@ def check_against_oracle(spec, tree, q, t, f0, factors, core, results, sweeps):
         assert got == want, (node, got, want)
 
 
-def run_virtual_case(ops, L, K, q, sweeps=2, seed=5):
+def run_virtual_case(ops, L, K, q, sweeps=2, seed=5, peer_scatter=True):
     spec = P.ProblemSpec(list(L), list(K))
     tree = P.optimal_tree(spec).tree
     cfg = W.Config(1, list(L), list(K), 1e-2, sweeps)
@@ -57,6 +57,7 @@ def run_virtual_case(ops, L, K, q, sweeps=2, seed=5):
     layout = D.GridLayout(q)
     ranks = [D.DistributedHooi(ops, spec, tree, q, r) for r in range(layout.procs)]
     for r, dh in enumerate(ranks):
+        dh.peer_scatter = peer_scatter
         dh.set_local_tensor(np.ascontiguousarray(t[layout.slices(r, spec.L)]))
         dh.set_factors(f0)
     results = None
@@ -72,6 +73,9 @@ def run_virtual_case(ops, L, K, q, sweeps=2, seed=5):
     tn = ho.frobenius_norm(t)
     want_fit = np.sqrt(max(tn ** 2 - np.sum(core * core), 0.0)) / tn
     assert all(abs(f[0] - want_fit) <= 1e-9 * max(want_fit, 1e-3) for f in fits)
+    # which form of the reduce-scatter ran: peer-slot stores (virtual ranks share one address space) or send/recv
+    splits = any(qn > 1 for qn in q)
+    assert all((dh.scatter_launches > 0) == (peer_scatter and splits) for dh in ranks)
 
 
 VIRTUAL_CASES = [
@@ -86,6 +90,12 @@ VIRTUAL_CASES = [
 @pytest.mark.parametrize("L,K,q", VIRTUAL_CASES)
 def test_virtual_ranks_numpy(L, K, q):
     run_virtual_case(NumpyOps(), L, K, q)
+
+
+@pytest.mark.parametrize("L,K,q", VIRTUAL_CASES[4:8])
+def test_virtual_ranks_numpy_send_recv_form(L, K, q):
+    """The same reduce-scatters through destination-major chunks + batched send/recv (what process groups use)."""
+    run_virtual_case(NumpyOps(), L, K, q, peer_scatter=False)
 
 
 def test_optimal_grids_of_scaled_configs():
@@ -380,11 +390,14 @@ GPU_CASES = [((48, 40, 36), (8, 6, 5), (1, 1, 4)), ((768, 36, 30), (12, 6, 5), (
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("L,K,q", GPU_CASES)
-def test_virtual_ranks_gpu(L, K, q):
+@pytest.mark.parametrize("peer_scatter", [True, False], ids=["peer_slots", "send_recv"])
+def test_virtual_ranks_gpu(L, K, q, peer_scatter):
+    """peer_slots: the TTM kernels store each chunk straight into the owning rank's receive slot (tp_dev_ttm_scatter,
+    the fused reduce-scatter epilogue); send_recv: packed chunks + exchange.  Same results either way."""
     from paper_1707_05594_b200 import engine as E
     ctx = E.Context(0)
     try:
-        run_virtual_case(D.GpuOps(ctx), L, K, q)
+        run_virtual_case(D.GpuOps(ctx), L, K, q, peer_scatter=peer_scatter)
     finally:
         ctx.close()
 
