@@ -99,6 +99,7 @@ class PeerSlots:     # ask the runner for peer-addressable receive slots of one 
     group: list      # ranks of the mode group in slot order
     me: int          # this rank's position in the group
     count: int       # elements of this rank's chunk = size of each of its receive slots
+    counts: list = field(default_factory=list)   # chunk sizes of all group members (what this rank writes to each)
 
 
 @dataclass
@@ -329,7 +330,8 @@ class DistributedHooi:
         if self.peer_scatter and hasattr(self.ops, "ttm_scatter"):
             # fused form: the kernel's epilogue stores every chunk into its owner's receive slot (peer memory over
             # NVLink); what remains of the reduce-scatter is a barrier and the ordered sum of the local slots
-            reply = yield PeerSlots(("ttm", node, mode, tuple(ldims)), group, me, mine)
+            reply = yield PeerSlots(("ttm", node, mode, tuple(ldims)), group, me, mine,
+                                    [offs[d + 1] - offs[d] for d in range(len(group))])
             if reply is not None:
                 self.ops.ttm_scatter(x, ldims, mode, factor, l_full, l0, k, kcuts, reply.targets)
                 self.scatter_launches += 1
@@ -520,14 +522,60 @@ def _stream_of(ops):
     return ops.stream_context() if ops is not None and hasattr(ops, "stream_context") else contextlib.nullcontext()
 
 
-def run_rank(gen: Generator, dist, ops=None, to_tensor=lambda b: b):
+class SymmetricSlots:
+    """Receive slots in NVLink-mapped symmetric memory (torch.distributed._symmetric_memory): the runner-side half of
+    the fused reduce-scatter.  Rank r keeps, per call site, one symmetric buffer of len(group) slots; slot s is
+    written by group member s directly from its TTM kernel's epilogue (tp_dev_ttm_scatter), through the peer view
+    `get_buffer(r, ...)` of that buffer.  Buffers are allocated once per call site and reused every sweep; a barrier
+    on the symmetric-memory signal pads before the stores (the owners are done reading the previous sweep's slots)
+    and one after (all stores have landed) replace the send/recv.
+
+    Opt-in (TPB_PEER_SLOTS=1): only one GPU was available while this was written, so it has run at world size 1
+    only (tests/test_distributed.py::test_symmetric_slots_world_size_one)."""
+
+    def __init__(self, dist, device):
+        import torch
+        import torch.distributed._symmetric_memory as symm
+        self.torch, self.symm, self.dist, self.device = torch, symm, dist, device
+        self.cache = {}
+
+    def slots(self, req: PeerSlots) -> PeerSlotsReply:
+        torch, q = self.torch, len(req.group)
+        entry = self.cache.get(req.key)
+        if entry is None:
+            # symmetric allocations must have one size on every rank: agree on the largest chunk once per call site
+            bound = torch.tensor([max(req.counts + [req.count, 1])], dtype=torch.int64, device=self.device)
+            self.dist.all_reduce(bound, op=self.dist.ReduceOp.MAX)
+            bound = (int(bound.item()) + 1) // 2 * 2            # keep every slot 16-byte aligned
+            buf = self.symm.empty(q_max_slots(self.dist) * bound, dtype=torch.float64, device=self.device)
+            handle = self.symm.rendezvous(buf, group=self.dist.group.WORLD)
+            entry = self.cache[req.key] = (buf, handle, bound)
+        buf, handle, bound = entry
+        my_slots = [buf[s * bound:s * bound + req.count] for s in range(q)]
+        targets = [handle.get_buffer(peer, (req.counts[d],), torch.float64, req.me * bound) if req.counts[d] else None
+                   for d, peer in enumerate(req.group)]
+        handle.barrier(channel=0)          # nobody is still summing the slots this sweep is about to overwrite
+        self.last = handle
+        return PeerSlotsReply(my_slots, targets)
+
+    def barrier(self):
+        self.last.barrier(channel=0)
+
+
+def q_max_slots(dist) -> int:
+    """Upper bound on a mode group's size: the world size (a grid extent cannot exceed it)."""
+    return dist.get_world_size()
+
+
+def run_rank(gen: Generator, dist, ops=None, to_tensor=lambda b: b, peer_slots: Optional[SymmetricSlots] = None):
     """Drive one rank program with torch.distributed (`dist`); buffers must be torch tensors of the right device.
-    Pass the rank's `ops` so that the collectives queue on the engine's stream."""
+    Pass the rank's `ops` so that the collectives queue on the engine's stream.  `peer_slots`: a SymmetricSlots
+    provider turns the reduce-scatters into direct peer stores; without it they go through send/recv."""
     with _stream_of(ops):
-        return _run_rank(gen, dist, to_tensor)
+        return _run_rank(gen, dist, to_tensor, peer_slots)
 
 
-def _run_rank(gen: Generator, dist, to_tensor):
+def _run_rank(gen: Generator, dist, to_tensor, peer_slots=None):
     try:
         req = next(gen)
         while True:
@@ -540,12 +588,14 @@ def _run_rank(gen: Generator, dist, to_tensor):
             elif isinstance(req, AllReduce):
                 dist.all_reduce(to_tensor(req.tensor))
             elif isinstance(req, PeerSlots):
-                # process groups reach each other through send/recv here; peer-mapped slots (symmetric memory over
-                # NVLink) are the runner-side half of the fused scatter that still needs multi-GPU hardware to build
-                req = gen.send(None)
+                # without a provider the program falls back to packed chunks + send/recv
+                req = gen.send(peer_slots.slots(req) if peer_slots is not None else None)
                 continue
             elif isinstance(req, GroupBarrier):
-                dist.barrier()
+                if peer_slots is not None:
+                    peer_slots.barrier()
+                else:
+                    dist.barrier()
             else:
                 raise TypeError("unknown request %r" % (req,))
             req = gen.send(None)
@@ -772,8 +822,11 @@ def run_bench_rank(args, rank: int, world: int, local_rank: int):
         ev.record(ops.stream)
         marks.append((what, node, ev))
 
+    # TPB_PEER_SLOTS=1: reduce-scatters as direct stores into NVLink-mapped peer slots (see SymmetricSlots)
+    peer_slots = SymmetricSlots(dist, ops.device) if os.environ.get("TPB_PEER_SLOTS") == "1" else None
+
     def one_sweep():
-        return run_rank(dh.sweep(), dist, ops)
+        return run_rank(dh.sweep(), dist, ops, peer_slots=peer_slots)
 
     # one HOOI run from the random orthonormal start: W warm-up iterations, then the K timed ones continue it
     dh.set_factors(f0)

@@ -418,6 +418,51 @@ def test_dynamic_scheme_virtual_ranks_gpu():
         ctx.close()
 
 
+def _symmetric_slots_worker(rank, world, port, out_path):
+    import torch
+    import torch.distributed as dist
+    from paper_1707_05594_b200 import engine as E
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", 0))
+    try:
+        ctx = E.Context(0)
+        ops = D.GpuOps(ctx)
+        rng = np.random.default_rng(3)
+        dims, mode, k, l_full, l0 = [40, 24, 36], 1, 10, 30, 4
+        x = rng.standard_normal(dims)
+        factor = rng.standard_normal((l_full, k))
+        dx, df = ops.from_host(x), ops.from_host(np.asfortranarray(factor).reshape(-1, order="F"))
+        cuts = [0, k]
+        count = dims[0] * k * dims[2]
+        with ops.stream_context():
+            provider = D.SymmetricSlots(dist, ops.device)
+            ok = True
+            for sweep in range(2):                     # second round reuses the cached symmetric buffer
+                reply = provider.slots(D.PeerSlots(("test", 0), [0], 0, count, [count]))
+                ops.ttm_scatter(dx, dims, mode, df, l_full, l0, k, cuts, reply.targets)
+                provider.barrier()
+                got = ops.to_host(ops.reduce_slots(reply.my_slots, count)).reshape(dims[0], k, dims[2])
+                want = ho.ttm(x, factor.T[:, l0:l0 + dims[mode]], mode)
+                ok = ok and bool(np.max(np.abs(got - want)) <= 1e-12 * np.max(np.abs(want)))
+                ok = ok and reply.targets[0].data_ptr() == reply.my_slots[0].data_ptr()
+        np.save(out_path, np.array([ok]))
+        ctx.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_symmetric_slots_world_size_one(tmp_path):
+    """The symmetric-memory slot provider (rendezvous, peer views, signal-pad barriers) with the real scatter kernel,
+    at the only world size one GPU allows: the 'peer' view is the rank's own slot."""
+    import torch.multiprocessing as mp
+    out = str(tmp_path / "ok.npy")
+    mp.spawn(_symmetric_slots_worker, args=(1, _free_port(), out), nprocs=1, join=True)
+    assert bool(np.load(out)[0])
+
+
 @pytest.mark.gpu
 def test_gpu_ops_match_numpy_ops():
     """Every local building block of the grid executor: CUDA (tp_dev_*) against the NumPy stand-in."""
