@@ -437,7 +437,13 @@ def _symmetric_slots_worker(rank, world, port, out_path):
         cuts = [0, k]
         count = dims[0] * k * dims[2]
         with ops.stream_context():
-            provider = D.SymmetricSlots(dist, ops.device)
+            try:
+                provider = D.SymmetricSlots(dist, ops.device)
+                provider.slots(D.PeerSlots(("probe", 0), [0], 0, 8, [8]))
+            except Exception as exc:               # no symmetric-memory support on this box / torch build
+                np.save(out_path, np.array([-1]))
+                print("symmetric memory unavailable:", repr(exc))
+                return
             ok = True
             for sweep in range(2):                     # second round reuses the cached symmetric buffer
                 reply = provider.slots(D.PeerSlots(("test", 0), [0], 0, count, [count]))
@@ -460,7 +466,10 @@ def test_symmetric_slots_world_size_one(tmp_path):
     import torch.multiprocessing as mp
     out = str(tmp_path / "ok.npy")
     mp.spawn(_symmetric_slots_worker, args=(1, _free_port(), out), nprocs=1, join=True)
-    assert bool(np.load(out)[0])
+    verdict = int(np.load(out)[0])
+    if verdict < 0:
+        pytest.skip("torch symmetric memory is not available here")
+    assert verdict == 1
 
 
 @pytest.mark.gpu
