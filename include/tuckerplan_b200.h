@@ -307,6 +307,14 @@ int tp_dev_leaf_solve(tp_ctx* ctx, double* gram, size_t rows, int k, double* fac
  * *used_fast (host, may be NULL) reports which path produced the factor. */
 int tp_dev_leaf_solve_warm(tp_ctx* ctx, double* gram, size_t rows, int k, const double* start, double* factor,
                            int* flag, int* info, int* used_fast);
+/* Asynchronous pair for executors that overlap the leaf solves with the tree (the grid executor): _begin queues the
+ * solve on side stream `lane` (0..3), ordered after everything queued on the context's stream so far, and returns;
+ * _finish makes the context's stream wait for it, checks the top-k certificate (one stream synchronisation) and
+ * falls back to the full solve on the intact Gram matrix.  gram, start, factor, flag and info must stay untouched
+ * between the two calls; one solve in flight per lane. */
+int tp_dev_leaf_solve_begin(tp_ctx* ctx, double* gram, size_t rows, int k, const double* start, double* factor,
+                            int* flag, int* info, int lane);
+int tp_dev_leaf_solve_finish(tp_ctx* ctx, int lane, double* factor, int* flag, int* info, int* used_fast);
 /* *out (device double) = sum x[i]^2 */
 int tp_dev_sum_squares(tp_ctx* ctx, const double* x, size_t count, double* out);
 

@@ -68,6 +68,16 @@ struct tp_ctx {
   // side streams for the eigen-solves of a Jacobi sweep: the leaves are independent of each other and of the
   // remaining tree TTMs, and an eigen-solve is latency-bound, so it runs beside the TTM kernels
   void* dev_scratch = nullptr;       // LeafScratch of the tp_dev_* entry points
+  // asynchronous leaf solves of the grid executor (tp_dev_leaf_solve_begin / _finish): one lane per side stream
+  struct Lane {
+    void* scratch = nullptr;         // LeafScratch
+    cudaEvent_t ready = nullptr, done = nullptr;
+    bool busy = false, fast = false;
+    double* gram = nullptr;
+    size_t rows = 0;
+    int k = 0;
+  };
+  Lane lanes[4];
   // by-value hooi_sweep calls in a loop (the reference CLI's pattern) keep their device tensor and plan between
   // calls as long as shape, ranks, tree and schedule repeat; only the tensor and factor bytes move again
   std::vector<long long> host_call_key;
@@ -1187,6 +1197,14 @@ int tp_ctx_destroy(tp_ctx* ctx) {
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     for (void* ws : ctx->blas_ws) cudaFree(ws);
     release_host_call_cache(ctx);
+    for (tp_ctx::Lane& lane : ctx->lanes) {
+      if (lane.scratch) {
+        static_cast<LeafScratch*>(lane.scratch)->release();
+        delete static_cast<LeafScratch*>(lane.scratch);
+      }
+      if (lane.ready) cudaEventDestroy(lane.ready);
+      if (lane.done) cudaEventDestroy(lane.done);
+    }
     if (ctx->dev_scratch) {
       static_cast<LeafScratch*>(ctx->dev_scratch)->release();
       delete static_cast<LeafScratch*>(ctx->dev_scratch);
@@ -2045,6 +2063,106 @@ int tp_dev_leaf_solve(tp_ctx* ctx, double* gram, size_t rows, int k, double* fac
   });
 }
 
+// Iteration buffers of a scratch that serves leaves of changing sizes (the tp_dev_* entry points).
+static void reserve_iteration_buffers(tp_ctx* ctx, LeafScratch& s, long long rows, int k) {
+  leaf_scratch_reserve(ctx, s, 1, 0);
+  if (s.block != 0 && (s.block != k + kSubspaceOversample || rows > s.fast_rows)) {
+    cudaFree(s.q); cudaFree(s.z); cudaFree(s.x); cudaFree(s.h); cudaFree(s.theta); cudaFree(s.small_work);
+    cudaFree(s.verdict); cudaFree(s.chol); cudaFree(s.ritz);
+    s.q = s.z = s.x = s.h = s.theta = s.small_work = s.chol = s.ritz = nullptr;
+    s.verdict = nullptr;
+    s.block = 0;
+    forget_recorded_solve(s);
+  }
+  if (s.block == 0) {
+    subspace_reserve(ctx, s, rows, k);
+    s.fast_rows = rows;
+  }
+}
+
+// Asynchronous pair: _begin queues the solve of `gram` on side stream `lane` (ordered after everything queued on the
+// main stream so far) and returns; the main stream goes on with the tree.  _finish makes the main stream wait for
+// it, reads the certificate of the top-k path and redoes the leaf with the full solve if it was missed.  Between
+// the two calls gram, start, factor, flag and info must stay untouched.  One solve in flight per lane.
+int tp_dev_leaf_solve_begin(tp_ctx* ctx, double* gram, size_t rows, int k, const double* start, double* factor,
+                            int* flag, int* info, int lane_index) {
+  return guarded([&] {
+    bind(ctx);
+    if (!gram || !factor || !flag || !info) raise(TP_ERR_BAD_ARGUMENT, "null pointer");
+    if (lane_index < 0 || lane_index >= tp_ctx::kAux) raise(TP_ERR_BAD_ARGUMENT, "lane outside 0..3");
+    check_leaf_args(static_cast<long long>(rows), 1, k);
+    tp_ctx::Lane& lane = ctx->lanes[lane_index];
+    if (lane.busy) raise(TP_ERR_BAD_ARGUMENT, "a solve is already in flight on this lane");
+    if (!lane.scratch) {
+      lane.scratch = new LeafScratch;
+      TPB_CUDA(cudaEventCreateWithFlags(&lane.ready, cudaEventDisableTiming));
+      TPB_CUDA(cudaEventCreateWithFlags(&lane.done, cudaEventDisableTiming));
+    }
+    LeafScratch& s = *static_cast<LeafScratch*>(lane.scratch);
+    cudaStream_t side = ctx->aux[lane_index];
+    lane.fast = start && subspace_eligible(static_cast<long long>(rows), k);
+    if (lane.fast)
+      reserve_iteration_buffers(ctx, s, static_cast<long long>(rows), k);
+    else
+      leaf_scratch_reserve(ctx, s, static_cast<long long>(rows), 0);
+    TPB_CUDA(cudaEventRecord(lane.ready, ctx->stream));
+    TPB_CUDA(cudaStreamWaitEvent(side, lane.ready, 0));
+    if (lane.fast) {
+      int* const saved_flag = s.flag;
+      s.flag = flag;
+      s.last_ritz = nullptr;  // a function of the arguments only
+      leaf_solve_subspace(ctx, s, gram, static_cast<long long>(rows), k, start, factor, lane_index);
+      s.flag = saved_flag;
+      s.fast_used = false;
+    } else {
+      TPB_SOLVER(cusolverDnDsyevd(ctx->aux_solver[lane_index], CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
+                                  static_cast<int>(rows), gram, static_cast<int>(rows), s.w, s.work, s.lwork, info));
+      ctx->library_calls += 1;
+      TPB_CUDA(launch_select_basis(side, gram, s.w, static_cast<int>(rows), static_cast<int>(rows), k, factor, flag));
+      ctx->own_kernels += 1;
+    }
+    TPB_CUDA(cudaEventRecord(lane.done, side));
+    lane.busy = true;
+    lane.gram = gram;
+    lane.rows = rows;
+    lane.k = k;
+  });
+}
+
+int tp_dev_leaf_solve_finish(tp_ctx* ctx, int lane_index, double* factor, int* flag, int* info, int* used_fast) {
+  return guarded([&] {
+    bind(ctx);
+    if (lane_index < 0 || lane_index >= tp_ctx::kAux) raise(TP_ERR_BAD_ARGUMENT, "lane outside 0..3");
+    if (!factor || !flag || !info) raise(TP_ERR_BAD_ARGUMENT, "null pointer");
+    tp_ctx::Lane& lane = ctx->lanes[lane_index];
+    if (!lane.busy) raise(TP_ERR_BAD_ARGUMENT, "no solve in flight on this lane");
+    lane.busy = false;
+    if (used_fast) *used_fast = 0;
+    TPB_CUDA(cudaStreamWaitEvent(ctx->stream, lane.done, 0));
+    if (!lane.fast) return;
+    LeafScratch& s = *static_cast<LeafScratch*>(lane.scratch);
+    int host[3] = {0, 0, 0};
+    TPB_CUDA(cudaMemcpyAsync(&host[0], s.verdict, 2 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    TPB_CUDA(cudaMemcpyAsync(&host[2], flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    TPB_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (host[0] == 0 && host[1] == 0 && host[2] == 0) {
+      TPB_CUDA(cudaMemsetAsync(info, 0, sizeof(int), ctx->stream));
+      if (used_fast) *used_fast = 1;
+      return;
+    }
+    // certificate missed: the Gram matrix is intact, let the exact spectrum decide (main stream)
+    TPB_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream));
+    leaf_scratch_reserve(ctx, s, static_cast<long long>(lane.rows), 0);
+    TPB_SOLVER(cusolverDnDsyevd(ctx->solver, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER,
+                                static_cast<int>(lane.rows), lane.gram, static_cast<int>(lane.rows), s.w, s.work,
+                                s.lwork, info));
+    ctx->library_calls += 1;
+    TPB_CUDA(launch_select_basis(ctx->stream, lane.gram, s.w, static_cast<int>(lane.rows),
+                                 static_cast<int>(lane.rows), lane.k, factor, flag));
+    ctx->own_kernels += 1;
+  });
+}
+
 int tp_dev_leaf_solve_warm(tp_ctx* ctx, double* gram, size_t rows, int k, const double* start, double* factor,
                            int* flag, int* info, int* used_fast) {
   return guarded([&] {
@@ -2054,26 +2172,7 @@ int tp_dev_leaf_solve_warm(tp_ctx* ctx, double* gram, size_t rows, int k, const 
     if (used_fast) *used_fast = 0;
     LeafScratch& s = dev_scratch(ctx);
     if (start && subspace_eligible(static_cast<long long>(rows), k)) {
-      leaf_scratch_reserve(ctx, s, 1, 0);
-      if (s.block != k + kSubspaceOversample) {  // a different block size: rebuild the iteration buffers
-        cudaFree(s.q); cudaFree(s.z); cudaFree(s.x); cudaFree(s.h); cudaFree(s.theta); cudaFree(s.small_work);
-        cudaFree(s.verdict); cudaFree(s.chol); cudaFree(s.ritz);
-        s.q = s.z = s.x = s.h = s.theta = s.small_work = s.chol = s.ritz = nullptr;
-        s.verdict = nullptr;
-        s.block = 0;
-        forget_recorded_solve(s);
-      }
-      if (s.block == 0 || static_cast<long long>(rows) > s.fast_rows) {
-        if (s.block) {
-          cudaFree(s.q); cudaFree(s.z); cudaFree(s.x); cudaFree(s.h); cudaFree(s.theta); cudaFree(s.small_work);
-          cudaFree(s.verdict); cudaFree(s.chol); cudaFree(s.ritz);
-          s.chol = s.ritz = nullptr;
-          s.block = 0;
-          forget_recorded_solve(s);
-        }
-        subspace_reserve(ctx, s, static_cast<long long>(rows), k);
-        s.fast_rows = static_cast<long long>(rows);
-      }
+      reserve_iteration_buffers(ctx, s, static_cast<long long>(rows), k);
       int* const saved_flag = s.flag;
       s.flag = flag;  // the caller's degenerate flag
       s.last_ritz = nullptr;  // the result of this entry point depends on its arguments only (replicas stay identical)

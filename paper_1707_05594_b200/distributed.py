@@ -25,6 +25,7 @@ only the allocator and the collective plumbing) or a NumPy backend that lives wi
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, field
 from typing import Callable, Dict, Generator, List, Optional, Sequence, Tuple
 
@@ -94,6 +95,12 @@ class AllReduce:     # sum over all ranks, in place
 
 
 @dataclass
+class Broadcast:     # root's tensor to every rank, in place
+    tensor: object
+    root: int
+
+
+@dataclass
 class PeerSlots:     # ask the runner for peer-addressable receive slots of one reduce-scatter (fused scatter epilogue)
     key: object      # stable per call site, so that runners can keep the buffers between sweeps
     group: list      # ranks of the mode group in slot order
@@ -130,6 +137,7 @@ class GpuOps:
         self.device = torch.device("cuda", device_index)
         self.stream = torch.cuda.ExternalStream(ctx.stream, device=self.device)
         self.fast_solves = 0   # leaves served by the certified subspace iteration
+        self._busy_lanes = set()
 
     def _ptr(self, t):
         return ctypes.cast(t.data_ptr(), dbl_p)
@@ -199,6 +207,40 @@ class GpuOps:
         self.fast_solves += used.value
         return factor, status
 
+    def leaf_solve_begin(self, gram, rows, k, start, lane):
+        """Queues the leaf solve on side stream `lane` and returns a handle for leaf_solve_finish; falls back to the
+        synchronous call when that lane is still busy."""
+        factor = self.empty(rows * k)
+        with self.torch.cuda.stream(self.stream):
+            status = self.torch.zeros(2, dtype=self.torch.int32, device=self.device)
+        if lane in self._busy_lanes:
+            done_factor, done_status = self.leaf_solve(gram, rows, k, start)
+            return {"lane": None, "factor": done_factor, "status": done_status}
+        flag = ctypes.cast(status.data_ptr(), ctypes.POINTER(ctypes.c_int))
+        info = ctypes.cast(status.data_ptr() + 4, ctypes.POINTER(ctypes.c_int))
+        check(lib.tp_dev_leaf_solve_begin(self.ctx._h, self._ptr(gram), ctypes.c_size_t(rows), int(k),
+                                          self._ptr(start) if start is not None else None, self._ptr(factor), flag,
+                                          info, int(lane)))
+        self._busy_lanes.add(lane)
+        return {"lane": lane, "factor": factor, "status": status, "gram": gram, "start": start}
+
+    def leaf_solve_finish(self, handle):
+        if handle["lane"] is None:
+            return handle["factor"], handle["status"]
+        status = handle["status"]
+        flag = ctypes.cast(status.data_ptr(), ctypes.POINTER(ctypes.c_int))
+        info = ctypes.cast(status.data_ptr() + 4, ctypes.POINTER(ctypes.c_int))
+        used = ctypes.c_int()
+        check(lib.tp_dev_leaf_solve_finish(self.ctx._h, int(handle["lane"]), self._ptr(handle["factor"]), flag, info,
+                                           ctypes.byref(used)))
+        self._busy_lanes.discard(handle["lane"])
+        self.fast_solves += used.value
+        return handle["factor"], status
+
+    def empty_status(self):
+        with self.torch.cuda.stream(self.stream):
+            return self.torch.zeros(2, dtype=self.torch.int32, device=self.device)
+
     def sum_squares(self, x, count):
         out = self.empty(1)
         check(lib.tp_dev_sum_squares(self.ctx._h, self._ptr(x), ctypes.c_size_t(count), self._ptr(out)))
@@ -259,6 +301,12 @@ class DistributedHooi:
         # Carried path (as in the single-GPU plan): the core chain contracts along one root-to-leaf
         # path of the tree with the new factors, on the grids of those nodes; its partial products are the next
         # sweep's intermediates at those nodes and are kept instead of recomputed.
+        # Leaf eigen-solves: queued on a side stream right after the Gram all-reduce and collected where the core
+        # chain first needs the factor, so they overlap the rest of the tree; with more than one rank each leaf has
+        # one owner rank that solves it and broadcasts the factor (replicating every solve on every rank would put
+        # P copies of the same latency-bound work on the critical path: at C5 / P = 8 more than the tree itself).
+        self.async_solve = hasattr(ops, "leaf_solve_begin") and os.environ.get("TPB_GRID_SYNC_SOLVE") != "1"
+        self.owner_solve = self.layout.procs > 1
         self.peer_scatter = True      # use peer-slot stores for reduce-scatters where the runner offers them
         self.scatter_launches = 0
         self.carry_enabled = self.n >= 2
@@ -390,7 +438,30 @@ class DistributedHooi:
                 yield Exchange([(group[0], y)], [])
                 gram = self.ops.zeros(rows * rows)
         yield AllReduce(gram)
-        factor, status = self.ops.leaf_solve(gram, rows, k, self.factors[mode])
+        index = len(self._pending)                       # position of this leaf in the walk
+        owner = index % lay.procs if self.owner_solve else None
+        entry = {"owner": owner, "rows": rows, "k": k, "handle": None, "done": None}
+        if owner is None or owner == self.rank:
+            if self.async_solve:
+                entry["handle"] = self.ops.leaf_solve_begin(gram, rows, k, self.factors[mode], index % 4)
+            else:
+                entry["done"] = self.ops.leaf_solve(gram, rows, k, self.factors[mode])
+        self._pending[mode] = entry
+        return None
+
+    def _collect(self, mode, statuses: list):
+        """New factor of `mode`: finish this rank's solve if it has one, then share the owner's result."""
+        entry = self._pending.pop(mode)
+        if entry["handle"] is not None:
+            factor, status = self.ops.leaf_solve_finish(entry["handle"])
+        elif entry["done"] is not None:
+            factor, status = entry["done"]
+        else:
+            factor = self.ops.empty(entry["rows"] * entry["k"])
+            status = self.ops.empty_status()
+        if entry["owner"] is not None:
+            yield Broadcast(factor, entry["owner"])
+            yield Broadcast(status, entry["owner"])
         statuses.append(status)
         return factor
 
@@ -401,13 +472,14 @@ class DistributedHooi:
         statuses: list = []
         fresh: List[object] = [None] * self.n
         tree = self.tree
+        self._pending = {}
 
         def walk(node, x, ext, ldims, lay):
             for c in tree.children[node]:
                 mode = tree.mode[c]
                 if tree.kind[c] == P.LEAF:
                     self._mark("begin_leaf", c)
-                    fresh[mode] = yield from self._leaf(x, ext, ldims, mode, res, statuses, lay)
+                    yield from self._leaf(x, ext, ldims, mode, res, statuses, lay)
                     self._mark("end_leaf", c)
                 elif c in self._carried:
                     # computed by the previous sweep's core chain with the factors this sweep starts from
@@ -449,6 +521,7 @@ class DistributedHooi:
             lay, carried = self.layout, {}
             for c in self._carry_path:
                 mode, target, ledger = tree.mode[c], self.node_layout[c], SweepResult()
+                fresh[mode] = yield from self._collect(mode, statuses)
                 if target.q != lay.q:
                     sends, _ = regrid_plan(ext, lay, target, self.rank)
                     ledger.regrid_sent[c] = sum(int(np.prod([hi - lo for lo, hi in o], dtype=np.int64))
@@ -461,6 +534,7 @@ class DistributedHooi:
                 carried[c] = (x, list(ext), list(ldims), ledger.volume_sent.get(c, 0), ledger.regrid_sent.get(c, 0))
                 lay = target
             m = self._carry_leaf_mode
+            fresh[m] = yield from self._collect(m, statuses)
             x, ext, ldims = yield from self._ttm(x, ext, ldims, m, fresh[m], -1, res, lay)
             if lay.q != self.layout.q:      # the core lives on the root grid
                 moved = yield from regrid(x.view(ldims), ext, lay, self.layout, self.rank, self.ops.empty)
@@ -469,6 +543,7 @@ class DistributedHooi:
         else:
             self._carried = {}
             for m in self.core_order:
+                fresh[m] = yield from self._collect(m, statuses)
                 x, ext, ldims = yield from self._ttm(x, ext, ldims, m, fresh[m], -1, res)
         self._mark("end_core")
         self.core, self.core_ldims = x, ldims
@@ -587,6 +662,8 @@ def _run_rank(gen: Generator, dist, to_tensor, peer_slots=None):
                         work.wait()
             elif isinstance(req, AllReduce):
                 dist.all_reduce(to_tensor(req.tensor))
+            elif isinstance(req, Broadcast):
+                dist.broadcast(to_tensor(req.tensor), src=req.root)
             elif isinstance(req, PeerSlots):
                 # without a provider the program falls back to packed chunks + send/recv
                 req = gen.send(peer_slots.slots(req) if peer_slots is not None else None)
@@ -653,6 +730,11 @@ def _run_virtual(gens, copy, add, alloc=None):
                 add(total, reqs[r].tensor)
             for r in range(n):
                 copy(reqs[r].tensor, total)
+        elif kind is Broadcast:
+            root = reqs[0].root
+            for r in range(n):
+                if r != root:
+                    copy(reqs[r].tensor, reqs[root].tensor)
         elif kind is PeerSlots:
             # one address space: a "peer" slot is simply the other rank program's buffer
             slots = [[alloc(reqs[r].count) for _ in reqs[r].group] for r in range(n)]

@@ -57,6 +57,9 @@ class NumpyOps:
         factor = torch.from_numpy(np.asfortranarray(vec).reshape(-1, order="F").copy())
         return factor, torch.tensor([int(deg), 0], dtype=torch.int32)
 
+    def empty_status(self):
+        return torch.zeros(2, dtype=torch.int32)
+
     def sum_squares(self, x, count):
         v = x.numpy()[:count]
         return torch.tensor([float(np.dot(v, v))], dtype=torch.float64)
