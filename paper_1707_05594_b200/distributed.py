@@ -187,8 +187,8 @@ class GpuOps:
                                        ctypes.c_size_t(inner), self._ptr(src), ctypes.c_size_t(l0),
                                        ctypes.c_size_t(count)))
 
-    def gram(self, y, outer, rows, inner):
-        g = self.empty(rows * rows)
+    def gram(self, y, outer, rows, inner, out=None):
+        g = out if out is not None else self.empty(rows * rows)
         check(lib.tp_dev_gram(self.ctx._h, self._ptr(y), ctypes.c_size_t(outer), ctypes.c_size_t(rows),
                               ctypes.c_size_t(inner), self._ptr(g)))
         return g
@@ -312,6 +312,7 @@ class DistributedHooi:
         self.carry_enabled = self.n >= 2
         self._carry_path, self._carry_leaf_mode = self._first_leaf_path()
         self._carried: Dict[int, tuple] = {}
+        self._gram_buf: Dict[int, object] = {}
 
     # -- state ------------------------------------------------------------------------------------
     def set_local_tensor(self, block: np.ndarray):
@@ -411,8 +412,13 @@ class DistributedHooi:
         rows, k = self.spec.L[mode], self.spec.K[mode]
         outer = int(np.prod(ldims[:mode], dtype=np.int64)) if mode else 1
         inner = int(np.prod(ldims[mode + 1:], dtype=np.int64)) if mode + 1 < self.n else 1
+        # one Gram buffer per mode for the life of the executor: the leaf solve records its kernel sequence as a
+        # CUDA graph on the buffers it first sees
+        if mode not in self._gram_buf:
+            self._gram_buf[mode] = self.ops.empty(rows * rows)
+        gram_out = self._gram_buf[mode]
         if q_n == 1:
-            gram = self.ops.gram(y, outer, rows, inner)
+            gram = self.ops.gram(y, outer, rows, inner, gram_out)
         else:
             # the unfolding's rows are split over the mode-n group: bring the slices to the group's first rank,
             # which then owns these columns of the unfolding; the other ranks add nothing to the Gram sum
@@ -433,10 +439,11 @@ class DistributedHooi:
                 yield Exchange([], recvs)
                 for buf, lo, count in pieces:
                     self.ops.assemble(full, outer, rows, inner, buf, lo, count)
-                gram = self.ops.gram(full, outer, rows, inner)
+                gram = self.ops.gram(full, outer, rows, inner, gram_out)
             else:
                 yield Exchange([(group[0], y)], [])
-                gram = self.ops.zeros(rows * rows)
+                gram = gram_out
+                gram.zero_()
         yield AllReduce(gram)
         index = len(self._pending)                       # position of this leaf in the walk
         owner = index % lay.procs if self.owner_solve else None

@@ -48,9 +48,13 @@ class NumpyOps:
     def assemble(self, dst, outer, full_len, inner, src, l0, count):
         dst.view(outer, full_len, inner)[:, l0:l0 + count, :] = src.view(outer, count, inner)
 
-    def gram(self, y, outer, rows, inner):
+    def gram(self, y, outer, rows, inner, out=None):
         u = ho.unfold(y.numpy().reshape(outer, rows, inner), 1)
-        return torch.from_numpy((u @ u.T).reshape(-1).copy())
+        g = torch.from_numpy((u @ u.T).reshape(-1).copy())
+        if out is None:
+            return g
+        out.copy_(g)
+        return out
 
     def leaf_solve(self, gram, rows, k, start=None):
         vec, deg = ho.leading_from_gram(gram.numpy().reshape(rows, rows), k)
