@@ -339,11 +339,19 @@ def run_b200(args):
         r["ms"] = node_ms[r["node"]]
         r["frac"] = r["t_roof_s"] * 1e3 / r["ms"] if r["ms"] > 0 else None
         r["tflops"] = r["flops"] / (r["ms"] * 1e-3) / 1e12 if r["ms"] > 0 else None
-    dom = max(rows, key=lambda r: r["ms"])
+    # `roofline`: the dominant tree node's kernel, timed where the contract asks -- CUDA events on the engine's
+    # stream inside the timed region (engine defaults: eigen-solve kernels may share the SMs with it and the grid
+    # leaves 6 SMs to them while any are in flight); the serial-pass figure of the same node is reported beside it.
+    dom_serial = max(rows, key=lambda r: r["ms"])
+    dom = dict(max(rows, key=lambda r: overlapped_node_ms[r["node"]]))
+    dom["ms"] = overlapped_node_ms[dom["node"]]
+    dom["tflops"] = dom["flops"] / (dom["ms"] * 1e-3) / 1e12
+    serial_same = next(r for r in rows if r["node"] == dom["node"])
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            traffic = json.load(f).get(cfg.name, {}).get("dominant_ttm_dram_bytes_per_launch")
+            entry = json.load(f).get(cfg.name, {})
+            traffic = entry.get("by_node", {}).get(str(dom["node"]), entry.get("dominant_ttm_dram_bytes_per_launch"))
     except Exception:
         pass
     if dom["bound"] == "tensor":
@@ -353,10 +361,16 @@ def run_b200(args):
         gbs = dom["bytes"] / (dom["ms"] * 1e-3) / 1e9
         roofline = {"bound": "hbm", "achieved": gbs, "peak": hbm_gbs, "unit": "GB/s", "frac": gbs / hbm_gbs,
                     "traffic": traffic}
-    roofline.update({"kernel": "ttm_dmma_kernel (tree node %d: mode %d, %s)" % (dom["node"], dom["mode"] + 1,
-                                                                                "FP64 DMMA pipe" if dom["bound"] == "tensor" else "HBM"),
+    serial_achieved = (serial_same["tflops"] if dom["bound"] == "tensor"
+                       else serial_same["bytes"] / (serial_same["ms"] * 1e-3) / 1e9)
+    roofline.update({"kernel": "ttm_tma_kernel / ttm_dmma_kernel (tree node %d: mode %d, %s)"
+                               % (dom["node"], dom["mode"] + 1, "FP64 DMMA pipe" if dom["bound"] == "tensor" else "HBM"),
                      "algorithmic_flops_per_launch": dom["flops"], "algorithmic_bytes_per_launch": dom["bytes"],
-                     "avg_launch_ms": dom["ms"], "peak_source": fp64_src if dom["bound"] == "tensor" else hbm_src})
+                     "avg_launch_ms": dom["ms"], "timed": "CUDA events around the launch, timed region, engine defaults",
+                     "serial_pass": {"avg_launch_ms": serial_same["ms"], "achieved": serial_achieved,
+                                     "frac": serial_achieved / (p_fp64 if dom["bound"] == "tensor" else hbm_gbs),
+                                     "slowest_node_in_serial_pass": dom_serial["node"]},
+                     "peak_source": fp64_src if dom["bound"] == "tensor" else hbm_src})
 
     # e2e: the reference-facing by-value call with HOST buffers (upload T + factors, sweep, download factors + core)
     e2e = None
