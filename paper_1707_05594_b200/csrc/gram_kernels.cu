@@ -19,7 +19,7 @@
 namespace tpb {
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 128;  // 4 warps x (32 x 32) warp tiles: 8 fragment loads per 16 DMMAs
 constexpr int kTile = 64;
 constexpr int kKC = 16;
 constexpr int kStages = 3;
@@ -58,7 +58,7 @@ struct GramParams {
 // INNER1: the contraction index (slab a) is the strided one and rows are contiguous -> stage as [kKC][64].
 // otherwise the contraction index b is contiguous -> stage as [64][kKC].
 template <bool INNER1>
-__global__ void __launch_bounds__(kThreads, 2) gram_dmma_kernel(const GramParams p) {
+__global__ void __launch_bounds__(kThreads, 4) gram_dmma_kernel(const GramParams p) {
   __shared__ __align__(16) double sa[kStages][kTile * kKC];
   __shared__ __align__(16) double sb[kStages][kTile * kKC];
 
@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(kThreads, 2) gram_dmma_kernel(const GramParams
   const long long i0 = static_cast<long long>(ti) * kTile, j0 = static_cast<long long>(tj) * kTile;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp >> 1, wn = warp & 1;  // warp tile: rows wm*16..+16, cols wn*32..+32
+  const int wm = warp >> 1, wn = warp & 1;  // warp tile: rows wm*32..+32, cols wn*32..+32
 
   const long long c_begin = static_cast<long long>(blockIdx.y) * p.chunks_per_split;
   const long long c_end = min(p.chunks, c_begin + p.chunks_per_split);
@@ -125,9 +125,9 @@ __global__ void __launch_bounds__(kThreads, 2) gram_dmma_kernel(const GramParams
     return INNER1 ? tile[l * kTile + (row ^ ((l & 3) << 2))] : tile[row * kKC + (l ^ ((row & 3) << 2))];
   };
 
-  double acc[2][4][2];
+  double acc[4][4][2];
 #pragma unroll
-  for (int a = 0; a < 2; ++a)
+  for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
@@ -149,13 +149,13 @@ __global__ void __launch_bounds__(kThreads, 2) gram_dmma_kernel(const GramParams
 #pragma unroll
     for (int s = 0; s < kKC / 4; ++s) {
       const int l = 4 * s + (lane & 3);
-      double fa[2], fb[4];
+      double fa[4], fb[4];
 #pragma unroll
-      for (int a = 0; a < 2; ++a) fa[a] = frag(ta, wm * 16 + a * 8 + (lane >> 2), l);
+      for (int a = 0; a < 4; ++a) fa[a] = frag(ta, wm * 32 + a * 8 + (lane >> 2), l);
 #pragma unroll
       for (int b = 0; b < 4; ++b) fb[b] = frag(tb, wn * 32 + b * 8 + (lane >> 2), l);
 #pragma unroll
-      for (int a = 0; a < 2; ++a)
+      for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) dmma884(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
     }
@@ -164,10 +164,10 @@ __global__ void __launch_bounds__(kThreads, 2) gram_dmma_kernel(const GramParams
 
   double* out = p.partial + static_cast<long long>(blockIdx.y) * p.rows * p.rows;
 #pragma unroll
-  for (int a = 0; a < 2; ++a)
+  for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
-      const long long i = i0 + wm * 16 + a * 8 + (lane >> 2);
+      const long long i = i0 + wm * 32 + a * 8 + (lane >> 2);
       const long long j = j0 + wn * 32 + b * 8 + 2 * (lane & 3);
       if (i < p.rows) {
         if (j < p.rows) out[i * p.rows + j] = acc[a][b][0];
@@ -196,8 +196,8 @@ GramLayout gram_layout(long long outer, long long rows, long long inner, int sm_
   g.tiles = static_cast<int>((rows + kTile - 1) / kTile);
   g.chunks = inner == 1 ? (outer + kKC - 1) / kKC : outer * ((inner + kKC - 1) / kKC);
   const long long lower_tiles = static_cast<long long>(g.tiles) * (g.tiles + 1) / 2;
-  // two CTAs fit per SM; aim for at least four full waves so that the last, partial wave costs little
-  long long want = (8LL * sm_count + lower_tiles - 1) / lower_tiles;
+  // four CTAs fit per SM; aim for at least four full waves so that the last, partial wave costs little
+  long long want = (16LL * sm_count + lower_tiles - 1) / lower_tiles;
   want = std::min(want, std::max(1LL, g.chunks / 8));                          // at least 8 chunks per split
   want = std::max(1LL, std::min(want, 512LL));
   const long long per = (g.chunks + want - 1) / want;
