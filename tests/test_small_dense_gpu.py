@@ -149,3 +149,48 @@ def test_small_dense_argument_checks(dev):
     with pytest.raises(TuckerplanError) as e:
         check(lib.tp_dev_trsm_right_lt(dev.ctx._h, None, ctypes.c_size_t(4), 2, dev.ptr(t)))
     assert e.value.code == Errc.bad_argument
+
+
+def test_async_leaf_solve_pair(dev):
+    """tp_dev_leaf_solve_begin / _finish: the solve runs on a side stream; both routes (full solve without a start
+    block, certified top-k with one) give the leading eigenvectors with the reference's sign rule (hooi.hpp:60-68)."""
+    torch = dev.torch
+    rng = np.random.default_rng(11)
+    rows, k = 96, 7
+    q, _ = np.linalg.qr(rng.standard_normal((rows, rows)))
+    lam = np.concatenate([1.0 + 4.0 * rng.random(k), 1e-6 * rng.random(rows - k)])
+    gram = (q * lam) @ q.T
+    gram = (gram + gram.T) / 2
+    w, v = np.linalg.eigh(gram)
+    want = v[:, ::-1][:, :k]
+    for col in range(k):
+        if want[np.argmax(np.abs(want[:, col])), col] < 0:
+            want[:, col] = -want[:, col]
+    start = want + 1e-3 * rng.standard_normal(want.shape)
+    int_p = ctypes.POINTER(ctypes.c_int)
+    for lane, use_start in ((0, False), (1, True), (3, True)):
+        d_gram = dev.up(colmajor(gram))
+        d_start = dev.up(colmajor(np.linalg.qr(start)[0]))
+        d_factor = dev.up(np.zeros(rows * k))
+        d_status = dev.up(np.zeros(2, dtype=np.int32))
+        flag = ctypes.cast(d_status.data_ptr(), int_p)
+        info = ctypes.cast(d_status.data_ptr() + 4, int_p)
+        check(lib.tp_dev_leaf_solve_begin(dev.ctx._h, dev.ptr(d_gram), ctypes.c_size_t(rows), k,
+                                          dev.ptr(d_start) if use_start else None, dev.ptr(d_factor), flag, info, lane))
+        with pytest.raises(TuckerplanError) as e:      # one solve in flight per lane
+            check(lib.tp_dev_leaf_solve_begin(dev.ctx._h, dev.ptr(d_gram), ctypes.c_size_t(rows), k, None,
+                                              dev.ptr(d_factor), flag, info, lane))
+        assert e.value.code == Errc.bad_argument
+        used = ctypes.c_int(-1)
+        check(lib.tp_dev_leaf_solve_finish(dev.ctx._h, lane, dev.ptr(d_factor), flag, info, ctypes.byref(used)))
+        got = dev.down(d_factor).reshape(rows, k, order="F")
+        assert used.value == (1 if use_start else 0)
+        assert list(dev.down(d_status)) == [0, 0]
+        assert np.max(np.abs(got - want)) < 1e-8
+    with pytest.raises(TuckerplanError) as e:          # nothing in flight
+        check(lib.tp_dev_leaf_solve_finish(dev.ctx._h, 2, dev.ptr(d_factor), flag, info, None))
+    assert e.value.code == Errc.bad_argument
+    with pytest.raises(TuckerplanError) as e:
+        check(lib.tp_dev_leaf_solve_begin(dev.ctx._h, dev.ptr(d_gram), ctypes.c_size_t(rows), k, None,
+                                          dev.ptr(d_factor), flag, info, 4))
+    assert e.value.code == Errc.bad_argument
