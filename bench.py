@@ -341,7 +341,7 @@ def run_b200(args):
         r["tflops"] = r["flops"] / (r["ms"] * 1e-3) / 1e12 if r["ms"] > 0 else None
     # `roofline`: the dominant tree node's kernel, timed where the contract asks -- CUDA events on the engine's
     # stream inside the timed region (engine defaults: eigen-solve kernels may share the SMs with it and the grid
-    # leaves 6 SMs to them while any are in flight); the serial-pass figure of the same node is reported beside it.
+    # leaves 2 SMs to them while any are in flight); the serial-pass figure of the same node is reported beside it.
     dom_serial = max(rows, key=lambda r: r["ms"])
     dom = dict(max(rows, key=lambda r: overlapped_node_ms[r["node"]]))
     dom["ms"] = overlapped_node_ms[dom["node"]]

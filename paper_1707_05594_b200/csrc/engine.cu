@@ -613,7 +613,8 @@ struct tp_plan {
   const tp_tensor* carry_tensor = nullptr;
   tp_u64 carry_stamp = 0;
   bool carry_live = false;                    // this sweep's walk starts from the carried products
-  int spare_sms = 6;                          // SMs left to the side streams while eigen-solves are in flight
+  int spare_sms = 2;                          // SMs left to the side streams while eigen-solves are in flight
+                                              // (measured on C5: 0-2 -> 58.4 ms/iter, 6 -> 58.9, 12 -> 60.0)
   int leaves_in_flight = 0;
   struct PendingLeaf {
     int mode, node;
@@ -1454,6 +1455,7 @@ int tp_plan_create(tp_ctx* ctx, int n_modes, const tp_u64* L, const tp_u64* K, i
       p->tree = tree_from_arrays(n_modes, n_nodes, kind, mode, parent);
       validate_tree(p->tree, p->spec);
       p->sweep_kind = sweep_kind;
+      if (const char* env = std::getenv("TPB_SPARE_SMS")) p->spare_sms = std::max(0, std::atoi(env));  // tuning knob
       Cards cards;
       const Cost cost = tree_cost(p->tree, p->spec, &cards);
       for (int m = 0; m < n_modes; ++m)
