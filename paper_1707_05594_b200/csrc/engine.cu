@@ -1154,6 +1154,10 @@ int tp_ctx_create(int device, tp_ctx** out) {
       // the TTM/Gram stream outranks the eigen-solve side streams: when both have CTAs pending, the tree goes first
       int prio_low = 0, prio_high = 0;
       TPB_CUDA(cudaDeviceGetStreamPriorityRange(&prio_low, &prio_high));
+      if (const char* env = std::getenv("TPB_AUX_PRIORITY")) {  // tuning knob: 0 = same as the tree, 1 = above it
+        if (env[0] == '0') prio_low = prio_high;
+        if (env[0] == '1') std::swap(prio_low, prio_high);
+      }
       TPB_CUDA(cudaStreamCreateWithPriority(&ctx->stream, cudaStreamNonBlocking, prio_high));
       TPB_SOLVER(cusolverDnCreate(&ctx->solver));
       TPB_SOLVER(cusolverDnSetStream(ctx->solver, ctx->stream));
