@@ -241,9 +241,11 @@ int tp_plan_set_option(tp_ctx* ctx, tp_plan* plan, int option, int value);
  * take the pointer again after writing through it).  SweepStats stay the analytic (reference) counts.
  * TP_OPT_FAST_EVD (default 1): leaves with 2 (K_n + 8) <= L_n (and K_n + 8 <= 112 or L_n >= 704) compute only
  * the K_n leading eigenvectors by warm-started block subspace iteration + Rayleigh-Ritz; every kept Ritz pair must satisfy
- * ||G x - theta x|| <= 1e-13 theta_max, otherwise (or when the gap estimate says "degenerate") the leaf is redone
- * with the full eigen-solve, so the factors are the reference's (hooi.hpp:55-69) to rounding either way.
- * tp_plan_last_evd_info: leaves eligible for the fast path, and how many of them the last sweep had to redo. */
+ * ||G x - theta x|| <= 1e-13 theta_max; a leaf that only misses this bound iterates on (up to three more rounds from
+ * the Ritz vectors it reached), and a leaf that still misses it, loses a factorisation or has a "degenerate" gap
+ * estimate is redone with the full eigen-solve, so the factors are the reference's (hooi.hpp:55-69) to rounding
+ * either way.  tp_plan_last_evd_info: leaves eligible for the fast path, and how many of them the last sweep had to
+ * redo with the full solve. */
 int tp_plan_last_evd_info(tp_ctx* ctx, tp_plan* plan, int* fast_eligible, int* rejected);
 /* Decomposition::factors (hooi.hpp:78-81) <-> device: factors[n] is L_n x K_n column-major on the host */
 int tp_plan_set_factors(tp_ctx* ctx, tp_plan* plan, const double* const* factors);

@@ -242,6 +242,7 @@ struct LeafScratch {
   int graph_state = 0;         // 0: not run yet (first run is eager), 1: eager run done, 2: graph ready, -1: disabled
   long long fast_rows = 0;     // rows the iteration buffers were sized for (tp_dev_leaf_solve_warm only)
   int failures = 0;            // consecutive warm sweeps in which the fast path was rejected
+  bool refinable = false;      // last rejection was a missed residual bound only (no failed factorisation / gap)
   bool was_cold = false;       // this sweep's solve started from the caller's factors
   bool cold_rejected = false;  // a cold start missed its certificate before: later cold starts take the full solve
   bool fast_used = false;      // this sweep's factor came from the fast path (verdict still to be checked)
@@ -760,11 +761,9 @@ std::vector<int> verify_fast_leaves(tp_ctx* ctx, tp_plan* p) {
                    m, s.block, host[4 * m], host[4 * m + 1], host[4 * m + 2], host[4 * m + 3], s.graph_state);
     if (bad) {
       rejected.push_back(m);
-      if (s.was_cold)
-        s.cold_rejected = true;  // arbitrary start factors need more than the fixed schedule on this problem
-      else
-        ++s.failures;
-      s.last_ritz = nullptr;
+      // only the residual bound missed: the block is sound and simply has not converged yet -> worth iterating on
+      s.refinable = host[4 * m + 1] == 0 && host[4 * m + 3] == 0;
+      if (!s.refinable) s.last_ritz = nullptr;
       TPB_CUDA(cudaMemsetAsync(s.flag, 0, sizeof(int), ctx->stream));
     } else {
       s.failures = 0;
@@ -772,6 +771,32 @@ std::vector<int> verify_fast_leaves(tp_ctx* ctx, tp_plan* p) {
     s.fast_used = false;
   }
   return rejected;
+}
+
+// A leaf whose certified solve was rejected: if only the residual bound was missed, repeat the iteration from the
+// Ritz vectors it reached (each round is six more power steps, a fraction of a full eigen-solve); otherwise, or if
+// that does not converge either, take the full solve on the intact Gram matrix.  Main stream.
+// Returns true if the full solve had to take over.
+bool redo_rejected_leaf(tp_ctx* ctx, tp_plan* p, int mode, double* dst) {
+  LeafScratch& s = p->leaf[mode];
+  const long long rows = static_cast<long long>(p->spec.L[mode]);
+  const int k = static_cast<int>(p->spec.K[mode]);
+  Span evd(ctx, p, kEvd, -1);
+  bool ok = false;
+  for (int round = 0; s.refinable && s.last_ritz && round < 3 && !ok; ++round) {
+    leaf_solve_subspace(ctx, s, s.gram, rows, k, p->cur[mode], dst, -1);
+    ok = verify_fast_leaves(ctx, p).empty();
+  }
+  if (!ok) {
+    if (s.was_cold)
+      s.cold_rejected = true;  // arbitrary start factors need more than a few rounds on this problem
+    else
+      ++s.failures;
+    s.last_ritz = nullptr;
+    leaf_solve(ctx, s, rows, k, dst, -1);
+  }
+  evd.close();
+  return !ok;
 }
 
 // Execution order of siblings.  A Jacobi sweep gives the same factors in any order (every product uses the
@@ -1694,14 +1719,9 @@ int tp_plan_sweep(tp_ctx* ctx, tp_plan* p, const tp_tensor* t, tp_sweep_stats* s
       // leaves solved by subspace iteration are accepted only with their residual certificate; a rejected leaf is
       // redone with the full eigen-solve on its (intact) Gram matrix, and the core with it
       const std::vector<int> rejected = verify_fast_leaves(ctx, p);
-      p->fast_rejected = static_cast<int>(rejected.size());
+      p->fast_rejected = 0;
       if (!rejected.empty()) {
-        for (int m : rejected) {
-          Span evd(ctx, p, kEvd, -1);
-          leaf_solve(ctx, p->leaf[m], static_cast<long long>(p->spec.L[m]), static_cast<int>(p->spec.K[m]),
-                     p->fresh[m], -1);
-          evd.close();
-        }
+        for (int m : rejected) p->fast_rejected += redo_rejected_leaf(ctx, p, m, p->fresh[m]) ? 1 : 0;
         plan_core(ctx, p, t->data, p->fresh);
       }
       std::swap(p->cur, p->fresh);
@@ -1744,13 +1764,7 @@ int tp_plan_sweep(tp_ctx* ctx, tp_plan* p, const tp_tensor* t, tp_sweep_stats* s
         plan_leaf(ctx, p, at, d, leaf, p->fresh[leaf], -1, false);
         // the next chain multiplies by this factor: a certified top-k solve is checked now, not at the end
         const std::vector<int> rejected = verify_fast_leaves(ctx, p);
-        if (!rejected.empty()) {
-          ++p->fast_rejected;
-          Span evd(ctx, p, kEvd, -1);
-          leaf_solve(ctx, p->leaf[leaf], static_cast<long long>(p->spec.L[leaf]), static_cast<int>(p->spec.K[leaf]),
-                     p->fresh[leaf], -1);
-          evd.close();
-        }
+        if (!rejected.empty()) p->fast_rejected += redo_rejected_leaf(ctx, p, leaf, p->fresh[leaf]) ? 1 : 0;
         std::swap(p->cur[leaf], p->fresh[leaf]);  // later chains see the fresh factor
         Span s(ctx, p, kTree);
         plan_refresh_fragments(ctx, p, leaf, p->cur[leaf]);
