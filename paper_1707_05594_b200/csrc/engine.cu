@@ -2165,6 +2165,18 @@ int tp_dev_leaf_solve_finish(tp_ctx* ctx, int lane_index, double* factor, int* f
     TPB_CUDA(cudaMemcpyAsync(&host[0], s.verdict, 2 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     TPB_CUDA(cudaMemcpyAsync(&host[2], flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     TPB_CUDA(cudaStreamSynchronize(ctx->stream));
+    // only the residual bound missed: iterate on from the Ritz vectors reached (as the plan does), main stream
+    for (int round = 0; round < 3 && host[0] != 0 && host[1] == 0 && host[2] == 0 && s.last_ritz; ++round) {
+      int* const saved_flag = s.flag;
+      s.flag = flag;
+      leaf_solve_subspace(ctx, s, lane.gram, static_cast<long long>(lane.rows), lane.k, factor, factor, -1);
+      s.flag = saved_flag;
+      s.fast_used = false;
+      TPB_CUDA(cudaMemcpyAsync(&host[0], s.verdict, 2 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+      TPB_CUDA(cudaMemcpyAsync(&host[2], flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+      TPB_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+    s.last_ritz = nullptr;
     if (host[0] == 0 && host[1] == 0 && host[2] == 0) {
       TPB_CUDA(cudaMemsetAsync(info, 0, sizeof(int), ctx->stream));
       if (used_fast) *used_fast = 1;
