@@ -22,6 +22,7 @@ constexpr int kSmallWarps = kSmallThreads / 32;
 // S(i,k) -= S(i,j) S(k,j) / d_j, so a step needs one barrier; the columns are scaled by 1/sqrt(d_j) on the way out.
 // *fail |= 1 when a pivot is not positive (rank-deficient iteration block -> the caller falls back to the full
 // eigen-solve).
+template <int kBlockCap>
 __global__ void __launch_bounds__(kSmallThreads) cholesky_kernel(const double* __restrict__ s_in, int b,
                                                                  double* __restrict__ l_out, int* __restrict__ fail) {
   extern __shared__ double sm[];  // b x b, column-major
@@ -39,8 +40,9 @@ __global__ void __launch_bounds__(kSmallThreads) cholesky_kernel(const double* _
     }
     if (tid == 0) pivot[j] = sqrt(d);
     const double dinv = 1.0 / d;
-    // this lane's rows of column j, shared by every trailing column the warp updates (b <= 112: four row passes)
-    constexpr int kPasses = (kMaxBlock + 31) / 32;
+    // this lane's rows of column j, shared by every trailing column the warp updates (as many 32-row passes as the
+    // block-size class needs)
+    constexpr int kPasses = (kBlockCap + 31) / 32;
     double cj[kPasses];
 #pragma unroll
     for (int r = 0; r < kPasses; ++r) {
@@ -78,7 +80,9 @@ __global__ void __launch_bounds__(kSmallThreads) cholesky_kernel(const double* _
 // A warp serves 4 rows, a CTA 32.
 constexpr int kTrsmThreads = 256;
 constexpr int kTrsmRows = kTrsmThreads / 8;
-constexpr int kTrsmSlots = kMaxBlock / 8;
+// kTrsmSlots = columns a lane keeps = block-size class / 8; the loops below are fully unrolled over it, so small
+// blocks get a small kernel (the 112-column instance alone is ~1600 predicated FMAs of straight-line code)
+template <int kTrsmSlots>
 __global__ void __launch_bounds__(kTrsmThreads) trsm_right_lt_kernel(double* __restrict__ z, int n, int b,
                                                                      const double* __restrict__ l) {
   extern __shared__ double ls[];  // b x b, column-major lower
@@ -300,18 +304,43 @@ cudaError_t allow_shared(Kernel kernel, size_t bytes, bool& configured) {
 size_t small_evd_max_block() { return kMaxBlock; }
 
 cudaError_t launch_cholesky(cudaStream_t stream, const double* s, int b, double* l, int* fail) {
-  static bool configured = false;
-  cudaError_t e = allow_shared(cholesky_kernel, sizeof(double) * kMaxBlock * kMaxBlock, configured);
-  if (e != cudaSuccess) return e;
-  cholesky_kernel<<<1, kSmallThreads, sizeof(double) * b * b, stream>>>(s, b, l, fail);
+  static bool configured[3] = {false, false, false};
+  const size_t smem = sizeof(double) * b * b;
+  cudaError_t e;
+  if (b <= 32) {
+    e = allow_shared(cholesky_kernel<32>, sizeof(double) * 32 * 32, configured[0]);
+    if (e != cudaSuccess) return e;
+    cholesky_kernel<32><<<1, kSmallThreads, smem, stream>>>(s, b, l, fail);
+  } else if (b <= 64) {
+    e = allow_shared(cholesky_kernel<64>, sizeof(double) * 64 * 64, configured[1]);
+    if (e != cudaSuccess) return e;
+    cholesky_kernel<64><<<1, kSmallThreads, smem, stream>>>(s, b, l, fail);
+  } else {
+    e = allow_shared(cholesky_kernel<kMaxBlock>, sizeof(double) * kMaxBlock * kMaxBlock, configured[2]);
+    if (e != cudaSuccess) return e;
+    cholesky_kernel<kMaxBlock><<<1, kSmallThreads, smem, stream>>>(s, b, l, fail);
+  }
   return cudaGetLastError();
 }
 
 cudaError_t launch_trsm_right_lt(cudaStream_t stream, double* z, int n, int b, const double* l) {
-  static bool configured = false;
-  cudaError_t e = allow_shared(trsm_right_lt_kernel, sizeof(double) * kMaxBlock * kMaxBlock, configured);
-  if (e != cudaSuccess) return e;
-  trsm_right_lt_kernel<<<(n + kTrsmRows - 1) / kTrsmRows, kTrsmThreads, sizeof(double) * b * b, stream>>>(z, n, b, l);
+  static bool configured[3] = {false, false, false};
+  const size_t smem = sizeof(double) * b * b;
+  const unsigned grid = static_cast<unsigned>((n + kTrsmRows - 1) / kTrsmRows);
+  cudaError_t e;
+  if (b <= 32) {
+    e = allow_shared(trsm_right_lt_kernel<4>, sizeof(double) * 32 * 32, configured[0]);
+    if (e != cudaSuccess) return e;
+    trsm_right_lt_kernel<4><<<grid, kTrsmThreads, smem, stream>>>(z, n, b, l);
+  } else if (b <= 64) {
+    e = allow_shared(trsm_right_lt_kernel<8>, sizeof(double) * 64 * 64, configured[1]);
+    if (e != cudaSuccess) return e;
+    trsm_right_lt_kernel<8><<<grid, kTrsmThreads, smem, stream>>>(z, n, b, l);
+  } else {
+    e = allow_shared(trsm_right_lt_kernel<kMaxBlock / 8>, sizeof(double) * kMaxBlock * kMaxBlock, configured[2]);
+    if (e != cudaSuccess) return e;
+    trsm_right_lt_kernel<kMaxBlock / 8><<<grid, kTrsmThreads, smem, stream>>>(z, n, b, l);
+  }
   return cudaGetLastError();
 }
 
