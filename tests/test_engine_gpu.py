@@ -573,6 +573,39 @@ def test_by_value_call_with_streamed_upload(ctx, monkeypatch, L, K, tree_kind, k
         assert all(np.array_equal(a, b) for a, b in zip(streamed.factors, whole.factors))
 
 
+def _random_specs(count, seed):
+    """Seeded random problems: 2-5 modes, odd and even extents, K_n = 1 allowed, every leaf with full rank
+    (K_n <= prod of the other K, else both sides flag a degenerate cut)."""
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < count:
+        n = int(rng.integers(2, 6))
+        L = [int(rng.integers(2, 26 if n < 5 else 12)) for _ in range(n)]
+        K = [int(rng.integers(1, min(l, 9) + 1)) for l in L]
+        if any(K[m] > np.prod([K[j] for j in range(n) if j != m]) for m in range(n)):
+            continue
+        out.append((L, K, ["optimal", "chain", "chain_by_cost", "balanced"][int(rng.integers(0, 4))],
+                    ["jacobi", "gauss_seidel"][int(rng.integers(0, 2))]))
+    return out
+
+
+@pytest.mark.parametrize("L,K,tree_kind,kind", _random_specs(24, 20261020),
+                         ids=lambda v: v if isinstance(v, str) else "x".join(map(str, v)))
+def test_sweep_parity_random_specs(ctx, L, K, tree_kind, kind):
+    """Three sweeps of a seeded random problem on a random tree strategy and schedule, resident plan vs oracle."""
+    cfg = W.scaled_config(3, L, K, 3)
+    spec = cfg.spec
+    if kind == "gauss_seidel" and tree_kind in ("optimal", "balanced"):
+        tree_kind = "chain"
+    tree = {"optimal": lambda: P.optimal_tree(spec).tree, "chain": lambda: P.chain_tree(spec),
+            "chain_by_cost": lambda: P.chain_tree(spec, P.CHAIN_BY_COST), "balanced": lambda: P.balanced_tree(spec)}[tree_kind]()
+    rows, err_gpu, err_oracle = run_both(ctx, cfg, 3, kind, tree)
+    for r in rows:
+        assert r["angle"] < 1e-9 and r["core_rel"] < 1e-10
+        assert abs(r["fit_gpu"] - r["fit_oracle"]) <= 1e-10 * max(r["fit_oracle"], 1e-3)
+    assert abs(err_gpu - err_oracle) <= 1e-10 * max(err_oracle, 1e-3)
+
+
 @pytest.mark.parametrize("index", [2, 3, 4])
 def test_sweep_parity_full_size_configs(ctx, index):
     """BASELINE.json configs[1..3] at full size, two Jacobi iterations on the optimal tree, against the oracle."""
