@@ -286,6 +286,35 @@ def test_carried_path_in_the_grid_executor(L, K, q):
         assert np.max(np.abs(ca - cb)) <= 1e-12 * np.max(np.abs(cb))    # the chain order differs: rounding only
 
 
+def _random_grid_cases(count, seed):
+    """Seeded random problems with a random valid grid (and, every other case, the planner's per-node scheme)."""
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < count:
+        n = int(rng.integers(2, 5))
+        L = [int(rng.integers(4, 15)) for _ in range(n)]
+        K = [int(rng.integers(2, min(l, 6) + 1)) for l in L]
+        if any(K[m] > np.prod([K[j] for j in range(n) if j != m]) for m in range(n)):
+            continue
+        spec = P.ProblemSpec(L, K)
+        procs = int(rng.choice([2, 3, 4, 6, 8]))
+        grids = P.enumerate_grids(procs, spec)
+        if not grids:
+            continue
+        out.append((tuple(L), tuple(K), tuple(grids[int(rng.integers(0, len(grids)))]), procs, len(out) % 2 == 1))
+    return out
+
+
+@pytest.mark.parametrize("L,K,q,procs,dynamic", _random_grid_cases(12, 1707),
+                         ids=lambda v: str(v) if not isinstance(v, tuple) else "x".join(map(str, v)))
+def test_virtual_ranks_random_grids(L, K, q, procs, dynamic):
+    if dynamic:
+        spec = P.ProblemSpec(list(L), list(K))
+        run_scheme_case(NumpyOps(), L, K, P.optimal_dynamic_scheme(P.optimal_tree(spec).tree, spec, procs).scheme)
+    else:
+        run_virtual_case(NumpyOps(), L, K, q)
+
+
 def test_regrid_roundtrip_and_counts():
     ext = (7, 6, 5)
     full = hostgen.random_tensor(ext, 3)
