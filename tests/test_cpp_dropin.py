@@ -40,3 +40,18 @@ def test_readme_transcript_through_cpp_headers(dropin, readme_kat):
     assert out[2].startswith("sweep 2: error 0.918925317677")
     assert out[3].startswith("resident jacobi: error ")
     assert out[4] == "error 11"                                                # Errc::needs_chain_tree
+
+
+def test_serialize_checks_through_cpp_headers():
+    """tests/cpp/serialize_check.cpp restates the reference's tests/test_serialize.cpp (golden strings included)."""
+    exe = os.path.join(ROOT, "build", "serialize_check")
+    os.makedirs(os.path.dirname(exe), exist_ok=True)
+    subprocess.check_call(["g++", "-std=c++20", "-O1", "-Wall", "-Wextra", "-I" + os.path.join(ROOT, "include"),
+                           os.path.join(ROOT, "tests", "cpp", "serialize_check.cpp"), "-o", exe, "-L" + LIBDIR,
+                           "-ltuckerplan_b200", "-Wl,-rpath," + LIBDIR])
+    p = subprocess.run([exe], stdout=subprocess.PIPE, stderr=subprocess.STDOUT)
+    out = p.stdout.decode()
+    assert p.returncode == 0, out
+    assert [l for l in out.splitlines() if l.startswith("ok ")] == [
+        "ok spec", "ok tree labels", "ok tree round trip", "ok tree labels rejected", "ok grid", "ok scheme",
+        "ok reports", "ok tensor files", "ok json"]
