@@ -4,6 +4,7 @@ bit-identical to the reference's, as recorded in tests/golden/planner_golden.jso
 import json
 import os
 
+import numpy as np
 import pytest
 
 from paper_1707_05594_b200 import Errc, TuckerplanError
@@ -270,3 +271,25 @@ def test_scheme_volume_error_codes():
     assert e.value.code == Errc.no_valid_grid
     assert P.count_moved([6, 5, 4], [2, 2, 1], [2, 2, 1]) == 0
     assert P.count_moved([6, 5, 4], [2, 2, 1], [1, 2, 2]) > 0
+
+
+def test_count_moved_known_answers():
+    """tests/test_simulate.cpp:162-167: the two regrids of the reference's hand-built scenario."""
+    assert P.count_moved([8, 8, 16, 64], [1, 1, 1, 64], [8, 8, 1, 1]) == 64512
+    assert P.count_moved([16, 16, 8, 64], [1, 1, 1, 64], [2, 4, 8, 1]) == 129024
+    # block-overlap counting against an element-by-element owner walk (what the reference does)
+    rng = np.random.default_rng(41)
+    for _ in range(20):
+        ext = [int(rng.integers(2, 8)) for _ in range(3)]
+        grids = P.enumerate_grids(int(rng.choice([2, 4, 6, 8])), P.ProblemSpec(ext, ext))
+        if len(grids) < 2:
+            continue
+        a, b = grids[int(rng.integers(0, len(grids)))], grids[int(rng.integers(0, len(grids)))]
+        moved = 0
+        for idx in np.ndindex(*ext):
+            ra = rb = 0
+            for m, c in enumerate(idx):
+                ra = ra * a[m] + P.block_of(c, ext[m], a[m])
+                rb = rb * b[m] + P.block_of(c, ext[m], b[m])
+            moved += ra != rb
+        assert P.count_moved(ext, a, b) == moved
