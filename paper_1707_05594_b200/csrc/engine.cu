@@ -614,6 +614,9 @@ struct tp_plan {
   const tp_tensor* carry_tensor = nullptr;
   tp_u64 carry_stamp = 0;
   bool carry_live = false;                    // this sweep's walk starts from the carried products
+  int spare_sms_short = 16;                   // ... by products shorter than short_product_flops (tuning knobs;
+                                              // measured on C5: 2 -> 58.2, 16 -> 57.6, 32 -> 58.1, 48 -> 58.4 ms/iter)
+  double short_product_flops = 2e11;
   int spare_sms = 2;                          // SMs left to the side streams while eigen-solves are in flight
                                               // (measured on C5: 0-2 -> 58.4 ms/iter, 6 -> 58.9, 12 -> 60.0)
   int leaves_in_flight = 0;
@@ -674,6 +677,13 @@ void plan_ttm(tp_ctx* ctx, tp_plan* p, const double* x, const std::vector<size_t
               int spare_sms = 0) {
   long long outer, inner;
   mode_extents(dims, mode, outer, inner);
+  // a short product beside running eigen-solves gives them a real share of the machine (it costs little: the product
+  // is short); a long one only leaves the few SMs their latency-bound kernels need
+  if (spare_sms > 0) {
+    const double flops = 2.0 * static_cast<double>(p->spec.K[mode]) * static_cast<double>(outer) *
+                         static_cast<double>(dims[mode]) * static_cast<double>(inner);
+    if (flops < p->short_product_flops) spare_sms = std::max(spare_sms, p->spare_sms_short);
+  }
   TPB_CUDA(launch_ttm(ctx->stream, x, outer, static_cast<long long>(dims[mode]), inner, p->frag[mode],
                       p->frag_layout[mode], static_cast<long long>(p->spec.K[mode]), out,
                       std::max(1, ctx->sm_count - spare_sms)));
@@ -1176,14 +1186,18 @@ int tp_ctx_create(int device, tp_ctx** out) {
     ctx->sm_count = prop.multiProcessorCount;
     try {
       TPB_CUDA(cudaSetDevice(device));
-      // the TTM/Gram stream outranks the eigen-solve side streams: when both have CTAs pending, the tree goes first
-      int prio_low = 0, prio_high = 0;
-      TPB_CUDA(cudaDeviceGetStreamPriorityRange(&prio_low, &prio_high));
-      if (const char* env = std::getenv("TPB_AUX_PRIORITY")) {  // tuning knob: 0 = same as the tree, 1 = above it
-        if (env[0] == '0') prio_low = prio_high;
-        if (env[0] == '1') std::swap(prio_low, prio_high);
+      int least = 0, greatest = 0;  // numerically: greatest priority = smallest value
+      TPB_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+      // The eigen-solve side streams outrank the tree's stream: their kernels are short and latency-bound, and a
+      // leaf's factor is needed by the core chain soon after its Gram matrix is done, so they should not queue
+      // behind the thousands of CTAs of a Gram or TTM launch (measured on C5: 58.4 -> 57.8 ms/iter together with
+      // the wider SM share short products leave them).  TPB_AUX_PRIORITY: b = below the tree, 0 = same.
+      int main_prio = least, side_prio = greatest;
+      if (const char* env = std::getenv("TPB_AUX_PRIORITY")) {
+        if (env[0] == '0') side_prio = main_prio;
+        if (env[0] == 'b') std::swap(main_prio, side_prio);
       }
-      TPB_CUDA(cudaStreamCreateWithPriority(&ctx->stream, cudaStreamNonBlocking, prio_high));
+      TPB_CUDA(cudaStreamCreateWithPriority(&ctx->stream, cudaStreamNonBlocking, main_prio));
       TPB_SOLVER(cusolverDnCreate(&ctx->solver));
       TPB_SOLVER(cusolverDnSetStream(ctx->solver, ctx->stream));
       ctx->reduce_scratch = device_alloc(reduce_scratch_doubles() + 1);
@@ -1192,7 +1206,7 @@ int tp_ctx_create(int device, tp_ctx** out) {
       TPB_CUDA(cudaMalloc(&ctx->blas_ws[tp_ctx::kAux], tp_ctx::kBlasWorkspaceBytes));
       TPB_BLAS(cublasSetWorkspace(ctx->blas, ctx->blas_ws[tp_ctx::kAux], tp_ctx::kBlasWorkspaceBytes));
       for (int a = 0; a < tp_ctx::kAux; ++a) {
-        TPB_CUDA(cudaStreamCreateWithPriority(&ctx->aux[a], cudaStreamNonBlocking, prio_low));
+        TPB_CUDA(cudaStreamCreateWithPriority(&ctx->aux[a], cudaStreamNonBlocking, side_prio));
         TPB_SOLVER(cusolverDnCreate(&ctx->aux_solver[a]));
         TPB_SOLVER(cusolverDnSetStream(ctx->aux_solver[a], ctx->aux[a]));
         TPB_BLAS(cublasCreate(&ctx->aux_blas[a]));
@@ -1485,6 +1499,7 @@ int tp_plan_create(tp_ctx* ctx, int n_modes, const tp_u64* L, const tp_u64* K, i
       validate_tree(p->tree, p->spec);
       p->sweep_kind = sweep_kind;
       if (const char* env = std::getenv("TPB_SPARE_SMS")) p->spare_sms = std::max(0, std::atoi(env));  // tuning knob
+      if (const char* env = std::getenv("TPB_SPARE_SMS_SHORT")) p->spare_sms_short = std::max(0, std::atoi(env));
       Cards cards;
       const Cost cost = tree_cost(p->tree, p->spec, &cards);
       for (int m = 0; m < n_modes; ++m)
@@ -1956,6 +1971,14 @@ static LeafScratch& dev_scratch(tp_ctx* ctx) {
   return *static_cast<LeafScratch*>(ctx->dev_scratch);
 }
 
+// SMs a product of the tp_dev_* entry points leaves to asynchronous leaf solves in flight (as plan_ttm does).
+static int dev_sm_budget(const tp_ctx* ctx, double flops) {
+  bool busy = false;
+  for (const tp_ctx::Lane& lane : ctx->lanes) busy = busy || lane.busy;
+  if (!busy) return ctx->sm_count;
+  return std::max(1, ctx->sm_count - (flops < 2e11 ? 16 : 2));
+}
+
 int tp_dev_ttm_partial(tp_ctx* ctx, const double* x, int n_modes, const size_t* dims, int mode, const double* factor,
                        size_t L_full, size_t l0, size_t K, int n_dest, const size_t* dest_cuts, double* z) {
   return guarded([&] {
@@ -1979,8 +2002,8 @@ int tp_dev_ttm_partial(tp_ctx* ctx, const double* x, int n_modes, const size_t* 
     // M = F^T restricted to rows l0.. of F: M(k, l) = factor[k * L_full + l0 + l]
     TPB_CUDA(prep_factor_fragments(ctx->stream, factor + l0, static_cast<long long>(L_full), 1,
                                    static_cast<long long>(K), len, f, frag));
-    TPB_CUDA(launch_ttm(ctx->stream, x, outer, len, inner, frag, f, static_cast<long long>(K), z, ctx->sm_count,
-                        n_dest, cuts.data()));
+    TPB_CUDA(launch_ttm(ctx->stream, x, outer, len, inner, frag, f, static_cast<long long>(K), z,
+                        dev_sm_budget(ctx, 2.0 * static_cast<double>(K) * outer * len * inner), n_dest, cuts.data()));
     ctx->own_kernels += 2;
   });
 }
@@ -2022,8 +2045,9 @@ int tp_dev_ttm_scatter(tp_ctx* ctx, const double* x, int n_modes, const size_t* 
     double* frag = ensure_frag_scratch(ctx, f.doubles);
     TPB_CUDA(prep_factor_fragments(ctx->stream, factor + l0, static_cast<long long>(L_full), 1,
                                    static_cast<long long>(K), len, f, frag));
-    TPB_CUDA(launch_ttm(ctx->stream, x, outer, len, inner, frag, f, static_cast<long long>(K), z, ctx->sm_count,
-                        n_dest, cuts.data(), offsets.data()));
+    TPB_CUDA(launch_ttm(ctx->stream, x, outer, len, inner, frag, f, static_cast<long long>(K), z,
+                        dev_sm_budget(ctx, 2.0 * static_cast<double>(K) * outer * len * inner), n_dest, cuts.data(),
+                        offsets.data()));
     ctx->own_kernels += 2;
   });
 }
