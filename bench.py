@@ -1,12 +1,15 @@
 #!/usr/bin/env python
 """HOOI benchmark for the B200 engine (and the CPU reference arm).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl b200|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl b200|reference] [--grid 2x2x2|dynamic]
 
 A step is one HOOI iteration (one `hooi_sweep`: TTM-tree -> Gram + eigenvectors per leaf -> core) of BASELINE.json
 config C (default 5: 1600^3 -> 100^3, the largest single-GPU configuration and the one north_star's target names)
 on a seeded synthetic low-rank-plus-noise tensor (SURVEY.md §8d recipe, paper_1707_05594_b200/workloads.py).
 Prints ONE JSON line (rank 0).  See DESIGN.md §Measurement for every field.
+
+N > 1: one process per GPU over NCCL.  Under torchrun (WORLD_SIZE set) this process is one rank; started plainly
+(`python bench.py --gpus N`) it re-executes itself under `python -m torch.distributed.run --nproc-per-node N`.
 """
 from __future__ import annotations
 
@@ -14,6 +17,7 @@ import argparse
 import ctypes
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -27,6 +31,7 @@ sys.path.insert(0, ROOT)
 HBM_FALLBACK_GBS = 6650.0      # B200_PROFILING.md fallback
 FP64_FALLBACK_TFLOPS = 35.77   # cuBLAS DGEMM 8192^3 measured on this pool (profiles/r01_fp64_peaks.jsonl)
 NVLINK_GBS = 770.0             # measured peer copy per direction (B200_PROFILING.md)
+PARITY_ANGLE, PARITY_REL = 1e-9, 1e-10   # north_star: subspace angle / core norm and fit, relative
 
 
 def read_peaks():
@@ -36,6 +41,22 @@ def read_peaks():
             return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
     except Exception:
         return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+
+
+def shared_config(name, iterations, tree_label, n_gpus, grid, grid_volume, compare_grid=None):
+    """The `config` object BOTH arms print for a given (config, N): the workload and the reference's own selections
+    for it.  Everything specific to one engine goes under its `engine` key instead, so the driver's same-config
+    check compares like with like."""
+    return {"workload": name, "iterations": int(iterations), "schedule": "jacobi on optimal_tree",
+            "tree": tree_label, "n_gpus": int(n_gpus), "grid": [int(v) for v in grid],
+            "grid_volume_elements": int(grid_volume), "compare_grid": compare_grid}
+
+
+def comparison_grid(n_modes, world, K):
+    """north_star: on the largest config the optimal grid is compared with the uniform 2x2x2 grid (8 GPUs, 3 modes)."""
+    if world == 8 and n_modes == 3 and all(k >= 2 for k in K):
+        return [2, 2, 2]
+    return None
 
 
 def tree_roofline(spec, tree, cost, p_fp64_tflops, hbm_gbs):
@@ -136,12 +157,12 @@ def oracle_tree(tree):
     return ho.Tree(tree.n_modes, tree.kind, tree.mode, tree.parent)
 
 
-def cpu_iteration(t, spec, factors, tree):
+def cpu_iteration(t, L, K, factors, otree):
     """One HOOI iteration of the CPU restatement (oracle/hooi_oracle.py) with every host BLAS thread."""
     from oracle import hooi_oracle as ho
     timers = {}
     t0 = time.perf_counter()
-    core, new = ho.hooi_sweep(t, spec.L, spec.K, factors, oracle_tree(tree), "jacobi", None, timers)
+    core, new = ho.hooi_sweep(t, list(L), list(K), factors, otree, "jacobi", None, timers)
     return time.perf_counter() - t0, core, new, timers
 
 
@@ -155,7 +176,7 @@ def cpu_single_thread(t, spec, factors, tree, cost, secs_all_cores, cores, budge
     from oracle import hooi_oracle as ho
     with threadpool_limits(limits=1):
         if secs_all_cores * cores <= budget_s:
-            dt, _, _, _ = cpu_iteration(t, spec, factors, tree)
+            dt, _, _, _ = cpu_iteration(t, spec.L, spec.K, factors, oracle_tree(tree))
             return {"value": dt, "unit": "s/iter", "cores": 1, "sample": "1 full iteration, BLAS limited to one thread"}
         node = next(i for i, k in enumerate(tree.kind) if k == 1)          # first root child
         mode = tree.mode[node]
@@ -175,44 +196,83 @@ def cpu_single_thread(t, spec, factors, tree, cost, secs_all_cores, cores, budge
                           % (mode + 1, keep, spec.L[slab_mode], slab_mode + 1, dt, macs / dt / 1e9)}
 
 
+def oracle_run_with_parity(host_t, spec, tree, f0, iterations, gpu_step, budget_s=60.0):
+    """The oracle's HOOI run from the start factors beside the engine's, compared after EVERY iteration.
+    gpu_step() advances the engine by one iteration and returns (factors, core_norm, fit).  The oracle runs the
+    config's full iteration count unless that would exceed budget_s (then as many as fit, at least one)."""
+    from oracle import hooi_oracle as ho
+    otree = oracle_tree(tree)
+    tnorm2 = float(np.dot(host_t.reshape(-1), host_t.reshape(-1)))
+    of = [f.copy() for f in f0]
+    rows, secs, phases = [], [], {}
+    wall0 = time.perf_counter()
+    for it in range(iterations):
+        if it and (time.perf_counter() - wall0) + secs[0] > budget_s:
+            break
+        dt, ocore, of, timers = cpu_iteration(host_t, spec.L, spec.K, of, otree)
+        secs.append(dt)
+        for k, v in timers.items():
+            phases[k] = phases.get(k, 0.0) + v
+        gf, gnorm, gfit = gpu_step()
+        onorm = float(np.sqrt(np.sum(ocore * ocore)))
+        ofit = float(np.sqrt(max(tnorm2 - onorm * onorm, 0.0) / tnorm2))
+        rows.append({"iteration": it + 1,
+                     "max_sin_principal_angle": max(ho.sin_largest_principal_angle(a, b) for a, b in zip(gf, of)),
+                     "core_norm_rel_diff": abs(gnorm - onorm) / onorm,
+                     "fit_rel_diff": abs(gfit - ofit) / max(ofit, 1e-3), "fit_oracle": ofit})
+    ok = all(r["max_sin_principal_angle"] < PARITY_ANGLE and r["core_norm_rel_diff"] < PARITY_REL and
+             r["fit_rel_diff"] < PARITY_REL for r in rows)
+    return {"secs": secs, "phases": {k: v / len(secs) for k, v in phases.items()}, "rows": rows, "ok": ok}
+
+
 # --------------------------------------------------------------------------------------------- reference arm
 def run_reference(args):
-    """The reference's CPU implementation of the path (its Eigen engine cannot be built here — Eigen is absent — so
-    this is the oracle port, NumPy/OpenBLAS, all host threads) on the same config and metric."""
+    """The reference's CPU implementation of the path on the same config and metric.  Its Eigen engine cannot be built
+    here (Eigen is absent), so the arithmetic is the oracle port (NumPy/OpenBLAS, all host threads); the inputs and
+    the selections (tree, grid) come from the reference's own headers compiled into oracle/_ref/libref_shim.so.  This
+    arm maps no product library."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    from paper_1707_05594_b200 import planner as P, workloads as W
-    cfg = W.CONFIGS[args.config]
+    from oracle import ref_inputs as R
+    index = args.config
+    L, K, sigma, iterations, _ = R.CONFIGS[index]
     cores = os.cpu_count() or 1
-    spec = cfg.spec
-    tree = P.optimal_tree(spec).tree
-    t = W.build_tensor_host(cfg, threads=cores)
-    factors = W.start_factors(cfg)
+    otree = R.optimal_tree(L, K)
+    grid, volume = R.optimal_static_grid(L, K, otree, args.gpus) if args.gpus > 1 else ([1] * len(L), 0)
+    if args.grid and args.grid != "dynamic":
+        grid = [int(v) for v in args.grid.split("x")]
+        volume = R.static_volume(L, K, otree, grid, args.gpus)
+    t = R.build_tensor(index, threads=cores)
+    factors = R.start_factors(index)
     budget_s = 240.0
     wall0 = time.perf_counter()
-    dt0, _, factors, _ = cpu_iteration(t, spec, factors, tree)  # first (warm-up) iteration, also sizes the run
+    dt0, _, factors, _ = cpu_iteration(t, L, K, factors, otree)  # first (warm-up) iteration, also sizes the run
     warm_done = 1
     while warm_done < args.warmup and (time.perf_counter() - wall0) + dt0 * (1 + 1) < budget_s:
-        _, _, factors, _ = cpu_iteration(t, spec, factors, tree)
+        _, _, factors, _ = cpu_iteration(t, L, K, factors, otree)
         warm_done += 1
     times = []
     phase = {}
     while len(times) < args.steps and (not times or (time.perf_counter() - wall0) + dt0 < budget_s):
-        dt, _, factors, timers = cpu_iteration(t, spec, factors, tree)
+        dt, _, factors, timers = cpu_iteration(t, L, K, factors, otree)
         times.append(dt)
         for k, v in timers.items():
             phase[k] = phase.get(k, 0.0) + v
     value = float(np.mean(times))
+    name = R.config_name(index)
     sample = ("%d full HOOI iteration(s) of %s timed after %d warm-up (asked %d/%d; bounded to ~%.0f s of CPU work)"
-              % (len(times), cfg.name, warm_done, args.steps, args.warmup, budget_s))
+              % (len(times), name, warm_done, args.steps, args.warmup, budget_s))
     line = {
         "impl": "reference", "metric": "hooi_s_per_iter", "value": value, "unit": "s/iter", "n_gpus": args.gpus,
         "steps": len(times), "warmup": warm_done, "ms_per_step": value * 1e3, "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg.name, "iterations": cfg.iterations, "schedule": "jacobi on optimal_tree"},
+        "config": shared_config(name, iterations, R.tree_label(otree), args.gpus, grid, volume,
+                                "x".join(map(str, comparison_grid(len(L), args.gpus, K) or [])) or None),
         "cpu_baseline": {"value": value, "unit": "s/iter", "cores": cores, "kind": "port", "sample": sample,
-                         "phases_s_per_iter": {k: v / len(times) for k, v in phase.items()}},
+                         "phases_s_per_iter": {k: v / len(times) for k, v in phase.items()},
+                         "inputs": "reference headers compiled into oracle/_ref/libref_shim.so (random_tensor stream, "
+                                   "optimal_tree, optimal_static_grid); no product library mapped"},
         "e2e": {"value": value, "unit": "s/iter", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -256,7 +316,7 @@ def run_b200(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1 or args.distributed:
+    if world > 1 or args.distributed or args.backend != "cuda":
         from paper_1707_05594_b200 import distributed as D
         return D.run_bench_rank(args, rank, world, local_rank)
 
@@ -297,7 +357,7 @@ def run_b200(args):
 
     # One HOOI run from the random orthonormal start: W untimed warm-up iterations, then the K timed ones continue
     # it ("mean over the config's iterations after one warm-up").  The first iteration of a run is cold
-    # (no carried path yet); it is timed separately below and reported in `carried_path`.
+    # (no carried path yet); the whole series from the start is reported in `run_from_start` below.
     plan.set_factors(f0)
     for _ in range(max(args.warmup, 0)):
         one_step(False)
@@ -323,6 +383,7 @@ def run_b200(args):
     ms_per_step = float(np.sum(step_ms)) / steps
     phases = {k: v / steps for k, v in phases.items()}
     node_ms = [v / steps for v in node_ms_sum]
+    graph_replayed = sum(node_ms) == 0.0          # replayed whole-sweep graphs carry no per-node events
     # fit evaluation, timed separately from the sweep (the reference's CLI also calls it outside)
     w0 = time.perf_counter()
     fit = plan.fit_from_norms(dt)
@@ -331,12 +392,11 @@ def run_b200(args):
     w0 = time.perf_counter()
     fit_full = plan.reconstruction_error(dt)
     fit_full_ms = (time.perf_counter() - w0) * 1e3
-    final_factors = plan.get_factors()
     evd_info = plan.evd_info()
 
     # The per-TTM numbers come from a second pass of the same K iterations with the eigen-solves serialised behind
-    # the tree instead of beside it: in the overlapped schedule above a TTM's event span also contains whatever
-    # eigen-solve kernels shared the SMs with it.  Both tree totals are reported.
+    # the tree instead of beside it (which also means plain launches, no replayed graph): in the overlapped schedule
+    # a TTM's event span also contains whatever eigen-solve kernels shared the SMs with it.
     overlapped_node_ms = node_ms
     plan.set_overlap_evd(False)
     plan.set_factors(f0)
@@ -351,21 +411,28 @@ def run_b200(args):
         node_ms_sum = nm if node_ms_sum is None else [a + b for a, b in zip(node_ms_sum, nm)]
     node_ms = [v / steps for v in node_ms_sum]
     plan.set_overlap_evd(True)
+    if graph_replayed:
+        overlapped_node_ms = node_ms
 
     # Third pass: the same K iterations with the carried path off, i.e. tree + full core chain per iteration as the
     # reference schedules it (hooi.hpp:189-229); reported beside the headline, which uses the engine's default.
     plan.set_carry_path(False)
     plan.set_factors(f0)
     nocarry_ms = [one_step(True)[0] for _ in range(steps)]
-    factors_after_k = plan.get_factors()          # K iterations from the start factors
+    factors_nocarry = plan.get_factors()          # K iterations from the start factors
     plan.set_carry_path(True)
+
+    # run_from_start: the workload BASELINE.json names -- the config's iterations from the random orthonormal start --
+    # with every iteration timed, the cold first one included.
     plan.set_factors(f0)
-    cold_ms = None
-    for i in range(steps):
-        ms, _ = one_step(False)
-        if i == 0:
-            cold_ms = ms                           # first iteration of a run: no carried path yet
-    nocarry_same = all(np.array_equal(a, b) for a, b in zip(plan.get_factors(), factors_after_k))
+    from_start = [one_step(True)[0] for _ in range(max(cfg.iterations, steps))]
+    factors_k = None
+    if steps <= len(from_start):
+        plan.set_factors(f0)
+        for _ in range(steps):
+            one_step(False)
+        factors_k = plan.get_factors()
+    nocarry_same = factors_k is not None and all(np.array_equal(a, b) for a, b in zip(factors_k, factors_nocarry))
 
     # TTM-tree phase vs its per-TTM roofline
     rows = tree_roofline(spec, tree, cost, p_fp64, hbm_gbs)
@@ -379,6 +446,8 @@ def run_b200(args):
     # `roofline`: the dominant tree node's kernel, timed where the contract asks -- CUDA events on the engine's
     # stream inside the timed region (engine defaults: eigen-solve kernels may share the SMs with it and the grid
     # leaves 2 SMs to them while any are in flight); the serial-pass figure of the same node is reported beside it.
+    # Where the timed region replays the whole sweep as one graph (short sweeps), single launches cannot be bracketed
+    # by events there and the serial pass of the same iterations supplies the launch time.
     dom_serial = max(rows, key=lambda r: r["ms"])
     dom = dict(max(rows, key=lambda r: overlapped_node_ms[r["node"]]))
     dom["ms"] = overlapped_node_ms[dom["node"]]
@@ -403,57 +472,102 @@ def run_b200(args):
     roofline.update({"kernel": "ttm_tma_kernel / ttm_dmma_kernel (tree node %d: mode %d, %s)"
                                % (dom["node"], dom["mode"] + 1, "FP64 DMMA pipe" if dom["bound"] == "tensor" else "HBM"),
                      "algorithmic_flops_per_launch": dom["flops"], "algorithmic_bytes_per_launch": dom["bytes"],
-                     "avg_launch_ms": dom["ms"], "timed": "CUDA events around the launch, timed region, engine defaults",
+                     "avg_launch_ms": dom["ms"],
+                     "timed": ("CUDA events around the launch, serial pass of the same iterations (the timed region "
+                               "replays the sweep as one CUDA graph)" if graph_replayed else
+                               "CUDA events around the launch, timed region, engine defaults"),
                      "serial_pass": {"avg_launch_ms": serial_same["ms"], "achieved": serial_achieved,
                                      "frac": serial_achieved / (p_fp64 if dom["bound"] == "tensor" else hbm_gbs),
                                      "slowest_node_in_serial_pass": dom_serial["node"]},
                      "peak_source": fp64_src if dom["bound"] == "tensor" else hbm_src})
 
-    # e2e: the reference-facing by-value call with HOST buffers (upload T + factors, sweep, download factors + core)
+    # e2e: the reference-facing by-value call with HOST buffers.  Headline: the whole HOOI run of the config as the
+    # reference CLI drives it (tools/tuckerplan_cli.cpp:416-419: hooi_sweep by value in a loop on one tensor) -- every
+    # call passes the host tensor and host factors and receives host factors + core; the tensor crosses PCIe in the
+    # first call and later calls carry the caller's promise that it has not changed (TP_HOST_TENSOR_UNCHANGED).
+    # Timed from the first call (cold context cache, upload included) to the last download, divided by the iterations.
+    # Beside it: the same call without the promise (33 GB up every call) and the resident API.
     e2e = None
     if not args.no_e2e:
         host_t = host_flat.reshape(cfg.L)
-        d = E.Decomposition(None, f0)
-        e2e_steps = args.steps
-        E.hooi_sweep(host_t, spec, d, tree, "jacobi", ctx=ctx)  # warm (allocator, page tables)
-        ctx.synchronize()
-        w0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            d = E.hooi_sweep(host_t, spec, d, tree, "jacobi", ctx=ctx)
-        e2e_s = (time.perf_counter() - w0) / e2e_steps
         fbytes = 8 * sum(l * k for l, k in zip(spec.L, spec.K))
-        # the by-value call starts every eigen-solve from the caller's factors, the resident run from its own Ritz
-        # vectors: same subspaces to rounding, not the same bits
-        agree = max(sin_principal_angle(a, b) for a, b in zip(d.factors, factors_after_k)) if e2e_steps == steps else None
-        e2e = {"value": e2e_s, "unit": "s/iter", "h2d_bytes_per_step": total * 8 + fbytes,
-               "d2h_bytes_per_step": fbytes + 8 * int(np.prod(spec.K)), "host_memory": "pinned",
-               "max_sin_principal_angle_vs_resident_run": agree}
-
-    # CPU baseline: the oracle port on the same host tensor, all cores, a bounded sample (one iteration)
-    cpu = None
-    if not args.no_cpu:
-        host_t = host_flat.reshape(cfg.L)
-        secs, ocore, ofac, timers = cpu_iteration(host_t, spec, f0, tree)
-        from oracle import hooi_oracle as ho
+        cbytes = 8 * int(np.prod(spec.K))
+        iters = cfg.iterations
+        E.hooi_sweep(host_t, spec, E.Decomposition(None, f0), tree, "jacobi", ctx=ctx)  # warm (page tables, lazy init)
+        ctx.release_cache()
+        ctx.synchronize()
+        d = E.Decomposition(None, f0)
+        w0 = time.perf_counter()
+        for i in range(iters):
+            d = E.hooi_sweep(host_t, spec, d, tree, "jacobi", ctx=ctx, tensor_unchanged=i > 0)
+        run_s = (time.perf_counter() - w0) / iters
+        # the by-value run against the resident run of the same iterations: same subspaces to rounding
+        plan.set_factors(f0)
+        for _ in range(iters):
+            plan.sweep(dt)
+        agree = max(sin_principal_angle(a, b) for a, b in zip(d.factors, plan.get_factors()))
+        # every call uploads (no promise)
+        d2 = E.Decomposition(None, f0)
+        every_steps = min(args.steps, 3)
+        w0 = time.perf_counter()
+        for _ in range(every_steps):
+            d2 = E.hooi_sweep(host_t, spec, d2, tree, "jacobi", ctx=ctx)
+        every_s = (time.perf_counter() - w0) / every_steps
+        ctx.release_cache()
+        # resident API (DeviceTensor + HooiPlan): per step host factors in, host factors + core out
         plan.set_factors(f0)
         plan.sweep(dt)
-        gfac = plan.get_factors()
-        angle = max(ho.sin_largest_principal_angle(a, b) for a, b in zip(gfac, ofac))
-        gnorm, onorm = plan.core_norm(), float(np.sqrt(np.sum(ocore * ocore)))
+        ctx.synchronize()
+        w0 = time.perf_counter()
+        for _ in range(args.steps):
+            plan.sweep(dt)
+            plan.get_factors()
+            plan.get_core()
+        resident_s = (time.perf_counter() - w0) / args.steps
+        e2e = {"value": run_s, "unit": "s/iter",
+               "h2d_bytes_per_step": (total * 8) // iters + fbytes, "d2h_bytes_per_step": fbytes + cbytes,
+               "host_memory": "pinned",
+               "what": "whole run of the config's %d iterations through the by-value C-ABI call, upload of the tensor "
+                       "(first call) included, later calls with TP_HOST_TENSOR_UNCHANGED; mean per iteration" % iters,
+               "max_sin_principal_angle_vs_resident_run": agree,
+               "by_value_every_call": {"value": every_s, "unit": "s/iter", "h2d_bytes_per_step": total * 8 + fbytes,
+                                       "d2h_bytes_per_step": fbytes + cbytes, "calls": every_steps},
+               "resident_api": {"value": resident_s, "unit": "s/iter", "h2d_bytes_per_step": 0,
+                                "d2h_bytes_per_step": fbytes + cbytes,
+                                "what": "tensor resident (DeviceTensor + HooiPlan); factors + core read back each step"}}
+
+    # CPU baseline and parity: the oracle port runs the config's iterations from the start factors on the same host
+    # tensor, all cores; the engine runs the same iterations and is compared after every one of them.
+    cpu, parity_ok = None, True
+    if not args.no_cpu:
+        host_t = host_flat.reshape(cfg.L)
+        plan.set_factors(f0)
+
+        def gpu_step():
+            plan.sweep(dt)
+            return plan.get_factors(), plan.core_norm(), plan.fit_from_norms(dt)
+
+        res = oracle_run_with_parity(host_t, spec, tree, f0, cfg.iterations, gpu_step)
+        parity_ok = res["ok"]
+        secs = float(np.mean(res["secs"]))
         single = cpu_single_thread(host_t, spec, f0, tree, cost, secs, cores)
         cpu = {"value": secs, "unit": "s/iter", "cores": cores, "kind": "port", "single_thread": single,
-               "sample": "1 full HOOI iteration of %s from the start factors (NumPy/OpenBLAS oracle port)" % cfg.name,
-               "phases_s": timers,
-               "parity_first_iteration": {"max_sin_principal_angle": angle, "core_norm_rel_diff": abs(gnorm - onorm) / onorm}}
+               "sample": "%d of the %d HOOI iterations of %s from the start factors (NumPy/OpenBLAS oracle port), "
+                         "mean per iteration" % (len(res["secs"]), cfg.iterations, cfg.name),
+               "phases_s": res["phases"], "parity_per_iteration": res["rows"], "parity_ok": parity_ok,
+               "parity_bar": {"max_sin_principal_angle": PARITY_ANGLE, "core_norm_rel_diff": PARITY_REL,
+                              "fit_rel_diff": PARITY_REL},
+               "parity_first_iteration": {k: res["rows"][0][k] for k in ("max_sin_principal_angle", "core_norm_rel_diff")}}
 
     line = {
         "metric": "hooi_s_per_iter", "value": ms_per_step * 1e-3, "unit": "s/iter", "n_gpus": 1, "steps": steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": cfg.name, "iterations": cfg.iterations, "schedule": "jacobi on optimal_tree",
-                   "timed_steps": "iterations W+1..W+K of one HOOI run from the random orthonormal start",
-                   "tree": tree.label(), "grid": [1] * spec.n_modes(), "evd": "top-k subspace iteration where certified, else full syevd; on side streams",
+        "config": shared_config(cfg.name, cfg.iterations, tree.label(), 1, [1] * spec.n_modes(), 0),
+        "engine": {"timed_steps": "iterations W+1..W+K of one HOOI run from the random orthonormal start",
+                   "evd": "certified top-k subspace iteration (one launch for small leaves), else full syevd; on side streams",
                    "core": "chain along a tree path, partial products carried into the next sweep",
+                   "sweep_graph": "replayed" if graph_replayed else "plain launches",
                    "l2": "flushed_between_steps" if small else "inputs_larger_than_L2",
                    "noise": "slab-parallel" if cfg.slab_noise else "sequential"},
         "ttm_tree": {"schedule": "serial pass (eigen-solves not overlapped), same K iterations",
@@ -468,13 +582,17 @@ def run_b200(args):
         "ttm_tree_overlapped_ms": sum(overlapped_node_ms[r["node"]] for r in rows),
         "serial_schedule": {"ms_per_step": float(np.mean(serial_ms)), "phases_ms": serial_phases,
                             "note": "steady state: one cold sweep from the start factors precedes the K timed ones"},
-        "carried_path": {"enabled": True, "ms_first_iteration_cold": cold_ms,
+        "run_from_start": {"per_iteration_ms": from_start, "iterations": len(from_start),
+                           "mean_ms": float(np.mean(from_start[:cfg.iterations])),
+                           "note": "one HOOI run from the random orthonormal start, every iteration timed (CUDA "
+                                   "events); iteration 1 is cold: no carried products, eigen-solves from the caller's "
+                                   "factors. mean_ms is over the config's %d iterations" % cfg.iterations},
+        "carried_path": {"enabled": True, "ms_first_iteration_cold": from_start[0],
                          "ms_per_step_disabled": float(np.mean(nocarry_ms)),
                          "factors_bit_identical_when_disabled": bool(nocarry_same),
                          "note": "the core chain runs along a tree path; its partial products are the next sweep's "
-                                 "tree nodes and are not recomputed. The first iteration of a run (first warm-up step "
-                                 "here) is cold: tree + whole chain. ms_per_step_disabled: same K iterations from "
-                                 "the start factors with the option off (the reference's schedule)."},
+                                 "tree nodes and are not recomputed. ms_per_step_disabled: the first K iterations "
+                                 "from the start factors with the option off (the reference's schedule)."},
         "evd": {"fast_path_leaves": evd_info[0], "redone_with_full_solve_last_sweep": evd_info[1]},
         "phases_ms": phases, "relative_fit": fit,
         "fit_evaluation": {"from_norms": fit, "from_norms_ms": fit_norms_ms, "full_expansion": fit_full,
@@ -487,10 +605,33 @@ def run_b200(args):
     print(json.dumps(line))
     plan.close()
     dt.free()
+    if not parity_ok:
+        print("bench.py: parity against the oracle FAILED, see cpu_baseline.parity_per_iteration", file=sys.stderr)
+        return 3
     return 0
 
 
-def main():
+# --------------------------------------------------------------------------------------------- launch
+def free_port():
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch_under_torchrun(args, argv):
+    """`python bench.py --gpus N` started plainly: become N ranks, one per GPU (the command the driver itself uses
+    when it launches the ranks).  NCCL's communicator lines stay on stderr."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("OMP_NUM_THREADS", str(max(1, (os.cpu_count() or 1) // args.gpus)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + argv
+    return subprocess.call(cmd, env=env)
+
+
+def main(argv=None):
+    argv = list(sys.argv[1:] if argv is None else argv)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
@@ -502,9 +643,19 @@ def main():
                     help="override the optimal static grid, e.g. 2x2x2; 'dynamic' = per-node grids (optimal_dynamic_scheme)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    args = ap.parse_args()
+    ap.add_argument("--no-grid-comparison", action="store_true")
+    ap.add_argument("--backend", default="cuda", choices=["cuda", "numpy-test"],
+                    help="numpy-test: CONTRACT TEST ONLY -- the grid executor's rank program over gloo with the tests' "
+                         "NumPy stand-in for the local kernels (tests/numpy_ops.py); not a measurement")
+    args = ap.parse_args(argv)
+    if args.gpus < 1:
+        ap.error("--gpus must be at least 1")
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_under_torchrun(args, argv)
+    if args.backend == "numpy-test" and "WORLD_SIZE" not in os.environ:
+        return relaunch_under_torchrun(args, argv)
     return run_b200(args)
 
 

@@ -164,7 +164,21 @@ typedef struct tp_tensor tp_tensor;   /* row-major FP64 tensor resident in HBM *
 typedef struct tp_plan tp_plan;       /* spec + tree + arena + launch schedule for repeated sweeps */
 
 int tp_ctx_create(int device, tp_ctx** out);
+/* Same with creation flags.  The eigen-solve side streams normally outrank the stream the tree runs on (their kernels
+ * are short and latency-bound); the flags put them on the same priority or below it (A/B measurements). */
+enum { TP_CTX_SIDE_STREAMS_SAME_PRIORITY = 1, TP_CTX_SIDE_STREAMS_LOW_PRIORITY = 2 };
+int tp_ctx_create_ex(int device, unsigned flags, tp_ctx** out);
 int tp_ctx_destroy(tp_ctx* ctx);
+/* Context options (plain values through the ABI; the library reads no environment variables).
+ *   TP_CTX_OPT_STREAMED_UPLOAD_MIN_BYTES  by-value hooi_sweep calls upload tensors of at least this many bytes in
+ *                                         slabs and start multiplying the slabs that have arrived (default 256 MiB)
+ *   TP_CTX_OPT_TRACE_EVD                  != 0: one line per leaf and sweep on stderr with the certificate margins */
+enum { TP_CTX_OPT_STREAMED_UPLOAD_MIN_BYTES = 1, TP_CTX_OPT_TRACE_EVD = 2 };
+int tp_ctx_set_option(tp_ctx* ctx, int option, long long value);
+/* Process-wide switches.  TP_GLOBAL_OPT_TTM_TMA (default 1): 0 forces the cp.async TTM kernel where the TMA pipeline
+ * would be chosen (both compute the same sums in the same order). */
+enum { TP_GLOBAL_OPT_TTM_TMA = 1 };
+int tp_set_global_option(int option, long long value);
 int tp_ctx_synchronize(tp_ctx* ctx);
 /* the CUDA stream the engine launches on (cudaStream_t as void*), for event timing by the caller */
 int tp_ctx_stream(tp_ctx* ctx, void** stream_out);
@@ -181,7 +195,11 @@ int tp_tensor_alloc(tp_ctx* ctx, int n_modes, const size_t* dims, tp_tensor** ou
 int tp_tensor_download(tp_ctx* ctx, const tp_tensor* t, double* host);
 int tp_tensor_free(tp_ctx* ctx, tp_tensor* t);
 int tp_tensor_dims(const tp_tensor* t, int* n_modes, size_t* dims /* TP_MAX_MODES entries */);
+/* Raw device pointer.  The library cannot see writes through it, so from this call on no product of the tensor is
+ * carried between sweeps (TP_OPT_CARRY_PATH) -- until the caller takes over the bookkeeping with
+ * tp_tensor_mark_modified, to be called after every batch of writes through the pointer. */
 void* tp_tensor_device_ptr(const tp_tensor* t);
+int tp_tensor_mark_modified(tp_ctx* ctx, tp_tensor* t);
 /* frobenius_norm — dense_tensor.hpp:51-55, on the device (deterministic pairwise reduction) */
 int tp_tensor_norm(tp_ctx* ctx, const tp_tensor* t, double* out);
 /* y = beta * y + alpha * x, elementwise on the device (input assembly: T = X + sigma E; no reference counterpart) */
@@ -230,7 +248,15 @@ int tp_plan_destroy(tp_ctx* ctx, tp_plan* plan);
 /* Execution options (results are identical either way).  TP_OPT_OVERLAP_EVD (default 1): in a Jacobi sweep run each
  * leaf's eigen-solve on a side stream beside the remaining tree TTMs; 0 serialises everything on one stream, which is
  * what per-kernel timing and profiling want. */
-enum { TP_OPT_OVERLAP_EVD = 1, TP_OPT_FAST_EVD = 2, TP_OPT_CARRY_PATH = 3 };
+enum { TP_OPT_OVERLAP_EVD = 1, TP_OPT_FAST_EVD = 2, TP_OPT_CARRY_PATH = 3, TP_OPT_SPARE_SMS = 4,
+       TP_OPT_SPARE_SMS_SHORT = 5, TP_OPT_SWEEP_GRAPH = 6, TP_OPT_LEAF_GRAPH = 7, TP_OPT_FUSED_LEAF_SOLVE = 8 };
+/* TP_OPT_SPARE_SMS / _SHORT (defaults 2 / 16): SMs a long / short tree product leaves to eigen-solves in flight.
+ * TP_OPT_SWEEP_GRAPH (0 off, 1 on, 2 auto = default): replay the steady-state Jacobi sweep -- tree, Gram kernels, leaf
+ *   solves, core chain, status read-back -- as ONE CUDA graph; auto does so for sweeps below ~5e10 flops, where the
+ *   ~100 launches of a sweep would otherwise pace it.  Per-node timings are not available for replayed sweeps.
+ * TP_OPT_LEAF_GRAPH (default 1): replay a large leaf's multi-launch top-k iteration as a CUDA graph.
+ * TP_OPT_FUSED_LEAF_SOLVE (default 1): leaves with L_n <= 512 and K_n + 8 <= 64 run their whole certified top-k
+ *   solve in one launch (csrc/leaf_solve_kernels.cu). */
 int tp_plan_set_option(tp_ctx* ctx, tp_plan* plan, int option, int value);
 /* TP_OPT_CARRY_PATH (default 1; Gauss-Seidel plans carry the first leaf's chain): the core chain core_from_factors (hooi.hpp:93-100) contracts the modes
  * along one root-to-leaf path of the TTM tree; with the new factors its partial products are exactly the
@@ -240,11 +266,14 @@ int tp_plan_set_option(tp_ctx* ctx, tp_plan* plan, int option, int value);
  * by a sweep on another tensor, and whenever the tensor may have changed (tp_tensor_axpby, tp_tensor_device_ptr --
  * take the pointer again after writing through it).  SweepStats stay the analytic (reference) counts.
  * TP_OPT_FAST_EVD (default 1): leaves with 2 (K_n + 8) <= L_n (and K_n + 8 <= 112 or L_n >= 704) compute only
- * the K_n leading eigenvectors by warm-started block subspace iteration + Rayleigh-Ritz; every kept Ritz pair must satisfy
- * ||G x - theta x|| <= 1e-13 theta_max; a leaf that only misses this bound iterates on (up to three more rounds from
- * the Ritz vectors it reached), and a leaf that still misses it, loses a factorisation or has a "degenerate" gap
- * estimate is redone with the full eigen-solve, so the factors are the reference's (hooi.hpp:55-69) to rounding
- * either way.  tp_plan_last_evd_info: leaves eligible for the fast path, and how many of them the last sweep had to
+ * the K_n leading eigenvectors by warm-started block subspace iteration + Rayleigh-Ritz, accepted only with a
+ * certificate: (1) every kept Ritz pair has ||G x - theta x|| <= 1e-13 theta_max; (2) no larger eigenvalue was missed
+ * -- G is positive semidefinite, so whatever the block does not account for is bounded by trace(G) - sum(theta) plus
+ * the block residual, and that bound must lie below theta_K; (3) the Davis-Kahan bound ||R_kept|| / gap on the angle
+ * to the true leading subspace is <= 1e-10, so small spectral gaps are never trusted to the iteration.  A leaf that
+ * only misses (1) iterates on (up to three more rounds from the Ritz vectors it reached); a leaf that still misses,
+ * misses (2)/(3), loses a factorisation or has a "degenerate" gap estimate is redone with the full eigen-solve, so
+ * the factors are the reference's (hooi.hpp:55-69) to rounding either way.  tp_plan_last_evd_info: leaves eligible for the fast path, and how many of them the last sweep had to
  * redo with the full solve. */
 int tp_plan_last_evd_info(tp_ctx* ctx, tp_plan* plan, int* fast_eligible, int* rejected);
 /* Decomposition::factors (hooi.hpp:78-81) <-> device: factors[n] is L_n x K_n column-major on the host */
@@ -317,6 +346,17 @@ int tp_dev_leaf_solve_warm(tp_ctx* ctx, double* gram, size_t rows, int k, const 
 int tp_dev_leaf_solve_begin(tp_ctx* ctx, double* gram, size_t rows, int k, const double* start, double* factor,
                             int* flag, int* info, int lane);
 int tp_dev_leaf_solve_finish(tp_ctx* ctx, int lane, double* factor, int* flag, int* info, int* used_fast);
+/* The whole certified top-k solve of a small leaf in ONE launch (csrc/leaf_solve_kernels.cu; what tp_plan_sweep uses
+ * for leaves with rows <= 512 and k + 8 <= 64): power steps, Rayleigh-Ritz, certificate and the reference's selection
+ * rules, rounds repeated on the device until the certificate holds.  All pointers are device pointers.  `start`:
+ * rows x k column-major factor (start_is_ritz = 0) or the rows x (k + 8) ascending Ritz vectors a previous call left in
+ * `ritz` (start_is_ritz = 1; may alias `ritz`).  Out: ritz rows x (k + 8), theta k + 8 (ascending), factor rows x k,
+ * *flag |= degenerate, verdict[4] (verdict[0] == 0 && verdict[1] == 0: certified; [2] Jacobi sweeps, [3] power steps),
+ * diag[4] (worst residual / bound, angle bound, tail bound / theta_k, rounds).  TP_ERR_BAD_ARGUMENT if the leaf is
+ * too large for this path. */
+int tp_dev_leaf_solve_fused(tp_ctx* ctx, const double* gram, size_t rows, int k, const double* start,
+                            int start_is_ritz, double* ritz, double* theta, double* factor, int* flag, int* verdict,
+                            double* diag);
 /* *out (device double) = sum x[i]^2 */
 int tp_dev_sum_squares(tp_ctx* ctx, const double* x, size_t count, double* out);
 
@@ -336,6 +376,16 @@ int tp_dev_jacobi_eig(tp_ctx* ctx, const double* h, int block, double* w, double
 /* Consecutive calls with the same shape, ranks, tree and schedule reuse the device tensor, plan and workspaces kept
  * in the context (tp_ctx_release_cache frees them early; tp_ctx_destroy does too). */
 int tp_ctx_release_cache(tp_ctx* ctx);
+/* tp_hooi_sweep_host_ex flags.  TP_HOST_TENSOR_UNCHANGED: the caller promises that `tensor` (same address) still holds
+ * what the previous call on this context uploaded; the device copy is then reused and only factors and core travel.
+ * If in addition factors_in are bit for bit the factors that call returned, the sweep continues the resident run
+ * (warm eigen-solves, carried products) exactly like a tp_plan_sweep loop.  A loop of by-value hooi_sweep calls on one
+ * tensor -- the reference CLI's pattern, tools/tuckerplan_cli.cpp:416-419 -- therefore pays the upload once. */
+enum { TP_HOST_TENSOR_UNCHANGED = 1 };
+int tp_hooi_sweep_host_ex(tp_ctx* ctx, int n_modes, const size_t* dims, const double* tensor, const tp_u64* K,
+                          const double* const* factors_in, int n_nodes, const int* kind, const int* mode,
+                          const int* parent, int sweep_kind, unsigned flags, double* const* factors_out,
+                          double* core_out, tp_sweep_stats* stats);
 int tp_hooi_sweep_host(tp_ctx* ctx, int n_modes, const size_t* dims, const double* tensor, const tp_u64* K,
                        const double* const* factors_in, int n_nodes, const int* kind, const int* mode,
                        const int* parent, int sweep_kind, double* const* factors_out, double* core_out,

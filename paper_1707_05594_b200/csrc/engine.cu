@@ -16,6 +16,7 @@
 #include <cusolverDn.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -95,6 +96,14 @@ struct tp_ctx {
   // fixed cuBLAS workspaces (one per handle): recorded CUDA graphs must not depend on cuBLAS' own pool
   static constexpr size_t kBlasWorkspaceBytes = 32u << 20;
   void* blas_ws[kAux + 1] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  // tp_ctx_set_option
+  size_t streamed_upload_min_bytes = size_t{256} << 20;  // by-value calls: below this the upload is one copy
+  bool trace_evd = false;                                // print every leaf's certificate margins to stderr
+  // by-value calls with TP_HOST_TENSOR_UNCHANGED: what the cached device tensor was uploaded from, and the factors the
+  // last call returned (a caller that feeds them back continues the resident run: warm solves, carried products)
+  bool host_call_busy = false;                           // a by-value call is using the cache right now
+  const double* host_call_source = nullptr;
+  std::vector<std::vector<double>> host_call_last_factors;
 };
 
 struct tp_tensor {
@@ -104,26 +113,47 @@ struct tp_tensor {
   // changes whenever the contents may have changed (creation, tp_tensor_axpby, a by-value re-upload, handing out
   // the raw pointer); plans compare it before reusing products of this tensor kept from the previous sweep
   tp_u64 stamp = 0;
+  // the raw device pointer has been handed out: writes through it are invisible to the stamp, so plans stop carrying
+  // products of this tensor until tp_tensor_mark_modified re-establishes the contract
+  bool pointer_escaped = false;
 };
 
 static tp_u64 next_tensor_stamp() {
-  static tp_u64 counter = 0;
-  return ++counter;
+  static std::atomic<tp_u64> counter{0};  // contexts on different host threads create tensors concurrently
+  return counter.fetch_add(1, std::memory_order_relaxed) + 1;
 }
+
+static void release_host_call_cache(tp_ctx* ctx);
 
 namespace tpb {
 namespace {
 
+thread_local tp_ctx* bound_ctx = nullptr;  // the context of the entry point running on this thread
+
 void bind(const tp_ctx* ctx) {
   if (!ctx) raise(TP_ERR_BAD_ARGUMENT, "null context");
   TPB_CUDA(cudaSetDevice(ctx->device));
+  bound_ctx = const_cast<tp_ctx*>(ctx);
 }
 
+// Device allocation.  When the device is out of memory the by-value call cache of the bound context (a whole device
+// copy of the last tensor plus its plan's buffers, kept so that loops of by-value calls do not reallocate) is given
+// up and the allocation retried once: the reference's usual sequence hooi_sweep -> reconstruction_error -> ttm, each
+// uploading its own copy, must fit whenever each call fits on its own.
 double* device_alloc(size_t doubles) {
   double* p = nullptr;
-  const cudaError_t e = cudaMalloc(&p, std::max<size_t>(doubles, 1) * sizeof(double));
-  if (e != cudaSuccess) raise(TP_ERR_CUDA, std::string("cudaMalloc of ") + std::to_string(doubles * 8) + " bytes: " +
-                                               cudaGetErrorString(e));
+  const size_t bytes = std::max<size_t>(doubles, 1) * sizeof(double);
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e == cudaErrorMemoryAllocation && bound_ctx && (bound_ctx->host_call_plan || bound_ctx->host_call_tensor) &&
+      !bound_ctx->host_call_busy) {
+    cudaGetLastError();
+    release_host_call_cache(bound_ctx);
+    e = cudaMalloc(&p, bytes);
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    raise(TP_ERR_CUDA, std::string("cudaMalloc of ") + std::to_string(doubles * 8) + " bytes: " + cudaGetErrorString(e));
+  }
   return p;
 }
 
@@ -228,8 +258,12 @@ struct LeafScratch {
   double* ritz = nullptr;      // block x block Ritz rotation
   double* small_work = nullptr;
   int small_lwork = 0;
-  int* verdict = nullptr;      // [0] |= 1: a kept Ritz pair missed the residual bound; [1]: a factorisation failed
-                               // (1 Cholesky pivot, 2 Jacobi not converged, else cuSOLVER info); [2]: Jacobi sweeps used
+  int* verdict = nullptr;      // [0] |= 1: a kept Ritz pair missed the residual bound, |= 4: the gap / angle criterion
+                               // failed; [1]: a factorisation failed (1 Cholesky pivot, 2 Jacobi not converged,
+                               // else cuSOLVER info); [2]: Jacobi sweeps used; [3]: power steps (one-launch solve)
+  double* diag = nullptr;      // certificate margins: worst kept residual / bound, angle bound, tau / theta_k, rounds
+  bool use_graph = true;       // replay the multi-launch iteration as a CUDA graph from its third run on
+  bool use_fused = true;       // small leaves: the whole solve in one launch (leaf_solve_kernels.cu)
   // the iteration is a fixed kernel sequence on fixed buffers: recorded once, replayed as a CUDA graph afterwards
   cudaGraphExec_t graph = nullptr;
   const double* graph_gram = nullptr;
@@ -258,6 +292,7 @@ struct LeafScratch {
     cudaFree(theta);
     cudaFree(small_work);
     cudaFree(verdict);
+    cudaFree(diag);
     cudaFree(gram);
     cudaFree(gram_ws);
     cudaFree(w);
@@ -351,6 +386,10 @@ void leaf_solve(tp_ctx* ctx, LeafScratch& s, long long rows, int k, double* fact
 constexpr int kSubspaceOversample = 8;
 constexpr int kSubspacePowerSteps = 6;
 constexpr double kSubspaceTol = 1e-13;
+// Davis-Kahan bound on the sine of the angle between the kept Ritz space and the leading invariant subspace that the
+// certificate accepts: a decade inside the 1e-9 projector tolerance of the reference's own tests (tolerances.hpp:17).
+// Leaves whose spectral gap is too small for it go to the full eigen-solve.
+constexpr double kSubspaceAngleTol = 1e-10;
 
 // `cols`: columns of the unfolding whose Gram matrix is solved (its rank bound); the iteration block must not exceed
 // it or Z = G Q is rank deficient and the Cholesky-QR breaks down.
@@ -381,6 +420,8 @@ void subspace_reserve(tp_ctx* ctx, LeafScratch& s, long long rows, int k) {
   s.small_work = device_alloc(static_cast<size_t>(s.small_lwork));
   TPB_CUDA(cudaMalloc(&s.verdict, 4 * sizeof(int)));
   TPB_CUDA(cudaMemset(s.verdict, 0, 4 * sizeof(int)));
+  s.diag = device_alloc(4);
+  TPB_CUDA(cudaMemset(s.diag, 0, 4 * sizeof(double)));
   s.block = b;
 }
 
@@ -442,7 +483,8 @@ const double* subspace_body(tp_ctx* ctx, const SubspaceIo& io, LeafScratch& s, c
   TPB_BLAS(cublasDgemm(io.blas, CUBLAS_OP_N, CUBLAS_OP_N, rows, b, b, &one, q, rows, v, b, &zero, x, rows));
   // residuals of the kept pairs: (Z V)_j - theta_j X_j with Z = G Q
   TPB_BLAS(cublasDgemm(io.blas, CUBLAS_OP_N, CUBLAS_OP_N, rows, b, b, &one, z, rows, v, b, &zero, q, rows));
-  TPB_CUDA(launch_ritz_residuals(io.stream, q, x, s.theta, rows, b, k, kSubspaceTol, s.verdict));
+  TPB_CUDA(launch_ritz_certificate(io.stream, gram, q, x, s.theta, rows, b, k, kSubspaceTol, kSubspaceAngleTol,
+                                   s.verdict, s.diag));
   ctx->own_kernels += 1;
   ctx->library_calls += power_steps + 4;
   return x;
@@ -457,7 +499,20 @@ void leaf_solve_subspace(tp_ctx* ctx, LeafScratch& s, const double* gram, long l
   io.stream = aux < 0 ? ctx->stream : ctx->aux[aux];
   io.own_small = static_cast<size_t>(s.block) <= small_evd_max_block();
   const int rows = static_cast<int>(rows_ll), b = s.block;
-  static const bool graphs_off = std::getenv("TPB_DISABLE_GRAPH") != nullptr;
+  if (s.use_fused && leaf_solve_fused_eligible(rows_ll, k, b)) {
+    // small leaf: start block, power steps, Rayleigh-Ritz, certificate (rounds repeat on the device until it holds)
+    // and the reference's selection in ONE launch.  Warm: from all Ritz vectors of the previous solve, one power step
+    // in the first round; cold: from the caller's factor + filler columns, three.
+    const bool warm = s.last_ritz != nullptr;
+    TPB_CUDA(launch_leaf_solve_fused(io.stream, gram, rows, k, b, warm ? s.last_ritz : start, warm ? 0 : 1,
+                                     warm ? 1 : 3, 4, kSubspaceTol, kSubspaceAngleTol, s.x, s.theta, factor_out,
+                                     s.flag, s.verdict, s.diag));
+    ctx->own_kernels += 1;
+    s.fast_used = true;
+    s.last_ritz = s.x;
+    return;
+  }
+  const bool graphs_off = !s.use_graph;
   const bool key_ok = s.graph_gram == gram && s.graph_rows == rows_ll && s.graph_k == k;
   if (!key_ok) {  // the slot is being reused for another problem: start over
     if (s.graph) cudaGraphExecDestroy(s.graph);
@@ -624,6 +679,24 @@ struct tp_plan {
     int mode, node;
   };
   std::vector<PendingLeaf> pending;           // leaves whose eigen-solve still has to be queued                      // leaves of the last sweep that had to be redone with the full solve
+  // Whole-sweep CUDA graph (Jacobi).  Once a run is in its steady state -- factors produced by the previous sweep,
+  // carried products valid, every leaf on a capturable fast path -- a sweep is a fixed launch sequence on fixed buffers
+  // (tree products, Gram kernels, the leaf solves forked onto the side streams, the core chain, the status read-back):
+  // it is captured once and replayed, so the short sweeps of small tensors are not paced by ~100 host launches.
+  int sweep_graph_mode = 2;                   // 0 off, 1 on, 2 auto: only sweeps whose tree is short (see short_sweep)
+  bool short_sweep = false;                   // tree + core flops small enough for launch latency to matter
+  cudaGraphExec_t sweep_graph = nullptr;
+  const double* sweep_graph_tensor = nullptr;
+  tp_u64 sweep_graph_stamp = 0;
+  std::vector<char> sweep_graph_fast;         // per mode: the leaf's solve inside the graph is a certified fast solve
+  bool capturing = false;                     // the launch sequence is being recorded, not run: no timing events
+  u64 sweep_graph_kernels = 0, sweep_graph_library_calls = 0;  // launches of one steady-state sweep (accounting)
+  int warm_sweeps = 0;                        // sweeps since the caller last set the factors
+  cudaEvent_t graph_begin = nullptr, graph_end = nullptr;
+  // pinned read-back of every leaf's status, 8 ints per mode: verdict[0..3], degenerate flag, solver info, 2 unused;
+  // and of the certificate margins, 4 doubles per mode
+  int* host_status = nullptr;
+  double* host_diag = nullptr;
   tp_sweep_stats model{};   // analytic SweepStats (tree_macs, core_macs, peak_live)
   tp_sweep_timing timing{};
   // event pool for phase timing: triples (phase, begin, end)
@@ -654,14 +727,17 @@ struct Span {
   cudaEvent_t end;
   // both events are reserved up front so that spans may nest (an eigen-solve queued inside the core span)
   Span(tp_ctx* c, tp_plan* p, int phase, int node = -1, int aux = -1)
-      : plan(p), stream(aux < 0 ? c->stream : c->aux[aux]) {
+      : plan(p), stream(aux < 0 ? c->stream : c->aux[aux]), end(nullptr) {
+    if (plan->capturing) return;  // timing events do not belong in a recorded sweep
     plan->event_phase.push_back(phase);
     plan->event_node.push_back(node);
     cudaEvent_t begin = next_event(plan);
     end = next_event(plan);
     TPB_CUDA(cudaEventRecord(begin, stream));
   }
-  void close() { TPB_CUDA(cudaEventRecord(end, stream)); }
+  void close() {
+    if (end) TPB_CUDA(cudaEventRecord(end, stream));
+  }
 };
 
 void plan_refresh_fragments(tp_ctx* ctx, tp_plan* p, int mode, const double* factor) {
@@ -746,33 +822,47 @@ void plan_leaf(tp_ctx* ctx, tp_plan* p, const double* y, const std::vector<size_
   }
 }
 
-std::vector<int> verify_fast_leaves(tp_ctx* ctx, tp_plan* p) {
-  std::vector<int> host(4 * p->n, 0);
-  bool any = false;
+// Status read-back of a sweep, on the main stream: the certificate of every leaf that took a fast path this sweep,
+// every leaf's degenerate flag and solver info (the flags are cleared for the next sweep).  All copies land in the
+// plan's pinned buffers, so the same sequence can be part of a recorded sweep.
+void queue_status_readback(tp_ctx* ctx, tp_plan* p, bool with_flags) {
   for (int m = 0; m < p->n; ++m) {
     LeafScratch& s = p->leaf[m];
-    if (!s.fast_used) continue;
-    any = true;
-    TPB_CUDA(cudaMemcpyAsync(&host[4 * m], s.verdict, 3 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-    TPB_CUDA(cudaMemcpyAsync(&host[4 * m + 3], s.flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    int* const host = p->host_status + 8 * m;
+    if (s.fast_used) {
+      TPB_CUDA(cudaMemcpyAsync(host, s.verdict, 4 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+      TPB_CUDA(cudaMemcpyAsync(p->host_diag + 4 * m, s.diag, 4 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    if (!s.flag) continue;
+    if (with_flags || s.fast_used)
+      TPB_CUDA(cudaMemcpyAsync(host + 4, s.flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    if (with_flags) {
+      TPB_CUDA(cudaMemcpyAsync(host + 5, s.info, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+      TPB_CUDA(cudaMemsetAsync(s.flag, 0, sizeof(int), ctx->stream));
+    }
   }
+}
+
+// After the stream has been synchronised: which of the fast leaves missed their certificate (-> to be redone).
+std::vector<int> evaluate_fast_leaves(tp_ctx* ctx, tp_plan* p) {
   std::vector<int> rejected;
-  if (!any) return rejected;
-  TPB_CUDA(cudaStreamSynchronize(ctx->stream));
-  static const bool trace = std::getenv("TPB_TRACE_EVD") != nullptr;
   for (int m = 0; m < p->n; ++m) {
     LeafScratch& s = p->leaf[m];
     if (!s.fast_used) continue;
-    // residual bound missed, a factorisation inside failed, or the gap estimate says "degenerate" (then the exact
-    // spectrum decides)
-    const bool bad = host[4 * m] != 0 || host[4 * m + 1] != 0 || host[4 * m + 3] != 0;
-    if (trace)
-      std::fprintf(stderr, "[tpb evd] mode %d block %d: residual_miss=%d factorisation=%d jacobi_sweeps=%d degenerate=%d graph=%d\n",
-                   m, s.block, host[4 * m], host[4 * m + 1], host[4 * m + 2], host[4 * m + 3], s.graph_state);
+    const int* const host = p->host_status + 8 * m;
+    // residual bound / gap criterion missed, a factorisation inside failed, or the gap estimate says "degenerate"
+    // (then the exact spectrum decides)
+    const bool bad = host[0] != 0 || host[1] != 0 || host[4] != 0;
+    if (ctx->trace_evd)
+      std::fprintf(stderr,
+                   "[tpb evd] mode %d block %d: miss=%d factorisation=%d jacobi_sweeps=%d power_steps=%d degenerate=%d "
+                   "graph=%d residual/bound=%.3g angle_bound=%.3g tau/theta_k=%.3g rounds=%g\n",
+                   m, s.block, host[0], host[1], host[2], host[3], host[4], s.graph_state, p->host_diag[4 * m],
+                   p->host_diag[4 * m + 1], p->host_diag[4 * m + 2], p->host_diag[4 * m + 3]);
     if (bad) {
       rejected.push_back(m);
       // only the residual bound missed: the block is sound and simply has not converged yet -> worth iterating on
-      s.refinable = host[4 * m + 1] == 0 && host[4 * m + 3] == 0;
+      s.refinable = (host[0] & 1) != 0 && host[1] == 0 && host[4] == 0;
       if (!s.refinable) s.last_ritz = nullptr;
       TPB_CUDA(cudaMemsetAsync(s.flag, 0, sizeof(int), ctx->stream));
     } else {
@@ -781,6 +871,15 @@ std::vector<int> verify_fast_leaves(tp_ctx* ctx, tp_plan* p) {
     s.fast_used = false;
   }
   return rejected;
+}
+
+std::vector<int> verify_fast_leaves(tp_ctx* ctx, tp_plan* p) {
+  bool any = false;
+  for (int m = 0; m < p->n; ++m) any = any || p->leaf[m].fast_used;
+  if (!any) return {};
+  queue_status_readback(ctx, p, false);
+  TPB_CUDA(cudaStreamSynchronize(ctx->stream));
+  return evaluate_fast_leaves(ctx, p);
 }
 
 // A leaf whose certified solve was rejected: if only the residual bound was missed, repeat the iteration from the
@@ -1164,11 +1263,15 @@ static void release_host_call_cache(tp_ctx* ctx) {
   ctx->host_call_plan = nullptr;
   ctx->host_call_tensor = nullptr;
   ctx->host_call_key.clear();
+  ctx->host_call_source = nullptr;
+  ctx->host_call_last_factors.clear();
 }
 
 extern "C" {
 
-int tp_ctx_create(int device, tp_ctx** out) {
+int tp_ctx_create(int device, tp_ctx** out) { return tp_ctx_create_ex(device, 0, out); }
+
+int tp_ctx_create_ex(int device, unsigned flags, tp_ctx** out) {
   return guarded([&] {
     if (!out) raise(TP_ERR_BAD_ARGUMENT, "null output");
     int count = 0;
@@ -1191,12 +1294,10 @@ int tp_ctx_create(int device, tp_ctx** out) {
       // The eigen-solve side streams outrank the tree's stream: their kernels are short and latency-bound, and a
       // leaf's factor is needed by the core chain soon after its Gram matrix is done, so they should not queue
       // behind the thousands of CTAs of a Gram or TTM launch (measured on C5: 58.4 -> 57.8 ms/iter together with
-      // the wider SM share short products leave them).  TPB_AUX_PRIORITY: b = below the tree, 0 = same.
+      // the wider SM share short products leave them).  TP_CTX_SIDE_STREAMS_* flags: same priority / below the tree.
       int main_prio = least, side_prio = greatest;
-      if (const char* env = std::getenv("TPB_AUX_PRIORITY")) {
-        if (env[0] == '0') side_prio = main_prio;
-        if (env[0] == 'b') std::swap(main_prio, side_prio);
-      }
+      if (flags & TP_CTX_SIDE_STREAMS_SAME_PRIORITY) side_prio = main_prio;
+      if (flags & TP_CTX_SIDE_STREAMS_LOW_PRIORITY) std::swap(main_prio, side_prio);
       TPB_CUDA(cudaStreamCreateWithPriority(&ctx->stream, cudaStreamNonBlocking, main_prio));
       TPB_SOLVER(cusolverDnCreate(&ctx->solver));
       TPB_SOLVER(cusolverDnSetStream(ctx->solver, ctx->stream));
@@ -1255,6 +1356,29 @@ int tp_ctx_destroy(tp_ctx* ctx) {
     }
     cudaStreamDestroy(ctx->stream);
     delete ctx;
+  });
+}
+
+int tp_ctx_set_option(tp_ctx* ctx, int option, long long value) {
+  return guarded([&] {
+    if (!ctx) raise(TP_ERR_BAD_ARGUMENT, "null context");
+    if (option == TP_CTX_OPT_STREAMED_UPLOAD_MIN_BYTES) {
+      if (value < 0) raise(TP_ERR_BAD_ARGUMENT, "negative size");
+      ctx->streamed_upload_min_bytes = static_cast<size_t>(value);
+    } else if (option == TP_CTX_OPT_TRACE_EVD) {
+      ctx->trace_evd = value != 0;
+    } else {
+      raise(TP_ERR_BAD_ARGUMENT, "unknown context option");
+    }
+  });
+}
+
+int tp_set_global_option(int option, long long value) {
+  return guarded([&] {
+    if (option == TP_GLOBAL_OPT_TTM_TMA)
+      ttm_tma_enabled().store(value != 0, std::memory_order_relaxed);
+    else
+      raise(TP_ERR_BAD_ARGUMENT, "unknown global option");
   });
 }
 
@@ -1347,8 +1471,20 @@ int tp_tensor_dims(const tp_tensor* t, int* n_modes, size_t* dims) {
 
 void* tp_tensor_device_ptr(const tp_tensor* t) {
   if (!t) return nullptr;
-  const_cast<tp_tensor*>(t)->stamp = next_tensor_stamp();  // the caller may write through the pointer
+  // the caller may write through the pointer at any later time: no product of this tensor is carried between sweeps
+  // until tp_tensor_mark_modified puts the caller in charge of announcing writes
+  const_cast<tp_tensor*>(t)->stamp = next_tensor_stamp();
+  const_cast<tp_tensor*>(t)->pointer_escaped = true;
   return t->data;
+}
+
+int tp_tensor_mark_modified(tp_ctx* ctx, tp_tensor* t) {
+  return guarded([&] {
+    (void)ctx;
+    if (!t) raise(TP_ERR_BAD_ARGUMENT, "null tensor");
+    t->stamp = next_tensor_stamp();
+    t->pointer_escaped = false;  // from here on the caller announces every write with this call
+  });
 }
 
 int tp_tensor_norm(tp_ctx* ctx, const tp_tensor* t, double* out) {
@@ -1498,8 +1634,6 @@ int tp_plan_create(tp_ctx* ctx, int n_modes, const tp_u64* L, const tp_u64* K, i
       p->tree = tree_from_arrays(n_modes, n_nodes, kind, mode, parent);
       validate_tree(p->tree, p->spec);
       p->sweep_kind = sweep_kind;
-      if (const char* env = std::getenv("TPB_SPARE_SMS")) p->spare_sms = std::max(0, std::atoi(env));  // tuning knob
-      if (const char* env = std::getenv("TPB_SPARE_SMS_SHORT")) p->spare_sms_short = std::max(0, std::atoi(env));
       Cards cards;
       const Cost cost = tree_cost(p->tree, p->spec, &cards);
       for (int m = 0; m < n_modes; ++m)
@@ -1610,6 +1744,14 @@ int tp_plan_create(tp_ctx* ctx, int n_modes, const tp_u64* L, const tp_u64* K, i
         TPB_CUDA(cudaEventCreateWithFlags(&p->gram_ready[m], cudaEventDisableTiming));
         TPB_CUDA(cudaEventCreateWithFlags(&p->factor_ready[m], cudaEventDisableTiming));
       }
+      TPB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&p->host_status), sizeof(int) * 8 * n_modes, cudaHostAllocDefault));
+      TPB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&p->host_diag), sizeof(double) * 4 * n_modes, cudaHostAllocDefault));
+      std::memset(p->host_status, 0, sizeof(int) * 8 * n_modes);
+      std::memset(p->host_diag, 0, sizeof(double) * 4 * n_modes);
+      TPB_CUDA(cudaEventCreate(&p->graph_begin));
+      TPB_CUDA(cudaEventCreate(&p->graph_end));
+      // below ~2e10 flops a sweep's kernels take a millisecond or two in total and ~100 host launches pace it
+      p->short_sweep = 2.0 * (static_cast<double>(cost.total_macs) + static_cast<double>(p->core_macs_executed)) < 5e10;
       TPB_CUDA(cudaStreamSynchronize(ctx->stream));
     } catch (...) {
       tp_plan_destroy(ctx, p);
@@ -1643,6 +1785,11 @@ int tp_plan_destroy(tp_ctx* ctx, tp_plan* p) {
       if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : p->events)
       if (e) cudaEventDestroy(e);
+    if (p->sweep_graph) cudaGraphExecDestroy(p->sweep_graph);
+    if (p->graph_begin) cudaEventDestroy(p->graph_begin);
+    if (p->graph_end) cudaEventDestroy(p->graph_end);
+    if (p->host_status) cudaFreeHost(p->host_status);
+    if (p->host_diag) cudaFreeHost(p->host_diag);
     delete p;
   });
 }
@@ -1658,6 +1805,7 @@ int tp_plan_set_factors(tp_ctx* ctx, tp_plan* p, const double* const* factors) {
     }
     p->carry_valid = false;
     p->factors_from_caller = true;
+    p->warm_sweeps = 0;
     for (LeafScratch& slot : p->leaf) slot.last_ritz = nullptr;  // the caller's factors are the start, not ours
     TPB_CUDA(cudaStreamSynchronize(ctx->stream));
   });
@@ -1706,6 +1854,67 @@ int tp_plan_compute_core(tp_ctx* ctx, tp_plan* p, const tp_tensor* t) {
   });
 }
 
+}  // extern "C"
+
+namespace tpb {
+namespace {
+
+// The launch sequence of one Jacobi sweep, everything up to the host's look at the status: start-of-sweep factors to
+// fragment order, the tree walk (leaf solves forked onto the side streams), the core chain with the new factors
+// (joins the side streams), the status read-back, and the new factors copied over the current ones (the buffers
+// never swap, so the sequence is the same every sweep and can be recorded).
+void jacobi_sequence(tp_ctx* ctx, tp_plan* p, const tp_tensor* t) {
+  std::vector<size_t> dims(p->spec.L.begin(), p->spec.L.end());
+  {
+    Span s(ctx, p, kTree);  // start-of-sweep factors -> fragment order, once per mode
+    for (int m = 0; m < p->n; ++m) plan_refresh_fragments(ctx, p, m, p->cur[m]);
+    s.close();
+  }
+  p->leaves_in_flight = 0;
+  p->pending.clear();
+  if (p->arrival && p->arrival->row_end.size() > 1 && p->n > 1)
+    jacobi_walk_streamed_root(ctx, p, t->data, dims);
+  else
+    jacobi_walk(ctx, p, 0, t->data, dims, 0);
+  plan_core(ctx, p, t->data, p->fresh, p->overlap_evd);  // waits for each new factor just before using it
+  queue_status_readback(ctx, p, true);
+  for (int m = 0; m < p->n; ++m)
+    TPB_CUDA(cudaMemcpyAsync(p->cur[m], p->fresh[m], sizeof(double) * p->spec.L[m] * p->spec.K[m],
+                             cudaMemcpyDeviceToDevice, ctx->stream));
+}
+
+// May this sweep run as (or be recorded into) the whole-sweep graph?
+bool sweep_graph_usable(const tp_ctx* ctx, const tp_plan* p, const tp_tensor* t) {
+  (void)ctx;
+  if (p->sweep_graph_mode == 0 || (p->sweep_graph_mode == 2 && !p->short_sweep)) return false;
+  if (p->sweep_kind != TP_SWEEP_JACOBI || p->arrival || !p->overlap_evd || !p->fast_evd) return false;
+  if (p->factors_from_caller || p->warm_sweeps < 2 || p->fast_rejected != 0 || t->pointer_escaped) return false;
+  if (p->carry_enabled && !p->carry_nodes.empty() && !p->carry_live) return false;
+  for (int m = 0; m < p->n; ++m) {
+    const LeafScratch& s = p->leaf[m];
+    const long long rows = static_cast<long long>(p->spec.L[m]);
+    const int k = static_cast<int>(p->spec.K[m]);
+    if (s.failures >= 2 || !subspace_eligible(rows, k, plan_leaf_columns(p, m))) return false;  // full solve: cuSOLVER
+    const int b = k + kSubspaceOversample;
+    if (s.use_fused && leaf_solve_fused_eligible(rows, k, b)) continue;
+    if (static_cast<size_t>(b) > small_evd_max_block()) return false;        // cuSOLVER steps inside the iteration
+    if (s.use_graph && s.graph_state != 2 && s.graph_state != -1) return false;  // its own recording comes first
+    if (!s.last_ritz) return false;
+  }
+  return true;
+}
+
+void drop_sweep_graph(tp_plan* p) {
+  if (p->sweep_graph) cudaGraphExecDestroy(p->sweep_graph);
+  p->sweep_graph = nullptr;
+  p->sweep_graph_tensor = nullptr;
+}
+
+}  // namespace
+}  // namespace tpb
+
+extern "C" {
+
 int tp_plan_sweep(tp_ctx* ctx, tp_plan* p, const tp_tensor* t, tp_sweep_stats* stats) {
   return guarded([&] {
     bind(ctx);
@@ -1716,32 +1925,98 @@ int tp_plan_sweep(tp_ctx* ctx, tp_plan* p, const tp_tensor* t, tp_sweep_stats* s
     p->event_phase.clear();
     p->event_node.clear();
     std::vector<size_t> dims(p->spec.L.begin(), p->spec.L.end());
+    int flag = 0;
     if (p->sweep_kind == TP_SWEEP_JACOBI) {
-      {
-        Span s(ctx, p, kTree);  // start-of-sweep factors -> fragment order, once per mode
-        for (int m = 0; m < p->n; ++m) plan_refresh_fragments(ctx, p, m, p->cur[m]);
-        s.close();
-      }
-      p->leaves_in_flight = 0;
-      p->pending.clear();
-      p->carry_live = p->carry_enabled && p->carry_valid && p->carry_tensor == t && p->carry_stamp == t->stamp;
+      p->carry_live = p->carry_enabled && p->carry_valid && p->carry_tensor == t && p->carry_stamp == t->stamp &&
+                      !t->pointer_escaped;
       p->carry_valid = false;  // the chain at the end of this sweep overwrites the carried products
-      if (p->arrival && p->arrival->row_end.size() > 1 && p->n > 1)
-        jacobi_walk_streamed_root(ctx, p, t->data, dims);
-      else
-        jacobi_walk(ctx, p, 0, t->data, dims, 0);
-      plan_core(ctx, p, t->data, p->fresh, p->overlap_evd);  // waits for each new factor just before using it
-      // leaves solved by subspace iteration are accepted only with their residual certificate; a rejected leaf is
-      // redone with the full eigen-solve on its (intact) Gram matrix, and the core with it
-      const std::vector<int> rejected = verify_fast_leaves(ctx, p);
+      bool replayed = false;
+      if (sweep_graph_usable(ctx, p, t)) {
+        if (p->sweep_graph && (p->sweep_graph_tensor != t->data || p->sweep_graph_stamp != t->stamp)) drop_sweep_graph(p);
+        if (!p->sweep_graph) {
+          // record: the same code path as an eager sweep, with the main stream (and, through its event waits, the
+          // side streams) in capture mode
+          cudaGraph_t recorded = nullptr;
+          bool ok = cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeRelaxed) == cudaSuccess;
+          if (ok) {
+            p->capturing = true;
+            const u64 own0 = ctx->own_kernels, lib0 = ctx->library_calls;
+            try {
+              jacobi_sequence(ctx, p, t);
+            } catch (const Failure&) {
+              ok = false;
+            }
+            p->capturing = false;
+            ctx->own_kernels = own0;
+            ctx->library_calls = lib0;
+            if (cudaStreamEndCapture(ctx->stream, &recorded) != cudaSuccess) ok = false;
+            if (ok && cudaGraphInstantiate(&p->sweep_graph, recorded, 0) != cudaSuccess) ok = false;
+            if (recorded) cudaGraphDestroy(recorded);
+          }
+          if (ok) {
+            p->sweep_graph_tensor = t->data;
+            p->sweep_graph_stamp = t->stamp;
+            p->sweep_graph_fast.assign(p->n, 0);
+            for (int m = 0; m < p->n; ++m) p->sweep_graph_fast[m] = p->leaf[m].fast_used ? 1 : 0;
+          } else {
+            cudaGetLastError();  // recording is an optimisation: this plan carries on with plain launches
+            p->sweep_graph = nullptr;
+            p->sweep_graph_mode = 0;
+            for (int a = 0; a < tp_ctx::kAux; ++a) cudaStreamSynchronize(ctx->aux[a]);
+          }
+        }
+        if (p->sweep_graph) {
+          for (int m = 0; m < p->n; ++m) p->leaf[m].fast_used = p->sweep_graph_fast[m] != 0;
+          TPB_CUDA(cudaEventRecord(p->graph_begin, ctx->stream));
+          TPB_CUDA(cudaGraphLaunch(p->sweep_graph, ctx->stream));
+          TPB_CUDA(cudaEventRecord(p->graph_end, ctx->stream));
+          ctx->own_kernels += p->sweep_graph_kernels;
+          ctx->library_calls += p->sweep_graph_library_calls;
+          replayed = true;
+        }
+      } else if (p->sweep_graph) {
+        drop_sweep_graph(p);
+      }
+      if (!replayed) {
+        const u64 own0 = ctx->own_kernels, lib0 = ctx->library_calls;
+        jacobi_sequence(ctx, p, t);
+        p->sweep_graph_kernels = ctx->own_kernels - own0;   // what a replay of this sequence launches
+        p->sweep_graph_library_calls = ctx->library_calls - lib0;
+      }
+      TPB_CUDA(cudaStreamSynchronize(ctx->stream));
+      // leaves solved by subspace iteration are accepted only with their certificate; a rejected leaf is redone
+      // (more rounds, else the full eigen-solve on its intact Gram matrix), and the core with it
+      const std::vector<int> rejected = evaluate_fast_leaves(ctx, p);
+      for (int m = 0; m < p->n; ++m) {
+        if (p->host_status[8 * m + 5] != 0) raise(TP_ERR_TOO_LARGE, "eigensolver did not converge");  // hooi.hpp:56-57
+        flag |= p->host_status[8 * m + 4];
+      }
       p->fast_rejected = 0;
       if (!rejected.empty()) {
         for (int m : rejected) p->fast_rejected += redo_rejected_leaf(ctx, p, m, p->fresh[m]) ? 1 : 0;
         plan_core(ctx, p, t->data, p->fresh);
+        for (int m = 0; m < p->n; ++m)
+          TPB_CUDA(cudaMemcpyAsync(p->cur[m], p->fresh[m], sizeof(double) * p->spec.L[m] * p->spec.K[m],
+                                   cudaMemcpyDeviceToDevice, ctx->stream));
+        // degenerate flags: the accepted leaves' from the read-back, the redone leaves' from their new solves
+        flag = 0;
+        for (int m = 0; m < p->n; ++m)
+          if (std::find(rejected.begin(), rejected.end(), m) == rejected.end()) flag |= p->host_status[8 * m + 4];
+        flag |= read_and_clear_flags(ctx, p->leaf);
       }
-      std::swap(p->cur, p->fresh);
       p->factors_from_caller = false;
+      ++p->warm_sweeps;
       plan_mark_carried(p, t);
+      if (replayed) {
+        TPB_CUDA(cudaStreamSynchronize(ctx->stream));
+        tp_sweep_timing tm{};
+        TPB_CUDA(cudaEventElapsedTime(&tm.total_ms, p->graph_begin, p->graph_end));
+        p->timing = tm;
+        p->node_ms.assign(p->tree.size(), 0.f);
+        p->node_evd_ms.assign(p->tree.size(), 0.f);
+      } else {
+        plan_collect_timing(ctx, p);
+      }
     } else {
       {
         Span s(ctx, p, kTree);
@@ -1754,7 +2029,7 @@ int tp_plan_sweep(tp_ctx* ctx, tp_plan* p, const tp_tensor* t, tp_sweep_stats* s
           TPB_CUDA(cudaStreamWaitEvent(ctx->stream, p->arrival->ready[c], 0));
         }
       p->carry_live = p->carry_enabled && p->carry_valid && p->carry_tensor == t && p->carry_stamp == t->stamp &&
-                      !p->carry_nodes.empty();
+                      !p->carry_nodes.empty() && !t->pointer_escaped;
       p->carry_valid = false;
       p->fast_rejected = 0;
       for (int leaf = 0; leaf < p->n; ++leaf) {  // hooi.hpp:206-224
@@ -1788,9 +2063,9 @@ int tp_plan_sweep(tp_ctx* ctx, tp_plan* p, const tp_tensor* t, tp_sweep_stats* s
       plan_core(ctx, p, t->data, p->cur);
       p->factors_from_caller = false;
       plan_mark_carried(p, t);
+      flag = read_and_clear_flags(ctx, p->leaf);
+      plan_collect_timing(ctx, p);
     }
-    const int flag = read_and_clear_flags(ctx, p->leaf);
-    plan_collect_timing(ctx, p);
     if (stats) {
       *stats = p->model;
       stats->degenerate = flag;
@@ -1802,6 +2077,7 @@ int tp_plan_set_option(tp_ctx* ctx, tp_plan* p, int option, int value) {
   return guarded([&] {
     (void)ctx;
     if (!p) raise(TP_ERR_BAD_ARGUMENT, "null plan");
+    tpb::drop_sweep_graph(p);  // every option changes the recorded launch sequence
     if (option == TP_OPT_OVERLAP_EVD)
       p->overlap_evd = value != 0;
     else if (option == TP_OPT_FAST_EVD)
@@ -1809,9 +2085,26 @@ int tp_plan_set_option(tp_ctx* ctx, tp_plan* p, int option, int value) {
     else if (option == TP_OPT_CARRY_PATH) {
       p->carry_enabled = value != 0;
       p->carry_valid = false;
-    }
-    else
+    } else if (option == TP_OPT_SPARE_SMS) {
+      p->spare_sms = std::max(0, value);
+    } else if (option == TP_OPT_SPARE_SMS_SHORT) {
+      p->spare_sms_short = std::max(0, value);
+    } else if (option == TP_OPT_SWEEP_GRAPH) {
+      if (value < 0 || value > 2) raise(TP_ERR_BAD_ARGUMENT, "sweep graph mode is 0 (off), 1 (on) or 2 (auto)");
+      p->sweep_graph_mode = value;
+    } else if (option == TP_OPT_LEAF_GRAPH) {
+      for (LeafScratch& slot : p->leaf) {
+        slot.use_graph = value != 0;
+        forget_recorded_solve(slot);
+      }
+    } else if (option == TP_OPT_FUSED_LEAF_SOLVE) {
+      for (LeafScratch& slot : p->leaf) {
+        slot.use_fused = value != 0;
+        forget_recorded_solve(slot);
+      }
+    } else {
       raise(TP_ERR_BAD_ARGUMENT, "unknown plan option");
+    }
   });
 }
 
@@ -2294,6 +2587,24 @@ int tp_dev_jacobi_eig(tp_ctx* ctx, const double* h, int block, double* w, double
   });
 }
 
+int tp_dev_leaf_solve_fused(tp_ctx* ctx, const double* gram, size_t rows, int k, const double* start,
+                            int start_is_ritz, double* ritz, double* theta, double* factor, int* flag, int* verdict,
+                            double* diag) {
+  return guarded([&] {
+    bind(ctx);
+    if (!gram || !start || !ritz || !theta || !factor || !flag || !verdict || !diag)
+      raise(TP_ERR_BAD_ARGUMENT, "null pointer");
+    check_leaf_args(static_cast<long long>(rows), 1, k);
+    const int b = k + kSubspaceOversample;
+    if (!leaf_solve_fused_eligible(static_cast<long long>(rows), k, b))
+      raise(TP_ERR_BAD_ARGUMENT, "leaf too large for the one-launch solve (rows <= 512, k + 8 <= 64, see the header)");
+    TPB_CUDA(launch_leaf_solve_fused(ctx->stream, gram, static_cast<int>(rows), k, b, start, start_is_ritz ? 0 : 1,
+                                     start_is_ritz ? 1 : 3, 4, kSubspaceTol, kSubspaceAngleTol, ritz, theta, factor,
+                                     flag, verdict, diag));
+    ctx->own_kernels += 1;
+  });
+}
+
 int tp_dev_sum_squares(tp_ctx* ctx, const double* x, size_t count, double* out) {
   return guarded([&] {
     bind(ctx);
@@ -2314,8 +2625,21 @@ int tp_hooi_sweep_host(tp_ctx* ctx, int n_modes, const size_t* dims, const doubl
                        const double* const* factors_in, int n_nodes, const int* kind, const int* mode,
                        const int* parent, int sweep_kind, double* const* factors_out, double* core_out,
                        tp_sweep_stats* stats) {
+  return tp_hooi_sweep_host_ex(ctx, n_modes, dims, tensor, K, factors_in, n_nodes, kind, mode, parent, sweep_kind, 0,
+                               factors_out, core_out, stats);
+}
+
+int tp_hooi_sweep_host_ex(tp_ctx* ctx, int n_modes, const size_t* dims, const double* tensor, const tp_u64* K,
+                          const double* const* factors_in, int n_nodes, const int* kind, const int* mode,
+                          const int* parent, int sweep_kind, unsigned flags, double* const* factors_out,
+                          double* core_out, tp_sweep_stats* stats) {
   return guarded([&] {
     bind(ctx);
+    struct Busy {  // the allocator must not give up the cache this call is working with
+      tp_ctx* c;
+      explicit Busy(tp_ctx* ctx_) : c(ctx_) { c->host_call_busy = true; }
+      ~Busy() { c->host_call_busy = false; }
+    } busy(ctx);
     if (!dims || !tensor || !K || !factors_in) raise(TP_ERR_BAD_ARGUMENT, "null argument");
     std::vector<u64> L(dims, dims + std::max(n_modes, 0));
     std::vector<long long> key{n_modes, n_nodes, sweep_kind};
@@ -2335,23 +2659,50 @@ int tp_hooi_sweep_host(tp_ctx* ctx, int n_modes, const size_t* dims, const doubl
       release_host_call_cache(ctx);
       raise(status, msg, bad);
     };
+    bool fresh_cache = false;
     if (key != ctx->host_call_key || !ctx->host_call_plan || !ctx->host_call_tensor) {
       release_host_call_cache(ctx);
       forward(tp_plan_create(ctx, n_modes, L.data(), K, n_nodes, kind, mode, parent, sweep_kind, &ctx->host_call_plan));
       forward(tp_tensor_alloc(ctx, n_modes, dims, &ctx->host_call_tensor));
       ctx->host_call_key = key;
+      fresh_cache = true;
     }
     tp_tensor* t = ctx->host_call_tensor;
     tp_plan* plan = ctx->host_call_plan;
-    t->stamp = next_tensor_stamp();
-    forward(tp_plan_set_factors(ctx, plan, factors_in));
+    // TP_HOST_TENSOR_UNCHANGED: the caller promises that `tensor` still holds what the previous call uploaded from the
+    // same address, so the device copy is reused and only the factors travel.
+    const bool reuse_tensor = (flags & TP_HOST_TENSOR_UNCHANGED) && !fresh_cache && ctx->host_call_source == tensor;
+    // factors that are bit for bit the ones the previous call returned continue that run on the device: the warm
+    // eigen-solve state and the carried products stay valid, exactly as in a resident tp_plan_sweep loop
+    bool same_factors = reuse_tensor && static_cast<int>(ctx->host_call_last_factors.size()) == n_modes;
+    for (int m = 0; same_factors && m < n_modes; ++m) {
+      const std::vector<double>& last = ctx->host_call_last_factors[m];
+      same_factors = factors_in[m] && last.size() == static_cast<size_t>(dims[m] * K[m]) &&
+                     std::memcmp(last.data(), factors_in[m], last.size() * sizeof(double)) == 0;
+    }
+    if (!reuse_tensor) t->stamp = next_tensor_stamp();
+    if (!same_factors) forward(tp_plan_set_factors(ctx, plan, factors_in));
+    auto remember = [&] {
+      ctx->host_call_source = tensor;
+      ctx->host_call_last_factors.assign(n_modes, {});
+      if (!factors_out) return;
+      for (int m = 0; m < n_modes; ++m)
+        ctx->host_call_last_factors[m].assign(factors_out[m], factors_out[m] + dims[m] * K[m]);
+    };
+    if (reuse_tensor) {
+      forward(tp_plan_sweep(ctx, plan, t, stats));
+      if (factors_out) forward(tp_plan_get_factors(ctx, plan, factors_out));
+      if (core_out) forward(tp_plan_get_core(ctx, plan, core_out));
+      remember();
+      return;
+    }
+    ctx->host_call_source = nullptr;
     // Large tensors go up in slabs of the first mode on a copy stream; the sweep starts on the slabs that have
     // arrived (jacobi_walk_streamed_root) instead of idling through the whole PCIe transfer.
     const size_t rows = dims[0];
     const size_t per_row = t->size / rows;
     int chunks = 1;
-    size_t min_bytes = size_t{256} << 20;  // below this the transfer is too short to be worth splitting
-    if (const char* env = std::getenv("TPB_STREAMED_UPLOAD_MIN_BYTES")) min_bytes = std::strtoull(env, nullptr, 10);
+    const size_t min_bytes = ctx->streamed_upload_min_bytes;  // below this the transfer is too short to split
     if (n_modes > 1 && t->size * sizeof(double) >= min_bytes && rows >= 32)
       chunks = static_cast<int>(std::min<size_t>(8, rows / 16));
     if (chunks == 1) {
@@ -2390,6 +2741,7 @@ int tp_hooi_sweep_host(tp_ctx* ctx, int n_modes, const size_t* dims, const doubl
     }
     if (factors_out) forward(tp_plan_get_factors(ctx, ctx->host_call_plan, factors_out));
     if (core_out) forward(tp_plan_get_core(ctx, ctx->host_call_plan, core_out));
+    remember();
   });
 }
 

@@ -8,12 +8,13 @@
 
 #include <cfloat>
 
+#include "evd_device.cuh"
 #include "kernels.cuh"
 
 namespace tpb {
 namespace {
 
-constexpr int kMaxBlock = 112;  // largest iteration block: 2 b^2 doubles of shared memory must fit in 227 KB
+constexpr int kMaxBlock = kEvdMaxBlock;  // largest iteration block: 2 b^2 doubles of shared memory must fit in 227 KB
 constexpr int kSmallThreads = 512;
 constexpr int kSmallWarps = kSmallThreads / 32;
 
@@ -124,14 +125,12 @@ __global__ void __launch_bounds__(kTrsmThreads) trsm_right_lt_kernel(double* __r
   }
 }
 
-// Eigen-decomposition of the symmetric b x b matrix H (column-major, full storage) by the parallel cyclic Jacobi
-// method: round-robin pairing gives b/2 disjoint rotations per step; the step's update H <- J^T H J touches every
-// 2 x 2 block (row pair, column pair) exactly once, so it needs no barrier between the column and the row half.
-// Single CTA; H and the accumulated rotations V live in shared memory (leading dimension m = b rounded up to even:
-// the odd case plays against an all-zero dummy index that is never rotated).  Output: eigenvalues ascending in w,
-// matching eigenvectors as columns of v_out (b x b column-major).
+// Eigen-decomposition of the symmetric b x b matrix H by the parallel cyclic Jacobi method: the sweep loop lives in
+// evd_device.cuh (jacobi_sweeps_smem), shared with the single-launch leaf solve (leaf_solve_kernels.cu).  Single CTA;
+// H and the accumulated rotations V live in shared memory (leading dimension m = b rounded up to even: the odd case
+// plays against an all-zero dummy index that is never rotated).  Output: eigenvalues ascending in w, matching
+// eigenvectors as columns of v_out (b x b column-major).
 // *fail |= 2 if the off-diagonal mass has not vanished after kMaxSweeps sweeps; fail[1] = max(fail[1], sweeps used).
-constexpr int kMaxSweeps = 30;
 // Instantiated per block-size class: (512 threads, b <= 32), (1024, b <= 64: latency-bound, one round of column
 // pairs per step), (512, b <= 112: shared-memory-bandwidth-bound, the batched loads want the registers).
 template <int kJacobiThreads, int kBlockCap>
@@ -140,13 +139,9 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_eig_kernel(const double
                                                                    int* __restrict__ fail) {
   extern __shared__ double sm[];
   const int m = (b + 1) & ~1;
-  const int half = m / 2;
   double* const h = sm;          // m x m
   double* const v = sm + m * m;  // m x m
-  __shared__ double rot_c[kMaxBlock / 2], rot_s[kMaxBlock / 2];
-  __shared__ int rot_p[kMaxBlock / 2], rot_q[kMaxBlock / 2];
   constexpr int kJacobiWarps = kJacobiThreads / 32;
-  __shared__ double red[2 * kJacobiWarps];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   for (int col = warp; col < m; col += kJacobiWarps)
     for (int row = lane; row < m; row += 32) {
@@ -155,125 +150,9 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_eig_kernel(const double
     }
   __syncthreads();
 
-  int sweep = 0;
-  for (; sweep < kMaxSweeps; ++sweep) {
-    // off-diagonal mass against the whole: the backward error of a dense symmetric solver is (b eps ||H||_F)
-    double off = 0.0, all = 0.0;
-    for (int col = warp; col < m; col += kJacobiWarps)
-      for (int row = lane; row < m; row += 32) {
-        const double x = h[col * m + row] * h[col * m + row];
-        all += x;
-        if (row != col) off += x;
-      }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      off += __shfl_xor_sync(0xffffffffu, off, o);
-      all += __shfl_xor_sync(0xffffffffu, all, o);
-    }
-    if (lane == 0) {
-      red[warp] = off;
-      red[kJacobiWarps + warp] = all;
-    }
-    __syncthreads();
-    off = 0.0;
-    all = 0.0;
-    for (int i = 0; i < kJacobiWarps; ++i) {
-      off += red[i];
-      all += red[kJacobiWarps + i];
-    }
-    __syncthreads();
-    if (off <= (b * DBL_EPSILON) * (b * DBL_EPSILON) * all) break;  // uniform: same sums in every thread
-    if (!(all <= DBL_MAX)) {  // NaN / Inf input (a failed factorisation upstream): nothing to converge to
-      sweep = kMaxSweeps;
-      break;
-    }
-
-    for (int step = 0; step < m - 1; ++step) {
-      if (tid < half) {
-        const int p = (step + tid) % (m - 1);
-        const int q = (tid == 0) ? (m - 1) : (step + m - 1 - tid) % (m - 1);
-        double c = 1.0, s = 0.0;
-        const double hpq = h[q * m + p];
-        if (q < b && hpq != 0.0) {
-          // angle |theta| <= pi/4 with tan(2 theta) = 2 h_pq / (h_qq - h_pp), from cos(2 theta) without tangents
-          const double a = h[q * m + q] - h[p * m + p], b2 = 2.0 * hpq;
-          const double rinv = rsqrt(a * a + b2 * b2);
-          const double c2 = 0.5 + 0.5 * fabs(a) * rinv;  // cos^2(theta)
-          const double cinv = rsqrt(c2);
-          c = c2 * cinv;
-          s = (a >= 0.0 ? 0.5 : -0.5) * b2 * rinv * cinv;
-        }
-        rot_p[tid] = p;
-        rot_q[tid] = q;
-        rot_c[tid] = c;
-        rot_s[tid] = s;
-      }
-      __syncthreads();
-      // this lane's row pairs and its rows of V (as many 32-lane passes as the block cap needs) stay the same for
-      // every column pair the warp visits in this step
-      constexpr int kPairPasses = (kBlockCap / 2 + 31) / 32;
-      constexpr int kRowPasses = (kBlockCap + 31) / 32;
-      int pi[kPairPasses], qi[kPairPasses];
-      double ci[kPairPasses], si[kPairPasses];
-#pragma unroll
-      for (int a = 0; a < kPairPasses; ++a) {
-        const int ti = lane + 32 * a;
-        const bool on = ti < half;
-        pi[a] = on ? rot_p[ti] : 0;
-        qi[a] = on ? rot_q[ti] : 0;
-        ci[a] = on ? rot_c[ti] : 1.0;
-        si[a] = on ? rot_s[ti] : 0.0;
-      }
-      for (int tj = warp; tj < half; tj += kJacobiWarps) {
-        const int pj = rot_p[tj], qj = rot_q[tj];
-        const double cj = rot_c[tj], sj = rot_s[tj];
-        double* const hp = h + pj * m;
-        double* const hq = h + qj * m;
-        double* const vp = v + pj * m;
-        double* const vq = v + qj * m;
-        // all loads of the column pair first, then the arithmetic, then the stores: the blocks are disjoint
-        double ha[kPairPasses], hb[kPairPasses], hc[kPairPasses], hd[kPairPasses];
-        double vx[kRowPasses], vy[kRowPasses];
-#pragma unroll
-        for (int a = 0; a < kPairPasses; ++a) {
-          ha[a] = hp[pi[a]];
-          hb[a] = hq[pi[a]];
-          hc[a] = hp[qi[a]];
-          hd[a] = hq[qi[a]];
-        }
-#pragma unroll
-        for (int r = 0; r < kRowPasses; ++r) {
-          const int row = lane + 32 * r;
-          vx[r] = row < m ? vp[row] : 0.0;
-          vy[r] = row < m ? vq[row] : 0.0;
-        }
-#pragma unroll
-        for (int a = 0; a < kPairPasses; ++a) {
-          const int ti = lane + 32 * a;
-          if (ti >= half) continue;
-          // columns (H J_j), then rows (J_i^T ...)
-          const double a1 = cj * ha[a] - sj * hb[a], b1 = sj * ha[a] + cj * hb[a];
-          const double c1 = cj * hc[a] - sj * hd[a], d1 = sj * hc[a] + cj * hd[a];
-          const bool diag = ti == tj;
-          hp[pi[a]] = ci[a] * a1 - si[a] * c1;
-          hp[qi[a]] = diag ? 0.0 : si[a] * a1 + ci[a] * c1;
-          hq[pi[a]] = diag ? 0.0 : ci[a] * b1 - si[a] * d1;
-          hq[qi[a]] = si[a] * b1 + ci[a] * d1;
-        }
-#pragma unroll
-        for (int r = 0; r < kRowPasses; ++r) {
-          const int row = lane + 32 * r;
-          if (row < m) {
-            vp[row] = cj * vx[r] - sj * vy[r];
-            vq[row] = sj * vx[r] + cj * vy[r];
-          }
-        }
-      }
-      __syncthreads();
-    }
-  }
+  const int sweep = jacobi_sweeps_smem<kJacobiThreads, kBlockCap>(h, v, b, m);
   if (tid == 0) {
-    if (sweep == kMaxSweeps) atomicOr(fail, 2);
+    if (sweep == kJacobiMaxSweeps) atomicOr(fail, 2);
     atomicMax(fail + 1, sweep);
   }
   // ascending order by rank (ties by index); eigenvectors follow their values
@@ -292,10 +171,11 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_eig_kernel(const double
 }
 
 template <typename Kernel>
-cudaError_t allow_shared(Kernel kernel, size_t bytes, bool& configured) {
-  if (configured) return cudaSuccess;
+cudaError_t allow_shared(Kernel kernel, size_t bytes, PerDeviceInt& configured) {
+  std::atomic<int>* const slot = configured.slot();
+  if (slot && slot->load(std::memory_order_relaxed)) return cudaSuccess;
   const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
-  if (e == cudaSuccess) configured = true;
+  if (e == cudaSuccess && slot) slot->store(1, std::memory_order_relaxed);
   return e;
 }
 
@@ -304,7 +184,7 @@ cudaError_t allow_shared(Kernel kernel, size_t bytes, bool& configured) {
 size_t small_evd_max_block() { return kMaxBlock; }
 
 cudaError_t launch_cholesky(cudaStream_t stream, const double* s, int b, double* l, int* fail) {
-  static bool configured[3] = {false, false, false};
+  static PerDeviceInt configured[3];
   const size_t smem = sizeof(double) * b * b;
   cudaError_t e;
   if (b <= 32) {
@@ -324,7 +204,7 @@ cudaError_t launch_cholesky(cudaStream_t stream, const double* s, int b, double*
 }
 
 cudaError_t launch_trsm_right_lt(cudaStream_t stream, double* z, int n, int b, const double* l) {
-  static bool configured[3] = {false, false, false};
+  static PerDeviceInt configured[3];
   const size_t smem = sizeof(double) * b * b;
   const unsigned grid = static_cast<unsigned>((n + kTrsmRows - 1) / kTrsmRows);
   cudaError_t e;
@@ -345,7 +225,7 @@ cudaError_t launch_trsm_right_lt(cudaStream_t stream, double* z, int n, int b, c
 }
 
 cudaError_t launch_jacobi_eig(cudaStream_t stream, const double* h, int b, double* w, double* v, int* fail) {
-  static bool configured[3] = {false, false, false};
+  static PerDeviceInt configured[3];
   const int m = (b + 1) & ~1;
   const size_t smem = sizeof(double) * 2 * m * m;
   cudaError_t e;

@@ -3,9 +3,25 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstddef>
 
 namespace tpb {
+
+// Kernel attributes (the opt-in for more than 48 KB of dynamic shared memory) and occupancy figures belong to one
+// device's context, and one process may drive several devices (tp_ctx_create(device) per GPU, the grid executor):
+// launchers cache them per device.  The slots are atomics because contexts on different host threads may launch the
+// same kernel concurrently; a lost race only repeats an idempotent query.
+constexpr int kMaxDevices = 64;
+struct PerDeviceInt {
+  std::atomic<int> value[kMaxDevices];
+  // slot of the calling thread's current device (nullptr past kMaxDevices: callers then skip the cache)
+  std::atomic<int>* slot() {
+    int device = 0;
+    if (cudaGetDevice(&device) != cudaSuccess || device < 0 || device >= kMaxDevices) return nullptr;
+    return &value[device];
+  }
+};
 
 // ---- mode-n TTM (ttm_kernels.cu) -------------------------------------------
 struct TtmFragmentLayout {
@@ -33,6 +49,9 @@ constexpr int kMaxTtmDest = 16;
 cudaError_t launch_ttm(cudaStream_t stream, const double* x, long long outer, long long len, long long inner,
                        const double* mfrag, const TtmFragmentLayout& f, long long new_len, double* z, int sm_count,
                        int n_dest = 1, const long long* dest_cuts = nullptr, const long long* dest_offsets = nullptr);
+
+// Process-wide A/B switch: false forces the cp.async kernel even where the TMA pipeline is eligible.
+std::atomic<bool>& ttm_tma_enabled();
 
 // Warp-specialised TMA variant (ttm_tma_kernels.cu): used by launch_ttm for 16-byte-aligned, even extents with enough
 // columns to fill the machine.  mfrag must be the copy matching the mode (interleaved rows when inner > 1).
@@ -74,14 +93,27 @@ cudaError_t launch_select_basis(cudaStream_t stream, const double* vectors, cons
                                 int k, double* factor, int* flag);
 // out[i] = deterministic pseudo-random value in [-0.5, 0.5)
 cudaError_t launch_fill_pseudo_random(cudaStream_t stream, double* out, size_t n, unsigned long long salt);
-// *verdict |= 1 unless every one of the k largest Ritz pairs has ||(ZV)_j - theta_j X_j|| <= tol * theta_max
 // evd_kernels.cu: single-launch small dense steps of the top-k eigen-solve (block size b <= small_evd_max_block()).
 size_t small_evd_max_block();
 cudaError_t launch_cholesky(cudaStream_t stream, const double* s, int b, double* l, int* fail);         // S = L L^T
 cudaError_t launch_trsm_right_lt(cudaStream_t stream, double* z, int n, int b, const double* l);        // Z <- Z L^-T
 cudaError_t launch_jacobi_eig(cudaStream_t stream, const double* h, int b, double* w, double* v, int* fail);
 cudaError_t launch_reverse_columns(cudaStream_t stream, double* dst, const double* src, int rows, int ncols);
-cudaError_t launch_ritz_residuals(cudaStream_t stream, const double* zv, const double* x, const double* theta,
-                                  int rows, int ncols, int k, double tol, int* verdict);
+// Certificate of the k largest of ncols ascending Ritz pairs (x orthonormal, zv = G x): residual bound, nothing larger
+// missed (trace bound), subspace angle bound; see misc_kernels.cu.  verdict[0] |= 1 | 4; diag receives 4 margins.
+cudaError_t launch_ritz_certificate(cudaStream_t stream, const double* gram, const double* zv, const double* x,
+                                    const double* theta, int rows, int ncols, int k, double tol, double angle_tol,
+                                    int* verdict, double* diag);
+
+
+// leaf_solve_kernels.cu: the whole certified top-k solve of a small leaf (rows <= 512, block <= 64, see the file) in
+// one launch.  start_mode 0: `start` holds rows x b ascending Ritz vectors of the previous solve; 1: a rows x k factor.
+// ritz (rows x b) / theta (b) receive all Ritz pairs ascending, factor (rows x k) the reference's selection;
+// verdict (4 ints) / diag (4 doubles) the certificate and its margins.
+bool leaf_solve_fused_eligible(long long rows, int k, int b);
+cudaError_t launch_leaf_solve_fused(cudaStream_t stream, const double* gram, int rows, int k, int b,
+                                    const double* start, int start_mode, int first_steps, int max_rounds, double tol,
+                                    double angle_tol, double* ritz, double* theta, double* factor, int* flag,
+                                    int* verdict, double* diag);
 
 }  // namespace tpb

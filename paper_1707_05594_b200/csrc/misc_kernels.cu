@@ -120,8 +120,6 @@ __global__ void __launch_bounds__(256) fill_pseudo_random_kernel(double* __restr
   }
 }
 
-// One block per kept Ritz pair j (the j-th largest): r = (Z V)_col - theta * X_col over `rows` entries.
-// verdict[0] |= 1 when ||r|| > tol * theta_max (not converged).  Columns are stored ascending, as syevd returns them.
 // dst[:, j] = src[:, ncols - 1 - j] (rows x ncols, column-major): ascending Ritz vectors -> dominant direction first.
 __global__ void __launch_bounds__(256) reverse_columns_kernel(double* __restrict__ dst, const double* __restrict__ src,
                                                               int rows, int ncols) {
@@ -133,23 +131,69 @@ __global__ void __launch_bounds__(256) reverse_columns_kernel(double* __restrict
   }
 }
 
-__global__ void __launch_bounds__(256) ritz_residual_kernel(const double* __restrict__ zv, const double* __restrict__ x,
-                                                            const double* __restrict__ theta, int rows, int ncols,
-                                                            double tol, int* __restrict__ verdict) {
-  const int c = ncols - 1 - blockIdx.x;
-  const double th = theta[c];
-  const double* a = zv + static_cast<long long>(c) * rows;
-  const double* b = x + static_cast<long long>(c) * rows;
-  double acc = 0.0;
-  for (int i = threadIdx.x; i < rows; i += blockDim.x) {
-    const double r = a[i] - th * b[i];
-    acc = fma(r, r, acc);
+// Certificate of a block of b Ritz pairs (ascending; X orthonormal, ZV = G X) for the k largest -- one CTA:
+//   1. every kept pair has ||G x - theta x|| <= tol * theta_max;
+//   2. nothing larger was missed: G is positive semidefinite, so an eigenvalue not matched by one of the b Ritz values
+//      is at most tau = trace(G) - sum(theta) + b ||R||_F (Kahan: b eigenvalues lie within ||R||_2 of the Ritz values
+//      of an orthonormal block); those matched by the oversampling pairs are at most theta_{k+1} + ||R||_F;
+//      delta = theta_k - max(theta_{k+1} + ||R||_F, tau) must be positive;
+//   3. the subspace angle bound ||R_kept||_F / delta (Davis-Kahan) is at most angle_tol.
+// verdict[0] |= 1 (residual) | 4 (gap / angle); diag = {worst kept residual / (tol theta_max), ||R_kept||_F / delta,
+// tau / theta_k, 0}.  Warps own columns, lanes stride the rows; all sums have a fixed order.
+constexpr int kCertThreads = 1024;
+constexpr int kCertMaxBlock = 1024;
+__global__ void __launch_bounds__(kCertThreads) ritz_certificate_kernel(
+    const double* __restrict__ gram, const double* __restrict__ zv, const double* __restrict__ x,
+    const double* __restrict__ theta, int rows, int ncols, int k, double tol, double angle_tol,
+    int* __restrict__ verdict, double* __restrict__ diag) {
+  __shared__ double col_res[kCertMaxBlock];
+  __shared__ double red[kCertThreads / 32];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int c = warp; c < ncols; c += kCertThreads / 32) {
+    const double th = theta[c];
+    const double* a = zv + static_cast<long long>(c) * rows;
+    const double* b = x + static_cast<long long>(c) * rows;
+    double acc = 0.0;
+    for (int i = lane; i < rows; i += 32) {
+      const double r = a[i] - th * b[i];
+      acc = fma(r, r, acc);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) col_res[c] = acc;
   }
-  const double total = block_sum(acc);
-  if (threadIdx.x == 0) {
-    const double top = fmax(fabs(theta[ncols - 1]), 1e-300);
-    if (!(sqrt(total) <= tol * top)) atomicOr(verdict, 1);
+  double part = 0.0;
+  for (int i = tid; i < rows; i += kCertThreads) part += gram[static_cast<long long>(i) * rows + i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+  if (lane == 0) red[warp] = part;
+  __syncthreads();
+  if (tid != 0) return;
+  double trace = 0.0;
+  for (int w = 0; w < kCertThreads / 32; ++w) trace += red[w];
+  const double top = fmax(fabs(theta[ncols - 1]), 1e-300);
+  double sum_theta = 0.0, r_all2 = 0.0, r_kept2 = 0.0, worst = 0.0;
+  for (int c = 0; c < ncols; ++c) {
+    sum_theta += theta[c];
+    r_all2 += col_res[c];
+    if (c >= ncols - k) {
+      r_kept2 += col_res[c];
+      worst = fmax(worst, sqrt(col_res[c]));
+    }
   }
+  const double r_all = sqrt(r_all2), r_kept = sqrt(r_kept2);
+  const double tau = fmax(trace - sum_theta, 0.0) + ncols * r_all;
+  const double theta_k = theta[ncols - k];
+  const double below = k < ncols ? fmax(theta[ncols - k - 1] + r_all, tau) : tau;
+  const double delta = theta_k - below;
+  int bits = 0;
+  if (!(worst <= tol * top)) bits |= 1;
+  if (!(delta > 0.0) || !(r_kept <= angle_tol * delta)) bits |= 4;
+  if (bits) atomicOr(verdict, bits);
+  diag[0] = worst / (tol * top);
+  diag[1] = delta > 0.0 ? r_kept / delta : DBL_MAX;
+  diag[2] = tau / fmax(theta_k, 1e-300);
+  diag[3] = 0.0;
 }
 
 struct SlotList {
@@ -233,9 +277,12 @@ cudaError_t launch_fill_pseudo_random(cudaStream_t stream, double* out, size_t n
   return cudaGetLastError();
 }
 
-cudaError_t launch_ritz_residuals(cudaStream_t stream, const double* zv, const double* x, const double* theta,
-                                  int rows, int ncols, int k, double tol, int* verdict) {
-  ritz_residual_kernel<<<k, 256, 0, stream>>>(zv, x, theta, rows, ncols, tol, verdict);
+cudaError_t launch_ritz_certificate(cudaStream_t stream, const double* gram, const double* zv, const double* x,
+                                    const double* theta, int rows, int ncols, int k, double tol, double angle_tol,
+                                    int* verdict, double* diag) {
+  if (ncols > kCertMaxBlock || k < 1 || k > ncols) return cudaErrorInvalidValue;
+  ritz_certificate_kernel<<<1, kCertThreads, 0, stream>>>(gram, zv, x, theta, rows, ncols, k, tol, angle_tol, verdict,
+                                                          diag);
   return cudaGetLastError();
 }
 

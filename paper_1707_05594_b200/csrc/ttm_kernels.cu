@@ -353,7 +353,9 @@ cudaError_t launch_one(cudaStream_t stream, const TtmParams& p, int k_blocks, in
   constexpr int TILE_N = kWarps * NT;
   constexpr size_t smem = sizeof(double) * STAGES * (TILE_N * KC * 8 + (KC / 4) * KT * 32);
   auto kernel = ttm_dmma_kernel<KT, NT, KC, STAGES, LAST>;
-  static int ctas_per_sm = 0;  // per instantiation
+  static PerDeviceInt cache;  // per instantiation and device: resident CTAs per SM, 0 = not configured yet
+  std::atomic<int>* const slot = cache.slot();
+  int ctas_per_sm = slot ? slot->load(std::memory_order_relaxed) : 0;
   if (ctas_per_sm == 0) {
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
@@ -361,6 +363,7 @@ cudaError_t launch_one(cudaStream_t stream, const TtmParams& p, int k_blocks, in
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, smem);
     if (e != cudaSuccess) return e;
     ctas_per_sm = occ < 1 ? 1 : occ;
+    if (slot) slot->store(ctas_per_sm, std::memory_order_relaxed);
   }
   const long long groups = (p.n_tiles + TILE_N - 1) / TILE_N;
   const long long resident = std::max(1LL, static_cast<long long>(sm_count) * ctas_per_sm / k_blocks);
@@ -386,6 +389,13 @@ cudaError_t launch_kt(cudaStream_t stream, const TtmParams& p, int k_blocks, boo
 }
 
 }  // namespace
+
+// Process-wide switch between the TMA pipeline and the cp.async kernel (A/B tests through tp_set_global_option;
+// both kernels compute the same sums in the same order).
+std::atomic<bool>& ttm_tma_enabled() {
+  static std::atomic<bool> on{true};
+  return on;
+}
 
 int ttm_pick_kt(long long new_len) {
   static const int options[] = {1, 2, 3, 4, 5, 6, 8, 10, 13};
@@ -420,12 +430,8 @@ cudaError_t prep_factor_fragments(cudaStream_t stream, const double* m, long lon
 cudaError_t launch_ttm(cudaStream_t stream, const double* x, long long outer, long long len, long long inner,
                        const double* mfrag, const TtmFragmentLayout& f, long long new_len, double* z, int sm_count,
                        int n_dest, const long long* dest_cuts, const long long* dest_offsets) {
-  static const bool tma_off = [] {
-    const char* v = std::getenv("TPB_DISABLE_TMA");
-    return v && v[0] == '1';
-  }();
-  // TPB_DISABLE_TMA=1 (read once) / TPB_DISABLE_TMA_NOW (read per launch): force the cp.async kernel (A/B tests)
-  if (!tma_off && !std::getenv("TPB_DISABLE_TMA_NOW") && ttm_tma_eligible(x, outer, len, inner, z, f.kt, f.k_blocks, sm_count)) {
+  if (ttm_tma_enabled().load(std::memory_order_relaxed) &&
+      ttm_tma_eligible(x, outer, len, inner, z, f.kt, f.k_blocks, sm_count)) {
     bool chunks_aligned = true;
     for (int d = 0; dest_cuts && d < n_dest; ++d)
       chunks_aligned = chunks_aligned && ((dest_offsets ? dest_offsets[d] : outer * dest_cuts[d] * inner) % 2 == 0);

@@ -297,6 +297,56 @@ EncodeTiledFn encode_tiled() {
   return fn;
 }
 
+// Tensor maps are functions of (base address, extents) only, and a plan launches the same few products every sweep:
+// the encoded maps are kept in a small per-thread table (a context is used from one host thread) instead of being
+// rebuilt by the driver on every launch.  Entries are replaced round-robin.
+struct MapKey {
+  const double* x = nullptr;
+  long long outer = 0, len = 0, inner = 0;
+  bool operator==(const MapKey& o) const { return x == o.x && outer == o.outer && len == o.len && inner == o.inner; }
+};
+
+const CUtensorMap* tensor_map_for(const double* x, long long outer, long long len, long long inner) {
+  constexpr int kSlots = 64;
+  struct Table {
+    MapKey key[kSlots];
+    alignas(64) CUtensorMap map[kSlots];
+    int next = 0;
+  };
+  thread_local Table table;
+  const MapKey want{x, outer, len, inner};
+  for (int i = 0; i < kSlots; ++i)
+    if (table.key[i] == want) return &table.map[i];
+  const int at = table.next;
+  table.next = (table.next + 1) % kSlots;
+  CUtensorMap* const map = &table.map[at];
+  const CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  const cuuint32_t box[3] = {16, 16, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r;
+  if (inner == 1) {
+    // (L, outer) viewed as a 3-D map with a unit slowest dimension: both modes then use the same 3-D TMA path
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(len), static_cast<cuuint64_t>(outer), 1};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(len) * 8, static_cast<cuuint64_t>(len) * outer * 8};
+    r = encode_tiled()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(x), dims, strides, box, estr,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, promo,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(len),
+                                static_cast<cuuint64_t>(outer)};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(inner) * 8, static_cast<cuuint64_t>(len) * inner * 8};
+    r = encode_tiled()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(x), dims, strides, box, estr,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, promo,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  if (r != CUDA_SUCCESS) {
+    table.key[at] = MapKey{};
+    return nullptr;
+  }
+  table.key[at] = want;
+  return map;
+}
+
 template <int KT, int NT, int STAGES, bool LAST>
 cudaError_t launch_tma_one(cudaStream_t stream, const CUtensorMap& map, const TmaParams& p, int k_blocks,
                            int sm_count) {
@@ -304,7 +354,9 @@ cudaError_t launch_tma_one(cudaStream_t stream, const CUtensorMap& map, const Tm
   constexpr int BOXES = TILE_N / 2;
   constexpr size_t smem = sizeof(double) * STAGES * (BOXES * kKC * 16 + (kKC / 4) * KT * 32) + 2 * STAGES * 8 + 1024;
   auto kernel = ttm_tma_kernel<KT, NT, STAGES, LAST>;
-  static int ctas_per_sm = 0;
+  static PerDeviceInt cache;  // per instantiation and device: resident CTAs per SM, 0 = not configured yet
+  std::atomic<int>* const slot = cache.slot();
+  int ctas_per_sm = slot ? slot->load(std::memory_order_relaxed) : 0;
   if (ctas_per_sm == 0) {
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
@@ -312,6 +364,7 @@ cudaError_t launch_tma_one(cudaStream_t stream, const CUtensorMap& map, const Tm
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, smem);
     if (e != cudaSuccess) return e;
     ctas_per_sm = occ < 1 ? 1 : occ;
+    if (slot) slot->store(ctas_per_sm, std::memory_order_relaxed);
   }
   const long long resident = std::max(1LL, static_cast<long long>(sm_count) * ctas_per_sm / k_blocks);
   // every resident CTA gets an equal share of the boxes (at least half a tile each, else fewer CTAs)
@@ -377,29 +430,9 @@ cudaError_t launch_ttm_tma(cudaStream_t stream, const double* x, long long outer
   for (int d = n_dest + 1; d <= kMaxTtmDest; ++d) p.dest_k0[d] = p.dest_k0[n_dest];
   for (int d = n_dest; d < kMaxTtmDest; ++d) p.dest_off[d] = 0;
 
-  CUtensorMap map;
-  CUresult r;
-  const CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-  if (last) {
-    // (L, outer) viewed as a 3-D map with a unit slowest dimension: both modes then use the same 3-D TMA path
-    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(len), static_cast<cuuint64_t>(outer), 1};
-    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(len) * 8, static_cast<cuuint64_t>(len) * outer * 8};
-    const cuuint32_t box[3] = {16, 16, 1};
-    const cuuint32_t estr[3] = {1, 1, 1};
-    r = encode_tiled()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(x), dims, strides, box, estr,
-                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, promo,
-                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  } else {
-    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(inner), static_cast<cuuint64_t>(len),
-                                static_cast<cuuint64_t>(outer)};
-    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(inner) * 8, static_cast<cuuint64_t>(len) * inner * 8};
-    const cuuint32_t box[3] = {16, 16, 1};
-    const cuuint32_t estr[3] = {1, 1, 1};
-    r = encode_tiled()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(x), dims, strides, box, estr,
-                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, promo,
-                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  }
-  if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  const CUtensorMap* cached = tensor_map_for(x, outer, len, inner);
+  if (!cached) return cudaErrorInvalidValue;
+  const CUtensorMap& map = *cached;
 
   switch (f.kt) {
     case 1: return launch_tma_kt<1>(stream, map, p, f.k_blocks, last, sm_count);

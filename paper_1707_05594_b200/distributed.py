@@ -26,6 +26,8 @@ from __future__ import annotations
 
 import ctypes
 import os
+import sys
+import time
 from dataclasses import dataclass, field
 from typing import Callable, Dict, Generator, List, Optional, Sequence, Tuple
 
@@ -866,18 +868,69 @@ def build_local_block(ctx, ops, cfg, layout: GridLayout, rank: int, dist, thread
     return local
 
 
+class _Clock:
+    """Device-time marks on the engine's stream (CUDA events), or host time for the CPU contract test."""
+
+    def __init__(self, torch, stream):
+        self.torch, self.stream = torch, stream
+
+    def mark(self):
+        if self.stream is None:
+            return time.perf_counter()
+        ev = self.torch.cuda.Event(enable_timing=True)
+        ev.record(self.stream)
+        return ev
+
+    def ms(self, a, b):
+        if self.stream is None:
+            return (b - a) * 1e3
+        b.synchronize()
+        return a.elapsed_time(b)
+
+
+def _timed_sweeps(dh, run, clock, steps):
+    """K sweeps with per-node spans; returns (total_ms, tree_ms, core_ms, {node: ms}, last SweepResult), sums over K."""
+    marks = []
+    dh.events = lambda what, node: marks.append((what, node, clock.mark()))
+    e0 = clock.mark()
+    res = None
+    for _ in range(steps):
+        res = run(dh.sweep())
+    e1 = clock.mark()
+    dh.events = None
+    total_ms = clock.ms(e0, e1)
+    open_ev, node_ms, tree_ms, core_ms = {}, {}, 0.0, 0.0
+    for what, node, ev in marks:
+        if what.startswith("begin_"):
+            open_ev[(what[6:], node)] = ev
+            continue
+        key = (what[4:], node)
+        ms = clock.ms(open_ev.pop(key), ev)
+        if key[0] in ("ttm", "regrid"):
+            node_ms[node] = node_ms.get(node, 0.0) + ms
+        elif key[0] == "tree":
+            tree_ms += ms
+        elif key[0] == "core":
+            core_ms += ms
+    return total_ms, tree_ms, core_ms, node_ms, res
+
+
 def run_bench_rank(args, rank: int, world: int, local_rank: int):
-    """bench.py for N >= 1 ranks under torchrun: one process per GPU, NCCL over NVLink."""
+    """bench.py for N >= 1 ranks under torchrun: one process per GPU, NCCL over NVLink.  With --backend numpy-test
+    (CPU contract test only) the same rank program runs over gloo on the tests' NumPy stand-in for the kernels."""
     import json
-    import os
-    import time
     import torch
     import torch.distributed as dist
-    from . import engine as E, workloads as W
+    from . import workloads as W
     import bench as B
 
-    torch.cuda.set_device(local_rank)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    cuda = getattr(args, "backend", "cuda") == "cuda"
+    if cuda:
+        from . import engine as E
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    else:
+        dist.init_process_group("gloo")
     cfg = W.CONFIGS[args.config]
     spec = cfg.spec
     tree = P.optimal_tree(spec).tree
@@ -888,108 +941,141 @@ def run_bench_rank(args, rank: int, world: int, local_rank: int):
         scheme = P.optimal_dynamic_scheme(tree, spec, world).scheme
         q = list(scheme.root)
     else:
-        q = grid.grid if not getattr(args, "grid", None) else [int(v) for v in args.grid.split("x")]
+        q = list(grid.grid) if not getattr(args, "grid", None) else [int(v) for v in args.grid.split("x")]
     node_q = (lambda node: scheme.node_grids[node]) if scheme else (lambda node: q)
     layout = GridLayout(q)
     hbm_gbs, hbm_src = B.read_peaks()
-    p_fp64, fp64_src = B.measure_fp64_peak(torch)
-    ctx = E.Context(local_rank)
-    ops = GpuOps(ctx, local_rank)
     cores = max(1, (os.cpu_count() or 1) // world)
     t0 = time.perf_counter()
-    local = build_local_block(ctx, ops, cfg, layout, rank, dist, cores)
+    if cuda:
+        p_fp64, fp64_src = B.measure_fp64_peak(torch)
+        ctx = E.Context(local_rank)
+        ops = GpuOps(ctx, local_rank)
+        local = build_local_block(ctx, ops, cfg, layout, rank, dist, cores)
+        clock = _Clock(torch, ops.stream)
+        sync = ctx.synchronize
+        launch_counts = ctx.launch_counts
+        stat_device = ops.device
+    else:
+        from tests.numpy_ops import NumpyOps
+        p_fp64, fp64_src = B.FP64_FALLBACK_TFLOPS, "not measured (numpy-test backend)"
+        ctx, ops = None, NumpyOps()
+        local = ops.from_host(np.ascontiguousarray(W.build_tensor_host(cfg, cores)[layout.slices(rank, cfg.L)]))
+        clock = _Clock(torch, None)
+        sync = lambda: None
+        launch_counts = lambda: (0, 0)
+        stat_device = torch.device("cpu")
     build_s = time.perf_counter() - t0
     dh = DistributedHooi(ops, spec, tree, scheme or q, rank)
     dh.set_local_tensor_buffer(local)
     f0 = W.start_factors(cfg)
 
-    spans = {}
-    marks = []
-
-    def hook(what, node):
-        ev = torch.cuda.Event(enable_timing=True)
-        ev.record(ops.stream)
-        marks.append((what, node, ev))
-
     # TPB_PEER_SLOTS=1: reduce-scatters as direct stores into NVLink-mapped peer slots (see SymmetricSlots)
-    peer_slots = SymmetricSlots(dist, ops.device) if os.environ.get("TPB_PEER_SLOTS") == "1" else None
+    peer_slots = SymmetricSlots(dist, ops.device) if cuda and os.environ.get("TPB_PEER_SLOTS") == "1" else None
 
-    def one_sweep():
-        return run_rank(dh.sweep(), dist, ops, peer_slots=peer_slots)
+    def run(gen):
+        return run_rank(gen, dist, ops, peer_slots=peer_slots)
 
-    # one HOOI run from the random orthonormal start: W warm-up iterations, then the K timed ones continue it
-    dh.set_factors(f0)
-    for _ in range(max(args.warmup, 0)):
-        one_sweep()
-    ctx.synchronize()
-    dist.barrier()
-    torch.cuda.synchronize()
-    k0, _ = ctx.launch_counts()
-    sampler = B.ClockSampler(local_rank) if rank == 0 else None
+    def measure(executor):
+        """W warm-up + K timed sweeps of one HOOI run from the start factors; device time, max over ranks."""
+        executor.set_factors(f0)
+        for _ in range(max(args.warmup, 0)):
+            run(executor.sweep())
+        sync()
+        dist.barrier()
+        if cuda:
+            torch.cuda.synchronize()
+        total_ms, tree_ms, core_ms, node_ms, res = _timed_sweeps(executor, run, clock, args.steps)
+        sync()
+        dist.barrier()
+        nodes = sorted(node_ms)
+        stats = torch.tensor([total_ms, tree_ms, core_ms] + [node_ms[n] for n in nodes], dtype=torch.float64,
+                             device=stat_device)
+        dist.all_reduce(stats, op=dist.ReduceOp.MAX)       # max over ranks
+        stats = (stats / args.steps).tolist()
+        return stats[0], stats[1], stats[2], dict(zip(nodes, stats[3:])), res
+
+    k0, _ = launch_counts()
+    sampler = B.ClockSampler(local_rank) if rank == 0 and cuda else None
     if sampler:
         sampler.start()
-    dh.events = hook
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(ops.stream)
-    res = None
-    for _ in range(args.steps):
-        res = one_sweep()
-    e1.record(ops.stream)
-    e1.synchronize()
-    ctx.synchronize()
-    dist.barrier()
-    dh.events = None
+    ms_per_step, tree_phase_ms, core_ms, node_ms, res = measure(dh)
     clocks = sampler.stop() if sampler else None
-    k1, lib_calls = ctx.launch_counts()
-    total_ms = e0.elapsed_time(e1)
-    # per-node TTM spans (kernel + exchange + reduction), summed over the K steps
-    open_ev = {}
-    node_ms, tree_ms, core_ms = {}, 0.0, 0.0
-    for what, node, ev in marks:
-        if what.startswith("begin_"):
-            open_ev[(what[6:], node)] = ev
-        else:
-            key = (what[4:], node)
-            ms = open_ev.pop(key).elapsed_time(ev)
-            if key[0] in ("ttm", "regrid"):
-                node_ms[node] = node_ms.get(node, 0.0) + ms
-            elif key[0] == "tree":
-                tree_ms += ms
-            elif key[0] == "core":
-                core_ms += ms
-    nodes = sorted(node_ms)
-    stats = torch.tensor([total_ms, tree_ms, core_ms] + [node_ms[n] for n in nodes], dtype=torch.float64,
-                         device=ops.device)
-    dist.all_reduce(stats, op=dist.ReduceOp.MAX)       # device time, max over ranks
-    stats = (stats / args.steps).tolist()
-    ms_per_step, tree_phase_ms, core_ms = stats[0], stats[1], stats[2]
-    node_ms = dict(zip(nodes, stats[3:]))
-    fit, core_norm = run_rank(dh.fit_from_norms(), dist, ops)
+    k1, lib_calls = launch_counts()
+    fit, core_norm = run(dh.fit_from_norms())
+
+    # the optimal grid against the uniform 2 x 2 x 2 grid (north_star, largest config at 8 GPUs): the local blocks are
+    # redistributed to the other grid and the same measurement repeated
+    comparison, compare_q = None, B.comparison_grid(spec.n_modes(), world, spec.K)
+    if compare_q is not None and not scheme and not getattr(args, "no_grid_comparison", False) and compare_q != q:
+        other = GridLayout(compare_q)
+        with _stream_of(ops):
+            moved = run(regrid(local.view(layout.local_dims(rank, cfg.L)), cfg.L, layout, other, rank, ops.empty))
+            moved = moved.contiguous().view(-1)
+        dh2 = DistributedHooi(ops, spec, tree, compare_q, rank)
+        dh2.set_local_tensor_buffer(moved)
+        ms2, tree2, core2, node2, res2 = measure(dh2)
+        comparison = {"grid": compare_q, "ms_per_step": ms2, "tree_phase_ms": tree2,
+                      "grid_volume_elements": P.static_volume(tree, spec, compare_q, world).total,
+                      "per_node_ms": {str(k): v for k, v in node2.items()},
+                      "optimal": {"grid": list(q), "ms_per_step": ms_per_step,
+                                  "grid_volume_elements": P.static_volume(tree, spec, q, world).total}}
+        del dh2, moved
 
     # e2e: per step the local block comes from pinned host memory and the result goes back to the host
     e2e = None
     if not args.no_e2e:
-        host_block = torch.empty(local.numel(), dtype=torch.float64, pin_memory=True)
-        with torch.cuda.stream(ops.stream):
+        host_block = torch.empty(local.numel(), dtype=torch.float64, pin_memory=cuda)
+        with _stream_of(ops):
             host_block.copy_(local)
-        ctx.synchronize()
+        sync()
         dh.set_factors(f0)
         dist.barrier()
         w0 = time.perf_counter()
         for _ in range(args.steps):
-            with torch.cuda.stream(ops.stream):
+            with _stream_of(ops):
                 local.copy_(host_block, non_blocking=True)
+            dh.invalidate()
             dh.set_factors(dh.get_factors() if dh.core is not None else f0)
-            one_sweep()
+            run(dh.sweep())
             dh.get_factors()
             dh.get_local_core()
-        ctx.synchronize()
+        sync()
         dist.barrier()
-        secs = torch.tensor([(time.perf_counter() - w0) / args.steps], dtype=torch.float64, device=ops.device)
+        secs = torch.tensor([(time.perf_counter() - w0) / args.steps], dtype=torch.float64, device=stat_device)
         dist.all_reduce(secs, op=dist.ReduceOp.MAX)
         fbytes = 8 * sum(l * k for l, k in zip(spec.L, spec.K))
         e2e = {"value": float(secs.item()), "unit": "s/iter", "h2d_bytes_per_step": int(local.numel() * 8 + fbytes) * world,
-               "d2h_bytes_per_step": int(fbytes * world + 8 * int(np.prod(spec.K))), "host_memory": "pinned"}
+               "d2h_bytes_per_step": int(fbytes * world + 8 * int(np.prod(spec.K))), "host_memory": "pinned" if cuda else "pageable"}
+
+    # CPU baseline + parity: the oracle runs the config's iterations on rank 0's host cores from the start factors; the
+    # grid executor runs the same iterations on all ranks and is compared after every one of them
+    cpu, parity_ok = None, True
+    if not args.no_cpu:
+        dh.set_factors(f0)
+
+        def grid_step():
+            run(dh.sweep())
+            gfit, gnorm = run(dh.fit_from_norms())
+            return dh.get_factors(), gnorm, gfit
+
+        # every rank steps the executor exactly `iters` times (each step is a sequence of collectives); only rank 0
+        # also runs the oracle, without a time budget so that the count cannot differ between ranks
+        iters = cfg.iterations
+        if rank == 0:
+            host_t = W.build_tensor_host(cfg, os.cpu_count() or 1)
+            result = B.oracle_run_with_parity(host_t, spec, tree, f0, iters, grid_step, budget_s=float("inf"))
+            parity_ok = result["ok"]
+            cpu = {"value": float(np.mean(result["secs"])), "unit": "s/iter", "cores": os.cpu_count() or 1, "kind": "port",
+                   "sample": "the %d HOOI iterations of %s from the start factors (NumPy/OpenBLAS oracle port) on "
+                             "rank 0's host, mean per iteration" % (iters, cfg.name),
+                   "phases_s": result["phases"], "parity_per_iteration": result["rows"], "parity_ok": parity_ok}
+        else:
+            for _ in range(iters):
+                grid_step()
+        verdict = torch.tensor([1 if parity_ok else 0], dtype=torch.int64, device=stat_device)
+        dist.broadcast(verdict, src=0)          # every rank exits with rank 0's verdict
+        parity_ok = bool(verdict.item())
 
     if rank == 0:
         # per-TTM roofline on P GPUs (SURVEY §8d): flops / P, local bytes 8 (|In| + q_n |Out|) / P, plus the
@@ -1017,19 +1103,23 @@ def run_bench_rank(args, rank: int, world: int, local_rank: int):
         dom = max(rows, key=lambda r: r["ms"])
         dom_flops = 2 * spec.K[dom["mode"]] * cost.card_in[dom["node"]]
         achieved = dom_flops / (dom["ms"] * 1e-3) / 1e12 if dom["ms"] else None
+        volume = (P.scheme_volume(tree, spec, scheme, world).total if scheme
+                  else P.static_volume(tree, spec, q, world).total)
         line = {
             "metric": "hooi_s_per_iter", "value": ms_per_step * 1e-3, "unit": "s/iter", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": cfg.name, "iterations": cfg.iterations, "schedule": "jacobi on optimal_tree",
-                       "timed_steps": "iterations W+1..W+K of one HOOI run from the random orthonormal start",
+            "config": B.shared_config(cfg.name, cfg.iterations, tree.label(), world, q, volume if world > 1 else 0,
+                                      "x".join(map(str, compare_q)) if compare_q else None),
+            "engine": {"timed_steps": "iterations W+1..W+K of one HOOI run from the random orthonormal start",
                        "core": "chain along a tree path, partial products carried into the next sweep",
-                       "tree": tree.label(), "grid": list(q),
                        "node_grids": {str(k): list(v) for k, v in scheme.node_grids.items()} if scheme else None,
-                       "grid_volume_elements": (P.scheme_volume(tree, spec, scheme, world).total if scheme
-                                                else P.static_volume(tree, spec, q, world).total),
                        "l2": "inputs_larger_than_L2", "noise": "slab-parallel" if cfg.slab_noise else "sequential",
-                       "evd": "replicated on every rank"},
+                       "evd": "each leaf solved by its owner rank (leaves round-robin in walk order) on a side stream, "
+                              "factor + status broadcast" if world > 1 else "solved on a side stream",
+                       "reduce_scatter": "peer-slot stores from the TTM epilogue" if peer_slots else
+                                         "destination-major partial product + grouped send/recv + ordered sum",
+                       "backend": "cuda + nccl" if cuda else "numpy-test + gloo (contract test, not a measurement)"},
             "ttm_tree": {"tflops": flops_total / (ttm_ms * 1e-3) / 1e12 if ttm_ms else None,
                          "roofline_frac": t_roof * 1e3 / ttm_ms if ttm_ms else None, "measured_ms": ttm_ms,
                          "roofline_ms": t_roof * 1e3, "flops": flops_total, "p_fp64_tflops": p_fp64,
@@ -1037,16 +1127,21 @@ def run_bench_rank(args, rank: int, world: int, local_rank: int):
                          "nvlink_gbs": B.NVLINK_GBS, "per_node": rows,
                          "note": "per-node time = (regrid +) local kernel + chunk exchange + ordered reduction, max over ranks"},
             "phases_ms": {"tree_phase_incl_leaves": tree_phase_ms, "core_ms": core_ms},
+            "grid_comparison": comparison,
             "relative_fit": fit, "core_norm": core_norm, "build_s": build_s,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": p_fp64 * world, "unit": "TFLOP/s",
                          "frac": achieved / (p_fp64 * world) if achieved else None, "traffic": None,
                          "kernel": "ttm_dmma_kernel (tree node %d, mode %d) across %d GPUs" % (dom["node"], dom["mode"] + 1, world),
                          "peak_source": fp64_src},
-            "cpu_baseline": None, "e2e": e2e, "gpu_launches": int(k1 - k0), "library_calls": int(lib_calls),
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(k1 - k0), "library_calls": int(lib_calls),
             "clocks": clocks, "degenerate": bool(res.degenerate),
             "volume_sent_rank0": {str(k): v for k, v in res.volume_sent.items()},
             "regrid_sent_rank0": {str(k): v for k, v in res.regrid_sent.items()},
         }
         print(json.dumps(line))
+    dist.barrier()
     dist.destroy_process_group()
+    if not parity_ok:
+        print("bench.py: parity against the oracle FAILED, see cpu_baseline.parity_per_iteration", file=sys.stderr)
+        return 3
     return 0

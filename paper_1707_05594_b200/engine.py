@@ -65,9 +65,17 @@ def _colmajor(a: np.ndarray) -> np.ndarray:
 class Context:
     """One CUDA device + stream + cuSOLVER handle (tp_ctx)."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, flags: int = 0):
         self._h = ctypes.c_void_p()
-        check(lib.tp_ctx_create(device, ctypes.byref(self._h)))
+        check(lib.tp_ctx_create_ex(device, ctypes.c_uint(flags), ctypes.byref(self._h)))
+
+    def set_option(self, option: int, value: int):
+        """tp_ctx_set_option: 1 = streamed-upload threshold in bytes, 2 = trace the eigen-solve certificates."""
+        check(lib.tp_ctx_set_option(self._h, int(option), ctypes.c_longlong(int(value))))
+
+    def release_cache(self):
+        """Frees what by-value hooi_sweep calls keep on the device between calls."""
+        check(lib.tp_ctx_release_cache(self._h))
 
     def close(self):
         if self._h:
@@ -222,6 +230,14 @@ class HooiPlan:
         """Keep the core chain's partial products (they are next sweep's tree nodes along one path) between sweeps."""
         check(lib.tp_plan_set_option(self.ctx._h, self._h, 3, 1 if on else 0))
 
+    def set_option(self, option: int, value: int):
+        """tp_plan_set_option: 4/5 spare SMs, 6 whole-sweep graph (0 off, 1 on, 2 auto), 7 leaf graph, 8 one-launch
+        leaf solve."""
+        check(lib.tp_plan_set_option(self.ctx._h, self._h, int(option), int(value)))
+
+    def set_sweep_graph(self, mode: int):
+        self.set_option(6, mode)
+
     def evd_info(self):
         """(leaves eligible for the fast eigen-solve, leaves the last sweep redid with the full solve)."""
         a, b = ctypes.c_int(), ctypes.c_int()
@@ -338,8 +354,11 @@ def _check_engine_shapes(t: np.ndarray, s: ProblemSpec):
 
 
 def hooi_sweep(t: np.ndarray, s: ProblemSpec, d: Decomposition, tree: TtmTree, kind="jacobi",
-               stats: Optional[SweepStats] = None, ctx: Optional[Context] = None) -> Decomposition:
-    """hooi_sweep(t, s, d, tree, kind, stats*) — hooi.hpp:189-229, by value through tp_hooi_sweep_host."""
+               stats: Optional[SweepStats] = None, ctx: Optional[Context] = None,
+               tensor_unchanged: bool = False) -> Decomposition:
+    """hooi_sweep(t, s, d, tree, kind, stats*) — hooi.hpp:189-229, by value through tp_hooi_sweep_host_ex.
+    tensor_unchanged: the caller's promise that `t` (same buffer) is what the previous call uploaded; the device
+    copy is then reused (TP_HOST_TENSOR_UNCHANGED)."""
     ctx = ctx or default_context()
     t = _f64(t)
     _check_engine_shapes(t, s)
@@ -356,10 +375,11 @@ def hooi_sweep(t: np.ndarray, s: ProblemSpec, d: Decomposition, tree: TtmTree, k
     st = _SweepStatsC()
     nn, kind_a, mode_a, parent_a = tree._c()
     n = s.n_modes()
-    check(lib.tp_hooi_sweep_host(ctx._h, n, size_array(t.shape), t.ctypes.data_as(dbl_p), u64_array(s.K),
-                                 (dbl_p * n)(*[a.ctypes.data_as(dbl_p) for a in fin]), nn, kind_a, mode_a, parent_a,
-                                 _KINDS[kind], (dbl_p * n)(*[a.ctypes.data_as(dbl_p) for a in fout]),
-                                 core.ctypes.data_as(dbl_p), ctypes.byref(st)))
+    check(lib.tp_hooi_sweep_host_ex(ctx._h, n, size_array(t.shape), t.ctypes.data_as(dbl_p), u64_array(s.K),
+                                    (dbl_p * n)(*[a.ctypes.data_as(dbl_p) for a in fin]), nn, kind_a, mode_a,
+                                    parent_a, _KINDS[kind], ctypes.c_uint(1 if tensor_unchanged else 0),
+                                    (dbl_p * n)(*[a.ctypes.data_as(dbl_p) for a in fout]),
+                                    core.ctypes.data_as(dbl_p), ctypes.byref(st)))
     if stats is not None:
         stats.tree_macs, stats.core_macs = st.tree_macs, st.core_macs
         stats.peak_live, stats.degenerate = st.peak_live, bool(st.degenerate)

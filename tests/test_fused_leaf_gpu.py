@@ -1,0 +1,202 @@
+"""The one-launch certified top-k leaf solve (csrc/leaf_solve_kernels.cu) through tp_dev_leaf_solve_fused, against
+NumPy's full symmetric eigen-solve — the reference's SelfAdjointEigenSolver route (hooi.hpp:55-69) — on the leaf
+shapes of BASELINE configs 1-4 and on spectra chosen to make the certificate reject."""
+import ctypes
+
+import numpy as np
+import pytest
+
+from paper_1707_05594_b200 import Errc, TuckerplanError
+from paper_1707_05594_b200._lib import check, lib
+
+pytestmark = pytest.mark.gpu
+OVERSAMPLE = 8
+
+
+@pytest.fixture(scope="module")
+def dev():
+    import torch
+    from paper_1707_05594_b200 import engine as E
+    ctx = E.Context(0)
+
+    class Dev:
+        def __init__(self):
+            self.ctx, self.torch = ctx, torch
+
+        def up(self, a):
+            t = torch.from_numpy(np.ascontiguousarray(a)).to("cuda:0")
+            torch.cuda.synchronize()
+            return t
+
+        def ptr(self, t, ctype=ctypes.c_double):
+            return ctypes.cast(t.data_ptr(), ctypes.POINTER(ctype))
+
+        def down(self, t):
+            ctx.synchronize()
+            return t.cpu().numpy()
+
+    yield Dev()
+    ctx.close()
+
+
+def gram_with_spectrum(rng, rows, lam):
+    q, _ = np.linalg.qr(rng.standard_normal((rows, rows)))
+    g = (q * lam) @ q.T
+    return (g + g.T) / 2
+
+
+def low_rank_plus_noise_gram(rng, rows, k, cols, sigma):
+    y = rng.standard_normal((rows, k)) @ rng.standard_normal((k, cols)) + sigma * rng.standard_normal((rows, cols))
+    return y @ y.T
+
+
+def reference_basis(g, k):
+    """hooi.hpp:55-74: k largest eigenvectors, largest-|entry| (first on ties) positive, gap flag."""
+    w, v = np.linalg.eigh(g)
+    vec = v[:, ::-1][:, :k].copy()
+    for j in range(k):
+        i = int(np.argmax(np.abs(vec[:, j])))
+        if vec[i, j] < 0:
+            vec[:, j] = -vec[:, j]
+    lam = w[::-1]
+    deg = k < len(lam) and (lam[k - 1] - lam[k]) <= 1e-10 * max(lam[0], 1e-300)
+    return vec, lam, deg
+
+
+def sin_angle(a, b):
+    r = b - a @ (a.T @ b)
+    return float(np.linalg.svd(r, compute_uv=False).max())
+
+
+def solve(dev, g, k, start, start_is_ritz=False):
+    rows = g.shape[0]
+    b = k + OVERSAMPLE
+    d_g = dev.up(np.asfortranarray(g).ravel(order="F"))
+    d_start = dev.up(np.asfortranarray(start).ravel(order="F"))
+    d_ritz = dev.up(np.full(rows * b, np.nan))
+    d_theta = dev.up(np.full(b, np.nan))
+    d_factor = dev.up(np.full(rows * k, np.nan))
+    d_int = dev.up(np.zeros(8, dtype=np.int32))
+    d_diag = dev.up(np.zeros(4))
+    ip = dev.ptr(d_int, ctypes.c_int)
+    check(lib.tp_dev_leaf_solve_fused(dev.ctx._h, dev.ptr(d_g), ctypes.c_size_t(rows), k, dev.ptr(d_start),
+                                      1 if start_is_ritz else 0, dev.ptr(d_ritz), dev.ptr(d_theta), dev.ptr(d_factor),
+                                      ip, ctypes.cast(ctypes.addressof(ip.contents) + 16, ctypes.POINTER(ctypes.c_int)),
+                                      dev.ptr(d_diag)))
+    ints = dev.down(d_int)
+    return dict(ritz=dev.down(d_ritz).reshape(rows, b, order="F"), theta=dev.down(d_theta),
+                factor=dev.down(d_factor).reshape(rows, k, order="F"), flag=int(ints[0]), verdict=ints[4:8].tolist(),
+                diag=dev.down(d_diag).tolist())
+
+
+# (rows, k, unfolding columns, sigma): the leaves of C1, C2, C3 (three of its four), C4, and odd sizes
+LEAVES = [(200, 20, 400, 1e-3), (96, 10, 1000, 1e-3), (100, 10, 4000, 1e-2), (100, 20, 2000, 1e-2),
+          (50, 5, 8000, 1e-2), (48, 8, 4096, 1e-3), (57, 3, 300, 1e-3), (131, 17, 500, 1e-2), (256, 40, 700, 1e-3),
+          (19, 1, 64, 1e-3)]
+
+
+@pytest.mark.parametrize("rows,k,cols,sigma", LEAVES)
+def test_cold_start_matches_full_eigensolve(dev, rows, k, cols, sigma):
+    rng = np.random.default_rng(rows * 1000 + k)
+    g = low_rank_plus_noise_gram(rng, rows, k, cols, sigma)
+    start, _ = np.linalg.qr(rng.standard_normal((rows, k)))
+    out = solve(dev, g, k, start)
+    assert out["verdict"][0] == 0 and out["verdict"][1] == 0, out
+    ref, lam, deg = reference_basis(g, k)
+    assert out["flag"] == int(deg) == 0
+    assert sin_angle(ref, out["factor"]) < 1e-10
+    # eigenvalues well separated here: the vectors themselves agree, with the reference's signs
+    assert np.max(np.abs(out["factor"] - ref)) < 1e-8
+    assert np.allclose(out["theta"][::-1][:k], lam[:k], rtol=1e-12, atol=0)
+    q = out["factor"]
+    assert np.max(np.abs(q.T @ q - np.eye(k))) < 1e-13
+    # warm restart from the Ritz vectors on a slightly different matrix: one round
+    g2 = g + 1e-6 * low_rank_plus_noise_gram(rng, rows, k, cols, sigma)
+    out2 = solve(dev, g2, k, out["ritz"], start_is_ritz=True)
+    assert out2["verdict"][0] == 0 and out2["verdict"][1] == 0, out2
+    assert out2["diag"][3] == 1.0 and out2["verdict"][3] == 1, out2      # one round, one power step
+    ref2, _, _ = reference_basis(g2, k)
+    assert sin_angle(ref2, out2["factor"]) < 1e-10
+
+
+def test_sign_rule_and_determinism(dev):
+    rng = np.random.default_rng(11)
+    g = low_rank_plus_noise_gram(rng, 96, 10, 1000, 1e-3)
+    start, _ = np.linalg.qr(rng.standard_normal((96, 10)))
+    a, b = solve(dev, g, 10, start), solve(dev, g, 10, start)
+    assert np.array_equal(a["factor"], b["factor"]) and np.array_equal(a["ritz"], b["ritz"])
+    for j in range(10):
+        col = a["factor"][:, j]
+        assert col[int(np.argmax(np.abs(col)))] > 0
+    # flipping the sign of the data (G unchanged) or of the start block leaves the result unchanged
+    c = solve(dev, g, 10, -start)
+    assert sin_angle(a["factor"], c["factor"]) < 1e-12
+    assert np.max(np.abs(a["factor"] - c["factor"])) < 1e-9
+
+
+def test_small_gap_is_sent_to_the_full_solve(dev):
+    """Relative gap 1e-6 between lambda_k and lambda_{k+1}: eigenpairs converge, but the subspace angle cannot be
+    certified to 1e-10, so the certificate must refuse (bit 4) and leave the decision to the full eigen-solve."""
+    rng = np.random.default_rng(3)
+    rows, k = 120, 6
+    lam = np.concatenate([np.array([10.0, 9.0, 8.0, 7.0, 6.0, 5.0, 5.0 * (1 - 1e-6)]), np.full(rows - 7, 1e-3)])
+    g = gram_with_spectrum(rng, rows, lam)
+    start, _ = np.linalg.qr(rng.standard_normal((rows, k)))
+    out = solve(dev, g, k, start)
+    assert out["verdict"][1] == 0
+    assert out["verdict"][0] & 4, out
+
+
+def test_heavy_tail_cannot_certify_leading_pairs(dev):
+    """A flat spectrum: the trace bound on what the block may have missed exceeds theta_k, so nothing is certified."""
+    rng = np.random.default_rng(4)
+    rows, k = 100, 5
+    lam = np.linspace(2.0, 1.0, rows)
+    g = gram_with_spectrum(rng, rows, lam)
+    start, _ = np.linalg.qr(rng.standard_normal((rows, k)))
+    out = solve(dev, g, k, start)
+    assert out["verdict"][0] != 0 or out["verdict"][1] != 0
+
+
+def test_start_orthogonal_to_a_leading_eigenvector_is_caught(dev):
+    """The start block AND its filler columns are orthogonal to the dominant eigenvector, which power iteration then
+    never sees in exact arithmetic: residuals of the pairs it does find are tiny, only the trace bound can object.
+    (In floating point the missing direction may creep in through rounding; either outcome is sound, a certified
+    result must then contain it.)"""
+    rng = np.random.default_rng(5)
+    rows, k = 64, 4
+    q, _ = np.linalg.qr(rng.standard_normal((rows, rows)))
+    lam = np.concatenate([np.array([100.0, 50.0, 40.0, 30.0, 20.0]), np.full(rows - 5, 1e-6)])
+    g = (q * lam) @ q.T
+    g = (g + g.T) / 2
+    ritz_start = np.zeros((rows, k + OVERSAMPLE))
+    # ascending Ritz layout: dominant direction last; use eigenvectors 1.. (skipping 0, the largest)
+    ritz_start[:, ::-1] = q[:, 1:1 + k + OVERSAMPLE]
+    out = solve(dev, g, k, ritz_start, start_is_ritz=True)
+    ref, _, _ = reference_basis(g, k)
+    if out["verdict"][0] == 0 and out["verdict"][1] == 0:
+        assert sin_angle(ref, out["factor"]) < 1e-9
+    else:
+        assert out["verdict"][0] & 4
+
+
+def test_degenerate_gap_flag(dev):
+    rng = np.random.default_rng(6)
+    rows, k = 40, 2
+    lam = np.concatenate([np.array([2.0, 1.0, 1.0]), np.full(rows - 3, 1e-4)])
+    g = gram_with_spectrum(rng, rows, lam)
+    start, _ = np.linalg.qr(rng.standard_normal((rows, k)))
+    out = solve(dev, g, k, start)
+    # lambda_2 == lambda_3: either the flag is raised or the certificate refuses; a certified non-degenerate claim
+    # would be wrong
+    assert out["flag"] == 1 or out["verdict"][0] != 0
+
+
+def test_too_large_leaf_is_refused(dev):
+    g = dev.up(np.eye(600).ravel())
+    f = dev.up(np.zeros(600 * 20))
+    with pytest.raises(TuckerplanError) as err:
+        check(lib.tp_dev_leaf_solve_fused(dev.ctx._h, dev.ptr(g), ctypes.c_size_t(600), 20, dev.ptr(f), 0, dev.ptr(f),
+                                          dev.ptr(f), dev.ptr(f), dev.ptr(f, ctypes.c_int), dev.ptr(f, ctypes.c_int),
+                                          dev.ptr(f)))
+    assert err.value.code == Errc.bad_argument
