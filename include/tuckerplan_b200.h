@@ -276,6 +276,9 @@ int tp_plan_set_option(tp_ctx* ctx, tp_plan* plan, int option, int value);
  * the factors are the reference's (hooi.hpp:55-69) to rounding either way.  tp_plan_last_evd_info: leaves eligible for the fast path, and how many of them the last sweep had to
  * redo with the full solve. */
 int tp_plan_last_evd_info(tp_ctx* ctx, tp_plan* plan, int* fast_eligible, int* rejected);
+/* whether the last tp_plan_sweep was a replay of the recorded whole-sweep graph (TP_OPT_SWEEP_GRAPH), and how many of
+ * the plan's leaves take the one-launch solve (TP_OPT_FUSED_LEAF_SOLVE) */
+int tp_plan_last_sweep_info(tp_ctx* ctx, tp_plan* plan, int* replayed_graph, int* one_launch_leaves);
 /* Decomposition::factors (hooi.hpp:78-81) <-> device: factors[n] is L_n x K_n column-major on the host */
 int tp_plan_set_factors(tp_ctx* ctx, tp_plan* plan, const double* const* factors);
 int tp_plan_get_factors(tp_ctx* ctx, tp_plan* plan, double* const* factors_out);
@@ -352,8 +355,9 @@ int tp_dev_leaf_solve_finish(tp_ctx* ctx, int lane, double* factor, int* flag, i
  * rows x k column-major factor (start_is_ritz = 0) or the rows x (k + 8) ascending Ritz vectors a previous call left in
  * `ritz` (start_is_ritz = 1; may alias `ritz`).  Out: ritz rows x (k + 8), theta k + 8 (ascending), factor rows x k,
  * *flag |= degenerate, verdict[4] (verdict[0] == 0 && verdict[1] == 0: certified; [2] Jacobi sweeps, [3] power steps),
- * diag[4] (worst residual / bound, angle bound, tail bound / theta_k, rounds).  TP_ERR_BAD_ARGUMENT if the leaf is
- * too large for this path. */
+ * diag[16] ([0..3] worst residual / bound, angle bound, tail bound / theta_k, rounds; [4..11] SM cycles spent in the
+ * kernel's phases: start block, G Q products, small Gram products, Cholesky, triangular solves, Jacobi, Ritz vectors +
+ * residuals, certificate).  TP_ERR_BAD_ARGUMENT if the leaf is too large for this path. */
 int tp_dev_leaf_solve_fused(tp_ctx* ctx, const double* gram, size_t rows, int k, const double* start,
                             int start_is_ritz, double* ritz, double* theta, double* factor, int* flag, int* verdict,
                             double* diag);

@@ -274,6 +274,8 @@ struct LeafScratch {
   // them the Rayleigh-Ritz matrix starts out nearly diagonal and the Jacobi solver needs few sweeps.
   const double* last_ritz = nullptr;
   int graph_state = 0;         // 0: not run yet (first run is eager), 1: eager run done, 2: graph ready, -1: disabled
+  int graph_aux = -2;          // side stream (cuBLAS handle and workspace with it) the graph belongs to: a replay
+                               // anywhere else could share that workspace with another leaf's concurrent solve
   long long fast_rows = 0;     // rows the iteration buffers were sized for (tp_dev_leaf_solve_warm only)
   int failures = 0;            // consecutive warm sweeps in which the fast path was rejected
   bool refinable = false;      // last rejection was a missed residual bound only (no failed factorisation / gap)
@@ -420,8 +422,8 @@ void subspace_reserve(tp_ctx* ctx, LeafScratch& s, long long rows, int k) {
   s.small_work = device_alloc(static_cast<size_t>(s.small_lwork));
   TPB_CUDA(cudaMalloc(&s.verdict, 4 * sizeof(int)));
   TPB_CUDA(cudaMemset(s.verdict, 0, 4 * sizeof(int)));
-  s.diag = device_alloc(4);
-  TPB_CUDA(cudaMemset(s.diag, 0, 4 * sizeof(double)));
+  s.diag = device_alloc(16);
+  TPB_CUDA(cudaMemset(s.diag, 0, 16 * sizeof(double)));
   s.block = b;
 }
 
@@ -491,8 +493,10 @@ const double* subspace_body(tp_ctx* ctx, const SubspaceIo& io, LeafScratch& s, c
 }
 
 // Enqueues the whole fast solve on the leaf's stream; the verdict is read by the caller at the end of the sweep.
+// `recording`: the caller is recording the whole sweep into a CUDA graph; the iteration's launches then go straight
+// into that recording instead of through the leaf's own graph.
 void leaf_solve_subspace(tp_ctx* ctx, LeafScratch& s, const double* gram, long long rows_ll, int k,
-                         const double* start, double* factor_out, int aux) {
+                         const double* start, double* factor_out, int aux, bool recording = false) {
   SubspaceIo io;
   io.solver = aux < 0 ? ctx->solver : ctx->aux_solver[aux];
   io.blas = aux < 0 ? ctx->blas : ctx->aux_blas[aux];
@@ -512,9 +516,9 @@ void leaf_solve_subspace(tp_ctx* ctx, LeafScratch& s, const double* gram, long l
     s.last_ritz = s.x;
     return;
   }
-  const bool graphs_off = !s.use_graph;
+  const bool graphs_off = !s.use_graph || recording;
   const bool key_ok = s.graph_gram == gram && s.graph_rows == rows_ll && s.graph_k == k;
-  if (!key_ok) {  // the slot is being reused for another problem: start over
+  if (!key_ok && !recording) {  // the slot is being reused for another problem: start over
     if (s.graph) cudaGraphExecDestroy(s.graph);
     s.graph = nullptr;
     if (s.graph_state > 0) s.graph_state = 0;
@@ -532,7 +536,7 @@ void leaf_solve_subspace(tp_ctx* ctx, LeafScratch& s, const double* gram, long l
     ctx->own_kernels += 1;
   }
   const double* ritz_vectors = nullptr;
-  if (io.own_small && !graphs_off && s.graph_state == 1) {
+  if (io.own_small && !graphs_off && s.graph_state == 1 && aux == s.graph_aux) {
     // second run on the same buffers: record the sequence.  Lazy initialisation (kernel attributes, cuBLAS
     // heuristics) happened during the eager first run.
     const unsigned long long own0 = ctx->own_kernels, lib0 = ctx->library_calls;
@@ -559,7 +563,7 @@ void leaf_solve_subspace(tp_ctx* ctx, LeafScratch& s, const double* gram, long l
     ctx->own_kernels = own0;
     ctx->library_calls = lib0;
   }
-  if (s.graph_state == 2) {
+  if (s.graph_state == 2 && !recording && aux == s.graph_aux) {
     ritz_vectors = s.graph_result;
     TPB_CUDA(cudaGraphLaunch(s.graph, io.stream));
     // same work as the eager body, for the launch accounting
@@ -569,6 +573,7 @@ void leaf_solve_subspace(tp_ctx* ctx, LeafScratch& s, const double* gram, long l
     ritz_vectors = subspace_body(ctx, io, s, gram, rows, k);
     if (io.own_small && !graphs_off && s.graph_state == 0) {
       s.graph_state = 1;
+      s.graph_aux = aux;
       s.graph_gram = gram;
       s.graph_rows = rows_ll;
       s.graph_k = k;
@@ -689,6 +694,7 @@ struct tp_plan {
   const double* sweep_graph_tensor = nullptr;
   tp_u64 sweep_graph_stamp = 0;
   std::vector<char> sweep_graph_fast;         // per mode: the leaf's solve inside the graph is a certified fast solve
+  bool last_sweep_replayed = false;
   bool capturing = false;                     // the launch sequence is being recorded, not run: no timing events
   u64 sweep_graph_kernels = 0, sweep_graph_library_calls = 0;  // launches of one steady-state sweep (accounting)
   int warm_sweeps = 0;                        // sweeps since the caller last set the factors
@@ -791,7 +797,7 @@ void plan_leaf_solve(tp_ctx* ctx, tp_plan* p, int mode, int node, double* dst, b
       subspace_eligible(rows, k, plan_leaf_columns(p, mode))) {
     subspace_reserve(ctx, slot, rows, k);
     slot.was_cold = cold;
-    leaf_solve_subspace(ctx, slot, slot.gram, rows, k, p->cur[mode], dst, aux);
+    leaf_solve_subspace(ctx, slot, slot.gram, rows, k, p->cur[mode], dst, aux, p->capturing);
   } else {
     leaf_solve(ctx, slot, rows, k, dst, aux);
   }
@@ -862,7 +868,9 @@ std::vector<int> evaluate_fast_leaves(tp_ctx* ctx, tp_plan* p) {
     if (bad) {
       rejected.push_back(m);
       // only the residual bound missed: the block is sound and simply has not converged yet -> worth iterating on
-      s.refinable = (host[0] & 1) != 0 && host[1] == 0 && host[4] == 0;
+      // (not when the tail bound already exceeds theta_k -- a flat spectrum, e.g. a start from random factors -- no
+      // amount of iterating certifies that)
+      s.refinable = (host[0] & 1) != 0 && host[1] == 0 && host[4] == 0 && p->host_diag[4 * m + 2] < 0.5;
       if (!s.refinable) s.last_ritz = nullptr;
       TPB_CUDA(cudaMemsetAsync(s.flag, 0, sizeof(int), ctx->stream));
     } else {
@@ -1959,7 +1967,10 @@ int tp_plan_sweep(tp_ctx* ctx, tp_plan* p, const tp_tensor* t, tp_sweep_stats* s
             p->sweep_graph_fast.assign(p->n, 0);
             for (int m = 0; m < p->n; ++m) p->sweep_graph_fast[m] = p->leaf[m].fast_used ? 1 : 0;
           } else {
-            cudaGetLastError();  // recording is an optimisation: this plan carries on with plain launches
+            const cudaError_t why = cudaGetLastError();  // recording is an optimisation: carry on with plain launches
+            if (ctx->trace_evd)
+              std::fprintf(stderr, "[tpb graph] recording the sweep failed (%s); plain launches from here on\n",
+                           cudaGetErrorString(why));
             p->sweep_graph = nullptr;
             p->sweep_graph_mode = 0;
             for (int a = 0; a < tp_ctx::kAux; ++a) cudaStreamSynchronize(ctx->aux[a]);
@@ -2006,6 +2017,7 @@ int tp_plan_sweep(tp_ctx* ctx, tp_plan* p, const tp_tensor* t, tp_sweep_stats* s
       }
       p->factors_from_caller = false;
       ++p->warm_sweeps;
+      p->last_sweep_replayed = replayed;
       plan_mark_carried(p, t);
       if (replayed) {
         TPB_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -2120,6 +2132,24 @@ int tp_plan_last_evd_info(tp_ctx* ctx, tp_plan* p, int* fast_eligible, int* reje
         ++eligible;
     if (fast_eligible) *fast_eligible = eligible;
     if (rejected) *rejected = p->fast_rejected;
+  });
+}
+
+int tp_plan_last_sweep_info(tp_ctx* ctx, tp_plan* p, int* replayed_graph, int* one_launch_leaves) {
+  return guarded([&] {
+    (void)ctx;
+    if (!p) raise(TP_ERR_BAD_ARGUMENT, "null plan");
+    if (replayed_graph) *replayed_graph = p->last_sweep_replayed ? 1 : 0;
+    int fused = 0;
+    for (int m = 0; m < p->n; ++m) {
+      const LeafScratch& s = p->leaf[m];
+      const long long rows = static_cast<long long>(p->spec.L[m]);
+      const int k = static_cast<int>(p->spec.K[m]);
+      if (p->fast_evd && s.use_fused && s.failures < 2 && subspace_eligible(rows, k, plan_leaf_columns(p, m)) &&
+          leaf_solve_fused_eligible(rows, k, k + kSubspaceOversample))
+        ++fused;
+    }
+    if (one_launch_leaves) *one_launch_leaves = fused;
   });
 }
 

@@ -238,6 +238,12 @@ class HooiPlan:
     def set_sweep_graph(self, mode: int):
         self.set_option(6, mode)
 
+    def sweep_info(self):
+        """(last sweep replayed the whole-sweep graph?, leaves on the one-launch solve)."""
+        a, b = ctypes.c_int(), ctypes.c_int()
+        check(lib.tp_plan_last_sweep_info(self.ctx._h, self._h, ctypes.byref(a), ctypes.byref(b)))
+        return bool(a.value), b.value
+
     def evd_info(self):
         """(leaves eligible for the fast eigen-solve, leaves the last sweep redid with the full solve)."""
         a, b = ctypes.c_int(), ctypes.c_int()

@@ -317,6 +317,7 @@ def test_fast_eigensolve_is_certified_and_matches(ctx):
     plan.set_factors(f0)
     of = [f.copy() for f in f0]
     rejected = []
+    ctx.set_option(2, 1)                          # certificate margins on stderr (shown if the test fails)
     for _ in range(cfg.iterations):
         st = plan.sweep(dt)
         ocore, of = ho.hooi_sweep(t, spec.L, spec.K, of, otree(tree), "jacobi")
@@ -329,6 +330,7 @@ def test_fast_eigensolve_is_certified_and_matches(ctx):
         # individual vectors too (same sign rule), not just the subspace
         for a, b in zip(plan.get_factors(), of):
             assert np.max(np.abs(a - b)) < 1e-7
+    ctx.set_option(2, 0)
     assert eligible == 3
     assert rejected[-1] == 0                      # warm-started sweeps are served by the fast path
     # the same sweeps with the fast path off give the same factors to rounding
@@ -660,7 +662,7 @@ def test_config5_full_size_against_oracle(ctx):
 
 
 @pytest.mark.parametrize("cfg", [W.CONFIGS[1], W.scaled_config(2, [40, 36, 32, 28], [6, 5, 4, 3], 8),
-                                 W.scaled_config(3, [120, 40, 30, 20], [20, 5, 6, 3], 8)], ids=lambda c: c.name)
+                                 W.scaled_config(3, [240, 60, 60, 40], [30, 5, 10, 3], 8)], ids=lambda c: c.name)
 def test_whole_sweep_graph_is_bit_identical(ctx, cfg):
     """TP_OPT_SWEEP_GRAPH: the steady-state sweep replayed as one CUDA graph launches the same kernels with the same
     arguments as the eager sweep, so factors and core must agree bit for bit, sweep by sweep; and both match the
@@ -681,6 +683,8 @@ def test_whole_sweep_graph_is_bit_identical(ctx, cfg):
             st = plan.sweep(dt)
             trail.append((plan.get_factors(), plan.get_core(), st))
         results[mode] = trail
+        replayed, one_launch = plan.sweep_info()
+        assert replayed == (mode == 1)          # every leaf of these cases is eligible for a capturable fast solve
         if mode == 1:
             # the replayed sweeps report only their total device time
             tm = plan.last_timing()
