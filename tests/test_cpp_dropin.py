@@ -54,4 +54,4 @@ def test_serialize_checks_through_cpp_headers():
     assert p.returncode == 0, out
     assert [l for l in out.splitlines() if l.startswith("ok ")] == [
         "ok spec", "ok tree labels", "ok tree round trip", "ok tree labels rejected", "ok grid", "ok scheme",
-        "ok reports", "ok tensor files", "ok json"]
+        "ok reports", "ok traced counts", "ok tensor files", "ok json"]
