@@ -192,4 +192,92 @@ class DeviceHooi {
   tp_plan* plan_ = nullptr;
 };
 
+// Jacobi sweeps on a Cartesian processor grid: rank p of `scheme` (row-major block order, simulate.hpp:69-73) runs on
+// CUDA device devices[p] of this box; the same device may be named several times.  A static grid is
+// uniform_scheme(tree, grid) (simulate.hpp:50-57); optimal_dynamic_scheme(...).scheme gives per-node grids with
+// regrids.  What the reference only simulates (simulate_distribution) is executed here; last_volumes() returns the
+// elements actually shipped per node, to be compared with the ledger's model columns.
+class GridHooi {
+ public:
+  GridHooi(const DenseTensor& t, const ProblemSpec& s, const TtmTree& tree, const DynamicGridScheme& scheme,
+           const std::vector<int>& devices, bool use_nccl = false)
+      : spec_(s), n_nodes_(static_cast<int>(tree.nodes.size())) {
+    detail::check_engine_shapes(t, s);
+    validate_tree(tree, s);
+    const detail::FlatTree f = detail::flatten(tree);
+    std::vector<u64> node_grids(static_cast<std::size_t>(f.size()) * s.n_modes(), 0);
+    for (int id = 0; id < f.size(); ++id) {
+      if (!tree.is_internal(id)) continue;
+      const auto it = scheme.node_grids.find(id);
+      if (it == scheme.node_grids.end()) fail(Errc::missing_assignment, "scheme has no grid for node " + std::to_string(id));
+      if (it->second.n_modes() != s.n_modes()) fail(Errc::invalid_grid, "grid and spec mode counts differ");
+      std::copy(it->second.q.begin(), it->second.q.end(), node_grids.begin() + static_cast<std::size_t>(id) * s.n_modes());
+    }
+    if (scheme.root.n_modes() != s.n_modes()) fail(Errc::invalid_grid, "grid and spec mode counts differ");
+    detail::check(tp_grid_create(static_cast<int>(devices.size()), devices.data(), s.n_modes(), s.L.data(), s.K.data(),
+                                 f.size(), f.kind.data(), f.mode.data(), f.parent.data(), scheme.root.q.data(),
+                                 node_grids.data(), use_nccl ? static_cast<unsigned>(TP_GRID_NCCL) : 0u, &grid_));
+    const int status = tp_grid_set_tensor(grid_, t.data.data());
+    if (status != TP_OK) {
+      tp_grid_destroy(grid_);
+      grid_ = nullptr;
+      detail::check(status);
+    }
+  }
+  ~GridHooi() { if (grid_) tp_grid_destroy(grid_); }
+  GridHooi(const GridHooi&) = delete;
+  GridHooi& operator=(const GridHooi&) = delete;
+
+  void set_factors(const std::vector<Matrix>& factors) {
+    if (factors.size() != static_cast<std::size_t>(spec_.n_modes()))
+      fail(Errc::shape_mismatch, "factor count differs from mode count");
+    std::vector<const double*> ptrs;
+    for (const Matrix& f : factors) ptrs.push_back(f.data());
+    detail::check(tp_grid_set_factors(grid_, ptrs.data()));
+  }
+  SweepStats sweep() {
+    tp_sweep_stats st{};
+    detail::check(tp_grid_sweep(grid_, &st));
+    return SweepStats{st.tree_macs, st.core_macs, st.peak_live, st.degenerate != 0};
+  }
+  Decomposition decomposition() {
+    Decomposition d;
+    std::vector<std::size_t> core_dims;
+    std::vector<double*> ptrs;
+    for (int n = 0; n < spec_.n_modes(); ++n) {
+      d.factors.emplace_back(spec_.L[n], spec_.K[n]);
+      core_dims.push_back(spec_.K[n]);
+    }
+    for (Matrix& f : d.factors) ptrs.push_back(f.data());
+    detail::check(tp_grid_get_factors(grid_, ptrs.data()));
+    d.core = zeros(core_dims);
+    detail::check(tp_grid_get_core(grid_, d.core.data.data()));
+    return d;
+  }
+  // sqrt(||T||^2 - ||G||^2) / ||T||: the relative error of a decomposition with orthonormal factors and their core
+  double fit_from_norms() {
+    double out = 0.0;
+    detail::check(tp_grid_fit_from_norms(grid_, &out));
+    return out;
+  }
+  struct Volumes {
+    std::vector<u64> ttm, regrid;  // per tree node, elements shipped by all ranks in the last sweep
+  };
+  Volumes last_volumes() const {
+    Volumes v{std::vector<u64>(n_nodes_, 0), std::vector<u64>(n_nodes_, 0)};
+    detail::check(tp_grid_last_volumes(grid_, n_nodes_, v.ttm.data(), v.regrid.data()));
+    return v;
+  }
+  float last_total_ms() const {
+    float ms = 0.f;
+    detail::check(tp_grid_last_timing(grid_, &ms, 0, nullptr, nullptr));
+    return ms;
+  }
+
+ private:
+  ProblemSpec spec_;
+  int n_nodes_ = 0;
+  tp_grid* grid_ = nullptr;
+};
+
 }  // namespace tuckerplan

@@ -163,6 +163,8 @@ typedef struct tp_ctx tp_ctx;
 typedef struct tp_tensor tp_tensor;   /* row-major FP64 tensor resident in HBM */
 typedef struct tp_plan tp_plan;       /* spec + tree + arena + launch schedule for repeated sweeps */
 
+/* number of CUDA devices visible to this process (0 and TP_OK when there is no driver) */
+int tp_device_count(int* out);
 int tp_ctx_create(int device, tp_ctx** out);
 /* Same with creation flags.  The eigen-solve side streams normally outrank the stream the tree runs on (their kernels
  * are short and latency-bound); the flags put them on the same priority or below it (A/B measurements). */
@@ -330,6 +332,11 @@ int tp_dev_reduce_slots(tp_ctx* ctx, double* out, const double* const* slots_hos
 /* dst(a, l0+l, b) = src(a, l, b): places a peer's mode slice (outer, count, inner) into (outer, full_len, inner). */
 int tp_dev_assemble_mode(tp_ctx* ctx, double* dst, size_t outer, size_t full_len, size_t inner, const double* src,
                          size_t l0, size_t count);
+/* dst[dst_lo + i] = src[src_lo + i] for every index i of the box (extents `box`), both tensors row-major with extents
+ * dst_dims / src_dims: one piece of a redistribution between two block layouts (the paper's regrid, PAPER.md:767;
+ * counted by simulate.hpp:97-113).  src may be memory of a peer device. */
+int tp_dev_copy_box(tp_ctx* ctx, double* dst, const size_t* dst_dims, const size_t* dst_lo, const double* src,
+                    const size_t* src_dims, const size_t* src_lo, const size_t* box, int n_modes);
 /* gram (rows x rows, full symmetric) of the mode-n unfolding of the block y viewed as (outer, rows, inner). */
 int tp_dev_gram(tp_ctx* ctx, const double* y, size_t outer, size_t rows, size_t inner, double* gram);
 /* top-k eigenvectors of gram (destroyed) with the reference's sign rule into factor (rows x k column-major);
@@ -374,6 +381,50 @@ int tp_dev_sum_squares(tp_ctx* ctx, const double* x, size_t count, double* out);
 int tp_dev_cholesky(tp_ctx* ctx, const double* s, int block, double* l, int* fail);
 int tp_dev_trsm_right_lt(tp_ctx* ctx, double* z, size_t rows, int block, const double* l);
 int tp_dev_jacobi_eig(tp_ctx* ctx, const double* h, int block, double* w, double* v, int* fail);
+
+/* ------------------------------------------------------------ grid executor: HOOI on P GPUs of one box
+ * The paper's distribution scheme executed inside ONE process ("single process driving P devices"):
+ * rank p of the Cartesian grid lives on CUDA device devices[p]; tensors are block-distributed by floor cuts
+ * (grid.hpp:114-119) with row-major owner ranks (simulate.hpp:69-73), factors replicated.  A product along a split
+ * mode is followed by the reduce-scatter of PAPER.md:582-588, done here by the TTM kernel's epilogue storing every
+ * chunk straight into its owner's memory over NVLink (peer access), an event, and an ordered sum; leaves add partial
+ * Gram matrices at an owner rank, which solves and copies the factor to every replica; a node whose grid differs from
+ * its parent's first redistributes its input (regrid).  The same device may be named more than once
+ * ("virtual ranks" on one GPU: same code, peer pointers are ordinary pointers).  Jacobi schedule only.
+ *   root_grid   n_modes extents, product = n_ranks, validated like validate_grid (grid.hpp:36-45)
+ *   node_grids  NULL (the root grid everywhere = a static grid, grid_volume.hpp) or n_nodes x n_modes as in
+ *               tp_scheme_volume (rows of TTM nodes are read), e.g. the output of tp_optimal_dynamic_scheme
+ *   flags       TP_GRID_NCCL: leaf all-reduce and factor broadcast through NCCL (ncclCommInitAll; libnccl.so.2 is
+ *               loaded at run time; needs distinct devices) instead of peer-memory reads and copies */
+typedef struct tp_grid tp_grid;
+enum { TP_GRID_NCCL = 1 };
+int tp_grid_create(int n_ranks, const int* devices, int n_modes, const tp_u64* L, const tp_u64* K, int n_nodes,
+                   const int* kind, const int* mode, const int* parent, const tp_u64* root_grid,
+                   const tp_u64* node_grids, unsigned flags, tp_grid** out);
+int tp_grid_destroy(tp_grid* grid);
+int tp_grid_ranks(const tp_grid* grid, int* n_ranks);
+/* rank's block of the input tensor under the root grid: first index and extent per mode (either may be NULL) */
+int tp_grid_block(const tp_grid* grid, int rank, size_t* lo, size_t* dims);
+/* the whole host tensor (row-major, extents L) cut into blocks and uploaded; or one rank's block, already cut */
+int tp_grid_set_tensor(tp_grid* grid, const double* host_tensor);
+int tp_grid_set_block(tp_grid* grid, int rank, const double* host_block);
+/* Decomposition::factors (hooi.hpp:78-81), L_n x K_n column-major each; replicated to every rank */
+int tp_grid_set_factors(tp_grid* grid, const double* const* factors);
+int tp_grid_get_factors(tp_grid* grid, double* const* factors_out);
+/* one hooi_sweep (hooi.hpp:189-229, SweepKind::jacobi) on the grid; the factors are replaced, the core recomputed */
+int tp_grid_sweep(tp_grid* grid, tp_sweep_stats* stats);
+/* the core (extents K, row-major) assembled from the ranks' blocks */
+int tp_grid_get_core(tp_grid* grid, double* core_out);
+int tp_grid_norms(tp_grid* grid, double* tensor_norm, double* core_norm);
+int tp_grid_fit_from_norms(tp_grid* grid, double* out);
+/* elements the ranks shipped in the last sweep, per tree node and summed over ranks: reduce-scatter of the node's
+ * product and regrid of its input -- the quantities simulate.hpp traces and grid_volume.hpp / grid_dynamic.hpp
+ * model (a product carried over from the previous core chain is booked to the sweep that consumes it) */
+int tp_grid_last_volumes(const tp_grid* grid, int n_nodes, tp_u64* ttm_elements, tp_u64* regrid_elements);
+/* device time of the last sweep, of each node's product (max over ranks; kernel + exchange + ordered sum), and the
+ * number of leaves served by the certified top-k solve so far */
+int tp_grid_last_timing(const tp_grid* grid, float* total_ms, int n_nodes, float* node_ms, int* fast_solves);
+int tp_grid_launch_counts(const tp_grid* grid, tp_u64* own_kernels, tp_u64* library_calls);
 
 /* By-value hooi_sweep (hooi.hpp:189-191): host tensor + host factors in, host factors + core out; uploads, runs,
  * downloads.  This is the call the reference-facing C++ wrapper makes. */

@@ -1277,6 +1277,18 @@ static void release_host_call_cache(tp_ctx* ctx) {
 
 extern "C" {
 
+int tp_device_count(int* out) {
+  return guarded([&] {
+    if (!out) raise(TP_ERR_BAD_ARGUMENT, "null output");
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess) {
+      cudaGetLastError();
+      count = 0;
+    }
+    *out = count;
+  });
+}
+
 int tp_ctx_create(int device, tp_ctx** out) { return tp_ctx_create_ex(device, 0, out); }
 
 int tp_ctx_create_ex(int device, unsigned flags, tp_ctx** out) {
@@ -2394,6 +2406,27 @@ int tp_dev_assemble_mode(tp_ctx* ctx, double* dst, size_t outer, size_t full_len
     TPB_CUDA(launch_assemble_mode(ctx->stream, dst, static_cast<long long>(outer), static_cast<long long>(full_len),
                                   static_cast<long long>(inner), src, static_cast<long long>(l0),
                                   static_cast<long long>(count)));
+    ctx->own_kernels += 1;
+  });
+}
+
+int tp_dev_copy_box(tp_ctx* ctx, double* dst, const size_t* dst_dims, const size_t* dst_lo, const double* src,
+                    const size_t* src_dims, const size_t* src_lo, const size_t* box, int n_modes) {
+  return guarded([&] {
+    bind(ctx);
+    if (!dst || !src || !dst_dims || !dst_lo || !src_dims || !src_lo || !box) raise(TP_ERR_BAD_ARGUMENT, "null pointer");
+    if (n_modes < 1 || n_modes > kMaxBoxModes) raise(TP_ERR_BAD_DIMS, "tensor needs 1..16 modes");
+    long long dd[kMaxBoxModes], dl[kMaxBoxModes], sd[kMaxBoxModes], sl[kMaxBoxModes], bx[kMaxBoxModes];
+    for (int m = 0; m < n_modes; ++m) {
+      if (dst_lo[m] + box[m] > dst_dims[m] || src_lo[m] + box[m] > src_dims[m])
+        raise(TP_ERR_SHAPE_MISMATCH, "box exceeds a tensor's extent", m);
+      dd[m] = static_cast<long long>(dst_dims[m]);
+      dl[m] = static_cast<long long>(dst_lo[m]);
+      sd[m] = static_cast<long long>(src_dims[m]);
+      sl[m] = static_cast<long long>(src_lo[m]);
+      bx[m] = static_cast<long long>(box[m]);
+    }
+    TPB_CUDA(launch_copy_box(ctx->stream, dst, dd, dl, src, sd, sl, bx, n_modes));
     ctx->own_kernels += 1;
   });
 }

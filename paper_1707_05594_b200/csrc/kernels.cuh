@@ -85,6 +85,12 @@ cudaError_t launch_reduce_slots(cudaStream_t stream, double* out, const double* 
 // dst(a, l0 + l, b) = src(a, l, b): drops the piece (outer, count, inner) into the tensor (outer, full_len, inner)
 cudaError_t launch_assemble_mode(cudaStream_t stream, double* dst, long long outer, long long full_len,
                                  long long inner, const double* src, long long l0, long long count);
+// dst[dst_lo + i] = src[src_lo + i] over an n-mode box (row-major tensors with extents dst_dims / src_dims): one piece
+// of a redistribution between block layouts; src may be memory of a peer device
+constexpr int kMaxBoxModes = 16;
+cudaError_t launch_copy_box(cudaStream_t stream, double* dst, const long long* dst_dims, const long long* dst_lo,
+                            const double* src, const long long* src_dims, const long long* src_lo,
+                            const long long* box, int n);
 // y[i] = beta * y[i] + alpha * x[i]
 cudaError_t launch_axpby(cudaStream_t stream, double* y, double beta, double alpha, const double* x, size_t n);
 // Top-k eigenvectors from an ascending eigen-solve result (vectors column-major rows x ncols, values w[ncols]) with

@@ -2,6 +2,7 @@
 // eigenvector selection with the reference's sign / gap rules.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cfloat>
 
 #include "kernels.cuh"
@@ -222,7 +223,55 @@ __global__ void __launch_bounds__(256) assemble_mode_kernel(double* __restrict__
   }
 }
 
+// dst[dst_lo + i] = src[src_lo + i] for every index i of an n-mode box; both tensors row-major with their own extents.
+struct BoxCopy {
+  int n;
+  long long box[kMaxBoxModes];         // extents of the box
+  long long src_stride[kMaxBoxModes];  // element strides of the source tensor
+  long long dst_stride[kMaxBoxModes];
+  long long src_base, dst_base;        // offsets of the box origin
+};
+
+__global__ void __launch_bounds__(256) copy_box_kernel(double* __restrict__ dst, const double* __restrict__ src,
+                                                       BoxCopy c, size_t total) {
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total; i += stride) {
+    long long rest = static_cast<long long>(i), s = c.src_base, d = c.dst_base;
+    for (int m = c.n - 1; m >= 0; --m) {
+      const long long at = rest % c.box[m];
+      rest /= c.box[m];
+      s += at * c.src_stride[m];
+      d += at * c.dst_stride[m];
+    }
+    dst[d] = src[s];
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_copy_box(cudaStream_t stream, double* dst, const long long* dst_dims, const long long* dst_lo,
+                            const double* src, const long long* src_dims, const long long* src_lo,
+                            const long long* box, int n) {
+  if (n < 1 || n > kMaxBoxModes) return cudaErrorInvalidValue;
+  BoxCopy c{};
+  c.n = n;
+  size_t total = 1;
+  long long ss = 1, ds = 1;
+  for (int m = n - 1; m >= 0; --m) {
+    c.box[m] = box[m];
+    c.src_stride[m] = ss;
+    c.dst_stride[m] = ds;
+    c.src_base += src_lo[m] * ss;
+    c.dst_base += dst_lo[m] * ds;
+    ss *= src_dims[m];
+    ds *= dst_dims[m];
+    total *= static_cast<size_t>(box[m]);
+  }
+  if (total == 0) return cudaSuccess;
+  const unsigned blocks = static_cast<unsigned>(std::min<size_t>((total + 255) / 256, kReduceBlocks));
+  copy_box_kernel<<<blocks, 256, 0, stream>>>(dst, src, c, total);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_reduce_slots(cudaStream_t stream, double* out, const double* const* slots, int n_slots, size_t n) {
   if (n_slots < 1 || n_slots > kMaxReduceSlots) return cudaErrorInvalidValue;

@@ -321,6 +321,96 @@ class HooiPlan:
             pass
 
 
+class GridHooi:
+    """Jacobi sweeps on a Cartesian processor grid inside this process (tp_grid_*): rank p runs on CUDA device
+    devices[p]; naming a device several times gives virtual ranks on one GPU.  `grid` is the root grid, `node_grids`
+    (optional, {node id: grid}) a per-node scheme as planner.optimal_dynamic_scheme returns."""
+
+    def __init__(self, spec: ProblemSpec, tree: TtmTree, grid: Sequence[int], devices: Sequence[int],
+                 node_grids=None, use_nccl: bool = False):
+        self.spec, self.tree = spec, tree
+        n, L, K = spec._c()
+        nn, kind_a, mode_a, parent_a = tree._c()
+        self._nn = nn
+        ng = None
+        if node_grids is not None:
+            flat = [0] * (nn * n)
+            for node, g in node_grids.items():
+                flat[node * n:(node + 1) * n] = [int(v) for v in g]
+            ng = u64_array(flat)
+        self._h = ctypes.c_void_p()
+        devs = (ctypes.c_int * len(devices))(*[int(d) for d in devices])
+        check(lib.tp_grid_create(len(devices), devs, n, L, K, nn, kind_a, mode_a, parent_a, u64_array(grid), ng,
+                                 ctypes.c_uint(1 if use_nccl else 0), ctypes.byref(self._h)))
+
+    def set_tensor(self, t: np.ndarray):
+        t = _f64(t)
+        _check_engine_shapes(t, self.spec)
+        check(lib.tp_grid_set_tensor(self._h, t.ctypes.data_as(dbl_p)))
+
+    def block(self, rank: int):
+        n = self.spec.n_modes()
+        lo, dims = (ctypes.c_size_t * n)(), (ctypes.c_size_t * n)()
+        check(lib.tp_grid_block(self._h, int(rank), lo, dims))
+        return list(lo), list(dims)
+
+    def set_factors(self, factors: Sequence[np.ndarray]):
+        fs = [_colmajor(f) for f in factors]
+        check(lib.tp_grid_set_factors(self._h, (dbl_p * len(fs))(*[a.ctypes.data_as(dbl_p) for a in fs])))
+
+    def get_factors(self) -> List[np.ndarray]:
+        outs = [np.zeros((l, k), dtype=np.float64, order="F") for l, k in zip(self.spec.L, self.spec.K)]
+        check(lib.tp_grid_get_factors(self._h, (dbl_p * len(outs))(*[a.ctypes.data_as(dbl_p) for a in outs])))
+        return outs
+
+    def sweep(self) -> SweepStats:
+        st = _SweepStatsC()
+        check(lib.tp_grid_sweep(self._h, ctypes.byref(st)))
+        return SweepStats(st.tree_macs, st.core_macs, st.peak_live, bool(st.degenerate))
+
+    def get_core(self) -> np.ndarray:
+        out = np.empty(tuple(self.spec.K), dtype=np.float64)
+        check(lib.tp_grid_get_core(self._h, out.ctypes.data_as(dbl_p)))
+        return out
+
+    def norms(self):
+        a, b = ctypes.c_double(), ctypes.c_double()
+        check(lib.tp_grid_norms(self._h, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
+    def fit_from_norms(self) -> float:
+        out = ctypes.c_double()
+        check(lib.tp_grid_fit_from_norms(self._h, ctypes.byref(out)))
+        return out.value
+
+    def last_volumes(self):
+        a, b = (ctypes.c_uint64 * self._nn)(), (ctypes.c_uint64 * self._nn)()
+        check(lib.tp_grid_last_volumes(self._h, self._nn, a, b))
+        return list(a), list(b)
+
+    def last_timing(self):
+        total, fast = ctypes.c_float(), ctypes.c_int()
+        per = (ctypes.c_float * self._nn)()
+        check(lib.tp_grid_last_timing(self._h, ctypes.byref(total), self._nn, per, ctypes.byref(fast)))
+        return total.value, list(per), fast.value
+
+    def launch_counts(self):
+        a, b = u64(), u64()
+        check(lib.tp_grid_launch_counts(self._h, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
+    def close(self):
+        if self._h:
+            lib.tp_grid_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 # ------------------------------------------------------------------ by-value API (reference signatures)
 def ttm(t: np.ndarray, m: np.ndarray, mode: int, macs: Optional[list] = None, ctx: Optional[Context] = None):
     """ttm(t, m, mode, macs*) — ttm.hpp:73-96."""

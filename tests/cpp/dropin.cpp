@@ -2,9 +2,14 @@
 // tests/test_engine.cpp), compiled against include/tuckerplan/ of THIS repo and linked to libtuckerplan_b200.so.
 //   dropin planner  -> planner selections for the cube / pinned specs (no GPU needed)
 //   dropin hooi     -> the README transcript: 12x10x8 seed 7, K = 4,3,2, Gauss-Seidel on the chain-input tree
+//   dropin grid     -> Jacobi sweeps on P = 2 and P = 4 ranks (GridHooi; virtual ranks on device 0) against the
+//                      single-device DeviceHooi on the same input: projector gaps, fit, shipped volumes vs the model
+#include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "tuckerplan/tuckerplan.hpp"
 
@@ -91,6 +96,61 @@ int main(int argc, char** argv) {
         tp::hooi_sweep(t, s, d, tp::balanced_tree(s), tp::SweepKind::gauss_seidel);
       } catch (const tp::Error& e) {
         std::printf("error %d\n", static_cast<int>(e.code()));
+      }
+      return 0;
+    }
+    if (cmd == "grid") {
+      const tp::DenseTensor noise = tp::random_tensor({30, 24, 20}, 11);
+      tp::ProblemSpec s{{30, 24, 20}, {5, 4, 3}};
+      // low-rank-plus-noise input assembled with the public API: X = G x A_0 x A_1 x A_2, T = X + 1e-2 E
+      const tp::Decomposition gen = tp::random_decomposition(noise, s, 3);
+      tp::DenseTensor x = tp::random_tensor({5, 4, 3}, 4);
+      for (int m = 0; m < 3; ++m) x = tp::ttm(x, gen.factors[m], m);
+      tp::DenseTensor t = x;
+      for (std::size_t i = 0; i < t.data.size(); ++i) t.data[i] += 1e-2 * noise.data[i];
+      const tp::TtmTree tree = tp::optimal_tree(s).tree;
+      const std::vector<tp::Matrix> start = tp::random_decomposition(t, s, 0).factors;
+      tp::DeviceHooi single(t, s, tree, tp::SweepKind::jacobi);
+      single.set_factors(start);
+      for (int i = 0; i < 3; ++i) single.sweep();
+      const tp::Decomposition want = single.decomposition();
+      const double want_fit = single.reconstruction_error();
+      auto projector_gap = [](const tp::Matrix& a, const tp::Matrix& b) {  // ||A A^T - B B^T||_F
+        double sum = 0.0;
+        for (std::size_t i = 0; i < a.rows(); ++i)
+          for (std::size_t j = 0; j < a.rows(); ++j) {
+            double pa = 0.0, pb = 0.0;
+            for (std::size_t c = 0; c < a.cols(); ++c) {
+              pa += a(i, c) * a(j, c);
+              pb += b(i, c) * b(j, c);
+            }
+            sum += (pa - pb) * (pa - pb);
+          }
+        return std::sqrt(sum);
+      };
+      for (const tp::u64 procs : {2, 4}) {
+        const tp::StaticGridResult best = tp::optimal_static_grid(tree, s, procs);
+        tp::GridHooi grid(t, s, tree, tp::uniform_scheme(tree, best.grid), std::vector<int>(procs, 0));
+        grid.set_factors(start);
+        tp::SweepStats st;
+        for (int i = 0; i < 3; ++i) st = grid.sweep();
+        const tp::Decomposition got = grid.decomposition();
+        double gap = 0.0;
+        for (int m = 0; m < 3; ++m) gap = std::max(gap, projector_gap(got.factors[m], want.factors[m]));
+        const tp::GridHooi::Volumes vol = grid.last_volumes();
+        tp::u64 shipped = 0;
+        for (tp::u64 v : vol.ttm) shipped += v;
+        std::printf("procs %llu grid %llux%llux%llu gap_ok %d fit_ok %d macs_ok %d shipped %llu model %llu\n",
+                    (unsigned long long)procs, (unsigned long long)best.grid.q[0], (unsigned long long)best.grid.q[1],
+                    (unsigned long long)best.grid.q[2], gap < 1e-9 ? 1 : 0,
+                    std::fabs(grid.fit_from_norms() - want_fit) < 1e-10 ? 1 : 0,
+                    st.tree_macs == tp::tree_cost(tree, s).total_macs ? 1 : 0, (unsigned long long)shipped,
+                    (unsigned long long)best.report.total);
+      }
+      try {
+        tp::GridHooi bad(t, s, tree, tp::uniform_scheme(tree, tp::Grid{{8, 1, 1}}), std::vector<int>(8, 0));
+      } catch (const tp::Error& e) {
+        std::printf("error %d\n", static_cast<int>(e.code()));  // q_0 = 8 > K_0 = 5: invalid_grid
       }
       return 0;
     }

@@ -223,3 +223,31 @@ def test_generated_tensor_feeds_the_sweep_runner(cli, tmp_path):       # test_cl
     assert report["tree"] == "opt" and report["sweeps"][0]["tree_macs"] == cost.total_macs
     assert report["sweeps"][0]["peak_live"] == cost.depth + 1
     assert cli("hooi", "--L", "20,18,16", "--K", "5,4,3", "--tree", "opt")[0] == 1   # Gauss-Seidel needs a chain tree
+
+
+@pytest.mark.gpu
+def test_hooi_on_a_processor_grid_through_the_cli(cli, tmp_path):
+    """`hooi --procs P` runs the Jacobi sweeps on the grid executor (tp_grid_*; with one GPU the ranks share it) and
+    must print the errors of the single-device run; the report names the grid and its model volume."""
+    path = tmp_path / "t.bin"
+    assert cli("gen-tensor", "--L", "24,20,16", "--seed", 5, "--out", path)[0] == 0
+    base = ["hooi", "--tensor", path, "--K", "4,3,2", "--scheme", "jacobi", "--sweeps", 3]
+    code, single = cli(*base)
+    assert code == 0
+    for extra in (["--procs", 2], ["--procs", 4, "--grid", "2x1x2"], ["--procs", 2, "--dynamic"]):
+        code, out = cli(*base, *extra)
+        assert code == 0, out
+        lines = out.splitlines()
+        assert lines[1].startswith("grid: %d ranks on 1 device(s), model volume" % extra[1])
+        want = [l for l in single.splitlines() if l.startswith("sweep")]
+        got = [l for l in lines if l.startswith("sweep")]
+        assert len(got) == 3
+        for a, b in zip(got, want):
+            ea, eb = float(a.split("error ")[1].split(",")[0]), float(b.split("error ")[1].split(",")[0])
+            assert abs(ea - eb) < 5e-10 and a.split(",", 1)[1] == b.split(",", 1)[1]
+    report = tmp_path / "r.json"
+    assert cli(*base, "--procs", 2, "--out", report, "--format", "json")[0] == 0
+    data = json.loads(report.read_text())
+    assert data["grid"]["procs"] == 2 and data["grid"]["model_volume"] > 0 and "root" in data["grid"]["scheme"]
+    assert cli(*base, "--procs", 2, "--scheme", "gauss-seidel")[0] == 1      # the grid runs jacobi only
+    assert cli(*base, "--procs", 3, "--grid", "2x1x1")[0] == 1                # grid does not multiply out to P

@@ -55,3 +55,18 @@ def test_serialize_checks_through_cpp_headers():
     assert [l for l in out.splitlines() if l.startswith("ok ")] == [
         "ok spec", "ok tree labels", "ok tree round trip", "ok tree labels rejected", "ok grid", "ok scheme",
         "ok reports", "ok traced counts", "ok tensor files", "ok json"]
+
+
+@pytest.mark.gpu
+def test_grid_executor_through_cpp_headers(dropin):
+    """GridHooi (include/tuckerplan/hooi.hpp -> tp_grid_*): P = 2 and P = 4 virtual ranks on one GPU give the single-
+    device engine's subspaces and fit, and ship exactly the volume optimal_static_grid predicted."""
+    out = subprocess.check_output([dropin, "grid"]).decode().splitlines()
+    assert len(out) == 3, out
+    for line, procs in zip(out[:2], (2, 4)):
+        words = line.split()
+        assert words[0] == "procs" and int(words[1]) == procs
+        fields = dict(zip(words[4::2], words[5::2]))
+        assert fields["gap_ok"] == "1" and fields["fit_ok"] == "1" and fields["macs_ok"] == "1", line
+        assert int(fields["shipped"]) == int(fields["model"]) > 0, line
+    assert out[2] == "error 6"                     # Errc::invalid_grid

@@ -12,6 +12,7 @@
 #include <map>
 #include <set>
 #include <sstream>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -71,6 +72,9 @@ const std::vector<Command>& commands() {
         {"--tree", false, "tree strategy (default fits the scheme)"},
         {"--scheme", false, "jacobi|gauss-seidel (default gauss-seidel)"},
         {"--sweeps", false, "sweep count (default 5)"},
+        {"--procs", false, "run on a processor grid of this many GPUs (jacobi only; default 1)"},
+        {"--grid", false, "grid for --procs, e.g. 1x1x8 (default: the volume-optimal static grid)"},
+        {"--dynamic", true, "with --procs: per-node grids (optimal_dynamic_scheme) instead of one static grid"},
         {"--out", false, "write the sweep report JSON here"},
         {"--format", false, "stdout format: text|json (default text)"}}},
   };
@@ -382,12 +386,56 @@ int cmd_hooi(const Args& a) {
   char line[160];
   std::snprintf(line, sizeof line, "start: error %.12f\n", tp::reconstruction_error(t, start));
   text += line;
-  tp::DeviceHooi engine(t, s, tree, kind);
-  engine.set_factors(start.factors);
+  // --procs P: the paper's block distribution on P GPUs of this box (rank p on device p modulo the device count:
+  // with fewer devices than ranks several ranks share one, which is only useful for trying the path out)
+  const u64 procs = a.has("--procs") ? parse_u64(a.get("--procs"), "--procs") : 1;
+  std::unique_ptr<tp::GridHooi> grid_engine;
+  std::unique_ptr<tp::DeviceHooi> engine;
+  tp::json grid_report;
+  if (procs > 1 || a.has("--grid")) {
+    if (kind != tp::SweepKind::jacobi) tp::fail(tp::Errc::bad_argument, "--procs runs the jacobi scheme only");
+    tp::DynamicGridScheme scheme;
+    if (a.flag("--dynamic")) {
+      scheme = tp::optimal_dynamic_scheme(tree, s, procs).scheme;
+    } else if (a.has("--grid")) {
+      tp::Grid g;
+      std::string item;
+      for (const char c : a.get("--grid") + "x") {
+        if (c == 'x') {
+          g.q.push_back(parse_u64(item, "--grid"));
+          item.clear();
+        } else {
+          item.push_back(c);
+        }
+      }
+      tp::validate_grid(g, s, procs);
+      scheme = tp::uniform_scheme(tree, g);
+    } else {
+      scheme = tp::uniform_scheme(tree, tp::optimal_static_grid(tree, s, procs).grid);
+    }
+    int device_count = 1;
+    tp::detail::check(tp_device_count(&device_count));
+    std::vector<int> devices;
+    for (u64 p = 0; p < procs; ++p) devices.push_back(static_cast<int>(p % static_cast<u64>(device_count)));
+    grid_engine = std::make_unique<tp::GridHooi>(t, s, tree, scheme, devices);
+    grid_engine->set_factors(start.factors);
+    grid_report = tp::json::object({{"procs", tp::json(procs)},
+                                    {"devices", tp::json(static_cast<u64>(std::min<u64>(procs, device_count)))},
+                                    {"scheme", tp::scheme_to_json(scheme)},
+                                    {"model_volume", tp::json(tp::scheme_volume(tree, s, scheme, procs).total)}});
+    std::snprintf(line, sizeof line, "grid: %llu ranks on %d device(s), model volume %llu elements per sweep\n",
+                  static_cast<unsigned long long>(procs), std::min<int>(static_cast<int>(procs), device_count),
+                  static_cast<unsigned long long>(tp::scheme_volume(tree, s, scheme, procs).total));
+    text += line;
+  } else {
+    engine = std::make_unique<tp::DeviceHooi>(t, s, tree, kind);
+    engine->set_factors(start.factors);
+  }
   double final_error = tp::reconstruction_error(t, start);
   for (u64 i = 0; i < sweeps; ++i) {
-    const tp::SweepStats stats = engine.sweep();
-    const double err = engine.reconstruction_error();
+    const tp::SweepStats stats = grid_engine ? grid_engine->sweep() : engine->sweep();
+    // on the grid the error comes from the norms (orthonormal factors): no rank holds the whole tensor
+    const double err = grid_engine ? grid_engine->fit_from_norms() : engine->reconstruction_error();
     final_error = err;
     steps.push_back(tp::json::object({{"sweep", tp::json(i + 1)},
                                       {"error", tp::json(err)},
@@ -400,11 +448,12 @@ int cmd_hooi(const Args& a) {
                   stats.peak_live, stats.degenerate ? " (degenerate cut)" : "");
     text += line;
   }
-  const tp::json report = tp::json::object({{"spec", tp::spec_to_json(s)},
-                                            {"tree", tp::json(tree_choice)},
-                                            {"scheme", tp::json(scheme_name)},
-                                            {"sweeps", steps},
-                                            {"final_error", tp::json(final_error)}});
+  tp::json report = tp::json::object({{"spec", tp::spec_to_json(s)},
+                                      {"tree", tp::json(tree_choice)},
+                                      {"scheme", tp::json(scheme_name)},
+                                      {"sweeps", steps},
+                                      {"final_error", tp::json(final_error)}});
+  if (grid_engine) report["grid"] = grid_report;
   emit(report.dump(2) + "\n", text, a);
   return 0;
 }
