@@ -611,6 +611,121 @@ def run_b200(args):
     return 0
 
 
+# --------------------------------------------------------------------------------------------- in-process grid
+def run_inprocess_grid(args):
+    """`--executor inprocess`: the C++ grid executor (tp_grid_*, csrc/grid_executor.cu) drives all N GPUs from this one
+    process over peer memory -- what a C++ caller of the reference API gets.  With fewer devices than ranks
+    (--virtual-ranks) several ranks share a GPU: a functional run of the same code path, not a scaling measurement."""
+    import torch
+    from paper_1707_05594_b200 import engine as E, planner as P, workloads as W
+    cfg = W.CONFIGS[args.config]
+    spec = cfg.spec
+    world = args.gpus
+    n_dev = torch.cuda.device_count()
+    if world > n_dev and not args.virtual_ranks:
+        print("bench.py: %d ranks but %d GPU(s); pass --virtual-ranks for a functional run" % (world, n_dev), file=sys.stderr)
+        return 2
+    devices = [r % n_dev for r in range(world)]
+    tree = P.optimal_tree(spec).tree
+    cost = P.tree_cost(tree, spec)
+    scheme = None
+    if args.grid == "dynamic":
+        scheme = P.optimal_dynamic_scheme(tree, spec, world).scheme
+        q = list(scheme.root)
+    else:
+        q = [int(v) for v in args.grid.split("x")] if args.grid else list(P.optimal_static_grid(tree, spec, world).grid)
+    volume = (P.scheme_volume(tree, spec, scheme, world).total if scheme else P.static_volume(tree, spec, q, world).total)
+    hbm_gbs, hbm_src = read_peaks()
+    torch.cuda.set_device(0)
+    p_fp64, fp64_src = measure_fp64_peak(torch)
+    cores = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    host_t = W.build_tensor_host(cfg, cores)
+    f0 = W.start_factors(cfg)
+    grid = E.GridHooi(spec, tree, q, devices, node_grids=scheme.node_grids if scheme else None)
+    grid.set_tensor(host_t)
+    build_s = time.perf_counter() - t0
+    grid.set_factors(f0)
+    for _ in range(max(args.warmup, 0)):
+        grid.sweep()
+    k0, _ = grid.launch_counts()
+    sampler = ClockSampler(0)
+    sampler.start()
+    step_ms, node_sum, volumes = [], None, None
+    for _ in range(args.steps):
+        grid.sweep()
+        total_ms, per_node, _ = grid.last_timing()
+        step_ms.append(total_ms)
+        node_sum = per_node if node_sum is None else [a + b for a, b in zip(node_sum, per_node)]
+        volumes = grid.last_volumes()
+    clocks = sampler.stop()
+    k1, lib_calls = grid.launch_counts()
+    ms_per_step = float(np.mean(step_ms))
+    node_ms = [v / args.steps for v in node_sum]
+    fit = grid.fit_from_norms()
+
+    cpu, parity_ok = None, True
+    if not args.no_cpu:
+        grid.set_factors(f0)
+
+        def step():
+            grid.sweep()
+            return grid.get_factors(), grid.norms()[1], grid.fit_from_norms()
+
+        res = oracle_run_with_parity(host_t, spec, tree, f0, cfg.iterations, step)
+        parity_ok = res["ok"]
+        cpu = {"value": float(np.mean(res["secs"])), "unit": "s/iter", "cores": cores, "kind": "port",
+               "sample": "%d of the %d HOOI iterations of %s from the start factors (NumPy/OpenBLAS oracle port)"
+                         % (len(res["secs"]), cfg.iterations, cfg.name),
+               "phases_s": res["phases"], "parity_per_iteration": res["rows"], "parity_ok": parity_ok}
+
+    node_q = (lambda node: scheme.node_grids[node]) if scheme else (lambda node: q)
+    rows, t_roof, flops_total = [], 0.0, 0
+    for node, kind in enumerate(tree.kind):
+        if kind != 1:
+            continue
+        n = tree.mode[node]
+        flops = 2 * spec.K[n] * cost.card_in[node]
+        qn = node_q(node)[n]
+        local_bytes = 8 * (cost.card_in[node] + qn * cost.card_out[node]) / world + 8 * spec.K[n] * spec.L[n]
+        link_bytes = 8 * (qn - 1) * cost.card_out[node] / world
+        t = max(flops / world / (p_fp64 * 1e12), local_bytes / (hbm_gbs * 1e9)) + link_bytes / (NVLINK_GBS * 1e9)
+        t_roof += t
+        flops_total += flops
+        rows.append({"node": node, "mode": n, "ms": node_ms[node], "roofline_ms": t * 1e3,
+                     "frac": t * 1e3 / node_ms[node] if node_ms[node] else None, "nvlink_bytes_per_gpu": link_bytes,
+                     "shipped_elements": volumes[0][node], "regrid_elements": volumes[1][node]})
+    ttm_ms = sum(r["ms"] for r in rows)
+    dom = max(rows, key=lambda r: r["ms"])
+    dom_flops = 2 * spec.K[dom["mode"]] * cost.card_in[dom["node"]]
+    achieved = dom_flops / (dom["ms"] * 1e-3) / 1e12 if dom["ms"] else None
+    compare_q = comparison_grid(spec.n_modes(), world, spec.K)
+    line = {
+        "metric": "hooi_s_per_iter", "value": ms_per_step * 1e-3, "unit": "s/iter", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": shared_config(cfg.name, cfg.iterations, tree.label(), world, q, volume if world > 1 else 0,
+                                "x".join(map(str, compare_q)) if compare_q else None),
+        "engine": {"executor": "in-process grid executor (tp_grid_*): peer-memory reduce-scatter from the TTM epilogue, "
+                               "owner-rank leaf solves", "devices": devices, "virtual_ranks": world > n_dev,
+                   "node_grids": {str(k): list(v) for k, v in scheme.node_grids.items()} if scheme else None},
+        "ttm_tree": {"tflops": flops_total / (ttm_ms * 1e-3) / 1e12 if ttm_ms else None,
+                     "roofline_frac": t_roof * 1e3 / ttm_ms if ttm_ms else None, "measured_ms": ttm_ms,
+                     "roofline_ms": t_roof * 1e3, "flops": flops_total, "p_fp64_tflops": p_fp64,
+                     "p_fp64_source": fp64_src, "hbm_gbs": hbm_gbs, "hbm_source": hbm_src, "nvlink_gbs": NVLINK_GBS,
+                     "per_node": rows},
+        "shipped_elements_per_sweep": sum(volumes[0]) + sum(volumes[1]), "relative_fit": fit, "build_s": build_s,
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": p_fp64 * min(world, n_dev), "unit": "TFLOP/s",
+                     "frac": achieved / (p_fp64 * min(world, n_dev)) if achieved else None, "traffic": None,
+                     "kernel": "ttm kernel (tree node %d, mode %d) across %d rank(s)" % (dom["node"], dom["mode"] + 1, world),
+                     "peak_source": fp64_src},
+        "cpu_baseline": cpu, "e2e": None, "gpu_launches": int(k1 - k0), "library_calls": int(lib_calls), "clocks": clocks,
+    }
+    print(json.dumps(line))
+    grid.close()
+    return 0 if parity_ok else 3
+
+
 # --------------------------------------------------------------------------------------------- launch
 def free_port():
     with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
@@ -644,6 +759,11 @@ def main(argv=None):
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-grid-comparison", action="store_true")
+    ap.add_argument("--executor", default="ranks", choices=["ranks", "inprocess"],
+                    help="N > 1: 'ranks' = one process per GPU over NCCL (torch.distributed); 'inprocess' = the C++ grid "
+                         "executor (tp_grid_*) driving all GPUs from one process over peer memory")
+    ap.add_argument("--virtual-ranks", action="store_true",
+                    help="with --executor inprocess: allow more ranks than GPUs (functional run on a small box)")
     ap.add_argument("--backend", default="cuda", choices=["cuda", "numpy-test"],
                     help="numpy-test: CONTRACT TEST ONLY -- the grid executor's rank program over gloo with the tests' "
                          "NumPy stand-in for the local kernels (tests/numpy_ops.py); not a measurement")
@@ -652,6 +772,8 @@ def main(argv=None):
         ap.error("--gpus must be at least 1")
     if args.impl == "reference":
         return run_reference(args)
+    if args.executor == "inprocess":
+        return run_inprocess_grid(args) if int(os.environ.get("RANK", "0")) == 0 else 0
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         return relaunch_under_torchrun(args, argv)
     if args.backend == "numpy-test" and "WORLD_SIZE" not in os.environ:
