@@ -131,6 +131,31 @@ inline double reconstruction_error(const DenseTensor& t, const Decomposition& d,
   return out;
 }
 
+// Sequentially truncated HOSVD start: for each mode in turn the leading K_n left singular vectors of the current
+// unfolding (selected and signed as leading_left_factors does), the tensor truncated along that mode before the next.
+// Not in the reference (SPEC.md:17 leaves starts other than random_decomposition out of scope); it is what HOOI is
+// usually started from and costs about one sweep.  `degenerate` (optional) receives the OR of the
+// leaves' gap flags.
+inline Decomposition sthosvd(const DenseTensor& t, const ProblemSpec& s, bool* degenerate = nullptr,
+                             DeviceContext& dev = DeviceContext::instance()) {
+  validate_spec(s);
+  detail::check_engine_shapes(t, s);
+  detail::TensorHandle handle(dev.get(), t);
+  Decomposition d;
+  std::vector<std::size_t> core_dims;
+  std::vector<double*> ptrs;
+  for (int n = 0; n < s.n_modes(); ++n) {
+    d.factors.emplace_back(s.L[n], s.K[n]);
+    core_dims.push_back(s.K[n]);
+  }
+  for (Matrix& f : d.factors) ptrs.push_back(f.data());
+  d.core = zeros(core_dims);
+  int flag = 0;
+  detail::check(tp_sthosvd(dev.get(), handle.t, s.K.data(), nullptr, ptrs.data(), d.core.data.data(), &flag, nullptr));
+  if (degenerate) *degenerate = flag != 0;
+  return d;
+}
+
 // Resident form of the sweep driver: tensor, factors, intermediates and the launch schedule stay in HBM.
 class DeviceHooi {
  public:

@@ -226,6 +226,15 @@ int tp_leaf_factor(tp_ctx* ctx, const tp_tensor* t, int mode, int k, double* vec
 /* Gram matrix Y_(n) Y_(n)^T only (rows x rows, symmetric, column-major, full storage) */
 int tp_gram(tp_ctx* ctx, const tp_tensor* t, int mode, double* gram_out);
 
+/* Sequentially truncated HOSVD start (no reference counterpart: SPEC.md:17 leaves initialisation beyond the random
+ * start out of the reference's scope; PAPER.md:53-54 names it as what HOOI is started from).  For each mode in `order`
+ * (NULL = 0 .. N-1, else a permutation): F_n = the K_n leading eigenvectors of the Gram matrix of the mode-n unfolding
+ * of the current tensor, selected and signed as hooi.hpp:60-68 does, then the tensor is truncated along that mode.
+ * factors_out[n]: L_n x K_n column-major (may be NULL), core_out: prod(K) doubles row-major (may be NULL),
+ * *degenerate: OR of the gap flags, *macs accumulates the exact multiply-adds of the truncations. */
+int tp_sthosvd(tp_ctx* ctx, const tp_tensor* t, const tp_u64* K, const int* order, double* const* factors_out,
+               double* core_out, int* degenerate, tp_u64* macs);
+
 typedef struct tp_sweep_stats {   /* SweepStats, hooi.hpp:125-130 */
   tp_u64 tree_macs;
   tp_u64 core_macs;
@@ -284,6 +293,8 @@ int tp_plan_last_sweep_info(tp_ctx* ctx, tp_plan* plan, int* replayed_graph, int
 /* Decomposition::factors (hooi.hpp:78-81) <-> device: factors[n] is L_n x K_n column-major on the host */
 int tp_plan_set_factors(tp_ctx* ctx, tp_plan* plan, const double* const* factors);
 int tp_plan_get_factors(tp_ctx* ctx, tp_plan* plan, double* const* factors_out);
+/* the plan's factors and core <- tp_sthosvd of the device tensor, without leaving the device */
+int tp_plan_init_sthosvd(tp_ctx* ctx, tp_plan* plan, const tp_tensor* t, const int* order);
 /* Decomposition::core — prod(K) doubles, row-major */
 int tp_plan_get_core(tp_ctx* ctx, tp_plan* plan, double* core_out);
 int tp_plan_core_norm(tp_ctx* ctx, tp_plan* plan, double* out);

@@ -1639,6 +1639,133 @@ int tp_leading_left_factors(tp_ctx* ctx, const double* m, size_t rows, size_t co
   });
 }
 
+// Sequentially truncated HOSVD (Vannieuwenhoven, Vandebril, Meerbergen 2012): for each mode in `order`, the leading
+// K_n left singular vectors of the mode-n unfolding of the CURRENT tensor become F_n (Gram + eigen-solve + the
+// reference's sign rule, exactly as a HOOI leaf, hooi.hpp:45-76), and the tensor is truncated, X <- X x_n F_n^T,
+// before the next mode.  The last X is the core of those factors.  What real users start HOOI from;
+// the reference itself only offers the random start.  Factors stay on the device in `factors_dev`.
+static tp_tensor* sthosvd_device(tp_ctx* ctx, const tp_tensor* t, const std::vector<u64>& K, const std::vector<int>& order,
+                                 const std::vector<double*>& factors_dev, int* degenerate, tp_u64* macs) {
+  const int n = static_cast<int>(t->dims.size());
+  const double* src = t->data;
+  std::vector<size_t> dims = t->dims;
+  tp_tensor* current = nullptr;
+  LeafScratch scratch;
+  try {
+    for (int step = 0; step < n; ++step) {
+      const int m = order[step];
+      const int k = static_cast<int>(K[m]);
+      leaf_update(ctx, scratch, src, dims, m, k, factors_dev[m]);
+      if (macs) {
+        size_t count = 1;
+        for (size_t d : dims) count *= d;
+        *macs = add_or_throw(*macs, mul_or_throw(static_cast<u64>(k), static_cast<u64>(count)));
+      }
+      std::vector<size_t> out_dims = dims;
+      out_dims[m] = static_cast<size_t>(k);
+      tp_tensor* next = new_tensor(out_dims);
+      try {
+        // M = F^T: M(k, l) = F[k * L + l]
+        run_ttm(ctx, src, dims, m, factors_dev[m], static_cast<long long>(dims[m]), 1, k, nullptr, next->data);
+        TPB_CUDA(cudaStreamSynchronize(ctx->stream));
+      } catch (...) {
+        cudaFree(next->data);
+        delete next;
+        throw;
+      }
+      if (current) {
+        cudaFree(current->data);
+        delete current;
+      }
+      current = next;
+      src = current->data;
+      dims = out_dims;
+    }
+    const int flag = read_and_clear_flag(ctx, scratch);
+    if (degenerate) *degenerate = flag;
+  } catch (...) {
+    cudaStreamSynchronize(ctx->stream);
+    if (current) {
+      cudaFree(current->data);
+      delete current;
+    }
+    scratch.release();
+    throw;
+  }
+  scratch.release();
+  return current;
+}
+
+static std::vector<int> sthosvd_order(int n, const int* order) {
+  std::vector<int> out(n);
+  std::vector<char> seen(n, 0);
+  for (int i = 0; i < n; ++i) {
+    out[i] = order ? order[i] : i;
+    if (out[i] < 0 || out[i] >= n || seen[out[i]]) raise(TP_ERR_BAD_ARGUMENT, "order must be a permutation of the modes");
+    seen[out[i]] = 1;
+  }
+  return out;
+}
+
+int tp_sthosvd(tp_ctx* ctx, const tp_tensor* t, const tp_u64* K, const int* order, double* const* factors_out,
+               double* core_out, int* degenerate, tp_u64* macs) {
+  return guarded([&] {
+    bind(ctx);
+    if (!t || !K) raise(TP_ERR_BAD_ARGUMENT, "null argument");
+    const int n = static_cast<int>(t->dims.size());
+    std::vector<u64> L(t->dims.begin(), t->dims.end()), ks(K, K + n);
+    validate_spec(make_spec(n, L.data(), ks.data()));
+    for (int m = 0; m < n; ++m)
+      if (L[m] > TP_MAX_GRAM_ROWS) raise(TP_ERR_TOO_LARGE, "unfolding has too many rows for the Gram route", m);
+    const std::vector<int> ord = sthosvd_order(n, order);
+    std::vector<double*> factors(n, nullptr);
+    tp_tensor* core = nullptr;
+    auto cleanup = [&] {
+      cudaStreamSynchronize(ctx->stream);
+      for (double* f : factors) cudaFree(f);
+      if (core) {
+        cudaFree(core->data);
+        delete core;
+      }
+    };
+    try {
+      for (int m = 0; m < n; ++m) factors[m] = device_alloc(static_cast<size_t>(L[m] * ks[m]));
+      core = sthosvd_device(ctx, t, ks, ord, factors, degenerate, macs);
+      for (int m = 0; m < n && factors_out; ++m)
+        TPB_CUDA(cudaMemcpyAsync(factors_out[m], factors[m], sizeof(double) * L[m] * ks[m], cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+      if (core_out)
+        TPB_CUDA(cudaMemcpyAsync(core_out, core->data, sizeof(double) * core->size, cudaMemcpyDeviceToHost, ctx->stream));
+      TPB_CUDA(cudaStreamSynchronize(ctx->stream));
+    } catch (...) {
+      cleanup();
+      throw;
+    }
+    cleanup();
+  });
+}
+
+int tp_plan_init_sthosvd(tp_ctx* ctx, tp_plan* p, const tp_tensor* t, const int* order) {
+  return guarded([&] {
+    bind(ctx);
+    if (!p) raise(TP_ERR_BAD_ARGUMENT, "null plan");
+    check_tensor_matches(p, t);
+    const std::vector<int> ord = sthosvd_order(p->n, order);
+    tp_tensor* core = sthosvd_device(ctx, t, p->spec.K, ord, p->cur, nullptr, nullptr);
+    // the plan's core is the core of its current factors (as after tp_plan_compute_core)
+    const cudaError_t e = cudaMemcpyAsync(p->core, core->data, sizeof(double) * p->core_size, cudaMemcpyDeviceToDevice,
+                                          ctx->stream);
+    cudaStreamSynchronize(ctx->stream);
+    cudaFree(core->data);
+    delete core;
+    if (e != cudaSuccess) cuda_fail(e, "copy of the truncated core");
+    p->carry_valid = false;
+    p->factors_from_caller = true;   // a start like any other: the first sweep's solves are cold
+    p->warm_sweeps = 0;
+    for (LeafScratch& slot : p->leaf) slot.last_ritz = nullptr;
+  });
+}
+
 int tp_plan_create(tp_ctx* ctx, int n_modes, const tp_u64* L, const tp_u64* K, int n_nodes, const int* kind,
                    const int* mode, const int* parent, int sweep_kind, tp_plan** out) {
   return guarded([&] {

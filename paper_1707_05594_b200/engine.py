@@ -268,6 +268,11 @@ class HooiPlan:
         check(lib.tp_plan_get_factors(self.ctx._h, self._h, self._factor_ptrs(outs)))
         return outs
 
+    def init_sthosvd(self, t: DeviceTensor, order: Optional[Sequence[int]] = None):
+        """Start factors (and their core) from the sequentially truncated HOSVD of the device tensor."""
+        arr = (ctypes.c_int * len(order))(*[int(v) for v in order]) if order is not None else None
+        check(lib.tp_plan_init_sthosvd(self.ctx._h, self._h, t._h, arr))
+
     def get_core(self) -> np.ndarray:
         out = np.empty(tuple(self.spec.K), dtype=np.float64)
         check(lib.tp_plan_get_core(self.ctx._h, self._h, out.ctypes.data_as(dbl_p)))
@@ -508,6 +513,27 @@ def random_decomposition(t: np.ndarray, s: ProblemSpec, seed: int, ctx: Optional
     _check_engine_shapes(t, s)
     factors = hostgen.random_orthonormal_factors(s.L, s.K, seed)
     return Decomposition(core_from_factors(t, factors, ctx), factors)
+
+
+def sthosvd(t: np.ndarray, s: ProblemSpec, order: Optional[Sequence[int]] = None, ctx: Optional[Context] = None):
+    """Sequentially truncated HOSVD start (tp_sthosvd; no reference counterpart, see the header).  Returns
+    (Decomposition, degenerate)."""
+    ctx = ctx or default_context()
+    validate_spec(s)
+    t = _f64(t)
+    _check_engine_shapes(t, s)
+    dt = DeviceTensor.upload(ctx, t)
+    try:
+        n = s.n_modes()
+        fout = [np.zeros((l, k), dtype=np.float64, order="F") for l, k in zip(s.L, s.K)]
+        core = np.empty(tuple(s.K), dtype=np.float64)
+        deg = ctypes.c_int()
+        arr = (ctypes.c_int * n)(*[int(v) for v in order]) if order is not None else None
+        check(lib.tp_sthosvd(ctx._h, dt._h, u64_array(s.K), arr, (dbl_p * n)(*[a.ctypes.data_as(dbl_p) for a in fout]),
+                             core.ctypes.data_as(dbl_p), ctypes.byref(deg), None))
+        return Decomposition(core, fout), bool(deg.value)
+    finally:
+        dt.free()
 
 
 def reconstruction_error(t: np.ndarray, d: Decomposition, ctx: Optional[Context] = None) -> float:

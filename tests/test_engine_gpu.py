@@ -841,3 +841,46 @@ def test_tma_kernel_is_stable_under_concurrent_kernels(ctx):
             got = ops.to_host(z)
             torch.cuda.synchronize()
             assert np.max(np.abs(got - ref)) <= 64 * EPS * np.sqrt(dims[1]) * np.max(np.abs(f)) * np.max(np.abs(x))
+
+
+@pytest.mark.parametrize("L,K,order", [([40, 36, 32], [6, 5, 4], None), ([40, 36, 32], [6, 5, 4], [2, 0, 1]),
+                                       ([20, 18, 16, 14], [4, 3, 3, 2], None), ([64, 48], [5, 5], [1, 0]),
+                                       ([9, 8, 7, 6, 5], [3, 2, 2, 2, 2], None)],
+                         ids=lambda v: "x".join(map(str, v)) if v is not None else "natural")
+def test_sthosvd_start_matches_the_published_algorithm(ctx, L, K, order):
+    """tp_sthosvd against the NumPy restatement of sequentially truncated HOSVD (oracle/hooi_oracle.py::sthosvd): same
+    subspaces, same core up to rounding, orthonormal factors, the error bound of the method, and a better start for
+    HOOI than random factors."""
+    cfg = W.scaled_config(3, L, K, 2)
+    spec = cfg.spec
+    t = W.build_tensor_host(cfg)
+    d, deg = E.sthosvd(t, spec, order, ctx=ctx)
+    ocore, ofac, odeg = ho.sthosvd(t, K, order)
+    assert deg == odeg == False
+    for a, b, k in zip(d.factors, ofac, K):
+        assert ho.sin_largest_principal_angle(a, b) < 1e-9
+        assert np.max(np.abs(a.T @ a - np.eye(k))) < 1e-12
+        assert np.max(np.abs(a - b)) < 1e-7                 # same sign rule: the vectors themselves agree
+    assert np.max(np.abs(d.core - ocore)) <= 1e-9 * np.max(np.abs(ocore))
+    err = E.reconstruction_error(t, d, ctx=ctx)
+    assert abs(err - ho.reconstruction_error(t, ocore, ofac)) <= 1e-10
+    # resident form: the plan starts from the same factors, and one HOOI sweep from there beats one from random factors
+    tree = P.optimal_tree(spec).tree
+    dt = E.DeviceTensor.upload(ctx, t)
+    plan = E.HooiPlan(ctx, spec, tree, "jacobi")
+    plan.init_sthosvd(dt, order)
+    for a, b in zip(plan.get_factors(), d.factors):
+        assert np.array_equal(a, b)
+    assert np.array_equal(plan.get_core(), d.core)
+    assert abs(plan.fit_from_norms(dt) - err) < 1e-12
+    plan.sweep(dt)
+    after_sthosvd = plan.fit_from_norms(dt)
+    plan.set_factors(W.start_factors(cfg))
+    plan.sweep(dt)
+    after_random = plan.fit_from_norms(dt)
+    assert after_sthosvd <= err + 1e-12 and after_sthosvd <= after_random + 1e-12
+    plan.close()
+    dt.free()
+    with pytest.raises(TuckerplanError) as bad:
+        E.sthosvd(t, spec, [0] * len(L), ctx=ctx)
+    assert bad.value.code == Errc.bad_argument

@@ -1,0 +1,199 @@
+"""Stand-in for compute-sanitizer, which this GPU pool refuses to run (profiles/r02_compute_sanitizer_unavailable.txt).
+
+Every hand-written kernel family is driven through the C ABI on torch-allocated buffers laid out as
+[guard | payload | guard]: output guards hold a canary bit pattern that must survive the launch (an out-of-bounds
+write), input guards hold NaN (an out-of-bounds read that reaches the arithmetic poisons the result, which is compared
+with the oracle), and every case is repeated beside a competing stream and must be bit-identical run to run (races)."""
+import ctypes
+
+import numpy as np
+import pytest
+
+from oracle import hooi_oracle as ho
+from paper_1707_05594_b200 import engine as E, hostgen
+from paper_1707_05594_b200._lib import check, dbl_p, lib, size_array
+
+pytestmark = pytest.mark.gpu
+GUARD = 4096                      # doubles on each side
+CANARY = np.float64(-6.02214076e23)
+EPS = np.finfo(float).eps
+
+
+@pytest.fixture(scope="module")
+def dev():
+    import torch
+    ctx = E.Context(0)
+
+    class Dev:
+        def __init__(self):
+            self.ctx, self.torch = ctx, torch
+            self.noise = torch.empty(16 << 20, dtype=torch.float64, device="cuda")
+            self.side = torch.cuda.Stream()
+
+        def guarded_input(self, a):
+            """payload a (flat) between NaN guard zones; returns (whole buffer, pointer to the payload)"""
+            a = np.ascontiguousarray(a, dtype=np.float64).reshape(-1)
+            # keep the payload 16-byte aligned like any cudaMalloc'ed tensor
+            host = np.full(2 * GUARD + a.size, np.nan)
+            host[GUARD:GUARD + a.size] = a
+            buf = torch.from_numpy(host).cuda()
+            return buf, ctypes.cast(buf.data_ptr() + 8 * GUARD, dbl_p)
+
+        def guarded_output(self, count):
+            host = np.full(2 * GUARD + count, CANARY)
+            buf = torch.from_numpy(host).cuda()
+            return buf, ctypes.cast(buf.data_ptr() + 8 * GUARD, dbl_p)
+
+        def payload(self, buf, count):
+            ctx.synchronize()
+            host = buf.cpu().numpy()
+            assert np.all(host[:GUARD] == CANARY), "write before the output buffer"
+            assert np.all(host[GUARD + count:] == CANARY), "write past the output buffer"
+            return host[GUARD:GUARD + count].copy()
+
+        def disturb(self):
+            with torch.cuda.stream(self.side):
+                for _ in range(8):
+                    self.noise.zero_()
+
+    yield Dev()
+    ctx.close()
+
+
+def repeat_identical(dev, launch, count, times=4):
+    first = None
+    for _ in range(times):
+        dev.disturb()
+        got = launch()
+        assert got.shape == (count,)
+        if first is None:
+            first = got
+        else:
+            assert np.array_equal(first, got), "run-to-run difference: a race"
+    dev.torch.cuda.synchronize()
+    return first
+
+
+# (dims, mode, K): odd and prime extents, one short of / one past a tile, inner == 1, tiny and TMA-sized problems
+TTM_CASES = [((7, 13, 5), 1, 3), ((33, 17), 1, 9), ((33, 17), 0, 5), ((3, 31, 129), 1, 8), ((129, 40, 3), 1, 20),
+             ((2, 770, 20000), 1, 24), ((40010, 50), 1, 20), ((38001, 34), 1, 33), ((5, 36, 9000), 1, 100),
+             ((1, 1, 1), 1, 1), ((63, 64, 65), 2, 13), ((16, 16, 16, 16), 2, 7)]
+
+
+@pytest.mark.parametrize("dims,mode,k", TTM_CASES, ids=lambda v: "x".join(map(str, v)) if isinstance(v, tuple) else str(v))
+@pytest.mark.parametrize("tma", [1, 0])
+def test_ttm_kernels_stay_inside_their_buffers(dev, dims, mode, k, tma):
+    x = hostgen.random_tensor(dims, 1)
+    f = hostgen.random_tensor([k, dims[mode]], 2)                      # M = F^T, K x L row-major = L x K column-major
+    xb, xp = dev.guarded_input(x)
+    fb, fp = dev.guarded_input(f)
+    count = x.size // dims[mode] * k
+    check(lib.tp_set_global_option(1, ctypes.c_longlong(tma)))
+    try:
+        def launch():
+            zb, zp = dev.guarded_output(count)
+            cuts = size_array([0, k])
+            check(lib.tp_dev_ttm_partial(dev.ctx._h, xp, len(dims), size_array(dims), mode, fp,
+                                         ctypes.c_size_t(dims[mode]), ctypes.c_size_t(0), ctypes.c_size_t(k), 1, cuts, zp))
+            return dev.payload(zb, count)
+        got = repeat_identical(dev, launch, count)
+    finally:
+        check(lib.tp_set_global_option(1, ctypes.c_longlong(1)))
+    want = ho.ttm(x, f, mode).reshape(-1)
+    assert np.all(np.isfinite(got)), "a NaN from an input guard zone reached the result"
+    assert np.max(np.abs(got - want)) <= 64 * EPS * np.sqrt(dims[mode]) * np.max(np.abs(f)) * np.max(np.abs(x))
+
+
+@pytest.mark.parametrize("outer,rows,inner", [(1, 7, 1), (5, 33, 1), (3, 65, 17), (2, 128, 130), (400, 20, 1),
+                                              (1, 200, 401), (9, 63, 63)])
+def test_gram_kernel_stays_inside_its_buffers(dev, outer, rows, inner):
+    y = hostgen.random_tensor([outer, rows, inner], 3)
+    yb, yp = dev.guarded_input(y)
+
+    def launch():
+        gb, gp = dev.guarded_output(rows * rows)
+        check(lib.tp_dev_gram(dev.ctx._h, yp, ctypes.c_size_t(outer), ctypes.c_size_t(rows), ctypes.c_size_t(inner), gp))
+        return dev.payload(gb, rows * rows)
+    got = repeat_identical(dev, launch, rows * rows).reshape(rows, rows)
+    u = ho.unfold(y, 1)
+    want = u @ u.T
+    assert np.all(np.isfinite(got))
+    assert np.max(np.abs(got - want)) <= 64 * EPS * outer * inner * np.max(np.abs(y)) ** 2
+    assert np.array_equal(got, got.T)
+
+
+@pytest.mark.parametrize("rows,k", [(19, 1), (48, 8), (57, 3), (96, 10), (131, 17), (200, 20)])
+def test_one_launch_leaf_solve_stays_inside_its_buffers(dev, rows, k):
+    rng = np.random.default_rng(rows)
+    b = k + 8
+    y = rng.standard_normal((rows, k)) @ rng.standard_normal((k, 6 * rows)) + 1e-3 * rng.standard_normal((rows, 6 * rows))
+    g = y @ y.T
+    start, _ = np.linalg.qr(rng.standard_normal((rows, k)))
+    gb, gp = dev.guarded_input(np.asfortranarray(g).ravel(order="F"))
+    sb, sp = dev.guarded_input(np.asfortranarray(start).ravel(order="F"))
+    status = dev.torch.zeros(8, dtype=dev.torch.int32, device="cuda")
+    ip = ctypes.cast(status.data_ptr(), ctypes.POINTER(ctypes.c_int))
+    vp = ctypes.cast(status.data_ptr() + 16, ctypes.POINTER(ctypes.c_int))
+
+    def launch():
+        rb, rp = dev.guarded_output(rows * b)
+        tb, tp = dev.guarded_output(b)
+        fb, fp = dev.guarded_output(rows * k)
+        db, dp = dev.guarded_output(16)
+        status.zero_()
+        check(lib.tp_dev_leaf_solve_fused(dev.ctx._h, gp, ctypes.c_size_t(rows), k, sp, 0, rp, tp, fp, ip, vp, dp))
+        dev.payload(db, 16)
+        return np.concatenate([dev.payload(rb, rows * b), dev.payload(tb, b), dev.payload(fb, rows * k)])
+    got = repeat_identical(dev, launch, rows * b + b + rows * k)
+    assert np.all(np.isfinite(got))
+    factor = got[rows * b + b:].reshape(rows, k, order="F")
+    w, v = np.linalg.eigh(g)
+    ref = v[:, ::-1][:, :k]
+    assert np.linalg.svd(factor - ref @ (ref.T @ factor), compute_uv=False).max() < 1e-10
+    ints = status.cpu().tolist()
+    assert ints[4] == 0 and ints[5] == 0            # certified, no factorisation failure
+
+
+def test_box_copy_slot_sum_and_assembly_stay_inside_their_buffers(dev):
+    rng = np.random.default_rng(9)
+    # box copy between two tensors of different extents
+    src = rng.standard_normal((7, 9, 11))
+    sb, sp = dev.guarded_input(src)
+    dst_dims, box, slo, dlo = [5, 12, 8], [3, 4, 5], [2, 1, 6], [1, 7, 0]
+
+    def copy():
+        db, dp = dev.guarded_output(int(np.prod(dst_dims)))
+        check(lib.tp_dev_copy_box(dev.ctx._h, dp, size_array(dst_dims), size_array(dlo), sp, size_array(src.shape),
+                                  size_array(slo), size_array(box), 3))
+        return dev.payload(db, int(np.prod(dst_dims)))
+    got = repeat_identical(dev, copy, int(np.prod(dst_dims))).reshape(dst_dims)
+    want = np.full(dst_dims, CANARY)
+    want[1:4, 7:11, 0:5] = src[2:5, 1:5, 6:11]
+    assert np.array_equal(got, want)
+    # ordered sum of slots
+    parts = [rng.standard_normal(1001) for _ in range(5)]
+    bufs = [dev.guarded_input(p) for p in parts]
+    ptrs = (dbl_p * 5)(*[b[1] for b in bufs])
+
+    def add():
+        ob, op = dev.guarded_output(1001)
+        check(lib.tp_dev_reduce_slots(dev.ctx._h, op, ptrs, 5, ctypes.c_size_t(1001)))
+        return dev.payload(ob, 1001)
+    got = repeat_identical(dev, add, 1001)
+    want = parts[0].copy()
+    for p in parts[1:]:
+        want = want + p
+    assert np.array_equal(got, want)
+    # a mode slice dropped into the full tensor
+    piece = rng.standard_normal((3, 4, 5))
+    pb, pp = dev.guarded_input(piece)
+
+    def assemble():
+        fb, fp = dev.guarded_output(3 * 10 * 5)
+        check(lib.tp_dev_assemble_mode(dev.ctx._h, fp, ctypes.c_size_t(3), ctypes.c_size_t(10), ctypes.c_size_t(5), pp,
+                                       ctypes.c_size_t(6), ctypes.c_size_t(4)))
+        return dev.payload(fb, 150)
+    got = repeat_identical(dev, assemble, 150).reshape(3, 10, 5)
+    want = np.full((3, 10, 5), CANARY)
+    want[:, 6:10, :] = piece
+    assert np.array_equal(got, want)

@@ -72,6 +72,7 @@ const std::vector<Command>& commands() {
         {"--tree", false, "tree strategy (default fits the scheme)"},
         {"--scheme", false, "jacobi|gauss-seidel (default gauss-seidel)"},
         {"--sweeps", false, "sweep count (default 5)"},
+        {"--init", false, "starting factors: random (default, as the reference) or sthosvd"},
         {"--procs", false, "run on a processor grid of this many GPUs (jacobi only; default 1)"},
         {"--grid", false, "grid for --procs, e.g. 1x1x8 (default: the volume-optimal static grid)"},
         {"--dynamic", true, "with --procs: per-node grids (optimal_dynamic_scheme) instead of one static grid"},
@@ -380,7 +381,9 @@ int cmd_hooi(const Args& a) {
 
   // same sequence as the reference (random start, error, then sweep / error pairs); the tensor is uploaded once
   // and every sweep and error evaluation runs on the device
-  const tp::Decomposition start = tp::random_decomposition(t, s, seed);
+  const std::string init = a.get("--init", "random");
+  if (init != "random" && init != "sthosvd") tp::fail(tp::Errc::bad_argument, "--init must be random or sthosvd");
+  const tp::Decomposition start = init == "sthosvd" ? tp::sthosvd(t, s) : tp::random_decomposition(t, s, seed);
   tp::json steps = tp::json::array();
   std::string text;
   char line[160];
