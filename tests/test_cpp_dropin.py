@@ -70,3 +70,15 @@ def test_grid_executor_through_cpp_headers(dropin):
         assert fields["gap_ok"] == "1" and fields["fit_ok"] == "1" and fields["macs_ok"] == "1", line
         assert int(fields["shipped"]) == int(fields["model"]) > 0, line
     assert out[2] == "error 6"                     # Errc::invalid_grid
+
+
+def test_supported_api_surface_compiles():
+    """tests/cpp/surface_check.cpp names every entry point provided under the reference's header names with the
+    reference's signature; its header comment lists what is deliberately absent (bench.hpp statistics, the tree
+    enumerator, brute_force_dynamic)."""
+    exe = os.path.join(ROOT, "build", "surface_check")
+    os.makedirs(os.path.dirname(exe), exist_ok=True)
+    subprocess.check_call(["g++", "-std=c++20", "-O0", "-Wall", "-Wextra", "-Werror", "-I" + os.path.join(ROOT, "include"),
+                           os.path.join(ROOT, "tests", "cpp", "surface_check.cpp"), "-o", exe, "-L" + LIBDIR,
+                           "-ltuckerplan_b200", "-Wl,-rpath," + LIBDIR])
+    assert subprocess.run([exe]).returncode == 0
