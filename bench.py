@@ -578,10 +578,22 @@ def run_b200(args):
                      "roofline_frac_nominal_peaks": sum(r["t_roof_s"] for r in tree_roofline(spec, tree, cost, 40.0, 8000.0))
                                                     * 1e3 / ttm_ms,
                      "nominal_peaks": {"fp64_tflops": 40.0, "hbm_gbs": 8000.0},
+                     # the FP64 pipe's own ceiling: one DMMA.8x8x4 (512 flop) per 4 cycles per SM at the sampled clock
+                     # (37.1 TF/s measured by tools/microbench/fp64_peaks.cu, profiles/r01_fp64_peaks.jsonl)
+                     "dmma_issue_ceiling_tflops": (torch.cuda.get_device_properties(0).multi_processor_count * 128
+                                                   * (clocks.get("sm_mhz") or 1965.0) * 1e6 / 1e12),
                      "per_node": [{k: r[k] for k in ("node", "mode", "bound", "ms", "tflops", "frac")} for r in rows]},
         "ttm_tree_overlapped_ms": sum(overlapped_node_ms[r["node"]] for r in rows),
         "serial_schedule": {"ms_per_step": float(np.mean(serial_ms)), "phases_ms": serial_phases,
                             "note": "steady state: one cold sweep from the start factors precedes the K timed ones"},
+        # what of the leaf solves is NOT hidden behind the tree: the timed step minus the serial pass's tree, Gram
+        # and core time (the summed evd_ms of the serial pass counts every leaf in full; on the side streams they
+        # overlap each other and the tree, and only this remainder is on the critical path)
+        "critical_path": {"step_ms": ms_per_step, "tree_ms": serial_phases.get("tree_ms"),
+                          "gram_ms": serial_phases.get("gram_ms"), "core_ms": serial_phases.get("core_ms"),
+                          "leaf_solves_summed_ms": serial_phases.get("evd_ms"),
+                          "leaf_solves_exposed_ms": max(0.0, ms_per_step - serial_phases.get("tree_ms", 0.0)
+                                                        - serial_phases.get("gram_ms", 0.0) - serial_phases.get("core_ms", 0.0))},
         "run_from_start": {"per_iteration_ms": from_start, "iterations": len(from_start),
                            "mean_ms": float(np.mean(from_start[:cfg.iterations])),
                            "note": "one HOOI run from the random orthonormal start, every iteration timed (CUDA "
