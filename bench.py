@@ -774,6 +774,9 @@ def main(argv=None):
     ap.add_argument("--executor", default="ranks", choices=["ranks", "inprocess"],
                     help="N > 1: 'ranks' = one process per GPU over NCCL (torch.distributed); 'inprocess' = the C++ grid "
                          "executor (tp_grid_*) driving all GPUs from one process over peer memory")
+    ap.add_argument("--peer-slots", action="store_true",
+                    help="with --executor ranks: reduce-scatters as direct stores into NVLink-mapped symmetric-memory "
+                         "slots (torch.distributed._symmetric_memory) instead of grouped send/recv")
     ap.add_argument("--virtual-ranks", action="store_true",
                     help="with --executor inprocess: allow more ranks than GPUs (functional run on a small box)")
     ap.add_argument("--backend", default="cuda", choices=["cuda", "numpy-test"],

@@ -367,6 +367,16 @@ int tp_dev_leaf_solve_warm(tp_ctx* ctx, double* gram, size_t rows, int k, const 
 int tp_dev_leaf_solve_begin(tp_ctx* ctx, double* gram, size_t rows, int k, const double* start, double* factor,
                             int* flag, int* info, int lane);
 int tp_dev_leaf_solve_finish(tp_ctx* ctx, int lane, double* factor, int* flag, int* info, int* used_fast);
+/* _begin with flags.  TP_LEAF_CONTINUE: when the lane's previous solve was of the same gram buffer and shape and was
+ * accepted with its certificate, its Ritz vectors (all K_n + 8 of them) are the start block instead of `start` -- the
+ * warm start of consecutive sweeps, as a resident plan does it.  The result then depends on the lane's history, which
+ * is fine where one rank solves a leaf and shares the factor (the grid executor), not where replicas must agree bit
+ * for bit. */
+/* tp_dev_leaf_solve_reset forgets every lane's history (a new run: results again depend on the arguments only). */
+enum { TP_LEAF_CONTINUE = 1 };
+int tp_dev_leaf_solve_reset(tp_ctx* ctx);
+int tp_dev_leaf_solve_begin_ex(tp_ctx* ctx, double* gram, size_t rows, int k, const double* start, double* factor,
+                               int* flag, int* info, int lane, unsigned flags);
 /* The whole certified top-k solve of a small leaf in ONE launch (csrc/leaf_solve_kernels.cu; what tp_plan_sweep uses
  * for leaves with rows <= 512 and k + 8 <= 64): power steps, Rayleigh-Ritz, certificate and the reference's selection
  * rules, rounds repeated on the device until the certificate holds.  All pointers are device pointers.  `start`:

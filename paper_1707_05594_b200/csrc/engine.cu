@@ -74,6 +74,8 @@ struct tp_ctx {
     void* scratch = nullptr;         // LeafScratch
     cudaEvent_t ready = nullptr, done = nullptr;
     bool busy = false, fast = false;
+    bool keep = false;               // TP_LEAF_CONTINUE: an accepted solve leaves its Ritz vectors as the next start
+    bool accepted = false;           // the lane's last solve was accepted with its certificate
     double* gram = nullptr;
     size_t rows = 0;
     int k = 0;
@@ -680,6 +682,7 @@ struct tp_plan {
   int spare_sms = 2;                          // SMs left to the side streams while eigen-solves are in flight
                                               // (measured on C5: 0-2 -> 58.4 ms/iter, 6 -> 58.9, 12 -> 60.0)
   int leaves_in_flight = 0;
+  int one_launch_leaves = 0;                  // leaves whose solve is the single-CTA kernel (leaf_solve_kernels.cu)
   struct PendingLeaf {
     int mode, node;
   };
@@ -764,7 +767,10 @@ void plan_ttm(tp_ctx* ctx, tp_plan* p, const double* x, const std::vector<size_t
   if (spare_sms > 0) {
     const double flops = 2.0 * static_cast<double>(p->spec.K[mode]) * static_cast<double>(outer) *
                          static_cast<double>(dims[mode]) * static_cast<double>(inner);
-    if (flops < p->short_product_flops) spare_sms = std::max(spare_sms, p->spare_sms_short);
+    if (p->one_launch_leaves == p->n)
+      spare_sms = std::max(spare_sms, p->n);  // every solve in flight is one CTA that needs a whole SM to itself
+    else if (flops < p->short_product_flops)
+      spare_sms = std::max(spare_sms, p->spare_sms_short);
   }
   TPB_CUDA(launch_ttm(ctx->stream, x, outer, static_cast<long long>(dims[mode]), inner, p->frag[mode],
                       p->frag_layout[mode], static_cast<long long>(p->spec.K[mode]), out,
@@ -1118,7 +1124,11 @@ void plan_core(tp_ctx* ctx, tp_plan* p, const double* tensor, const std::vector<
     Span s = (carry && !last) ? Span(ctx, p, kTree, p->carry_nodes[i]) : Span(ctx, p, kCore);
     plan_refresh_fragments(ctx, p, m, factors[m]);
     double* dst = last ? p->core : (carry ? p->carry_buf[i] : p->core_tmp[i & 1]);
-    plan_ttm(ctx, p, src, dims, m, dst, (wait_for_leaves && i == 0 && !p->pending.empty()) ? p->spare_sms : 0);
+    // solves of the modes the chain has not waited for yet may still be running on the side streams: the persistent
+    // product grid must leave them SMs (its CTAs would otherwise hold every SM until the product ends, and a solve
+    // queued meanwhile would start only then -- exposed on the critical path of short sweeps)
+    const bool solves_running = wait_for_leaves && !last && (p->leaves_in_flight > 0 || !p->pending.empty());
+    plan_ttm(ctx, p, src, dims, m, dst, solves_running ? p->spare_sms : 0);
     s.close();
     if (wait_for_leaves) plan_flush_pending(ctx, p);
     dims[m] = static_cast<size_t>(p->spec.K[m]);
@@ -2019,6 +2029,14 @@ void jacobi_sequence(tp_ctx* ctx, tp_plan* p, const tp_tensor* t) {
   }
   p->leaves_in_flight = 0;
   p->pending.clear();
+  p->one_launch_leaves = 0;
+  for (int m = 0; m < p->n; ++m) {
+    const long long rows = static_cast<long long>(p->spec.L[m]);
+    const int k = static_cast<int>(p->spec.K[m]);
+    if (p->fast_evd && p->leaf[m].use_fused && p->leaf[m].failures < 2 &&
+        subspace_eligible(rows, k, plan_leaf_columns(p, m)) && leaf_solve_fused_eligible(rows, k, k + kSubspaceOversample))
+      ++p->one_launch_leaves;
+  }
   if (p->arrival && p->arrival->row_end.size() > 1 && p->n > 1)
     jacobi_walk_streamed_root(ctx, p, t->data, dims);
   else
@@ -2613,6 +2631,11 @@ static void reserve_iteration_buffers(tp_ctx* ctx, LeafScratch& s, long long row
 // the two calls gram, start, factor, flag and info must stay untouched.  One solve in flight per lane.
 int tp_dev_leaf_solve_begin(tp_ctx* ctx, double* gram, size_t rows, int k, const double* start, double* factor,
                             int* flag, int* info, int lane_index) {
+  return tp_dev_leaf_solve_begin_ex(ctx, gram, rows, k, start, factor, flag, info, lane_index, 0);
+}
+
+int tp_dev_leaf_solve_begin_ex(tp_ctx* ctx, double* gram, size_t rows, int k, const double* start, double* factor,
+                               int* flag, int* info, int lane_index, unsigned flags) {
   return guarded([&] {
     bind(ctx);
     if (!gram || !factor || !flag || !info) raise(TP_ERR_BAD_ARGUMENT, "null pointer");
@@ -2637,7 +2660,10 @@ int tp_dev_leaf_solve_begin(tp_ctx* ctx, double* gram, size_t rows, int k, const
     if (lane.fast) {
       int* const saved_flag = s.flag;
       s.flag = flag;
-      s.last_ritz = nullptr;  // a function of the arguments only
+      // by default the result is a function of the arguments only; with TP_LEAF_CONTINUE the lane's previous,
+      // accepted solve of the same buffer and shape supplies the start block (its Ritz vectors), as a plan does
+      lane.keep = (flags & TP_LEAF_CONTINUE) != 0;
+      if (!(lane.keep && lane.accepted && lane.gram == gram && lane.rows == rows && lane.k == k)) s.last_ritz = nullptr;
       leaf_solve_subspace(ctx, s, gram, static_cast<long long>(rows), k, start, factor, lane_index);
       s.flag = saved_flag;
       s.fast_used = false;
@@ -2653,6 +2679,16 @@ int tp_dev_leaf_solve_begin(tp_ctx* ctx, double* gram, size_t rows, int k, const
     lane.gram = gram;
     lane.rows = rows;
     lane.k = k;
+  });
+}
+
+int tp_dev_leaf_solve_reset(tp_ctx* ctx) {
+  return guarded([&] {
+    if (!ctx) raise(TP_ERR_BAD_ARGUMENT, "null context");
+    for (tp_ctx::Lane& lane : ctx->lanes) {
+      if (lane.busy) raise(TP_ERR_BAD_ARGUMENT, "a solve is still in flight");
+      lane.accepted = false;
+    }
   });
 }
 
@@ -2673,7 +2709,7 @@ int tp_dev_leaf_solve_finish(tp_ctx* ctx, int lane_index, double* factor, int* f
     TPB_CUDA(cudaMemcpyAsync(&host[2], flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     TPB_CUDA(cudaStreamSynchronize(ctx->stream));
     // only the residual bound missed: iterate on from the Ritz vectors reached (as the plan does), main stream
-    for (int round = 0; round < 3 && host[0] != 0 && host[1] == 0 && host[2] == 0 && s.last_ritz; ++round) {
+    for (int round = 0; round < 3 && (host[0] & 1) != 0 && host[1] == 0 && host[2] == 0 && s.last_ritz; ++round) {
       int* const saved_flag = s.flag;
       s.flag = flag;
       leaf_solve_subspace(ctx, s, lane.gram, static_cast<long long>(lane.rows), lane.k, factor, factor, -1);
@@ -2683,8 +2719,9 @@ int tp_dev_leaf_solve_finish(tp_ctx* ctx, int lane_index, double* factor, int* f
       TPB_CUDA(cudaMemcpyAsync(&host[2], flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
       TPB_CUDA(cudaStreamSynchronize(ctx->stream));
     }
-    s.last_ritz = nullptr;
-    if (host[0] == 0 && host[1] == 0 && host[2] == 0) {
+    lane.accepted = host[0] == 0 && host[1] == 0 && host[2] == 0;
+    if (!(lane.keep && lane.accepted)) s.last_ritz = nullptr;
+    if (lane.accepted) {
       TPB_CUDA(cudaMemsetAsync(info, 0, sizeof(int), ctx->stream));
       if (used_fast) *used_fast = 1;
       return;

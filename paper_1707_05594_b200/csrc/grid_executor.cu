@@ -262,6 +262,8 @@ void wait(const Rank& r, cudaEvent_t e) {
 
 // Products kept from the last core chain are functions of (tensor, factors): forget them when either changes.
 void invalidate(tp_grid* g) {
+  for (Rank& rk : g->ranks)
+    if (rk.ctx) ok(tp_dev_leaf_solve_reset(rk.ctx));  // a new run starts its solves from its own factors
   for (NodeState& st : g->nodes) {
     st.carried = false;
     st.pending_ttm = st.pending_regrid = 0;
@@ -434,8 +436,9 @@ void leaf(tp_grid* g, int mode, const Piece& y) {
     }
     ok(tp_dev_reduce_slots(owner.ctx, owner.gram_sum[mode], parts.data(), static_cast<int>(parts.size()), rows * rows));
   }
-  ok(tp_dev_leaf_solve_begin(owner.ctx, owner.gram_sum[mode], rows, k, owner.cur[mode], owner.fresh[mode],
-                             owner.status[mode], owner.status[mode] + 1, job.lane));
+  // the same leaf lands on the same owner and lane every sweep, so the lane's accepted Ritz vectors start the next one
+  ok(tp_dev_leaf_solve_begin_ex(owner.ctx, owner.gram_sum[mode], rows, k, owner.cur[mode], owner.fresh[mode],
+                                owner.status[mode], owner.status[mode] + 1, job.lane, TP_LEAF_CONTINUE));
   job.begun = true;
   job.collected = false;
 }

@@ -280,7 +280,7 @@ class DistributedHooi:
     (grid_dynamic.hpp: `q` may be a planner.DynamicGridScheme; the tensor and the core live on its root grid, a node
     whose grid differs from its parent's first redistributes its input)."""
 
-    def __init__(self, ops, spec: P.ProblemSpec, tree: P.TtmTree, q, rank: int):
+    def __init__(self, ops, spec: P.ProblemSpec, tree: P.TtmTree, q, rank: int, async_solve: bool = True):
         self.ops, self.spec, self.tree, self.rank = ops, spec, tree, int(rank)
         scheme = q if isinstance(q, P.DynamicGridScheme) else P.uniform_scheme(tree, q)
         self.scheme = scheme
@@ -307,7 +307,7 @@ class DistributedHooi:
         # chain first needs the factor, so they overlap the rest of the tree; with more than one rank each leaf has
         # one owner rank that solves it and broadcasts the factor (replicating every solve on every rank would put
         # P copies of the same latency-bound work on the critical path: at C5 / P = 8 more than the tree itself).
-        self.async_solve = hasattr(ops, "leaf_solve_begin") and os.environ.get("TPB_GRID_SYNC_SOLVE") != "1"
+        self.async_solve = async_solve and hasattr(ops, "leaf_solve_begin")
         self.owner_solve = self.layout.procs > 1
         self.peer_scatter = True      # use peer-slot stores for reduce-scatters where the runner offers them
         self.scatter_launches = 0
@@ -614,7 +614,7 @@ class SymmetricSlots:
     on the symmetric-memory signal pads before the stores (the owners are done reading the previous sweep's slots)
     and one after (all stores have landed) replace the send/recv.
 
-    Opt-in (TPB_PEER_SLOTS=1): only one GPU was available while this was written, so it has run at world size 1
+    Opt-in (`bench.py --peer-slots`): only one GPU was available while this was written, so it has run at world size 1
     only (tests/test_distributed.py::test_symmetric_slots_world_size_one)."""
 
     def __init__(self, dist, device):
@@ -970,8 +970,8 @@ def run_bench_rank(args, rank: int, world: int, local_rank: int):
     dh.set_local_tensor_buffer(local)
     f0 = W.start_factors(cfg)
 
-    # TPB_PEER_SLOTS=1: reduce-scatters as direct stores into NVLink-mapped peer slots (see SymmetricSlots)
-    peer_slots = SymmetricSlots(dist, ops.device) if cuda and os.environ.get("TPB_PEER_SLOTS") == "1" else None
+    # --peer-slots: reduce-scatters as direct stores into NVLink-mapped peer slots (see SymmetricSlots)
+    peer_slots = SymmetricSlots(dist, ops.device) if cuda and getattr(args, "peer_slots", False) else None
 
     def run(gen):
         return run_rank(gen, dist, ops, peer_slots=peer_slots)
