@@ -493,12 +493,17 @@ def run_b200(args):
         fbytes = 8 * sum(l * k for l, k in zip(spec.L, spec.K))
         cbytes = 8 * int(np.prod(spec.K))
         iters = cfg.iterations
-        E.hooi_sweep(host_t, spec, E.Decomposition(None, f0), tree, "jacobi", ctx=ctx)  # warm (page tables, lazy init)
+        # warm-up call: creates the context's cached plan and device tensor (allocation, handle and kernel set-up are
+        # one-off costs of a process, reported separately); the timed run below still moves every byte
         ctx.release_cache()
+        w0 = time.perf_counter()
+        E.hooi_sweep(host_t, spec, E.Decomposition(None, f0), tree, "jacobi", ctx=ctx)
+        first_call_s = time.perf_counter() - w0
         ctx.synchronize()
         d = E.Decomposition(None, f0)
         w0 = time.perf_counter()
         for i in range(iters):
+            # call 1 makes no promise: the tensor is uploaded (and the start factors make it a cold sweep)
             d = E.hooi_sweep(host_t, spec, d, tree, "jacobi", ctx=ctx, tensor_unchanged=i > 0)
         run_s = (time.perf_counter() - w0) / iters
         # the by-value run against the resident run of the same iterations: same subspaces to rounding
@@ -528,7 +533,9 @@ def run_b200(args):
                "h2d_bytes_per_step": (total * 8) // iters + fbytes, "d2h_bytes_per_step": fbytes + cbytes,
                "host_memory": "pinned",
                "what": "whole run of the config's %d iterations through the by-value C-ABI call, upload of the tensor "
-                       "(first call) included, later calls with TP_HOST_TENSOR_UNCHANGED; mean per iteration" % iters,
+                       "(first call) included, later calls with TP_HOST_TENSOR_UNCHANGED; mean per iteration; device "
+                       "allocations warm (one earlier call on the same context)" % iters,
+               "first_call_of_a_process_s": first_call_s,
                "max_sin_principal_angle_vs_resident_run": agree,
                "by_value_every_call": {"value": every_s, "unit": "s/iter", "h2d_bytes_per_step": total * 8 + fbytes,
                                        "d2h_bytes_per_step": fbytes + cbytes, "calls": every_steps},
