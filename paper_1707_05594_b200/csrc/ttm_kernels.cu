@@ -291,6 +291,9 @@ __global__ void __launch_bounds__(kThreads, (KT * NT <= 20) ? 2 : 1) ttm_dmma_ke
     const double* const xd = xs + cons_stage * XS + (warp * NT) * (KC * 8);
     const double* const md = ms + cons_stage * MS + lane;
     cons_stage = (cons_stage + 1 == STAGES) ? 0 : cons_stage + 1;
+    bool live[NT];
+#pragma unroll
+    for (int j = 0; j < NT; ++j) live[j] = tile_lim[cons_j % RING][warp * NT + j] != 0;
 #pragma unroll
     for (int s = 0; s < KC / 4; ++s) {
       double a[KT];
@@ -299,6 +302,7 @@ __global__ void __launch_bounds__(kThreads, (KT * NT <= 20) ? 2 : 1) ttm_dmma_ke
       const int l = 4 * s + frag_k;
 #pragma unroll
       for (int j = 0; j < NT; ++j) {
+        if (!live[j]) continue;  // n-tile past the end: nothing but zeros (uniform in the warp)
         double b;
         if (LAST)
           b = xd[j * (KC * 8) + frag_n * KC + (l ^ ((frag_n & 3) << 2))];

@@ -205,6 +205,11 @@ __global__ void __launch_bounds__(kThreads, (KT * NT <= 12) ? 2 : 1)
   int stage = 0;
   unsigned parity = 0;
   for (long long j = 0; j < my_tiles; ++j) {
+    // n-tiles of this warp whose box lies inside the CTA's range: the balanced partition hands small problems less
+    // than a full tile per CTA, and multiplying the zero-filled rest would cost as many DMMAs as the real part
+    bool live[NT];
+#pragma unroll
+    for (int jj = 0; jj < NT; ++jj) live[jj] = first_box(j) + ((cw * NT + jj) >> 1) < cta_end;
     for (int chunk = 0; chunk < p.n_chunks; ++chunk) {
       mbar_wait(&full[stage], parity);
       const double* const xd = xs + stage * XS;
@@ -216,6 +221,7 @@ __global__ void __launch_bounds__(kThreads, (KT * NT <= 12) ? 2 : 1)
         for (int i = 0; i < KT; ++i) a[i] = md[(s * KT + i) * 32];
 #pragma unroll
         for (int jj = 0; jj < NT; ++jj) {
+          if (!live[jj]) continue;  // uniform in the warp
           const int t = cw * NT + jj;
           const double b = box_elem(xd + (t >> 1) * (kKC * 16), s, t & 1);
 #pragma unroll
