@@ -206,4 +206,190 @@ __device__ int jacobi_sweeps_smem(double* __restrict__ h, double* __restrict__ v
   return sweep;
 }
 
+__device__ __forceinline__ double rsqrt_seed(double x) {  // ~23 bits, straight from the special function unit
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  return y;
+}
+
+// The same iteration with ONE barrier per step and step-independent addressing, for blocks of at most 64 (every
+// rotation of a step fits one lane of a warp), run by the first kActiveWarps warps of the CTA only; the others wait at
+// the closing barrier.  A step of this kernel is bound by the number of instructions its warps issue and by one chain
+// of dependent operations, so both are kept short:
+//   * pairs sit at fixed positions (2t, 2t + 1); instead of re-pairing indices, a step writes the rotated matrix into
+//     a second buffer at positions moved by the round-robin permutation pi (position 0 stays, the other m - 1 cycle),
+//     so every address is computed once, before the first step.  pi^(m - 1) = id: after a whole sweep everything is
+//     back in place.  h/h2 and v/v2 are the two buffers of H (m x m) and V; every entry is written exactly once per
+//     step, so nothing a slower warp still reads is overwritten: read -> rotate -> write -> barrier;
+//   * every active warp forms all m/2 rotations of the step itself, in its lanes, instead of waiting for them to be
+//     published.
+// The caller scales h so that its largest entry is of order one (a power of two: exact); pairs whose
+// (h_qq - h_pp)^2 + (2 h_pq)^2 underflows against that are left alone (the zero row and column that pad an odd block
+// rotate by the identity: b2 = 0 gives s = 0, c = 1).  With cos 2t = |a| / r and sin 2t = b2 / r,
+//     c = sqrt((1 + cos 2t) / 2),   s = sgn(a) sin 2t / (2 c),
+// which has no cancellation and needs two reciprocal square roots (hardware seed, Newton in double); c^2 + s^2 = 1 to
+// rounding whatever the seed's error, so every step is an exact similarity transform, and the rotated h_pq is
+// computed, not set to zero.  h, h2, v, v2 16-byte aligned, m even.  On return (after a CTA barrier) the result is in
+// h and v; same return value as above; prof: [0] convergence checks, [2] steps.
+template <int kThreads, int kBlockCap, int kActiveWarps>
+__device__ int jacobi_pingpong_smem(double* h, double* h2, double* v, double* v2, int b, int m,
+                                    long long* prof = nullptr) {
+  static_assert(kBlockCap <= 64, "one rotation per lane");
+  static_assert(kActiveWarps * 32 <= kThreads, "active warps are warps of the CTA");
+  const int half = m / 2;
+  constexpr int kRowPasses = (kBlockCap + 31) / 32;
+  constexpr int kMaxPairs = (kBlockCap / 2 + kActiveWarps - 1) / kActiveWarps;  // column pairs of a warp
+  __shared__ double red[2 * kActiveWarps];
+  __shared__ int sweeps_used;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  auto team_barrier = [] { asm volatile("bar.sync 1, %0;\n" ::"n"(kActiveWarps * 32) : "memory"); };
+  // where the content of position x goes in a step
+  auto moved = [&](int x) {
+    if (x != 0 && half > 1) x = (x & 1) ? (x == 1 ? 2 : x - 2) : (x == m - 2 ? m - 1 : x + 2);
+    return x;
+  };
+
+  if (warp < kActiveWarps) {
+    double* hc = h;
+    double* hn = h2;
+    double* vc = v;
+    double* vn = v2;
+    long long mark = prof ? clock64() : 0;
+    auto lap = [&](int which) {
+      if (prof && tid == 0) {
+        const long long now = clock64();
+        prof[which] += now - mark;
+        mark = now;
+      }
+    };
+    // this lane's row pair (2 lane, 2 lane + 1): offsets of its diagonal block and where its rows go
+    const bool rot_on = lane < half;
+    const int my = rot_on ? lane : 0;
+    const int diag_off = 2 * my * m + 2 * my;
+    const int to_p = moved(2 * my), to_q = moved(2 * my + 1);
+    // this warp's column pairs: read offsets and write offsets
+    int col_off[kMaxPairs], to_pc[kMaxPairs], to_qc[kMaxPairs];
+#pragma unroll
+    for (int u = 0; u < kMaxPairs; ++u) {
+      const int tj = warp + u * kActiveWarps;
+      const int j = tj < half ? tj : 0;
+      col_off[u] = 2 * j * m;
+      to_pc[u] = moved(2 * j) * m;
+      to_qc[u] = moved(2 * j + 1) * m;
+    }
+    int sweep = 0;
+    for (; sweep < kJacobiMaxSweeps; ++sweep) {
+      double off = 0.0, all = 0.0;
+      for (int col = warp; col < m; col += kActiveWarps)
+        for (int row = lane; row < m; row += 32) {
+          const double x = hc[col * m + row] * hc[col * m + row];
+          all += x;
+          if (row != col) off += x;
+        }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        off += __shfl_xor_sync(0xffffffffu, off, o);
+        all += __shfl_xor_sync(0xffffffffu, all, o);
+      }
+      if (lane == 0) {
+        red[warp] = off;
+        red[kActiveWarps + warp] = all;
+      }
+      team_barrier();
+      off = 0.0;
+      all = 0.0;
+      for (int i = 0; i < kActiveWarps; ++i) {
+        off += red[i];
+        all += red[kActiveWarps + i];
+      }
+      team_barrier();
+      lap(0);
+      if (off <= (b * DBL_EPSILON) * (b * DBL_EPSILON) * all) break;  // uniform: same sums in every thread
+      if (!(all <= DBL_MAX)) {  // NaN / Inf input (a failed factorisation upstream): nothing to converge to
+        sweep = kJacobiMaxSweeps;
+        break;
+      }
+
+      for (int step = 0; step < m - 1; ++step) {
+        // operands first (they do not depend on the rotations): all loads of a step are in flight before its first
+        // store, and the column pairs of a warp are not serialised behind one another
+        double2 top[kMaxPairs], bot[kMaxPairs];  // (row p_i, row q_i) of column p_j, of column q_j
+        double vx[kMaxPairs][kRowPasses], vy[kMaxPairs][kRowPasses];
+#pragma unroll
+        for (int u = 0; u < kMaxPairs; ++u) {
+          if (warp + u * kActiveWarps >= half) break;  // uniform in the warp
+          const double* const cp = hc + col_off[u] + 2 * my;
+          top[u] = *reinterpret_cast<const double2*>(cp);
+          bot[u] = *reinterpret_cast<const double2*>(cp + m);
+#pragma unroll
+          for (int r = 0; r < kRowPasses; ++r) {
+            const int row = lane + 32 * r;
+            vx[u][r] = row < m ? vc[col_off[u] + row] : 0.0;
+            vy[u][r] = row < m ? vc[col_off[u] + m + row] : 0.0;
+          }
+        }
+        double ci = 1.0, si = 0.0;
+        {
+          const double2 pq = *reinterpret_cast<const double2*>(hc + diag_off);  // h_pp, h_qp
+          const double a = hc[diag_off + m + 1] - pq.x, b2 = 2.0 * pq.y;
+          const double n2 = fma(a, a, b2 * b2);
+          if (rot_on && n2 > 1e-290) {
+            double y = rsqrt_seed(n2);
+            const double hn2 = 0.5 * n2;
+            y = fma(y, fma(-hn2 * y, y, 0.5), y);
+            y = fma(y, fma(-hn2 * y, y, 0.5), y);           // 1 / r
+            const double x = fma(0.5 * fabs(a), y, 0.5);    // cos^2: in [1/2, 1]
+            double w = rsqrt_seed(x);
+            const double hx = 0.5 * x;
+            w = fma(w, fma(-hx * w, w, 0.5), w);
+            w = fma(w, fma(-hx * w, w, 0.5), w);            // 1 / c
+            ci = x * w;
+            si = (a >= 0.0 ? 0.5 : -0.5) * (b2 * y) * w;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kMaxPairs; ++u) {
+          const int tj = warp + u * kActiveWarps;
+          if (tj >= half) break;  // uniform in the warp
+          const double cj = __shfl_sync(0xffffffffu, ci, tj), sj = __shfl_sync(0xffffffffu, si, tj);
+          if (rot_on) {
+            // columns (H J_j), then rows (J_i^T ...)
+            const double a1 = cj * top[u].x - sj * bot[u].x, b1 = sj * top[u].x + cj * bot[u].x;
+            const double c1 = cj * top[u].y - sj * bot[u].y, d1 = sj * top[u].y + cj * bot[u].y;
+            hn[to_pc[u] + to_p] = ci * a1 - si * c1;
+            hn[to_pc[u] + to_q] = si * a1 + ci * c1;
+            hn[to_qc[u] + to_p] = ci * b1 - si * d1;
+            hn[to_qc[u] + to_q] = si * b1 + ci * d1;
+          }
+#pragma unroll
+          for (int r = 0; r < kRowPasses; ++r) {
+            const int row = lane + 32 * r;
+            if (row < m) {
+              vn[to_pc[u] + row] = cj * vx[u][r] - sj * vy[u][r];
+              vn[to_qc[u] + row] = sj * vx[u][r] + cj * vy[u][r];
+            }
+          }
+        }
+        team_barrier();
+        double* t = hc;
+        hc = hn;
+        hn = t;
+        t = vc;
+        vc = vn;
+        vn = t;
+      }
+      lap(2);
+    }
+    if (hc != h) {  // uniform: an odd number of steps in all
+      for (int e = tid; e < m * m; e += kActiveWarps * 32) {
+        h[e] = hc[e];
+        v[e] = vc[e];
+      }
+    }
+    if (tid == 0) sweeps_used = sweep;
+  }
+  __syncthreads();
+  return sweeps_used;
+}
+
 }  // namespace tpb

@@ -36,7 +36,6 @@ namespace {
 constexpr int kFusedThreads = 512;
 constexpr int kFusedWarps = kFusedThreads / 32;
 constexpr int kFusedMaxRows = 512;
-constexpr int kFusedMaxRowBlocks = kFusedMaxRows / 32;
 
 struct FusedParams {
   const double* __restrict__ gram;   // rows x rows, symmetric, full storage
@@ -72,116 +71,176 @@ __device__ __forceinline__ double filler_value(unsigned long long index, unsigne
   return static_cast<double>(z >> 11) * (1.0 / 9007199254740992.0) - 0.5;
 }
 
-// out (rows x b, leading dimension ld, shared) = G * in (shared), G symmetric (column l doubles as row l).
-// A thread owns up to kItems tiles of two rows by eight columns (16 accumulators: per contraction index one 128-bit
-// load of the row pair and eight broadcast loads feed 16 FMAs, which keeps the product on the FP64 pipe rather than on
-// shared-memory bandwidth); a warp covers 64 consecutive rows of one column group.  Two sources of G:
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// Every product of the solve runs on the FP64 tensor pipe (DMMA.8x8x4), fragments straight from shared memory:
+//   lane (g = lane / 4, t = lane % 4) holds A(row g, k t), B(k t, column g), C(row g, columns 2t and 2t + 1).
+// Leading dimensions are chosen so that a fragment load is conflict free: the rows x b blocks (Q, Z) have
+// ld = 4 (mod 8), ld >= rows -- eight columns a multiple of 32 bytes apart and four consecutive rows each -- and the
+// columns of G sit lda = 8 (mod 16) apart -- four columns, eight consecutive rows each.  Rows [rows, ld) of Q and Z are
+// kept zero, so contractions over the rows may run to the next multiple of four unguarded.
+constexpr int kRing = 3;  // streamed G: slabs of columns through a ring of shared-memory buffers
+constexpr int kGramSlack = 8;  // doubles behind the G buffer: the last m-tile may read up to 7 rows past a column
+
+__host__ __device__ inline int block_ld(int rows) { return rows + ((4 - rows % 8) + 8) % 8; }
+__host__ __device__ inline int gram_ld(int rows) { return rows + ((8 - rows % 16) + 16) % 16; }
+
+// acc += A[:, 0 .. width) * B[l0 .. l0 + width, :]  for the first MTA of the m-tiles warp, warp + 16, ... and the first
+// NTA n-tiles (both compile-time: the loop below is straight-line code, no guard around a DMMA).
+// A: column kk at a_cols + kk * lda; B: columns ldb apart, entry (l, c) at bm[c * ldb + l].
+// Rows of A beyond `rows` and columns of B beyond the block are read as whatever shared memory holds there (inside
+// the allocation): a row of the product depends on its own row of A only and a column on its own column of B, and
+// dmma_store drops exactly those rows and columns.  Only the ragged end of the contraction is guarded.
+template <int MT, int NT, int MTA, int NTA>
+__device__ __forceinline__ void dmma_accumulate_fixed(double (&acc)[MT][NT][2], const double* __restrict__ a_cols,
+                                                      int lda, int width, const double* __restrict__ bm, int ldb,
+                                                      int l0) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const double* bp = bm + g * ldb + l0 + t;
+  const double* ap = a_cols + t * lda + 8 * warp + g;
+  const int tile_stride = 8 * ldb;
+  const int a_step = 4 * lda;
+  const int whole = width & ~3;
+#pragma unroll 2
+  for (int kk = 0; kk < whole; kk += 4) {
+    double bf[NTA], af[MTA];
+#pragma unroll
+    for (int j = 0; j < NTA; ++j) bf[j] = bp[j * tile_stride];
+#pragma unroll
+    for (int i = 0; i < MTA; ++i) af[i] = ap[8 * kFusedWarps * i];
+#pragma unroll
+    for (int i = 0; i < MTA; ++i)
+#pragma unroll
+      for (int j = 0; j < NTA; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    bp += 4;
+    ap += a_step;
+  }
+  if (whole < width) {  // uniform
+    const bool kin = whole + t < width;
+    double bf[NTA], af[MTA];
+#pragma unroll
+    for (int j = 0; j < NTA; ++j) bf[j] = kin ? bp[j * tile_stride] : 0.0;
+#pragma unroll
+    for (int i = 0; i < MTA; ++i) af[i] = kin ? ap[8 * kFusedWarps * i] : 0.0;
+#pragma unroll
+    for (int i = 0; i < MTA; ++i)
+#pragma unroll
+      for (int j = 0; j < NTA; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+  }
+}
+
+template <int MT, int NT, int NTA>
+__device__ __forceinline__ void dmma_accumulate_rows(double (&acc)[MT][NT][2], const double* __restrict__ a_cols,
+                                                     int lda, int width, const double* __restrict__ bm, int ldb,
+                                                     int l0, int mt_mine) {
+  if constexpr (MT * NTA <= 16) {
+    switch (mt_mine) {  // uniform in the warp
+      case 1: dmma_accumulate_fixed<MT, NT, 1, NTA>(acc, a_cols, lda, width, bm, ldb, l0); break;
+      case 2: if constexpr (MT >= 2) dmma_accumulate_fixed<MT, NT, 2, NTA>(acc, a_cols, lda, width, bm, ldb, l0); break;
+      case 3: if constexpr (MT >= 3) dmma_accumulate_fixed<MT, NT, 3, NTA>(acc, a_cols, lda, width, bm, ldb, l0); break;
+      case 4: if constexpr (MT >= 4) dmma_accumulate_fixed<MT, NT, 4, NTA>(acc, a_cols, lda, width, bm, ldb, l0); break;
+      default: break;
+    }
+  }
+}
+
+// mt_mine: m-tiles of this warp that hold rows of the matrix; n: columns of B
+template <int MT, int NT>
+__device__ __forceinline__ void dmma_accumulate(double (&acc)[MT][NT][2], const double* __restrict__ a_cols, int lda,
+                                                int width, const double* __restrict__ bm, int ldb, int n, int l0,
+                                                int mt_mine) {
+  switch ((n + 7) / 8) {  // uniform in the CTA
+    case 1: dmma_accumulate_rows<MT, NT, 1>(acc, a_cols, lda, width, bm, ldb, l0, mt_mine); break;
+    case 2: if constexpr (NT >= 2) dmma_accumulate_rows<MT, NT, 2>(acc, a_cols, lda, width, bm, ldb, l0, mt_mine); break;
+    case 3: if constexpr (NT >= 3) dmma_accumulate_rows<MT, NT, 3>(acc, a_cols, lda, width, bm, ldb, l0, mt_mine); break;
+    case 4: if constexpr (NT >= 4) dmma_accumulate_rows<MT, NT, 4>(acc, a_cols, lda, width, bm, ldb, l0, mt_mine); break;
+    case 5: if constexpr (NT >= 5) dmma_accumulate_rows<MT, NT, 5>(acc, a_cols, lda, width, bm, ldb, l0, mt_mine); break;
+    case 6: if constexpr (NT >= 6) dmma_accumulate_rows<MT, NT, 6>(acc, a_cols, lda, width, bm, ldb, l0, mt_mine); break;
+    case 7: if constexpr (NT >= 7) dmma_accumulate_rows<MT, NT, 7>(acc, a_cols, lda, width, bm, ldb, l0, mt_mine); break;
+    case 8: if constexpr (NT >= 8) dmma_accumulate_rows<MT, NT, 8>(acc, a_cols, lda, width, bm, ldb, l0, mt_mine); break;
+    default: break;
+  }
+}
+
+__device__ __forceinline__ int warp_m_tiles(int rows) {  // m-tiles warp, warp + 16, ... below ceil(rows / 8)
+  const int warp = threadIdx.x >> 5;
+  const int tiles = (rows + 7) / 8;
+  return tiles > warp ? (tiles - warp + kFusedWarps - 1) / kFusedWarps : 0;
+}
+
+// out(r, c) = acc for r < rows, 0 for rows <= r < ld (the padding stays zero), c < n
+template <int MT, int NT>
+__device__ __forceinline__ void dmma_store(const double (&acc)[MT][NT][2], double* __restrict__ out, int rows, int ld,
+                                           int n, int mt_mine) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int i = 0; i < MT; ++i) {
+    const int r = 8 * (warp + kFusedWarps * i) + g;
+    if (i >= mt_mine || r >= ld) continue;
+    const bool real = r < rows;
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      const int c = 8 * j + 2 * t;
+      if (c < n) out[c * ld + r] = real ? acc[i][j][0] : 0.0;
+      if (c + 1 < n) out[(c + 1) * ld + r] = real ? acc[i][j][1] : 0.0;
+    }
+  }
+}
+
+// `count` whole columns of G (from global column first) into shared memory, lda apart; 16-byte copies where the
+// addresses allow
+__device__ __forceinline__ void copy_gram_columns(const double* __restrict__ g, double* __restrict__ dst, int rows,
+                                                  int lda, int first, int count, bool wide) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int col = warp; col < count; col += kFusedWarps) {
+    const double* const src = g + static_cast<size_t>(first + col) * rows;
+    double* const to = dst + col * lda;
+    if (wide)
+      for (int ch = lane; 2 * ch < rows; ch += 32) cp_async16(to + 2 * ch, src + 2 * ch);
+    else
+      for (int i = lane; i < rows; i += 32) cp_async8(to + i, src + i);
+  }
+}
+
+// out (rows x b, shared) = G * in (shared), G symmetric.  Two sources of G:
 //   * resident: the whole matrix was copied into shared memory at kernel start (rows <= ~110: every leaf of
 //     BASELINE configs 2-4) -- the product is pure arithmetic;
 //   * streamed: slabs of `slab` columns through a ring of kRing shared-memory buffers filled by cp.async, kRing - 1
 //     slabs in flight while one is multiplied, so every entry of G is read from L2 exactly once per product.
 // The caller synchronises afterwards.
-constexpr int kRing = 3;
-// Tile shapes: 2 x 8 with one tile per thread for the streamed product (large leaves: enough tiles to fill the CTA,
-// FP64-pipe bound); 2 x 4 with up to three tiles per thread for the resident one (small leaves: more, shorter
-// threads -- at 2 x 8 only a few warps would have work and the product becomes latency bound).
-template <int TC>
-struct TileShape {
-  static constexpr int kItems = TC == 8 ? 1 : 3;
-};
-
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-  const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(gmem) : "memory");
-}
-
-template <int TC>
-struct ProductTiles {
-  int i0[TileShape<TC>::kItems], c0[TileShape<TC>::kItems];
-  bool on[TileShape<TC>::kItems];
-};
-
-template <int TC>
-__device__ __forceinline__ ProductTiles<TC> product_tiles(int rows, int b) {
-  constexpr int kItems = TileShape<TC>::kItems;
-  constexpr int kTileCols = TC;
-  const int row_pairs = (rows + 1) / 2;
-  const int pair_slots = (row_pairs + 31) & ~31;  // whole warps per column group
-  const int n_items = pair_slots * ((b + kTileCols - 1) / kTileCols);
-  ProductTiles<TC> t;
+template <int MT, int NT>
+__device__ void product_gq(const double* __restrict__ g, const double* __restrict__ in, double* __restrict__ out,
+                           double* __restrict__ gbuf, bool resident, bool wide, int slab, int rows, int b, int ld,
+                           int lda) {
+  double acc[MT][NT][2];
 #pragma unroll
-  for (int it = 0; it < kItems; ++it) {
-    const int item = threadIdx.x + it * kFusedThreads;
-    const int cg = item / pair_slots, rp = item - cg * pair_slots;
-    t.on[it] = item < n_items && rp < row_pairs;
-    t.i0[it] = t.on[it] ? 2 * rp : 0;
-    t.c0[it] = t.on[it] ? kTileCols * cg : 0;
-  }
-  return t;
-}
-
-// acc += G[:, l0 .. l0 + width) (columns held in `cols`, leading dimension rows) * in[l0 .. l0 + width, :]
-template <int TC>
-__device__ __forceinline__ void product_accumulate(const ProductTiles<TC>& t,
-                                                   double (&acc)[TileShape<TC>::kItems][2 * TC],
-                                                   const double* __restrict__ cols, const double* __restrict__ in,
-                                                   int rows, int b, int ld, int l0, int width) {
-  constexpr int kItems = TileShape<TC>::kItems;
-  constexpr int kTileCols = TC;
-  // 16-byte loads of the row pair need an even leading dimension (and the buffers are 16-byte aligned)
-  const bool paired = (rows & 1) == 0;
+  for (int i = 0; i < MT; ++i)
 #pragma unroll
-  for (int it = 0; it < kItems; ++it) {
-    if (!t.on[it]) continue;
-    const int r0 = t.i0[it], r1 = min(r0 + 1, rows - 1);
-    const double* y[kTileCols];
-#pragma unroll
-    for (int c = 0; c < kTileCols; ++c) y[c] = in + static_cast<size_t>(min(t.c0[it] + c, b - 1)) * ld + l0;
-#pragma unroll 2
-    for (int l = 0; l < width; ++l) {
-      double x0, x1;
-      if (paired) {
-        const double2 x = *reinterpret_cast<const double2*>(cols + l * rows + r0);
-        x0 = x.x;
-        x1 = x.y;
-      } else {
-        x0 = cols[l * rows + r0];
-        x1 = cols[l * rows + r1];
-      }
-#pragma unroll
-      for (int c = 0; c < kTileCols; ++c) {
-        const double v = y[c][l];
-        acc[it][c] = fma(x0, v, acc[it][c]);
-        acc[it][kTileCols + c] = fma(x1, v, acc[it][kTileCols + c]);
-      }
-    }
-  }
-}
-
-template <int TC>
-__device__ void product_gq_tiles(const double* __restrict__ g, const double* __restrict__ in, double* __restrict__ out,
-                                 double* __restrict__ gbuf, bool resident, int slab, int rows, int b, int ld) {
-  constexpr int kItems = TileShape<TC>::kItems;
-  constexpr int kTileCols = TC;
-  const ProductTiles<TC> t = product_tiles<TC>(rows, b);
-  double acc[kItems][2 * kTileCols];
-#pragma unroll
-  for (int it = 0; it < kItems; ++it)
-#pragma unroll
-    for (int e = 0; e < 2 * kTileCols; ++e) acc[it][e] = 0.0;
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const int mt_mine = warp_m_tiles(rows);
   if (resident) {
-    product_accumulate<TC>(t, acc, gbuf, in, rows, b, ld, 0, rows);
+    dmma_accumulate<MT, NT>(acc, gbuf, lda, rows, in, ld, b, 0, mt_mine);
   } else {
-    const int slab_elems = rows * slab;
+    const int slab_elems = lda * slab;
     const int n_slabs = (rows + slab - 1) / slab;
     auto issue = [&](int index) {  // one commit group per slab, empty past the end so that the group count is uniform
-      if (index < n_slabs) {
-        const int l0 = index * slab;
-        const int count = min(slab, rows - l0) * rows;  // whole columns, contiguous in G
-        const double* const src = g + static_cast<size_t>(l0) * rows;
-        double* const dst = gbuf + (index % kRing) * slab_elems;
-        for (int e = threadIdx.x; e < count; e += kFusedThreads) cp_async8(dst + e, src + e);
-      }
+      if (index < n_slabs)
+        copy_gram_columns(g, gbuf + (index % kRing) * slab_elems, rows, lda, index * slab,
+                          min(slab, rows - index * slab), wide);
       asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
     __syncthreads();  // the previous users of the ring are done
@@ -192,96 +251,75 @@ __device__ void product_gq_tiles(const double* __restrict__ g, const double* __r
       __syncthreads();  // slab has landed for everyone; everyone is done with the buffer the next issue refills
       issue(index + kRing - 1);
       const int l0 = index * slab;
-      product_accumulate<TC>(t, acc, gbuf + (index % kRing) * slab_elems, in, rows, b, ld, l0, min(slab, rows - l0));
+      dmma_accumulate<MT, NT>(acc, gbuf + (index % kRing) * slab_elems, lda, min(slab, rows - l0), in, ld, b, l0,
+                              mt_mine);
     }
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   }
-#pragma unroll
-  for (int it = 0; it < kItems; ++it) {
-    if (!t.on[it]) continue;
-#pragma unroll
-    for (int c = 0; c < kTileCols; ++c) {
-      if (t.c0[it] + c >= b) break;
-      out[static_cast<size_t>(t.c0[it] + c) * ld + t.i0[it]] = acc[it][c];
-      if (t.i0[it] + 1 < rows) out[static_cast<size_t>(t.c0[it] + c) * ld + t.i0[it] + 1] = acc[it][kTileCols + c];
-    }
-  }
+  dmma_store<MT, NT>(acc, out, rows, ld, b, mt_mine);
 }
 
-__device__ void product_gq(const double* __restrict__ g, const double* __restrict__ in, double* __restrict__ out,
-                           double* __restrict__ gbuf, bool resident, int slab, int rows, int b, int ld) {
-  if (resident)
-    product_gq_tiles<4>(g, in, out, gbuf, true, slab, rows, b, ld);
-  else
-    product_gq_tiles<8>(g, in, out, gbuf, false, slab, rows, b, ld);
+// x (rows x b, shared, leading dimension ld) <- x * vs (b x b, leading dimension m), in place: a warp reads only the
+// rows it writes, and all of them before it writes any.
+template <int MT, int NT>
+__device__ void rotate_block(double* __restrict__ x, const double* __restrict__ vs, int rows, int b, int ld, int m) {
+  double acc[MT][NT][2];
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const int mt_mine = warp_m_tiles(rows);
+  dmma_accumulate<MT, NT>(acc, x, ld, b, vs, m, b, 0, mt_mine);
+  __syncwarp();
+  dmma_store<MT, NT>(acc, x, rows, ld, b, mt_mine);
 }
 
-// s (b x b, leading dimension m, shared) = A^T B for A, B rows x b in shared memory; only the tiles on and below
-// the diagonal are computed and mirrored (both uses are symmetric: Z^T Z and Q^T (G Q)).  A warp owns a 4 x 4 tile:
-// lanes stride the rows, then a fixed butterfly sums the lanes (same order every run).
+// s (b x b, leading dimension m, shared) = A^T B for A, B rows x b in shared memory (rows beyond `rows` zero); only
+// the 8 x 8 tiles on and below the diagonal are computed and mirrored (both uses are symmetric: Z^T Z and Q^T (G Q)).
+// A warp owns a tile; two accumulator pairs alternate along the contraction to halve the dependent chain, and the
+// order of the sums is fixed.
 __device__ void small_gram(const double* __restrict__ a, const double* __restrict__ bm, double* __restrict__ s,
                            int rows, int b, int ld, int m) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tiles = (b + 3) / 4;
+  const int g = lane >> 2, t = lane & 3;
+  const int tiles = (b + 7) / 8;
   const int n_lower = tiles * (tiles + 1) / 2;
-  for (int t = warp; t < n_lower; t += kFusedWarps) {
-    int ti = 0, tj = t;
+  const int rows4 = (rows + 3) & ~3;
+  for (int tile = warp; tile < n_lower; tile += kFusedWarps) {
+    int ti = 0, tj = tile;
     while (tj > ti) {
       tj -= ti + 1;
       ++ti;
     }
-    double acc[4][4];
-#pragma unroll
-    for (int x = 0; x < 4; ++x)
-#pragma unroll
-      for (int y = 0; y < 4; ++y) acc[x][y] = 0.0;
-    const double* ap[4];
-    const double* bp[4];
-#pragma unroll
-    for (int x = 0; x < 4; ++x) {
-      ap[x] = a + static_cast<size_t>(min(4 * ti + x, b - 1)) * ld;
-      bp[x] = bm + static_cast<size_t>(min(4 * tj + x, b - 1)) * ld;
+    const double* const ap = a + static_cast<size_t>(min(8 * ti + g, b - 1)) * ld + t;
+    const double* const bp = bm + static_cast<size_t>(min(8 * tj + g, b - 1)) * ld + t;
+    double c0 = 0.0, c1 = 0.0, d0 = 0.0, d1 = 0.0;
+    int r = 0;
+    for (; r + 8 <= rows4; r += 8) {
+      dmma884(c0, c1, ap[r], bp[r]);
+      dmma884(d0, d1, ap[r + 4], bp[r + 4]);
     }
-    for (int i = lane; i < rows; i += 32) {
-      double av[4], bv[4];
+    if (r < rows4) dmma884(c0, c1, ap[r], bp[r]);
+    c0 += d0;
+    c1 += d1;
+    const int row = 8 * ti + g, col = 8 * tj + 2 * t;  // entry (row, col) with row's tile >= col's tile
 #pragma unroll
-      for (int x = 0; x < 4; ++x) {
-        av[x] = ap[x][i];
-        bv[x] = bp[x][i];
+    for (int e = 0; e < 2; ++e) {
+      const int c = col + e;
+      const double val = e == 0 ? c0 : c1;
+      if (row < b && c < b && (ti > tj || row >= c)) {
+        s[c * m + row] = val;
+        s[row * m + c] = val;
       }
-#pragma unroll
-      for (int x = 0; x < 4; ++x)
-#pragma unroll
-        for (int y = 0; y < 4; ++y) acc[x][y] = fma(av[x], bv[y], acc[x][y]);
-    }
-#pragma unroll
-    for (int x = 0; x < 4; ++x)
-#pragma unroll
-      for (int y = 0; y < 4; ++y) {
-        double v = acc[x][y];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        acc[x][y] = v;
-      }
-    if (lane == 0) {
-#pragma unroll
-      for (int x = 0; x < 4; ++x)
-#pragma unroll
-        for (int y = 0; y < 4; ++y) {
-          const int r = 4 * ti + x, c = 4 * tj + y;  // entry (r, c) with r's tile >= c's tile
-          if (r < b && c < b && (ti > tj || r >= c)) {
-            s[c * m + r] = acc[x][y];
-            s[r * m + c] = acc[x][y];
-          }
-        }
     }
   }
 }
 
 // In-place Cholesky factorisation of the symmetric positive definite b x b matrix s + shift I (leading dimension m,
-// shared): on return the lower triangle holds L and invd[j] = 1 / L(j, j).  The trailing update works on the unscaled
-// column, S(i,k) -= S(i,j) S(k,j) / d_j, so a step needs one barrier.  Returns false (uniformly) when a pivot is not
-// positive.  kCap >= b.
+// shared) by ONE warp: lane i owns rows i, i + 32, ...; column j is scaled by 1 / sqrt(d_j) and pushed into the trailing
+// columns through shuffles, so a column costs one reciprocal square root, one warp-level synchronisation and no CTA
+// barrier (with sixteen warps and a barrier per column the barrier and its stragglers were most of the time).  On
+// return the lower triangle holds L and invd[j] = 1 / L(j, j); false (uniformly) when a pivot is not positive.
 //
 // shift > 0 is the first pass of a shifted Cholesky QR: the oversampling columns of Z = G Q lie, up to the ratio
 // lambda_noise / lambda_signal, inside the span of the leading ones, so Z^T Z is numerically singular whenever that
@@ -289,102 +327,188 @@ __device__ void small_gram(const double* __restrict__ a, const double* __restric
 // columns it touches come out shorter than unit length, the span is unchanged, and the unshifted passes that follow
 // (on a block whose condition number is now moderate) restore orthonormality.
 template <int kCap>
-__device__ bool cholesky_smem(double* __restrict__ s, double* __restrict__ invd, int b, int m, double shift) {
+__device__ bool cholesky_warp(double* __restrict__ s, double* __restrict__ invd, int b, int m, double shift) {
+  constexpr int kPasses = kCap / 32;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  __shared__ double pivot[64];
+  __shared__ int ok_flag;
   __syncthreads();
-  if (shift > 0.0) {
-    for (int j = threadIdx.x; j < b; j += kFusedThreads) s[j * m + j] += shift;
-    __syncthreads();
-  }
-  for (int j = 0; j < b; ++j) {
-    const double d = s[j * m + j];  // final since the previous step's barrier
-    if (!(d > 0.0) || !(d <= DBL_MAX)) return false;  // uniform: every thread reads the same value
-    if (threadIdx.x == 0) pivot[j] = sqrt(d);
-    const double dinv = fast_rcp(d);
-    constexpr int kPasses = (kCap + 31) / 32;
-    double cj[kPasses];
-#pragma unroll
-    for (int r = 0; r < kPasses; ++r) {
-      const int i = lane + 32 * r;
-      cj[r] = (i > j && i < b) ? s[j * m + i] : 0.0;
-    }
-    for (int k = j + 1 + warp; k < b; k += kFusedWarps) {
-      const double skj = s[j * m + k] * dinv;
+  if (warp == 0) {
+    bool ok = true;
+    for (int j = 0; j < b; ++j) {
+      const double d = s[j * m + j] + shift;  // the trailing updates work on the unshifted diagonal
+      if (!(d > 0.0) || !(d <= DBL_MAX)) {    // uniform: every lane reads the same value
+        ok = false;
+        break;
+      }
+      double rinv = rsqrt(d);
+      rinv = fma(rinv, fma(-0.5 * d * rinv, rinv, 0.5), rinv);  // one Newton step: within an ulp or two
+      double lij[kPasses];
 #pragma unroll
       for (int r = 0; r < kPasses; ++r) {
         const int i = lane + 32 * r;
-        if (i >= k && i < b) s[k * m + i] = fma(-cj[r], skj, s[k * m + i]);
+        const bool mine = i > j && i < b;
+        lij[r] = mine ? s[j * m + i] * rinv : 0.0;
+        if (mine) s[j * m + i] = lij[r];
+        if (i == j) {
+          s[j * m + j] = d * rinv;
+          invd[j] = rinv;
+        }
       }
+      // four trailing columns at a time, every load before the first store: the columns are independent, but the
+      // compiler cannot know that the stores of one do not feed the loads of the next
+      for (int k0 = j + 1; k0 < b; k0 += 4) {
+        double lkj[4], old[4][kPasses];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int k = min(k0 + e, b - 1);
+          lkj[e] = __shfl_sync(0xffffffffu, lij[0], k & 31);
+          if constexpr (kPasses > 1) {
+            const double upper = __shfl_sync(0xffffffffu, lij[kPasses - 1], k & 31);
+            if (k >= 32) lkj[e] = upper;
+          }
+#pragma unroll
+          for (int r = 0; r < kPasses; ++r) {
+            const int i = lane + 32 * r;
+            old[e][r] = (k0 + e < b && i >= k && i < b) ? s[k * m + i] : 0.0;
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int k = k0 + e;
+#pragma unroll
+          for (int r = 0; r < kPasses; ++r) {
+            const int i = lane + 32 * r;
+            if (k < b && i >= k && i < b) s[k * m + i] = fma(-lij[r], lkj[e], old[e][r]);
+          }
+        }
+      }
+      __syncwarp();
     }
-    __syncthreads();
-  }
-  // scale the columns: L(i, j) = S(i, j) / sqrt(d_j)
-  for (int col = warp; col < b; col += kFusedWarps) {
-    const double piv = pivot[col];
-    const double pinv = 1.0 / piv;
-    for (int row = lane; row < b; row += 32)
-      if (row > col) s[col * m + row] *= pinv;
-      else if (row == col) s[col * m + row] = piv;
-    if (lane == 0) invd[col] = pinv;
+    if (lane == 0) ok_flag = ok ? 1 : 0;
   }
   __syncthreads();
-  return true;
+  return ok_flag != 0;
 }
 
-// z (rows x b, shared) <- z L^{-T}, in place: row i solves x L^T = z_i.  Right-looking: once x_j = z_j / L(j,j) is
-// known, the later columns of the row are updated independently (z_c -= x_j L(c,j)), so the dependent chain is one
-// multiplication and one update per column instead of a length-j sum; two rows per thread where there are threads to
-// spare would not help, the chain is what costs.
-template <int kCap>
-__device__ void trsm_rows(double* __restrict__ z, const double* __restrict__ l, const double* __restrict__ invd,
-                          int rows, int b, int ld, int m) {
-  for (int i = threadIdx.x; i < rows; i += kFusedThreads) {
-    double* const zi = z + i;
-    double next = zi[0];
-    for (int j = 0; j < b; ++j) {
-      const double xj = next * invd[j];
-      zi[static_cast<size_t>(j) * ld] = xj;
-      const double* const lj = l + j * m;
-      // column j + 1 first and kept in a register: it is the next step's pivot entry
-      if (j + 1 < b) next = fma(-xj, lj[j + 1], zi[static_cast<size_t>(j + 1) * ld]);
-#pragma unroll 4
-      for (int c = j + 2; c < b; ++c) zi[static_cast<size_t>(c) * ld] = fma(-xj, lj[c], zi[static_cast<size_t>(c) * ld]);
+// z (rows x b, shared) <- z L^{-T}, in place, in blocks of eight columns; a warp owns 32 consecutive rows for the
+// whole solve, so the blocks are separated by warp-level synchronisation only.  Per block:
+//   * a thread solves its row against the 8 x 8 diagonal block in registers (right-looking: once x_j = z_j / L(j,j)
+//     is known the later columns of the block are updated independently -- one multiplication and one update on the
+//     dependent chain per column);
+//   * the warp subtracts X_block L(trailing, block)^T from its rows of every later column block on the FP64 tensor
+//     pipe (fragment layout as in dmma_accumulate).
+// Entries of L read beyond row b only reach registers and columns that are never stored.
+__device__ void trsm_rows_blocked(double* __restrict__ z, const double* __restrict__ l,
+                                  const double* __restrict__ invd, int rows, int b, int ld, int m) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int base = 32 * warp, row = base + lane;
+  const bool live = row < rows;
+  const int blocks = (b + 7) / 8;
+  if (base < rows) {  // uniform in the warp
+    for (int blk = 0; blk < blocks; ++blk) {
+      const int c0 = 8 * blk;
+      double x[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) x[e] = (live && c0 + e < b) ? z[(c0 + e) * ld + row] : 0.0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        if (c0 + e >= b) break;  // uniform
+        const double xe = x[e] * invd[c0 + e];
+        x[e] = xe;
+        const double* const le = l + (c0 + e) * m + c0;
+#pragma unroll
+        for (int f = e + 1; f < 8; ++f) x[f] = fma(-xe, le[f], x[f]);
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (live && c0 + e < b) z[(c0 + e) * ld + row] = x[e];
+      if (blk + 1 == blocks) break;  // nothing behind the last block (all eight columns of the others exist)
+      __syncwarp();
+      const double* const lb0 = l + (c0 + t) * m + g;      // B(k, n) = L(n, block column k): k-step 0
+      const double* const lb1 = l + (c0 + 4 + t) * m + g;  // k-step 1
+      // the four m-tiles of the warp together, every load of a column block before its first store (the m-tiles
+      // beyond the matrix read rows of the following columns and store nothing)
+      double a0[4], a1[4];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        const int r = base + 8 * mt + g;
+        a0[mt] = -z[(c0 + t) * ld + r];
+        a1[mt] = -z[(c0 + 4 + t) * ld + r];
+      }
+      for (int later = blk + 1; later < blocks; ++later) {
+        const int cn = 8 * later;
+        const double b0 = lb0[cn], b1 = lb1[cn];
+        double* const out0 = z + (cn + 2 * t) * ld + base + g;
+        double c0v[4], c1v[4];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) {
+          c0v[mt] = out0[8 * mt];
+          c1v[mt] = out0[ld + 8 * mt];
+        }
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) {
+          dmma884(c0v[mt], c1v[mt], a0[mt], b0);
+          dmma884(c0v[mt], c1v[mt], a1[mt], b1);
+        }
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) {
+          if (base + 8 * mt + g < rows) {
+            if (cn + 2 * t < b) out0[8 * mt] = c0v[mt];
+            if (cn + 2 * t + 1 < b) out0[ld + 8 * mt] = c1v[mt];
+          }
+        }
+      }
+      __syncwarp();
     }
   }
   __syncthreads();
 }
+
+// m-tiles per warp and n-tiles of the DMMA products: 32 accumulators per thread either way
+template <int kCap>
+struct ProductShape {
+  static constexpr int kMT = kCap <= 32 ? 4 : 2;  // rows <= 128 kMT
+  static constexpr int kNT = kCap / 8;
+};
 
 template <int kCap>
 __global__ void __launch_bounds__(kFusedThreads, 1) leaf_solve_fused_kernel(const FusedParams p) {
+  constexpr int MT = ProductShape<kCap>::kMT, NT = ProductShape<kCap>::kNT;
   extern __shared__ __align__(16) double sm[];
   const int rows = p.rows, b = p.b, k = p.k;
-  const int ld = rows | 1;            // odd leading dimension: column-strided accesses spread over the banks
+  const int ld = block_ld(rows);
+  const int lda = gram_ld(rows);
   const int m = (b + 1) & ~1;
   double* q = sm;                     // ld x b
   double* z = q + static_cast<size_t>(ld) * b;
   double* const h = z + static_cast<size_t>(ld) * b;  // m x m
-  double* const v = h + m * m;        // m x m
-  double* const theta = v + m * m;    // m (ascending)
+  double* const h2 = h + m * m;       // m x m: the Jacobi iteration's second buffer
+  double* const v = h2 + m * m;       // m x m
+  double* const v2 = v + m * m;       // m x m: the second buffer of the eigenvectors
+  double* const theta = v2 + m * m;   // m (ascending)
   double* const invd = theta + m;     // m
   double* const col_res = invd + m;   // m: squared residual norm per sorted column
-  double* const part_res = col_res + m;                   // [row blocks][m]
-  double* const part_abs = part_res + kFusedMaxRowBlocks * m;  // [row blocks][m]
-  int* const part_idx = reinterpret_cast<int*>(part_abs + kFusedMaxRowBlocks * m);  // [row blocks][m]
-  int* const order = part_idx + kFusedMaxRowBlocks * m;   // m: sorted position -> Jacobi column
-  // G itself (resident) or the slab ring of product_gq, 16-byte aligned behind the int arrays
-  double* const gbuf =
-      reinterpret_cast<double*>((reinterpret_cast<unsigned long long>(order + m) + 15ull) & ~15ull);
+  // G itself (resident) or the slab ring of product_gq; every count so far is even, so this is 16-byte aligned
+  double* const gbuf = col_res + m;
   const bool resident = p.resident != 0;
+  const int gram_doubles = resident ? lda * rows : kRing * lda * p.slab;
+  int* const order = reinterpret_cast<int*>(gbuf + gram_doubles + kGramSlack);  // m: sorted position -> Jacobi column
+  int* const col_idx = order + m;     // m: first row of the largest magnitude per sorted column
+  const bool wide = (rows & 1) == 0 && (reinterpret_cast<unsigned long long>(p.gram) & 15ull) == 0;
   __shared__ double scal[8];
   __shared__ double red[kFusedWarps];
   __shared__ int ctl[4];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  // phase accounting (thread 0, after the barrier that ends a phase)
-  long long phase_cycles[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  long long jacobi_prof[3] = {0, 0, 0};
-  long long phase_mark = clock64();
+  // phase accounting (thread 0, after the barrier that ends a phase; in shared memory: the registers are the
+  // products' accumulators)
+  __shared__ long long phase_cycles[8], jacobi_prof[4], phase_mark;
+  if (tid == 0) {
+    for (int i = 0; i < 8; ++i) phase_cycles[i] = 0;
+    for (int i = 0; i < 4; ++i) jacobi_prof[i] = 0;
+    phase_mark = clock64();
+  }
   auto end_phase = [&](int which) {
     if (tid == 0) {
       const long long now = clock64();
@@ -394,20 +518,22 @@ __global__ void __launch_bounds__(kFusedThreads, 1) leaf_solve_fused_kernel(cons
   };
 
   if (resident) {
-    const int count = rows * rows;
-    for (int e = tid; e < count; e += kFusedThreads) cp_async8(gbuf + e, p.gram + e);
+    copy_gram_columns(p.gram, gbuf, rows, lda, 0, rows, wide);
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   }
-  // ---- start block
-  for (int e = tid; e < rows * b; e += kFusedThreads) {
-    const int c = e / rows, i = e - c * rows;
-    double val;
-    if (p.start_mode == 0)
-      val = p.start[static_cast<size_t>(b - 1 - c) * rows + i];
-    else
-      val = c < k ? p.start[static_cast<size_t>(c) * rows + i]
-                  : filler_value(static_cast<unsigned long long>(c - k) * rows + i, 0x7461636bull);
-    q[static_cast<size_t>(c) * ld + i] = val;
+  // ---- start block (rows [rows, ld) of both blocks zero, once: nothing below writes anything else there)
+  for (int e = tid; e < ld * b; e += kFusedThreads) {
+    const int c = e / ld, i = e - c * ld;
+    double val = 0.0;
+    if (i < rows) {
+      if (p.start_mode == 0)
+        val = p.start[static_cast<size_t>(b - 1 - c) * rows + i];
+      else
+        val = c < k ? p.start[static_cast<size_t>(c) * rows + i]
+                    : filler_value(static_cast<unsigned long long>(c - k) * rows + i, 0x7461636bull);
+    }
+    q[e] = val;
+    z[e] = 0.0;
   }
   // trace(G): fixed-order tree, once (the certificate of every round uses it)
   {
@@ -432,26 +558,45 @@ __global__ void __launch_bounds__(kFusedThreads, 1) leaf_solve_fused_kernel(cons
   end_phase(0);
 
   int steps_total = 0, rounds = 0, sweeps = 0, miss = 1 | 4;
-  double d_res = 0.0, d_angle = 0.0, d_tau = 0.0;
   bool failed = false;
+  if (tid == 0) scal[0] = scal[1] = scal[2] = 0.0;
   for (int round = 0; round < p.max_rounds && !failed; ++round) {
     ++rounds;
     const int steps = round == 0 ? p.first_steps : round + 1;
     for (int s = 0; s < steps && !failed; ++s) {
-      product_gq(p.gram, q, z, gbuf, resident, p.slab, rows, b, ld);
+      product_gq<MT, NT>(p.gram, q, z, gbuf, resident, wide, p.slab, rows, b, ld, lda);
       __syncthreads();
       end_phase(1);
-      // shifted Cholesky QR: one shifted pass keeps the span and tames the conditioning; the last step of a round
-      // adds two plain passes, after which Q is orthonormal to rounding (the Rayleigh-Ritz step needs that)
-      const int passes = (s + 1 == steps) ? 3 : 1;
+      // Cholesky QR of Z.  Its loss of orthogonality is governed by the condition number of Z^T Z with the column
+      // norms scaled out (the Gram product, the factorisation and the triangular solve are all invariant under a
+      // column scaling up to rounding).  A warm start makes the columns of Z nearly orthogonal -- they are close to
+      // eigenvectors times eigenvalues -- so when every scaled off-diagonal entry is below 1 / (2 (b - 1)) that
+      // condition number is below 3 (Gershgorin) and ONE plain pass leaves Q orthonormal to rounding.  Otherwise:
+      // a shifted pass, which keeps the span and tames the conditioning, and on the last step of a round two plain
+      // passes after it (the Rayleigh-Ritz step needs an orthonormal block).
+      int passes = (s + 1 == steps) ? 3 : 1;
+      bool plain = false;
       for (int pass = 0; pass < passes && !failed; ++pass) {
         small_gram(z, z, h, rows, b, ld, m);
         __syncthreads();
         double shift = 0.0;
         if (pass == 0) {
-          double tr = 0.0;  // ||Z||_F^2, same fixed-order sum in every thread
-          for (int j = 0; j < b; ++j) tr += h[j * m + j];
-          shift = 1e-11 * tr;
+          const double bound = 0.25 / (static_cast<double>(b - 1) * (b - 1));
+          int fine = 1;
+          for (int e = tid; e < b * b; e += kFusedThreads) {
+            const int c = e / b, r = e - c * b;
+            const double x = h[c * m + r], dd = h[c * m + c] * h[r * m + r];
+            if (r != c && !(x * x <= bound * dd)) fine = 0;
+            if (r == c && !(x > 0.0 && x <= DBL_MAX)) fine = 0;
+          }
+          plain = __syncthreads_and(fine) != 0;
+          if (plain) {
+            passes = 1;
+          } else {
+            double tr = 0.0;  // ||Z||_F^2, same fixed-order sum in every thread
+            for (int j = 0; j < b; ++j) tr += h[j * m + j];
+            shift = 1e-11 * tr;
+          }
         } else if (pass == 2) {
           // Z^T Z of the block the second pass produced: if it is the identity to rounding already (the usual case:
           // the shift of the first pass was below every pivot), the third pass has nothing left to do
@@ -467,12 +612,12 @@ __global__ void __launch_bounds__(kFusedThreads, 1) leaf_solve_fused_kernel(cons
           }
         }
         end_phase(2);
-        if (!cholesky_smem<kCap>(h, invd, b, m, shift)) {
+        if (!cholesky_warp<kCap>(h, invd, b, m, shift)) {
           failed = true;
           break;
         }
         end_phase(3);
-        trsm_rows<kCap>(z, h, invd, rows, b, ld, m);
+        trsm_rows_blocked(z, h, invd, rows, b, ld, m);
         end_phase(4);
       }
       double* const t = q;
@@ -483,18 +628,32 @@ __global__ void __launch_bounds__(kFusedThreads, 1) leaf_solve_fused_kernel(cons
     if (failed) break;
 
     // ---- Rayleigh-Ritz on span(Q)
-    product_gq(p.gram, q, z, gbuf, resident, p.slab, rows, b, ld);
+    product_gq<MT, NT>(p.gram, q, z, gbuf, resident, wide, p.slab, rows, b, ld, lda);
     __syncthreads();
     end_phase(1);
     small_gram(q, z, h, rows, b, ld, m);
+    __syncthreads();
+    // scale H by a power of two so that its largest entry (on the diagonal: H is positive semidefinite) is of order
+    // one -- exact, and the Jacobi rotations then need no scaling of their own
+    double top_diag = 0.0;
+    for (int j = 0; j < b; ++j) top_diag = fmax(top_diag, fabs(h[j * m + j]));  // same in every thread
+    double scale = 1.0, unscale = 1.0;
+    {
+      const int e = (__double2hiint(top_diag) >> 20) & 0x7ff;
+      if (e >= 64 && e <= 1982) {
+        scale = __hiloint2double((2046 - e) << 20, 0);
+        unscale = __hiloint2double(e << 20, 0);
+      }
+    }
+    __syncthreads();
     for (int e = tid; e < m * m; e += kFusedThreads) {
       const int c = e / m, r = e - c * m;
       v[e] = (r == c) ? 1.0 : 0.0;
-      if (r >= b || c >= b) h[e] = 0.0;
+      h[e] = (r >= b || c >= b) ? 0.0 : h[e] * scale;
     }
     __syncthreads();
     end_phase(2);
-    sweeps = jacobi_sweeps_smem<kFusedThreads, kCap>(h, v, b, m, jacobi_prof);
+    sweeps = jacobi_pingpong_smem<kFusedThreads, kCap, 16>(h, h2, v, v2, b, m, jacobi_prof);
     end_phase(5);
     if (sweeps == kJacobiMaxSweeps) {
       failed = true;
@@ -511,66 +670,54 @@ __global__ void __launch_bounds__(kFusedThreads, 1) leaf_solve_fused_kernel(cons
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) rank += __shfl_xor_sync(0xffffffffu, rank, o);
       if (lane == 0) {
-        theta[rank] = li;
+        theta[rank] = li * unscale;
         order[rank] = i;
       }
     }
     __syncthreads();
 
-    // ---- X = Q V (sorted columns) to global; residual R = (G Q) V - X Theta and the column maxima on the way.
-    // A warp owns 32 consecutive rows (one row block) and four sorted columns.
-    const int row_blocks = (rows + 31) / 32;
-    const int col_groups = (b + 3) / 4;
-    for (int item = warp; item < row_blocks * col_groups; item += kFusedWarps) {
-      const int cg = item / row_blocks, rb = item - cg * row_blocks;
-      const int i = rb * 32 + lane;
-      const bool live = i < rows;
-      double x[4] = {0.0, 0.0, 0.0, 0.0}, w[4] = {0.0, 0.0, 0.0, 0.0};
-      const double* vc[4];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) vc[c] = v + order[min(4 * cg + c, b - 1)] * m;
-      if (live) {
-        for (int l = 0; l < b; ++l) {
-          const double qv = q[static_cast<size_t>(l) * ld + i], zv = z[static_cast<size_t>(l) * ld + i];
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const double vv = vc[c][l];
-            x[c] = fma(qv, vv, x[c]);
-            w[c] = fma(zv, vv, w[c]);
-          }
-        }
-      }
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const int col = 4 * cg + c;
-        if (col >= b) break;  // uniform in the warp
-        if (live) p.ritz[static_cast<size_t>(col) * rows + i] = x[c];
-        const double r = live ? w[c] - theta[col] * x[c] : 0.0;
-        double r2 = r * r;
-        double ax = live ? fabs(x[c]) : -1.0;
-        int ai = live ? i : 0x7fffffff;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          r2 += __shfl_xor_sync(0xffffffffu, r2, o);
-          const double oa = __shfl_xor_sync(0xffffffffu, ax, o);
-          const int oi = __shfl_xor_sync(0xffffffffu, ai, o);
-          if (oa > ax || (oa == ax && oi < ai)) {
-            ax = oa;
-            ai = oi;
-          }
-        }
-        if (lane == 0) {
-          part_res[rb * m + col] = r2;
-          part_abs[rb * m + col] = ax;
-          part_idx[rb * m + col] = ai;
-        }
-      }
+    // ---- X = Q V and W = (G Q) V (sorted columns), in place; then per column the Ritz vector to global memory, the
+    // residual norm of R = W - X Theta and the first row of the largest magnitude
+    // (columns of V gathered in DESCENDING order of the Ritz values: the dominant direction first, as the start
+    // block of another round wants it)
+    for (int e = tid; e < b * m; e += kFusedThreads) {
+      const int c = e / m, l = e - c * m;
+      h2[e] = v[order[b - 1 - c] * m + l];
     }
     __syncthreads();
-    for (int col = tid; col < b; col += kFusedThreads) {
-      double r2 = 0.0;
-      for (int rb = 0; rb < row_blocks; ++rb) r2 += part_res[rb * m + col];
-      col_res[col] = r2;
+    rotate_block<MT, NT>(q, h2, rows, b, ld, m);
+    rotate_block<MT, NT>(z, h2, rows, b, ld, m);
+    __syncthreads();
+    for (int col = warp; col < b; col += kFusedWarps) {  // col: ascending position; stored at b - 1 - col
+      const double th = theta[col];
+      const double* const xc = q + static_cast<size_t>(b - 1 - col) * ld;
+      const double* const wc = z + static_cast<size_t>(b - 1 - col) * ld;
+      double r2 = 0.0, ax = -1.0;
+      int ai = 0x7fffffff;
+      for (int i = lane; i < rows; i += 32) {
+        const double x = xc[i];
+        p.ritz[static_cast<size_t>(col) * rows + i] = x;
+        const double r = wc[i] - th * x;
+        r2 = fma(r, r, r2);
+        if (fabs(x) > ax) {
+          ax = fabs(x);
+          ai = i;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+        const double oa = __shfl_xor_sync(0xffffffffu, ax, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, ai, o);
+        if (oa > ax || (oa == ax && oi < ai)) {
+          ax = oa;
+          ai = oi;
+        }
+      }
+      if (lane == 0) {
+        col_res[col] = r2;
+        col_idx[col] = ai;
+      }
     }
     __syncthreads();
     end_phase(6);
@@ -603,13 +750,11 @@ __global__ void __launch_bounds__(kFusedThreads, 1) leaf_solve_fused_kernel(cons
     }
     __syncthreads();
     miss = ctl[1];
-    d_res = scal[0];
-    d_angle = scal[1];
-    d_tau = scal[2];
     __syncthreads();
     end_phase(7);
     // certified; or the pairs have converged and the gap / tail criterion still fails: more rounds cannot change that
     if (miss == 0 || (miss & 1) == 0) break;
+    // another round continues from the Ritz vectors (orthonormal, dominant first; the span is Q's)
   }
 
   if (tid == 0) {
@@ -617,30 +762,19 @@ __global__ void __launch_bounds__(kFusedThreads, 1) leaf_solve_fused_kernel(cons
     p.verdict[1] = failed ? 1 : 0;
     p.verdict[2] = sweeps;
     p.verdict[3] = steps_total;
-    p.diag[0] = d_res;
-    p.diag[1] = d_angle;
-    p.diag[2] = d_tau;
+    p.diag[0] = scal[0];
+    p.diag[1] = scal[1];
+    p.diag[2] = scal[2];
     p.diag[3] = rounds;
     for (int i = 0; i < 8; ++i) p.diag[4 + i] = static_cast<double>(phase_cycles[i]);
-    for (int i = 0; i < 3; ++i) p.diag[12 + i] = static_cast<double>(jacobi_prof[i]);  // checks / rotations / updates
+    for (int i = 0; i < 4; ++i) p.diag[12 + i] = static_cast<double>(jacobi_prof[i]);  // checks / rotations / updates / barriers
   }
   if (failed) return;
 
-  // ---- the reference's selection (hooi.hpp:60-74) from the sorted Ritz vectors just written to global memory
-  const int row_blocks = (rows + 31) / 32;
+  // ---- the reference's selection (hooi.hpp:60-74) from the sorted Ritz vectors (still in shared memory)
   for (int j = warp; j < k; j += kFusedWarps) {
-    const int col = b - 1 - j;
-    double ax = -1.0;
-    int ai = 0x7fffffff;
-    for (int rb = 0; rb < row_blocks; ++rb) {  // first index of the largest magnitude
-      const double oa = part_abs[rb * m + col];
-      const int oi = part_idx[rb * m + col];
-      if (oa > ax || (oa == ax && oi < ai)) {
-        ax = oa;
-        ai = oi;
-      }
-    }
-    const double* const src = p.ritz + static_cast<size_t>(col) * rows;
+    const double* const src = q + static_cast<size_t>(j) * ld;  // dominant first
+    const int ai = col_idx[b - 1 - j];
     const double sign = (ai < rows && src[ai] < 0.0) ? -1.0 : 1.0;
     double* const dst = p.factor + static_cast<size_t>(j) * rows;
     for (int i = lane; i < rows; i += 32) dst[i] = sign * src[i];
@@ -656,11 +790,13 @@ __global__ void __launch_bounds__(kFusedThreads, 1) leaf_solve_fused_kernel(cons
 constexpr size_t kFusedSmemBudget = 200 * 1024;
 
 size_t fused_smem_bytes(int rows, int b, bool resident, int slab) {
-  const size_t ld = static_cast<size_t>(rows | 1), m = static_cast<size_t>((b + 1) & ~1);
-  const size_t gdoubles = resident ? static_cast<size_t>(rows) * rows : static_cast<size_t>(kRing) * rows * slab;
-  const size_t doubles = 2 * ld * b + 2 * m * m + 3 * m + 2 * kFusedMaxRowBlocks * m + gdoubles;
-  const size_t ints = kFusedMaxRowBlocks * m + m;
-  return doubles * sizeof(double) + ints * sizeof(int) + 32;  // + alignment of the G buffer
+  const size_t ld = static_cast<size_t>(block_ld(rows)), lda = static_cast<size_t>(gram_ld(rows));
+  const size_t m = static_cast<size_t>((b + 1) & ~1);
+  const size_t gdoubles = resident ? lda * rows : static_cast<size_t>(kRing) * lda * slab;
+  const size_t doubles = 2 * ld * b + 4 * m * m + 3 * m + gdoubles + kGramSlack;
+  const size_t ints = 2 * m;
+  // + room for the fragment reads past the last column of a block (rotate_block: up to 7 columns of V)
+  return doubles * sizeof(double) + ints * sizeof(int) + 8 * m * sizeof(double);
 }
 
 bool fused_resident(int rows, int b) { return fused_smem_bytes(rows, b, true, 0) <= kFusedSmemBudget; }
@@ -676,12 +812,10 @@ int fused_slab(int rows, int b) {
 
 bool leaf_solve_fused_eligible(long long rows, int k, int b) {
   if (rows < 2 || rows > kFusedMaxRows || b > 64 || b <= k || k < 1 || b > rows) return false;
-  // product_gq: resident G -> up to 3 tiles of 2 x 4 per thread; streamed G -> one tile of 2 x 8 per thread
-  const long long pair_slots = (((rows + 1) / 2) + 31) & ~31LL;
-  if (fused_resident(static_cast<int>(rows), b))
-    return pair_slots * ((b + 3) / 4) <= static_cast<long long>(TileShape<4>::kItems) * kFusedThreads;
-  return fused_slab(static_cast<int>(rows), b) > 0 &&
-         pair_slots * ((b + 7) / 8) <= static_cast<long long>(TileShape<8>::kItems) * kFusedThreads;
+  // the DMMA products keep 128 kMT rows in the accumulators of the CTA
+  const int max_rows = 128 * (b <= 32 ? ProductShape<32>::kMT : ProductShape<64>::kMT);
+  if (rows > max_rows) return false;
+  return fused_resident(static_cast<int>(rows), b) || fused_slab(static_cast<int>(rows), b) > 0;
 }
 
 cudaError_t launch_leaf_solve_fused(cudaStream_t stream, const double* gram, int rows, int k, int b,

@@ -61,7 +61,7 @@ def main():
             out.append({"warm": warm, "us": e0.elapsed_time(e1) * 1e3, "miss": iv[4], "fail": iv[5],
                         "jacobi_sweeps": iv[6], "power_steps": iv[7], "rounds": dv[3],
                         "phase_us_at_1965MHz": {n: round(c / 1965.0, 1) for n, c in zip(PHASES, dv[4:12])},
-                        "jacobi_us_checks_rotations_updates": [round(c / 1965.0, 1) for c in dv[12:15]]})
+                        "jacobi_us_checks_rotations_updates_barriers": [round(c / 1965.0, 1) for c in dv[12:16]]})
         print(json.dumps({"rows": rows, "k": k, "block": b, "runs": out}))
     ctx.close()
 
