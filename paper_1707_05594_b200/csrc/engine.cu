@@ -280,6 +280,12 @@ struct LeafScratch {
                                // anywhere else could share that workspace with another leaf's concurrent solve
   long long fast_rows = 0;     // rows the iteration buffers were sized for (tp_dev_leaf_solve_warm only)
   int failures = 0;            // consecutive warm sweeps in which the fast path was rejected
+  // Launch-sequence solves (leaves too large for the one-launch kernel): power steps of the next solve.  A cold solve
+  // takes kSubspacePowerSteps; each certified warm solve that beat the residual bound by two orders of magnitude
+  // gives two steps back, a rejected one restores the count and raises the floor (so the count settles).
+  int power_steps = 0, power_steps_floor = 1;
+  int graph_steps = 0;         // step count the leaf's recorded graph was built with
+  bool launch_sequence = false;  // the last solve ran as a launch sequence (not the one-launch kernel)
   bool refinable = false;      // last rejection was a missed residual bound only (no failed factorisation / gap)
   bool was_cold = false;       // this sweep's solve started from the caller's factors
   bool cold_rejected = false;  // a cold start missed its certificate before: later cold starts take the full solve
@@ -516,15 +522,20 @@ void leaf_solve_subspace(tp_ctx* ctx, LeafScratch& s, const double* gram, long l
     ctx->own_kernels += 1;
     s.fast_used = true;
     s.last_ritz = s.x;
+    s.launch_sequence = false;
     return;
   }
   const bool graphs_off = !s.use_graph || recording;
-  const bool key_ok = s.graph_gram == gram && s.graph_rows == rows_ll && s.graph_k == k;
-  if (!key_ok && !recording) {  // the slot is being reused for another problem: start over
+  // a cold start (the caller's factors plus filler columns) always takes the full count
+  if (s.power_steps < 1 || !s.last_ritz) s.power_steps = kSubspacePowerSteps;
+  const int steps = s.power_steps;
+  s.launch_sequence = true;
+  const bool key_ok = s.graph_gram == gram && s.graph_rows == rows_ll && s.graph_k == k && s.graph_steps == steps;
+  if (!key_ok && !recording) {  // the slot is being reused for another problem, or the step count moved: start over
     if (s.graph) cudaGraphExecDestroy(s.graph);
     s.graph = nullptr;
     if (s.graph_state > 0) s.graph_state = 0;
-    s.last_ritz = nullptr;
+    if (s.graph_gram != gram || s.graph_rows != rows_ll || s.graph_k != k) s.last_ritz = nullptr;
   }
   if (s.last_ritz) {
     // start block: the previous solve's Ritz vectors, dominant first (Cholesky QR orthogonalises in column order)
@@ -546,7 +557,7 @@ void leaf_solve_subspace(tp_ctx* ctx, LeafScratch& s, const double* gram, long l
     bool ok = cudaStreamBeginCapture(io.stream, cudaStreamCaptureModeRelaxed) == cudaSuccess;
     if (ok) {
       try {
-        ritz_vectors = subspace_body(ctx, io, s, gram, rows, k);
+        ritz_vectors = subspace_body(ctx, io, s, gram, rows, k, steps);
       } catch (const Failure&) {
         ok = false;
       }
@@ -569,17 +580,20 @@ void leaf_solve_subspace(tp_ctx* ctx, LeafScratch& s, const double* gram, long l
     ritz_vectors = s.graph_result;
     TPB_CUDA(cudaGraphLaunch(s.graph, io.stream));
     // same work as the eager body, for the launch accounting
-    ctx->own_kernels += 2 * (kSubspacePowerSteps + 1) + 2;
-    ctx->library_calls += (kSubspacePowerSteps + 1) + kSubspacePowerSteps + 4;
+    ctx->own_kernels += 2 * (steps + 1) + 2;
+    ctx->library_calls += (steps + 1) + steps + 4;
   } else {
-    ritz_vectors = subspace_body(ctx, io, s, gram, rows, k);
+    ritz_vectors = subspace_body(ctx, io, s, gram, rows, k, steps);
     if (io.own_small && !graphs_off && s.graph_state == 0) {
       s.graph_state = 1;
       s.graph_aux = aux;
-      s.graph_gram = gram;
-      s.graph_rows = rows_ll;
-      s.graph_k = k;
     }
+  }
+  if (!recording) {  // what the buffers (and a recorded graph) now belong to
+    s.graph_steps = steps;
+    s.graph_gram = gram;
+    s.graph_rows = rows_ll;
+    s.graph_k = k;
   }
   TPB_CUDA(launch_select_basis(io.stream, ritz_vectors, s.theta, rows, b, k, factor_out, s.flag));
   ctx->own_kernels += 1;
@@ -647,6 +661,7 @@ struct tp_plan {
   std::vector<cudaEvent_t> gram_ready, factor_ready;
   bool overlap_evd = true;                    // Jacobi: eigen-solves on side streams beside the tree TTMs
   bool fast_evd = true;                       // top-k subspace iteration where eligible, verified, full solve otherwise
+  bool leaf_steps_changed = false;            // a leaf's power-step count moved: the recorded sweep is stale
   int fast_rejected = 0;
   std::vector<std::vector<int>> visit_order;  // per node: children in execution order (see plan_visit_order)
   std::vector<int> leaf_rank;                 // per mode: position of its leaf in the execution order
@@ -878,9 +893,18 @@ std::vector<int> evaluate_fast_leaves(tp_ctx* ctx, tp_plan* p) {
       // amount of iterating certifies that)
       s.refinable = (host[0] & 1) != 0 && host[1] == 0 && host[4] == 0 && p->host_diag[4 * m + 2] < 0.5;
       if (!s.refinable) s.last_ritz = nullptr;
+      if (s.launch_sequence && s.power_steps < kSubspacePowerSteps) {
+        s.power_steps_floor = std::min(kSubspacePowerSteps, s.power_steps + 2);
+        s.power_steps = kSubspacePowerSteps;
+        p->leaf_steps_changed = true;
+      }
       TPB_CUDA(cudaMemsetAsync(s.flag, 0, sizeof(int), ctx->stream));
     } else {
       s.failures = 0;
+      if (s.launch_sequence && p->host_diag[4 * m] < 1e-2 && s.power_steps > s.power_steps_floor) {
+        s.power_steps = std::max(s.power_steps_floor, s.power_steps - 2);
+        p->leaf_steps_changed = true;
+      }
     }
     s.fast_used = false;
   }
@@ -2155,6 +2179,10 @@ int tp_plan_sweep(tp_ctx* ctx, tp_plan* p, const tp_tensor* t, tp_sweep_stats* s
       // leaves solved by subspace iteration are accepted only with their certificate; a rejected leaf is redone
       // (more rounds, else the full eigen-solve on its intact Gram matrix), and the core with it
       const std::vector<int> rejected = evaluate_fast_leaves(ctx, p);
+      if (p->leaf_steps_changed) {
+        drop_sweep_graph(p);
+        p->leaf_steps_changed = false;
+      }
       for (int m = 0; m < p->n; ++m) {
         if (p->host_status[8 * m + 5] != 0) raise(TP_ERR_TOO_LARGE, "eigensolver did not converge");  // hooi.hpp:56-57
         flag |= p->host_status[8 * m + 4];

@@ -30,6 +30,13 @@ __device__ __forceinline__ double fast_rsqrt_1_2(double x) {
   return y;
 }
 
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+
 constexpr int kEvdMaxBlock = 112;     // largest block the single-CTA kernels take (2 b^2 doubles of shared memory)
 constexpr int kJacobiMaxSweeps = 30;
 
@@ -206,6 +213,191 @@ __device__ int jacobi_sweeps_smem(double* __restrict__ h, double* __restrict__ v
   return sweep;
 }
 
+// In-place Cholesky factorisation of the symmetric positive definite b x b matrix s + shift I (leading dimension m,
+// shared) by ONE warp, lane i owning rows i, i + 32, ...: no CTA barrier per column (with sixteen warps and a barrier
+// per column the barrier and its stragglers were most of the time).  On return the lower triangle holds L and
+// invd[j] = 1 / L(j, j); false (uniformly) when a pivot is not positive.
+//
+// shift > 0 is the first pass of a shifted Cholesky QR: the oversampling columns of Z = G Q lie, up to the ratio
+// lambda_noise / lambda_signal, inside the span of the leading ones, so Z^T Z is numerically singular whenever that
+// ratio drops below ~1e-8 and an unshifted factorisation breaks down.  With the shift every pivot is positive; the
+// columns it touches come out shorter than unit length, the span is unchanged, and the unshifted passes that follow
+// (on a block whose condition number is now moderate) restore orthonormality.
+template <int kCap>
+__device__ __noinline__ bool cholesky_warp(double* __restrict__ s, double* __restrict__ invd, int b, int m, double shift) {
+  constexpr int kPasses = kCap / 32;  // rows per lane
+  constexpr int kTiles = kCap / 8;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  __shared__ int ok_flag;
+  __syncthreads();
+  if (warp == 0) {
+    bool ok = true;
+    // panels of eight columns.  The panel lives in registers, row i = lane + 32 r in x[r][.]: a column is scaled by
+    // 1 / sqrt(d) and pushed into the later columns of the panel through shuffles, nothing touches shared memory on
+    // the dependent chain; the columns behind the panel then take S -= L_panel L_panel^T on the FP64 tensor pipe.
+    for (int j0 = 0; j0 < b && ok; j0 += 8) {
+      double x[kPasses][8];
+#pragma unroll
+      for (int r = 0; r < kPasses; ++r)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int i = lane + 32 * r, c = j0 + e;
+          x[r][e] = (c < b && i < b && i >= c) ? s[c * m + i] + (i == c ? shift : 0.0) : 0.0;
+        }
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int c = j0 + e;
+        if (c >= b || !ok) break;  // uniform in the warp
+        double d = __shfl_sync(0xffffffffu, x[0][e], c & 31);
+        if constexpr (kPasses > 1) {
+          const double upper = __shfl_sync(0xffffffffu, x[kPasses - 1][e], c & 31);
+          if (c >= 32) d = upper;
+        }
+        if (!(d > 0.0) || !(d <= DBL_MAX)) {
+          ok = false;
+          break;
+        }
+        double rinv = rsqrt(d);
+        rinv = fma(rinv, fma(-0.5 * d * rinv, rinv, 0.5), rinv);  // one Newton step: within an ulp or two
+#pragma unroll
+        for (int r = 0; r < kPasses; ++r) {
+          const int i = lane + 32 * r;
+          x[r][e] = i > c ? x[r][e] * rinv : (i == c ? d * rinv : 0.0);
+          if (i == c) invd[c] = rinv;
+        }
+#pragma unroll
+        for (int f = e + 1; f < 8; ++f) {
+          const int cf = j0 + f;  // L(cf, c) sits in the lane that owns row cf
+          double lf = __shfl_sync(0xffffffffu, x[0][e], cf & 31);
+          if constexpr (kPasses > 1) {
+            const double upper = __shfl_sync(0xffffffffu, x[kPasses - 1][e], cf & 31);
+            if (cf >= 32) lf = upper;
+          }
+#pragma unroll
+          for (int r = 0; r < kPasses; ++r) x[r][f] = fma(-x[r][e], lf, x[r][f]);
+        }
+      }
+      if (!ok) break;
+#pragma unroll
+      for (int r = 0; r < kPasses; ++r)
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int i = lane + 32 * r, c = j0 + e;
+          if (c < b && i < b && i >= c) s[c * m + i] = x[r][e];
+        }
+      __syncwarp();
+      // trailing update, tile row by tile row: every load of a tile row before its first store.  Fragments:
+      // A(row, k) = -L(row, j0 + k), B(k, n) = L(column n, j0 + k); a tile may reach past row / column
+      // b (reads whatever is there, stores nothing) -- only entries on and below the diagonal are kept.
+      const int first = j0 / 8 + 1, tiles = (b + 7) / 8;
+      for (int ti = first; ti < tiles; ++ti) {
+        const int row = 8 * ti + g;
+        const double a0 = -s[(j0 + t) * m + row], a1 = -s[(j0 + 4 + t) * m + row];
+        double c0v[kTiles], c1v[kTiles];
+#pragma unroll
+        for (int tj = 1; tj < kTiles; ++tj) {
+          if (tj < first || tj > ti) continue;  // uniform
+          const int col = 8 * tj + 2 * t;
+          c0v[tj] = s[col * m + row];
+          c1v[tj] = s[(col + 1) * m + row];
+          dmma884(c0v[tj], c1v[tj], a0, s[(j0 + t) * m + 8 * tj + g]);
+          dmma884(c0v[tj], c1v[tj], a1, s[(j0 + 4 + t) * m + 8 * tj + g]);
+        }
+#pragma unroll
+        for (int tj = 1; tj < kTiles; ++tj) {
+          if (tj < first || tj > ti) continue;
+          const int col = 8 * tj + 2 * t;
+          if (row < b && col <= row) s[col * m + row] = c0v[tj];
+          if (row < b && col + 1 <= row) s[(col + 1) * m + row] = c1v[tj];
+        }
+        __syncwarp();
+      }
+    }
+    if (lane == 0) ok_flag = ok ? 1 : 0;
+  }
+  __syncthreads();
+  return ok_flag != 0;
+}
+
+// z (rows x b, shared) <- z L^{-T}, in place, in blocks of eight columns; a warp owns 32 consecutive rows for the
+// whole solve, so the blocks are separated by warp-level synchronisation only.  Per block:
+//   * a thread solves its row against the 8 x 8 diagonal block in registers (right-looking: once x_j = z_j / L(j,j)
+//     is known the later columns of the block are updated independently -- one multiplication and one update on the
+//     dependent chain per column);
+//   * the warp subtracts X_block L(trailing, block)^T from its rows of every later column block on the FP64 tensor
+//     pipe (fragment layout as in dmma_accumulate).
+// Entries of L read beyond row b only reach registers and columns that are never stored.
+static __device__ __noinline__ void trsm_rows_blocked(double* __restrict__ z, const double* __restrict__ l,
+                                  const double* __restrict__ invd, int rows, int b, int ld, int m) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int base = 32 * warp, row = base + lane;
+  const bool live = row < rows;
+  const int blocks = (b + 7) / 8;
+  if (base < rows) {  // uniform in the warp
+    for (int blk = 0; blk < blocks; ++blk) {
+      const int c0 = 8 * blk;
+      double x[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) x[e] = (live && c0 + e < b) ? z[static_cast<size_t>(c0 + e) * ld + row] : 0.0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        if (c0 + e >= b) break;  // uniform
+        const double xe = x[e] * invd[c0 + e];
+        x[e] = xe;
+        const double* const le = l + (c0 + e) * m + c0;
+#pragma unroll
+        for (int f = e + 1; f < 8; ++f) x[f] = fma(-xe, le[f], x[f]);
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (live && c0 + e < b) z[static_cast<size_t>(c0 + e) * ld + row] = x[e];
+      if (blk + 1 == blocks) break;  // nothing behind the last block (all eight columns of the others exist)
+      __syncwarp();
+      const double* const lb0 = l + (c0 + t) * m + g;      // B(k, n) = L(n, block column k): k-step 0
+      const double* const lb1 = l + (c0 + 4 + t) * m + g;  // k-step 1
+      // the four m-tiles of the warp together, every load of a column block before its first store (the m-tiles
+      // beyond the matrix read rows of the following columns and store nothing)
+      double a0[4], a1[4];
+      int rr[4];  // rows beyond the matrix read its last row instead (z may be global memory) and store nothing
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        rr[mt] = min(base + 8 * mt + g, rows - 1);
+        a0[mt] = -z[static_cast<size_t>(c0 + t) * ld + rr[mt]];
+        a1[mt] = -z[static_cast<size_t>(c0 + 4 + t) * ld + rr[mt]];
+      }
+      for (int later = blk + 1; later < blocks; ++later) {
+        const int cn = 8 * later;
+        const double b0 = lb0[cn], b1 = lb1[cn];
+        // (columns beyond b exist only as fragment padding: read the last column instead)
+        double* const out0 = z + static_cast<size_t>(min(cn + 2 * t, b - 1)) * ld;
+        double* const out1 = z + static_cast<size_t>(min(cn + 2 * t + 1, b - 1)) * ld;
+        double c0v[4], c1v[4];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) {
+          c0v[mt] = out0[rr[mt]];
+          c1v[mt] = out1[rr[mt]];
+        }
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) {
+          dmma884(c0v[mt], c1v[mt], a0[mt], b0);
+          dmma884(c0v[mt], c1v[mt], a1[mt], b1);
+        }
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) {
+          if (base + 8 * mt + g < rows) {
+            if (cn + 2 * t < b) out0[rr[mt]] = c0v[mt];
+            if (cn + 2 * t + 1 < b) out1[rr[mt]] = c1v[mt];
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+}
+
 __device__ __forceinline__ double rsqrt_seed(double x) {  // ~23 bits, straight from the special function unit
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
@@ -230,9 +422,10 @@ __device__ __forceinline__ double rsqrt_seed(double x) {  // ~23 bits, straight 
 // which has no cancellation and needs two reciprocal square roots (hardware seed, Newton in double); c^2 + s^2 = 1 to
 // rounding whatever the seed's error, so every step is an exact similarity transform, and the rotated h_pq is
 // computed, not set to zero.  h, h2, v, v2 16-byte aligned, m even.  On return (after a CTA barrier) the result is in
-// h and v; same return value as above; prof: [0] convergence checks, [2] steps.
+// h and v; same return value as above; prof: [0] convergence checks, [2] steps.  Not inlined: inside a large kernel
+// the register allocator otherwise recomputes the step-independent addresses in every step.
 template <int kThreads, int kBlockCap, int kActiveWarps>
-__device__ int jacobi_pingpong_smem(double* h, double* h2, double* v, double* v2, int b, int m,
+__device__ __noinline__ int jacobi_pingpong_smem(double* h, double* h2, double* v, double* v2, int b, int m,
                                     long long* prof = nullptr) {
   static_assert(kBlockCap <= 64, "one rotation per lane");
   static_assert(kActiveWarps * 32 <= kThreads, "active warps are warps of the CTA");

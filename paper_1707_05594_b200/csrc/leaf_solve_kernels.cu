@@ -79,12 +79,6 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(gmem) : "memory");
 }
-__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(c0), "+d"(c1)
-               : "d"(a), "d"(b));
-}
-
 // Every product of the solve runs on the FP64 tensor pipe (DMMA.8x8x4), fragments straight from shared memory:
 //   lane (g = lane / 4, t = lane % 4) holds A(row g, k t), B(k t, column g), C(row g, columns 2t and 2t + 1).
 // Leading dimensions are chosen so that a fragment load is conflict free: the rows x b blocks (Q, Z) have
@@ -223,7 +217,7 @@ __device__ __forceinline__ void copy_gram_columns(const double* __restrict__ g, 
 //     slabs in flight while one is multiplied, so every entry of G is read from L2 exactly once per product.
 // The caller synchronises afterwards.
 template <int MT, int NT>
-__device__ void product_gq(const double* __restrict__ g, const double* __restrict__ in, double* __restrict__ out,
+__device__ __noinline__ void product_gq(const double* __restrict__ g, const double* __restrict__ in, double* __restrict__ out,
                            double* __restrict__ gbuf, bool resident, bool wide, int slab, int rows, int b, int ld,
                            int lda) {
   double acc[MT][NT][2];
@@ -262,7 +256,7 @@ __device__ void product_gq(const double* __restrict__ g, const double* __restric
 // x (rows x b, shared, leading dimension ld) <- x * vs (b x b, leading dimension m), in place: a warp reads only the
 // rows it writes, and all of them before it writes any.
 template <int MT, int NT>
-__device__ void rotate_block(double* __restrict__ x, const double* __restrict__ vs, int rows, int b, int ld, int m) {
+__device__ __noinline__ void rotate_block(double* __restrict__ x, const double* __restrict__ vs, int rows, int b, int ld, int m) {
   double acc[MT][NT][2];
 #pragma unroll
   for (int i = 0; i < MT; ++i)
@@ -278,7 +272,7 @@ __device__ void rotate_block(double* __restrict__ x, const double* __restrict__ 
 // the 8 x 8 tiles on and below the diagonal are computed and mirrored (both uses are symmetric: Z^T Z and Q^T (G Q)).
 // A warp owns a tile; two accumulator pairs alternate along the contraction to halve the dependent chain, and the
 // order of the sums is fixed.
-__device__ void small_gram(const double* __restrict__ a, const double* __restrict__ bm, double* __restrict__ s,
+__device__ __noinline__ void small_gram(const double* __restrict__ a, const double* __restrict__ bm, double* __restrict__ s,
                            int rows, int b, int ld, int m) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
@@ -313,156 +307,6 @@ __device__ void small_gram(const double* __restrict__ a, const double* __restric
       }
     }
   }
-}
-
-// In-place Cholesky factorisation of the symmetric positive definite b x b matrix s + shift I (leading dimension m,
-// shared) by ONE warp: lane i owns rows i, i + 32, ...; column j is scaled by 1 / sqrt(d_j) and pushed into the trailing
-// columns through shuffles, so a column costs one reciprocal square root, one warp-level synchronisation and no CTA
-// barrier (with sixteen warps and a barrier per column the barrier and its stragglers were most of the time).  On
-// return the lower triangle holds L and invd[j] = 1 / L(j, j); false (uniformly) when a pivot is not positive.
-//
-// shift > 0 is the first pass of a shifted Cholesky QR: the oversampling columns of Z = G Q lie, up to the ratio
-// lambda_noise / lambda_signal, inside the span of the leading ones, so Z^T Z is numerically singular whenever that
-// ratio drops below ~1e-8 and an unshifted factorisation breaks down.  With the shift every pivot is positive; the
-// columns it touches come out shorter than unit length, the span is unchanged, and the unshifted passes that follow
-// (on a block whose condition number is now moderate) restore orthonormality.
-template <int kCap>
-__device__ bool cholesky_warp(double* __restrict__ s, double* __restrict__ invd, int b, int m, double shift) {
-  constexpr int kPasses = kCap / 32;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  __shared__ int ok_flag;
-  __syncthreads();
-  if (warp == 0) {
-    bool ok = true;
-    for (int j = 0; j < b; ++j) {
-      const double d = s[j * m + j] + shift;  // the trailing updates work on the unshifted diagonal
-      if (!(d > 0.0) || !(d <= DBL_MAX)) {    // uniform: every lane reads the same value
-        ok = false;
-        break;
-      }
-      double rinv = rsqrt(d);
-      rinv = fma(rinv, fma(-0.5 * d * rinv, rinv, 0.5), rinv);  // one Newton step: within an ulp or two
-      double lij[kPasses];
-#pragma unroll
-      for (int r = 0; r < kPasses; ++r) {
-        const int i = lane + 32 * r;
-        const bool mine = i > j && i < b;
-        lij[r] = mine ? s[j * m + i] * rinv : 0.0;
-        if (mine) s[j * m + i] = lij[r];
-        if (i == j) {
-          s[j * m + j] = d * rinv;
-          invd[j] = rinv;
-        }
-      }
-      // four trailing columns at a time, every load before the first store: the columns are independent, but the
-      // compiler cannot know that the stores of one do not feed the loads of the next
-      for (int k0 = j + 1; k0 < b; k0 += 4) {
-        double lkj[4], old[4][kPasses];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int k = min(k0 + e, b - 1);
-          lkj[e] = __shfl_sync(0xffffffffu, lij[0], k & 31);
-          if constexpr (kPasses > 1) {
-            const double upper = __shfl_sync(0xffffffffu, lij[kPasses - 1], k & 31);
-            if (k >= 32) lkj[e] = upper;
-          }
-#pragma unroll
-          for (int r = 0; r < kPasses; ++r) {
-            const int i = lane + 32 * r;
-            old[e][r] = (k0 + e < b && i >= k && i < b) ? s[k * m + i] : 0.0;
-          }
-        }
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int k = k0 + e;
-#pragma unroll
-          for (int r = 0; r < kPasses; ++r) {
-            const int i = lane + 32 * r;
-            if (k < b && i >= k && i < b) s[k * m + i] = fma(-lij[r], lkj[e], old[e][r]);
-          }
-        }
-      }
-      __syncwarp();
-    }
-    if (lane == 0) ok_flag = ok ? 1 : 0;
-  }
-  __syncthreads();
-  return ok_flag != 0;
-}
-
-// z (rows x b, shared) <- z L^{-T}, in place, in blocks of eight columns; a warp owns 32 consecutive rows for the
-// whole solve, so the blocks are separated by warp-level synchronisation only.  Per block:
-//   * a thread solves its row against the 8 x 8 diagonal block in registers (right-looking: once x_j = z_j / L(j,j)
-//     is known the later columns of the block are updated independently -- one multiplication and one update on the
-//     dependent chain per column);
-//   * the warp subtracts X_block L(trailing, block)^T from its rows of every later column block on the FP64 tensor
-//     pipe (fragment layout as in dmma_accumulate).
-// Entries of L read beyond row b only reach registers and columns that are never stored.
-__device__ void trsm_rows_blocked(double* __restrict__ z, const double* __restrict__ l,
-                                  const double* __restrict__ invd, int rows, int b, int ld, int m) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = lane >> 2, t = lane & 3;
-  const int base = 32 * warp, row = base + lane;
-  const bool live = row < rows;
-  const int blocks = (b + 7) / 8;
-  if (base < rows) {  // uniform in the warp
-    for (int blk = 0; blk < blocks; ++blk) {
-      const int c0 = 8 * blk;
-      double x[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) x[e] = (live && c0 + e < b) ? z[(c0 + e) * ld + row] : 0.0;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        if (c0 + e >= b) break;  // uniform
-        const double xe = x[e] * invd[c0 + e];
-        x[e] = xe;
-        const double* const le = l + (c0 + e) * m + c0;
-#pragma unroll
-        for (int f = e + 1; f < 8; ++f) x[f] = fma(-xe, le[f], x[f]);
-      }
-#pragma unroll
-      for (int e = 0; e < 8; ++e)
-        if (live && c0 + e < b) z[(c0 + e) * ld + row] = x[e];
-      if (blk + 1 == blocks) break;  // nothing behind the last block (all eight columns of the others exist)
-      __syncwarp();
-      const double* const lb0 = l + (c0 + t) * m + g;      // B(k, n) = L(n, block column k): k-step 0
-      const double* const lb1 = l + (c0 + 4 + t) * m + g;  // k-step 1
-      // the four m-tiles of the warp together, every load of a column block before its first store (the m-tiles
-      // beyond the matrix read rows of the following columns and store nothing)
-      double a0[4], a1[4];
-#pragma unroll
-      for (int mt = 0; mt < 4; ++mt) {
-        const int r = base + 8 * mt + g;
-        a0[mt] = -z[(c0 + t) * ld + r];
-        a1[mt] = -z[(c0 + 4 + t) * ld + r];
-      }
-      for (int later = blk + 1; later < blocks; ++later) {
-        const int cn = 8 * later;
-        const double b0 = lb0[cn], b1 = lb1[cn];
-        double* const out0 = z + (cn + 2 * t) * ld + base + g;
-        double c0v[4], c1v[4];
-#pragma unroll
-        for (int mt = 0; mt < 4; ++mt) {
-          c0v[mt] = out0[8 * mt];
-          c1v[mt] = out0[ld + 8 * mt];
-        }
-#pragma unroll
-        for (int mt = 0; mt < 4; ++mt) {
-          dmma884(c0v[mt], c1v[mt], a0[mt], b0);
-          dmma884(c0v[mt], c1v[mt], a1[mt], b1);
-        }
-#pragma unroll
-        for (int mt = 0; mt < 4; ++mt) {
-          if (base + 8 * mt + g < rows) {
-            if (cn + 2 * t < b) out0[8 * mt] = c0v[mt];
-            if (cn + 2 * t + 1 < b) out0[ld + 8 * mt] = c1v[mt];
-          }
-        }
-      }
-      __syncwarp();
-    }
-  }
-  __syncthreads();
 }
 
 // m-tiles per warp and n-tiles of the DMMA products: 32 accumulators per thread either way
