@@ -178,8 +178,10 @@ int tp_ctx_destroy(tp_ctx* ctx);
 enum { TP_CTX_OPT_STREAMED_UPLOAD_MIN_BYTES = 1, TP_CTX_OPT_TRACE_EVD = 2 };
 int tp_ctx_set_option(tp_ctx* ctx, int option, long long value);
 /* Process-wide switches.  TP_GLOBAL_OPT_TTM_TMA (default 1): 0 forces the cp.async TTM kernel where the TMA pipeline
- * would be chosen (both compute the same sums in the same order). */
-enum { TP_GLOBAL_OPT_TTM_TMA = 1 };
+ * would be chosen (both compute the same sums in the same order).  TP_GLOBAL_OPT_TTM_PACKED (default 1): 0 sends
+ * products with a short trailing extent (1 < inner < 8) to the general kernels instead of the packed-column one
+ * (same sums, same order). */
+enum { TP_GLOBAL_OPT_TTM_TMA = 1, TP_GLOBAL_OPT_TTM_PACKED = 2 };
 int tp_set_global_option(int option, long long value);
 int tp_ctx_synchronize(tp_ctx* ctx);
 /* the CUDA stream the engine launches on (cudaStream_t as void*), for event timing by the caller */

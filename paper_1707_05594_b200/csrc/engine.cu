@@ -1431,6 +1431,8 @@ int tp_set_global_option(int option, long long value) {
   return guarded([&] {
     if (option == TP_GLOBAL_OPT_TTM_TMA)
       ttm_tma_enabled().store(value != 0, std::memory_order_relaxed);
+    else if (option == TP_GLOBAL_OPT_TTM_PACKED)
+      ttm_packed_enabled().store(value != 0, std::memory_order_relaxed);
     else
       raise(TP_ERR_BAD_ARGUMENT, "unknown global option");
   });

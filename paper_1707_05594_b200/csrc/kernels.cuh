@@ -52,6 +52,13 @@ cudaError_t launch_ttm(cudaStream_t stream, const double* x, long long outer, lo
 
 // Process-wide A/B switch: false forces the cp.async kernel even where the TMA pipeline is eligible.
 std::atomic<bool>& ttm_tma_enabled();
+// Short trailing extents (1 < inner < 8): columns packed across slabs, contiguous slab chunks (ttm_packed_kernels.cu).
+std::atomic<bool>& ttm_packed_enabled();
+bool ttm_packed_eligible(const double* x, long long outer, long long len, long long inner, const double* z, int kt,
+                         int n_dest);
+cudaError_t launch_ttm_packed(cudaStream_t stream, const double* x, long long outer, long long len, long long inner,
+                              const double* mfrag, const TtmFragmentLayout& f, long long new_len, double* z,
+                              int sm_count);
 
 // Warp-specialised TMA variant (ttm_tma_kernels.cu): used by launch_ttm for 16-byte-aligned, even extents with enough
 // columns to fill the machine.  mfrag must be the copy matching the mode (interleaved rows when inner > 1).

@@ -78,6 +78,29 @@ struct TtmParams {
   long long dest_off[kMaxTtmDest];
 };
 
+// One stage (KC contraction steps) for the first NL n-tiles of a warp.  NL is a compile-time count on purpose: a
+// run-time guard around a DMMA is compiled into a predicate, and a predicated-off DMMA still takes its turn on the
+// tensor pipe -- skipping dead tiles has to be a branch to another instantiation.
+template <int KT, int NT, int NL, int KC, bool LAST>
+__device__ __forceinline__ void consume_stage(double (&acc)[KT][NT][2], const double* __restrict__ xd,
+                                              const double* __restrict__ md, int frag_k, int frag_n) {
+#pragma unroll
+  for (int s = 0; s < KC / 4; ++s) {
+    double a[KT], b[NL];
+#pragma unroll
+    for (int i = 0; i < KT; ++i) a[i] = md[(s * KT + i) * 32];
+    const int l = 4 * s + frag_k;
+#pragma unroll
+    for (int j = 0; j < NL; ++j)
+      b[j] = LAST ? xd[j * (KC * 8) + frag_n * KC + (l ^ ((frag_n & 3) << 2))]
+                  : xd[j * (KC * 8) + l * 8 + (frag_n ^ (((l >> 1) & 1) << 2))];
+#pragma unroll
+    for (int j = 0; j < NL; ++j)
+#pragma unroll
+      for (int i = 0; i < KT; ++i) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+  }
+}
+
 // Persistent CTA: K block blockIdx.y; tile groups blockIdx.x, blockIdx.x + gridDim.x, ... of TILE_N n-tiles each.
 template <int KT, int NT, int KC, int STAGES, bool LAST>
 __global__ void __launch_bounds__(kThreads, (KT * NT <= 20) ? 2 : 1) ttm_dmma_kernel(const TtmParams p) {
@@ -291,26 +314,18 @@ __global__ void __launch_bounds__(kThreads, (KT * NT <= 20) ? 2 : 1) ttm_dmma_ke
     const double* const xd = xs + cons_stage * XS + (warp * NT) * (KC * 8);
     const double* const md = ms + cons_stage * MS + lane;
     cons_stage = (cons_stage + 1 == STAGES) ? 0 : cons_stage + 1;
-    bool live[NT];
+    // n-tiles past the end of the tensor hold nothing but zeros; they are the last ones of the warp's NT
+    int n_live = 0;
 #pragma unroll
-    for (int j = 0; j < NT; ++j) live[j] = tile_lim[cons_j % RING][warp * NT + j] != 0;
-#pragma unroll
-    for (int s = 0; s < KC / 4; ++s) {
-      double a[KT];
-#pragma unroll
-      for (int i = 0; i < KT; ++i) a[i] = md[(s * KT + i) * 32];
-      const int l = 4 * s + frag_k;
-#pragma unroll
-      for (int j = 0; j < NT; ++j) {
-        if (!live[j]) continue;  // n-tile past the end: nothing but zeros (uniform in the warp)
-        double b;
-        if (LAST)
-          b = xd[j * (KC * 8) + frag_n * KC + (l ^ ((frag_n & 3) << 2))];
-        else
-          b = xd[j * (KC * 8) + l * 8 + (frag_n ^ (((l >> 1) & 1) << 2))];
-#pragma unroll
-        for (int i = 0; i < KT; ++i) dmma884(acc[i][j][0], acc[i][j][1], a[i], b);
-      }
+    for (int j = 0; j < NT; ++j) n_live += tile_lim[cons_j % RING][warp * NT + j] != 0 ? 1 : 0;
+    if (n_live == NT) {
+      consume_stage<KT, NT, NT, KC, LAST>(acc, xd, md, frag_k, frag_n);
+    } else if (NT >= 4 && n_live == 3) {
+      consume_stage<KT, NT, (NT >= 4 ? 3 : 1), KC, LAST>(acc, xd, md, frag_k, frag_n);
+    } else if (NT >= 2 && n_live == 2) {
+      consume_stage<KT, NT, (NT >= 2 ? 2 : 1), KC, LAST>(acc, xd, md, frag_k, frag_n);
+    } else if (n_live == 1) {
+      consume_stage<KT, NT, 1, KC, LAST>(acc, xd, md, frag_k, frag_n);
     }
     if (++cons_c == p.n_chunks) {
       store_tile(cons_j);
@@ -434,6 +449,9 @@ cudaError_t prep_factor_fragments(cudaStream_t stream, const double* m, long lon
 cudaError_t launch_ttm(cudaStream_t stream, const double* x, long long outer, long long len, long long inner,
                        const double* mfrag, const TtmFragmentLayout& f, long long new_len, double* z, int sm_count,
                        int n_dest, const long long* dest_cuts, const long long* dest_offsets) {
+  if (ttm_packed_eligible(x, outer, len, inner, z, f.kt, n_dest) && (!dest_cuts || (dest_cuts[0] == 0 && dest_cuts[1] == new_len)) &&
+      (!dest_offsets || dest_offsets[0] == 0))
+    return launch_ttm_packed(stream, x, outer, len, inner, mfrag, f, new_len, z, sm_count);
   if (ttm_tma_enabled().load(std::memory_order_relaxed) &&
       ttm_tma_eligible(x, outer, len, inner, z, f.kt, f.k_blocks, sm_count)) {
     bool chunks_aligned = true;

@@ -86,6 +86,32 @@ struct TmaParams {
   long long dest_off[kMaxTtmDest];
 };
 
+// One stage (kKC contraction steps) for the first NL n-tiles of a consumer warp.  NL is a compile-time count on
+// purpose: a run-time guard around a DMMA is compiled into a predicate, and a predicated-off DMMA still takes its
+// turn on the tensor pipe -- skipping dead tiles has to be a branch to another instantiation.
+template <int KT, int NT, int NL, bool LAST>
+__device__ __forceinline__ void consume_stage(double (&acc)[KT][NT][2], const double* __restrict__ xd,
+                                              const double* __restrict__ md, const int (&frag_off)[4], int cw) {
+#pragma unroll
+  for (int s = 0; s < kKC / 4; ++s) {
+    double a[KT], b[NL];
+#pragma unroll
+    for (int i = 0; i < KT; ++i) a[i] = md[(s * KT + i) * 32];
+#pragma unroll
+    for (int jj = 0; jj < NL; ++jj) {
+      const int t = cw * NT + jj;
+      const double* const box = xd + (t >> 1) * (kKC * 16);
+      // the half-box term: LAST -> rows 8..15 (offset 8 * 16, same swizzle since 8 & 7 == 0);
+      //                    !LAST -> columns 8..15 = chunks 4..7 -> XOR with 4 on the chunk index = +/- 8 doubles
+      b[jj] = LAST ? box[frag_off[s] + (t & 1) * (8 * 16)] : box[frag_off[s] ^ ((t & 1) << 3)];
+    }
+#pragma unroll
+    for (int jj = 0; jj < NL; ++jj)
+#pragma unroll
+      for (int i = 0; i < KT; ++i) dmma884(acc[i][jj][0], acc[i][jj][1], a[i], b[jj]);
+  }
+}
+
 template <int KT, int NT, int STAGES, bool LAST>
 __global__ void __launch_bounds__(kThreads, (KT * NT <= 12) ? 2 : 1)
     ttm_tma_kernel(const __grid_constant__ CUtensorMap xmap, const TmaParams p) {
@@ -195,38 +221,28 @@ __global__ void __launch_bounds__(kThreads, (KT * NT <= 12) ? 2 : 1)
       frag_off[s] = l * 16 + ((((col >> 1) ^ (l & 7)) << 1) | (col & 1));
     }
   }
-  // the half-box term: LAST -> rows 8..15 (offset 8 * 16, same swizzle since 8 & 7 == 0);
-  //                    !LAST -> columns 8..15 = chunks 4..7 -> XOR with 4 on the chunk index = +/- 8 doubles
-  auto box_elem = [&](const double* box, int s, int half) -> double {
-    if (LAST) return box[frag_off[s] + half * (8 * 16)];
-    return box[frag_off[s] ^ (half << 3)];
-  };
 
   int stage = 0;
   unsigned parity = 0;
   for (long long j = 0; j < my_tiles; ++j) {
     // n-tiles of this warp whose box lies inside the CTA's range: the balanced partition hands small problems less
     // than a full tile per CTA, and multiplying the zero-filled rest would cost as many DMMAs as the real part
-    bool live[NT];
+    // (the live n-tiles of a warp are a prefix of its NT: the boxes past the range are the last ones of the tile)
+    int n_live = 0;
 #pragma unroll
-    for (int jj = 0; jj < NT; ++jj) live[jj] = first_box(j) + ((cw * NT + jj) >> 1) < cta_end;
+    for (int jj = 0; jj < NT; ++jj) n_live += first_box(j) + ((cw * NT + jj) >> 1) < cta_end ? 1 : 0;
     for (int chunk = 0; chunk < p.n_chunks; ++chunk) {
       mbar_wait(&full[stage], parity);
       const double* const xd = xs + stage * XS;
       const double* const md = ms + stage * MS + lane;
-#pragma unroll
-      for (int s = 0; s < kKC / 4; ++s) {
-        double a[KT];
-#pragma unroll
-        for (int i = 0; i < KT; ++i) a[i] = md[(s * KT + i) * 32];
-#pragma unroll
-        for (int jj = 0; jj < NT; ++jj) {
-          if (!live[jj]) continue;  // uniform in the warp
-          const int t = cw * NT + jj;
-          const double b = box_elem(xd + (t >> 1) * (kKC * 16), s, t & 1);
-#pragma unroll
-          for (int i = 0; i < KT; ++i) dmma884(acc[i][jj][0], acc[i][jj][1], a[i], b);
-        }
+      if (n_live == NT) {
+        consume_stage<KT, NT, NT, LAST>(acc, xd, md, frag_off, cw);
+      } else if (NT >= 4 && n_live == 3) {
+        consume_stage<KT, NT, (NT >= 4 ? 3 : 1), LAST>(acc, xd, md, frag_off, cw);
+      } else if (NT >= 2 && n_live == 2) {
+        consume_stage<KT, NT, (NT >= 2 ? 2 : 1), LAST>(acc, xd, md, frag_off, cw);
+      } else if (n_live == 1) {
+        consume_stage<KT, NT, 1, LAST>(acc, xd, md, frag_off, cw);
       }
       // The stage was read with ordinary (generic-proxy) shared loads; the producer will refill it through the TMA
       // unit (async proxy).  Ordering across the two proxies needs this fence before the stage is handed back —

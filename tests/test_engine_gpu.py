@@ -64,6 +64,32 @@ def test_ttm_matches_oracle(ctx, dims, mode, new_len):
     assert np.max(np.abs(got - want)) <= 64 * EPS * np.sqrt(dims[mode]) * np.max(np.abs(m)) * np.max(np.abs(t))
 
 
+PACKED_SHAPES = [
+    # dims, mode, new_len: trailing extents 2..7 behind the contracted mode, slab counts around the 32-slab tile,
+    # ragged last chunks of the contraction, K blocks of one to four m-tiles and more than one K block
+    ((33, 50, 5), 1, 20), ((64, 100, 5), 1, 20), ((31, 16, 3), 1, 8), ((97, 34, 7), 1, 9), ((40, 7, 2), 1, 3),
+    ((5, 18, 3), 1, 32), ((70, 20, 5), 1, 40), ((3, 6, 4, 10, 3), 3, 5), ((130, 48, 6), 1, 17), ((1, 22, 3), 1, 4),
+    ((400, 100, 5), 1, 20),
+]
+
+
+@pytest.mark.parametrize("dims,mode,new_len", PACKED_SHAPES)
+def test_ttm_packed_columns_kernel_is_bit_identical_to_the_general_one(ctx, dims, mode, new_len):
+    """csrc/ttm_packed_kernels.cu (1 < inner < 8): same sums in the same order as the general kernels."""
+    seed = (sum(dims) * 17 + new_len) % 10000
+    t = hostgen.random_tensor(dims, seed)
+    m = hostgen.random_tensor([new_len, dims[mode]], seed + 1)
+    packed = E.ttm(t, m, mode, ctx=ctx)
+    E.check(E.lib.tp_set_global_option(2, E.ctypes.c_longlong(0)))   # TP_GLOBAL_OPT_TTM_PACKED off
+    try:
+        general = E.ttm(t, m, mode, ctx=ctx)
+    finally:
+        E.check(E.lib.tp_set_global_option(2, E.ctypes.c_longlong(1)))
+    assert np.array_equal(packed, general)
+    want = ho.ttm(t, m, mode)
+    assert np.max(np.abs(packed - want)) <= 64 * EPS * np.sqrt(dims[mode]) * np.max(np.abs(m)) * np.max(np.abs(t))
+
+
 def test_ttm_linearity_and_identity(ctx):
     """Size-independent properties at a size the oracle would not finish quickly: identity and linearity."""
     dims = (96, 96, 96, 12)
