@@ -262,14 +262,18 @@ int tp_plan_destroy(tp_ctx* ctx, tp_plan* plan);
  * leaf's eigen-solve on a side stream beside the remaining tree TTMs; 0 serialises everything on one stream, which is
  * what per-kernel timing and profiling want. */
 enum { TP_OPT_OVERLAP_EVD = 1, TP_OPT_FAST_EVD = 2, TP_OPT_CARRY_PATH = 3, TP_OPT_SPARE_SMS = 4,
-       TP_OPT_SPARE_SMS_SHORT = 5, TP_OPT_SWEEP_GRAPH = 6, TP_OPT_LEAF_GRAPH = 7, TP_OPT_FUSED_LEAF_SOLVE = 8 };
+       TP_OPT_SPARE_SMS_SHORT = 5, TP_OPT_SWEEP_GRAPH = 6, TP_OPT_LEAF_GRAPH = 7, TP_OPT_FUSED_LEAF_SOLVE = 8,
+       TP_OPT_FORK_SUBTREES = 9 };
 /* TP_OPT_SPARE_SMS / _SHORT (defaults 2 / 16): SMs a long / short tree product leaves to eigen-solves in flight.
  * TP_OPT_SWEEP_GRAPH (0 off, 1 on, 2 auto = default): replay the steady-state Jacobi sweep -- tree, Gram kernels, leaf
  *   solves, core chain, status read-back -- as ONE CUDA graph; auto does so for sweeps below ~5e10 flops, where the
  *   ~100 launches of a sweep would otherwise pace it.  Per-node timings are not available for replayed sweeps.
  * TP_OPT_LEAF_GRAPH (default 1): replay a large leaf's multi-launch top-k iteration as a CUDA graph.
  * TP_OPT_FUSED_LEAF_SOLVE (default 1): leaves with L_n <= 512 and K_n + 8 <= 64 run their whole certified top-k
- *   solve in one launch (csrc/leaf_solve_kernels.cu). */
+ *   solve in one launch (csrc/leaf_solve_kernels.cu).
+ * TP_OPT_FORK_SUBTREES (0 off, 1 on, 2 auto = default): in a Jacobi sweep the subtrees below a tree node run on
+ *   streams of their own (siblings get one output buffer each instead of one per depth), so the short products and
+ *   Gram kernels of small tensors overlap; auto forks the sweeps TP_OPT_SWEEP_GRAPH's auto replays. */
 int tp_plan_set_option(tp_ctx* ctx, tp_plan* plan, int option, int value);
 /* TP_OPT_CARRY_PATH (default 1; Gauss-Seidel plans carry the first leaf's chain): the core chain core_from_factors (hooi.hpp:93-100) contracts the modes
  * along one root-to-leaf path of the TTM tree; with the new factors its partial products are exactly the

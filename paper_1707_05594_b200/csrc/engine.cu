@@ -652,6 +652,17 @@ struct tp_plan {
   std::vector<double*> frag;                  // fragment-ordered copies, rebuilt when a factor changes
   std::vector<double*> depth_buf;             // one intermediate per tree depth
   std::vector<size_t> depth_cap;
+  // Forked walk (TP_OPT_FORK_SUBTREES; auto = short sweeps).  The subtrees below a node are independent: every child
+  // but the last visited runs on a stream of its own, so the short, latency-bound products and Gram kernels of small
+  // tensors overlap instead of queueing behind one another.  Siblings then need an output buffer each.
+  int fork_mode = 2;                          // 0 off, 1 on, 2 auto
+  bool forking = false;                       // this sweep's walk forks
+  std::vector<size_t> node_cap;               // per node: elements of its product (0 for leaves)
+  std::vector<double*> node_buf;              // allocated on first use
+  std::vector<cudaStream_t> branch;           // branch streams, created on first use
+  std::vector<cudaEvent_t> fork_events;
+  size_t branches_used = 0, fork_events_used = 0;
+  std::vector<cudaEvent_t> branch_done;       // recorded at the end of every branch of this sweep: the join list
   double* core = nullptr;
   double* core_tmp[2] = {nullptr, nullptr};
   size_t core_size = 0, core_tmp_cap = 0;
@@ -682,6 +693,8 @@ struct tp_plan {
   std::vector<double*> arrival_frag;           // fragment-ordered row slices of F_0, one per slab
   std::vector<size_t> arrival_frag_doubles;
   bool factors_from_caller = true;            // no sweep has run since the factors were set
+  bool frags_match_cur = false;               // frag[m] holds the fragments of cur[m] for every mode (the core chain of
+                                              // a Jacobi sweep prepares them from the new factors it then copies to cur)
   bool carry_enabled = true;
   std::vector<int> carry_nodes;               // TTM nodes of the path, root child first (empty: no carrying)
   int carry_leaf_mode = -1;                   // mode of the leaf the path ends in = last product of the core chain
@@ -980,13 +993,85 @@ void plan_visit_order(tp_plan* p) {
   }
 }
 
+cudaEvent_t next_fork_event(tp_plan* p) {
+  if (p->fork_events_used == p->fork_events.size()) {
+    cudaEvent_t e;
+    TPB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    p->fork_events.push_back(e);
+  }
+  return p->fork_events[p->fork_events_used++];
+}
+
+cudaStream_t next_branch_stream(tp_plan* p) {
+  if (p->branches_used == p->branch.size()) {
+    int least = 0, greatest = 0;
+    TPB_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    cudaStream_t st;
+    TPB_CUDA(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, least));  // the tree's priority
+    p->branch.push_back(st);
+  }
+  return p->branch[p->branches_used++];
+}
+
+// Whether this sweep's walk forks, and the per-node buffers it then needs.
+void plan_begin_walk(tp_plan* p) {
+  p->forking = p->sweep_kind == TP_SWEEP_JACOBI && !p->arrival && p->overlap_evd &&
+               (p->fork_mode == 1 || (p->fork_mode == 2 && p->short_sweep));
+  p->branches_used = 0;
+  p->fork_events_used = 0;
+  p->branch_done.clear();
+  if (!p->forking) return;
+  if (p->node_buf.empty()) p->node_buf.assign(p->tree.size(), nullptr);
+  for (int id = 1; id < p->tree.size(); ++id)
+    if (p->node_cap[id] > 0 && !p->node_buf[id]) p->node_buf[id] = device_alloc(p->node_cap[id]);
+}
+
+// The main stream waits for every branch of the walk (before the core chain rewrites the carried products the
+// branches read, and so that a recorded sweep's capture forest joins its origin stream).
+void plan_join_branches(tp_ctx* ctx, tp_plan* p) {
+  for (cudaEvent_t e : p->branch_done) TPB_CUDA(cudaStreamWaitEvent(ctx->stream, e, 0));
+  p->branch_done.clear();
+}
+
 void jacobi_walk(tp_ctx* ctx, tp_plan* p, int node, const double* tensor, std::vector<size_t>& dims, int depth) {
-  for (int c : p->visit_order[node]) {
+  const std::vector<int>& order = p->visit_order[node];
+  const bool fork = p->forking && order.size() > 1;
+  cudaStream_t const home = ctx->stream;
+  cudaEvent_t input_ready = nullptr;
+  if (fork) {
+    input_ready = next_fork_event(p);
+    TPB_CUDA(cudaEventRecord(input_ready, home));
+  }
+  for (size_t i = 0; i < order.size(); ++i) {
+    const int c = order[i];
     const int mode = p->tree.mode[c];
+    // every child but the last visited gets a stream of its own; launches go to ctx->stream, which is switched for
+    // the duration of the child's subtree
+    struct OnBranch {
+      tp_ctx* ctx;
+      tp_plan* plan;
+      cudaStream_t home;
+      bool active;
+      ~OnBranch() {
+        if (!active) return;
+        cudaEvent_t done = nullptr;
+        try {
+          done = next_fork_event(plan);
+        } catch (...) {
+        }
+        if (done && cudaEventRecord(done, ctx->stream) == cudaSuccess) plan->branch_done.push_back(done);
+        ctx->stream = home;
+      }
+    } on_branch{ctx, p, home, fork && i + 1 < order.size()};
+    if (on_branch.active) {
+      cudaStream_t st = next_branch_stream(p);
+      TPB_CUDA(cudaStreamWaitEvent(st, input_ready, 0));
+      ctx->stream = st;
+    }
     if (p->tree.kind[c] == TP_NODE_LEAF) {
       plan_leaf(ctx, p, tensor, dims, mode, p->fresh[mode], c, p->overlap_evd);
     } else {
-      double* out = p->depth_buf[depth];
+      double* out = p->forking ? p->node_buf[c] : p->depth_buf[depth];
       if (p->carry_live && p->on_carry[c]) {
         out = p->carry_buf[depth];  // computed by the previous sweep's core chain (path depth == tree depth)
       } else {
@@ -1797,6 +1882,7 @@ int tp_plan_init_sthosvd(tp_ctx* ctx, tp_plan* p, const tp_tensor* t, const int*
     if (e != cudaSuccess) cuda_fail(e, "copy of the truncated core");
     p->carry_valid = false;
     p->factors_from_caller = true;   // a start like any other: the first sweep's solves are cold
+    p->frags_match_cur = false;
     p->warm_sweeps = 0;
     for (LeafScratch& slot : p->leaf) slot.last_ritz = nullptr;
   });
@@ -1862,6 +1948,9 @@ int tp_plan_create(tp_ctx* ctx, int n_modes, const tp_u64* L, const tp_u64* K, i
       }
       p->depth_buf.assign(p->depth_cap.size(), nullptr);
       for (size_t d = 0; d < p->depth_cap.size(); ++d) p->depth_buf[d] = device_alloc(p->depth_cap[d]);
+      p->node_cap.assign(p->tree.size(), 0);
+      for (int id = 1; id < p->tree.size(); ++id)
+        if (p->tree.internal(id)) p->node_cap[id] = static_cast<size_t>(cards.out[id]);
 
       // core chain in its cheapest order; ping-pong buffers hold its largest partial product
       plan_choose_carry(p);
@@ -1955,6 +2044,9 @@ int tp_plan_destroy(tp_ctx* ctx, tp_plan* p) {
     for (double* d : p->fresh) cudaFree(d);
     for (double* d : p->frag) cudaFree(d);
     for (double* d : p->depth_buf) cudaFree(d);
+    for (double* d : p->node_buf) cudaFree(d);
+    for (cudaStream_t st : p->branch) cudaStreamDestroy(st);
+    for (cudaEvent_t e : p->fork_events) cudaEventDestroy(e);
     for (double* d : p->carry_buf) cudaFree(d);
     for (double* d : p->arrival_slots) cudaFree(d);
     for (double* d : p->arrival_frag) cudaFree(d);
@@ -1988,6 +2080,7 @@ int tp_plan_set_factors(tp_ctx* ctx, tp_plan* p, const double* const* factors) {
     }
     p->carry_valid = false;
     p->factors_from_caller = true;
+    p->frags_match_cur = false;
     p->warm_sweeps = 0;
     for (LeafScratch& slot : p->leaf) slot.last_ritz = nullptr;  // the caller's factors are the start, not ours
     TPB_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -2048,11 +2141,12 @@ namespace {
 // never swap, so the sequence is the same every sweep and can be recorded).
 void jacobi_sequence(tp_ctx* ctx, tp_plan* p, const tp_tensor* t) {
   std::vector<size_t> dims(p->spec.L.begin(), p->spec.L.end());
-  {
+  if (!p->frags_match_cur) {
     Span s(ctx, p, kTree);  // start-of-sweep factors -> fragment order, once per mode
     for (int m = 0; m < p->n; ++m) plan_refresh_fragments(ctx, p, m, p->cur[m]);
     s.close();
   }
+  p->frags_match_cur = false;
   p->leaves_in_flight = 0;
   p->pending.clear();
   p->one_launch_leaves = 0;
@@ -2063,15 +2157,18 @@ void jacobi_sequence(tp_ctx* ctx, tp_plan* p, const tp_tensor* t) {
         subspace_eligible(rows, k, plan_leaf_columns(p, m)) && leaf_solve_fused_eligible(rows, k, k + kSubspaceOversample))
       ++p->one_launch_leaves;
   }
+  plan_begin_walk(p);
   if (p->arrival && p->arrival->row_end.size() > 1 && p->n > 1)
     jacobi_walk_streamed_root(ctx, p, t->data, dims);
   else
     jacobi_walk(ctx, p, 0, t->data, dims, 0);
+  plan_join_branches(ctx, p);
   plan_core(ctx, p, t->data, p->fresh, p->overlap_evd);  // waits for each new factor just before using it
   queue_status_readback(ctx, p, true);
   for (int m = 0; m < p->n; ++m)
     TPB_CUDA(cudaMemcpyAsync(p->cur[m], p->fresh[m], sizeof(double) * p->spec.L[m] * p->spec.K[m],
                              cudaMemcpyDeviceToDevice, ctx->stream));
+  p->frags_match_cur = true;  // plan_core prepared every mode's fragments from fresh[m], now also cur[m]
 }
 
 // May this sweep run as (or be recorded into) the whole-sweep graph?
@@ -2217,6 +2314,7 @@ int tp_plan_sweep(tp_ctx* ctx, tp_plan* p, const tp_tensor* t, tp_sweep_stats* s
         plan_collect_timing(ctx, p);
       }
     } else {
+      p->frags_match_cur = false;
       {
         Span s(ctx, p, kTree);
         for (int m = 0; m < p->n; ++m) plan_refresh_fragments(ctx, p, m, p->cur[m]);
@@ -2291,6 +2389,10 @@ int tp_plan_set_option(tp_ctx* ctx, tp_plan* p, int option, int value) {
     } else if (option == TP_OPT_SWEEP_GRAPH) {
       if (value < 0 || value > 2) raise(TP_ERR_BAD_ARGUMENT, "sweep graph mode is 0 (off), 1 (on) or 2 (auto)");
       p->sweep_graph_mode = value;
+    } else if (option == TP_OPT_FORK_SUBTREES) {
+      if (value < 0 || value > 2) raise(TP_ERR_BAD_ARGUMENT, "fork mode is 0 (off), 1 (on) or 2 (auto)");
+      if (p->fork_mode != value) drop_sweep_graph(p);
+      p->fork_mode = value;
     } else if (option == TP_OPT_LEAF_GRAPH) {
       for (LeafScratch& slot : p->leaf) {
         slot.use_graph = value != 0;

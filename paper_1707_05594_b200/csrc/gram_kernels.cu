@@ -184,7 +184,8 @@ __global__ void gram_reduce_kernel(const double* __restrict__ partial, int split
   const long long i = e / rows, j = e % rows;
   if (j > i) return;
   double sum = 0.0;
-  for (int s = 0; s < splits; ++s) sum += partial[static_cast<long long>(s) * rows * rows + e];
+#pragma unroll 8
+  for (int s = 0; s < splits; ++s) sum += __ldcg(partial + static_cast<long long>(s) * rows * rows + e);
   gram[i * rows + j] = sum;
   gram[j * rows + i] = sum;
 }
@@ -196,13 +197,26 @@ GramLayout gram_layout(long long outer, long long rows, long long inner, int sm_
   g.tiles = static_cast<int>((rows + kTile - 1) / kTile);
   g.chunks = inner == 1 ? (outer + kKC - 1) / kKC : outer * ((inner + kKC - 1) / kKC);
   const long long lower_tiles = static_cast<long long>(g.tiles) * (g.tiles + 1) / 2;
-  // four CTAs fit per SM; aim for at least four full waves so that the last, partial wave costs little
-  long long want = (16LL * sm_count + lower_tiles - 1) / lower_tiles;
-  want = std::min(want, std::max(1LL, g.chunks / 8));                          // at least 8 chunks per split
-  want = std::max(1LL, std::min(want, 512LL));
-  const long long per = (g.chunks + want - 1) / want;
-  g.splits = static_cast<int>((g.chunks + per - 1) / std::max(1LL, per));
-  if (g.splits < 1) g.splits = 1;
+  // Four CTAs fit per SM.  The split count s is the one that minimises waves(s) x chunks per CTA: a grid that ends
+  // just past a wave boundary wastes most of its last wave (C5 leaf: 325 tiles x 8 splits = 4.4 waves cost 5; 9 splits
+  // fill 4.94).  A CTA walks at least 8 chunks, except when the whole problem is a few waves of single chunks (the
+  // leaves of small tensors): there the serial chunk loop of a CTA is the whole kernel time, so it is cut down to what
+  // the cp.async ring holds in flight at once.
+  const long long per_wave = 4LL * sm_count;
+  const long long min_chunks = (g.chunks * lower_tiles <= 4 * per_wave * kStages) ? kStages : 8;
+  const long long max_splits = std::max(1LL, std::min(512LL, g.chunks / min_chunks));
+  long long best = 1, best_cost = -1;
+  for (long long s = 1; s <= max_splits; ++s) {
+    const long long per = (g.chunks + s - 1) / s;
+    const long long used = (g.chunks + per - 1) / per;  // splits that actually get chunks
+    const long long waves = (lower_tiles * used + per_wave - 1) / per_wave;
+    const long long cost = waves * (per + 2) * 64 + used * 8;  // + 2: pipeline fill per CTA; used: the ordered sum
+    if (best_cost < 0 || cost < best_cost) {
+      best_cost = cost;
+      best = used;
+    }
+  }
+  g.splits = static_cast<int>(best);
   g.workspace_doubles = static_cast<size_t>(g.splits) * rows * rows;
   return g;
 }

@@ -232,11 +232,15 @@ class HooiPlan:
 
     def set_option(self, option: int, value: int):
         """tp_plan_set_option: 4/5 spare SMs, 6 whole-sweep graph (0 off, 1 on, 2 auto), 7 leaf graph, 8 one-launch
-        leaf solve."""
+        leaf solve, 9 forked subtrees (0 off, 1 on, 2 auto)."""
         check(lib.tp_plan_set_option(self.ctx._h, self._h, int(option), int(value)))
 
     def set_sweep_graph(self, mode: int):
         self.set_option(6, mode)
+
+    def set_fork_subtrees(self, mode: int):
+        """TP_OPT_FORK_SUBTREES: sibling subtrees of the TTM tree on streams of their own (0 off, 1 on, 2 auto)."""
+        self.set_option(9, mode)
 
     def sweep_info(self):
         """(last sweep replayed the whole-sweep graph?, leaves on the one-launch solve)."""

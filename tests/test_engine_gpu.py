@@ -730,6 +730,45 @@ def test_whole_sweep_graph_is_bit_identical(ctx, cfg):
     dt.free()
 
 
+@pytest.mark.parametrize("graph", [0, 1], ids=["eager", "graph"])
+@pytest.mark.parametrize("cfg", [W.scaled_config(1, [64, 56, 48], [8, 6, 5], 6),
+                                 W.scaled_config(2, [40, 36, 32, 28], [6, 5, 4, 3], 6),
+                                 W.scaled_config(4, [24, 24, 24, 22, 20], [3, 3, 2, 2, 2], 6)], ids=lambda c: c.name)
+def test_forked_subtrees_are_bit_identical(ctx, cfg, graph):
+    """TP_OPT_FORK_SUBTREES: sibling subtrees on streams of their own (one output buffer per node) run the same
+    kernels on the same data as the one-stream walk, so factors and core agree bit for bit, sweep by sweep, eager and
+    as a replayed graph; repeated runs of the forked walk are bit-identical too (no race between the branches)."""
+    spec = cfg.spec
+    tree = P.optimal_tree(spec).tree
+    t = W.build_tensor_host(cfg)
+    f0 = W.start_factors(cfg)
+    dt = E.DeviceTensor.upload(ctx, t)
+    sweeps = 6
+    trails = []
+    for fork in (0, 1, 1):
+        plan = E.HooiPlan(ctx, spec, tree, "jacobi")
+        plan.set_sweep_graph(graph)
+        plan.set_fork_subtrees(fork)
+        plan.set_factors(f0)
+        trail = []
+        for _ in range(sweeps):
+            plan.sweep(dt)
+            trail.append((plan.get_factors(), plan.get_core()))
+        assert plan.sweep_info()[0] == (graph == 1)
+        trails.append(trail)
+        plan.close()
+    for i in range(sweeps):
+        for other in trails[1:]:
+            for a, b in zip(trails[0][i][0], other[i][0]):
+                assert np.array_equal(a, b), i
+            assert np.array_equal(trails[0][i][1], other[i][1]), i
+    of = [f.copy() for f in f0]
+    for i in range(sweeps):
+        ocore, of = ho.hooi_sweep(t, spec.L, spec.K, of, otree(tree), "jacobi", None)
+    assert max(ho.sin_largest_principal_angle(a, b) for a, b in zip(trails[1][-1][0], of)) < 1e-9
+    dt.free()
+
+
 def test_small_spectral_gap_parity(ctx):
     """A tensor whose mode-0 Gram matrix has lambda_K / lambda_{K+1} - 1 = 1e-6: not degenerate by the reference's
     1e-10 rule, but too close for a residual-only certificate (angle error ~ residual / gap).  The gap-aware
