@@ -732,8 +732,9 @@ struct tp_plan {
   cudaEvent_t graph_begin = nullptr, graph_end = nullptr;
   // pinned read-back of every leaf's status, 8 ints per mode: verdict[0..3], degenerate flag, solver info, 2 unused;
   // and of the certificate margins, 4 doubles per mode
-  int* host_status = nullptr;
+  int* host_status = nullptr;    // one pinned block: 8 n ints, then (host_diag) 4 n doubles
   double* host_diag = nullptr;
+  void* dev_status = nullptr;    // the same layout on the device, written by finish_sweep_kernel
   tp_sweep_stats model{};   // analytic SweepStats (tree_macs, core_macs, peak_live)
   tp_sweep_timing timing{};
   // event pool for phase timing: triples (phase, begin, end)
@@ -1217,6 +1218,30 @@ void plan_core(tp_ctx* ctx, tp_plan* p, const double* tensor, const std::vector<
   const bool carry = p->carry_enabled && !p->carry_nodes.empty();
   std::vector<size_t> dims(p->spec.L.begin(), p->spec.L.end());
   const double* src = tensor;
+  // Short sweeps: each new factor is put into fragment order on its solve's side stream, right behind the solve
+  // (once the walk, which still reads the old fragments, is through), instead of in front of every chain product on
+  // the main stream -- all but the first-needed factor's preparation then hides behind the chain.
+  const bool side_prep = wait_for_leaves && p->forking;
+  if (side_prep) {
+    plan_flush_pending(ctx, p);
+    cudaEvent_t walk_done = next_fork_event(p);
+    TPB_CUDA(cudaEventRecord(walk_done, ctx->stream));
+    cudaStream_t const home = ctx->stream;
+    for (int i = 0; i < p->n; ++i) {
+      const int m = p->core_order[i];
+      cudaStream_t const side = ctx->aux[m % tp_ctx::kAux];
+      TPB_CUDA(cudaStreamWaitEvent(side, walk_done, 0));
+      ctx->stream = side;
+      try {
+        plan_refresh_fragments(ctx, p, m, factors[m]);
+      } catch (...) {
+        ctx->stream = home;
+        throw;
+      }
+      ctx->stream = home;
+      TPB_CUDA(cudaEventRecord(p->factor_ready[m], side));
+    }
+  }
   for (int i = 0; i < p->n; ++i) {
     const int m = p->core_order[i];
     if (wait_for_leaves) {
@@ -1231,7 +1256,7 @@ void plan_core(tp_ctx* ctx, tp_plan* p, const double* tensor, const std::vector<
     const bool last = i == p->n - 1;
     // along a carried path the partial products are next sweep's tree nodes: timed as such, kept in their buffers
     Span s = (carry && !last) ? Span(ctx, p, kTree, p->carry_nodes[i]) : Span(ctx, p, kCore);
-    plan_refresh_fragments(ctx, p, m, factors[m]);
+    if (!side_prep) plan_refresh_fragments(ctx, p, m, factors[m]);
     double* dst = last ? p->core : (carry ? p->carry_buf[i] : p->core_tmp[i & 1]);
     // solves of the modes the chain has not waited for yet may still be running on the side streams: the persistent
     // product grid must leave them SMs (its CTAs would otherwise hold every SM until the product ends, and a solve
@@ -2016,10 +2041,12 @@ int tp_plan_create(tp_ctx* ctx, int n_modes, const tp_u64* L, const tp_u64* K, i
         TPB_CUDA(cudaEventCreateWithFlags(&p->gram_ready[m], cudaEventDisableTiming));
         TPB_CUDA(cudaEventCreateWithFlags(&p->factor_ready[m], cudaEventDisableTiming));
       }
-      TPB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&p->host_status), sizeof(int) * 8 * n_modes, cudaHostAllocDefault));
-      TPB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&p->host_diag), sizeof(double) * 4 * n_modes, cudaHostAllocDefault));
-      std::memset(p->host_status, 0, sizeof(int) * 8 * n_modes);
-      std::memset(p->host_diag, 0, sizeof(double) * 4 * n_modes);
+      TPB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&p->host_status), 64 * static_cast<size_t>(n_modes),
+                             cudaHostAllocDefault));
+      p->host_diag = reinterpret_cast<double*>(p->host_status + 8 * n_modes);
+      std::memset(p->host_status, 0, 64 * static_cast<size_t>(n_modes));
+      TPB_CUDA(cudaMalloc(&p->dev_status, 64 * static_cast<size_t>(n_modes)));
+      TPB_CUDA(cudaMemset(p->dev_status, 0, 64 * static_cast<size_t>(n_modes)));
       TPB_CUDA(cudaEventCreate(&p->graph_begin));
       TPB_CUDA(cudaEventCreate(&p->graph_end));
       // below ~2e10 flops a sweep's kernels take a millisecond or two in total and ~100 host launches pace it
@@ -2064,7 +2091,7 @@ int tp_plan_destroy(tp_ctx* ctx, tp_plan* p) {
     if (p->graph_begin) cudaEventDestroy(p->graph_begin);
     if (p->graph_end) cudaEventDestroy(p->graph_end);
     if (p->host_status) cudaFreeHost(p->host_status);
-    if (p->host_diag) cudaFreeHost(p->host_diag);
+    cudaFree(p->dev_status);
     delete p;
   });
 }
@@ -2164,10 +2191,26 @@ void jacobi_sequence(tp_ctx* ctx, tp_plan* p, const tp_tensor* t) {
     jacobi_walk(ctx, p, 0, t->data, dims, 0);
   plan_join_branches(ctx, p);
   plan_core(ctx, p, t->data, p->fresh, p->overlap_evd);  // waits for each new factor just before using it
-  queue_status_readback(ctx, p, true);
-  for (int m = 0; m < p->n; ++m)
-    TPB_CUDA(cudaMemcpyAsync(p->cur[m], p->fresh[m], sizeof(double) * p->spec.L[m] * p->spec.K[m],
-                             cudaMemcpyDeviceToDevice, ctx->stream));
+  // one launch copies the new factors over the current ones and gathers every leaf's status words, one copy brings
+  // them to the host (instead of a copy per word and per factor: ~6 graph nodes per mode at the end of every sweep)
+  FinishSweepArgs fin;
+  fin.n_modes = p->n;
+  for (int m = 0; m < p->n; ++m) {
+    const LeafScratch& s = p->leaf[m];
+    fin.cur[m] = p->cur[m];
+    fin.fresh[m] = p->fresh[m];
+    fin.elems[m] = static_cast<size_t>(p->spec.L[m] * p->spec.K[m]);
+    fin.verdict[m] = s.fast_used ? s.verdict : nullptr;
+    fin.diag[m] = s.fast_used ? s.diag : nullptr;
+    fin.flag[m] = s.flag;
+    fin.info[m] = s.info;
+  }
+  fin.status_ints = static_cast<int*>(p->dev_status);
+  fin.status_doubles = reinterpret_cast<double*>(static_cast<int*>(p->dev_status) + 8 * p->n);
+  TPB_CUDA(launch_finish_sweep(ctx->stream, fin));
+  ctx->own_kernels += 1;
+  TPB_CUDA(cudaMemcpyAsync(p->host_status, p->dev_status, 64 * static_cast<size_t>(p->n), cudaMemcpyDeviceToHost,
+                           ctx->stream));
   p->frags_match_cur = true;  // plan_core prepared every mode's fragments from fresh[m], now also cur[m]
 }
 

@@ -89,6 +89,23 @@ cudaError_t launch_diff_sum_squares(cudaStream_t stream, const double* x, const 
 // out[i] = slots[0][i] + slots[1][i] + ... in that order (the reduction half of a reduce-scatter; fixed order)
 constexpr int kMaxReduceSlots = 16;
 cudaError_t launch_reduce_slots(cudaStream_t stream, double* out, const double* const* slots, int n_slots, size_t n);
+// End of a sweep (engine.cu jacobi_sequence): cur[m] <- fresh[m] for every mode, and the leaves' status words gathered
+// into status_ints (8 per mode: verdict[0..3] where verdict[m] != null, flag, info) / status_doubles (4 per mode: the
+// certificate margins); the degenerate flags are cleared.
+constexpr int kMaxFinishModes = 16;  // TP_MAX_MODES
+struct FinishSweepArgs {
+  int n_modes = 0;
+  double* cur[kMaxFinishModes];
+  const double* fresh[kMaxFinishModes];
+  size_t elems[kMaxFinishModes];
+  const int* verdict[kMaxFinishModes];
+  const double* diag[kMaxFinishModes];
+  int* flag[kMaxFinishModes];
+  const int* info[kMaxFinishModes];
+  int* status_ints = nullptr;
+  double* status_doubles = nullptr;
+};
+cudaError_t launch_finish_sweep(cudaStream_t stream, const FinishSweepArgs& args);
 // dst(a, l0 + l, b) = src(a, l, b): drops the piece (outer, count, inner) into the tensor (outer, full_len, inner)
 cudaError_t launch_assemble_mode(cudaStream_t stream, double* dst, long long outer, long long full_len,
                                  long long inner, const double* src, long long l0, long long count);

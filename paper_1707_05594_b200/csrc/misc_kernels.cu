@@ -201,6 +201,33 @@ struct SlotList {
   const double* p[kMaxReduceSlots];
 };
 
+// End of a Jacobi sweep in one launch: every mode's new factor copied over the current one, and the leaves' status
+// words gathered into one block the host reads with a single copy (8 ints per mode: verdict[0..3], degenerate flag,
+// solver info; then 4 doubles per mode: the certificate margins); the degenerate flags are cleared for the next sweep.
+__global__ void __launch_bounds__(256) finish_sweep_kernel(const FinishSweepArgs a) {
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  const size_t first = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+  for (int m = 0; m < a.n_modes; ++m) {
+    const double* __restrict__ src = a.fresh[m];
+    double* __restrict__ dst = a.cur[m];
+    for (size_t i = first; i < a.elems[m]; i += stride) dst[i] = src[i];
+  }
+  if (blockIdx.x == 0 && threadIdx.x < a.n_modes) {
+    const int m = threadIdx.x;
+    int* const si = a.status_ints + 8 * m;
+    double* const sd = a.status_doubles + 4 * m;
+    if (a.verdict[m]) {
+      for (int i = 0; i < 4; ++i) si[i] = a.verdict[m][i];
+      for (int i = 0; i < 4; ++i) sd[i] = a.diag[m][i];
+    }
+    if (a.flag[m]) {
+      si[4] = *a.flag[m];
+      si[5] = *a.info[m];
+      *a.flag[m] = 0;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) reduce_slots_kernel(double* __restrict__ out, SlotList slots, int n_slots,
                                                            size_t n) {
   const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
@@ -270,6 +297,15 @@ cudaError_t launch_copy_box(cudaStream_t stream, double* dst, const long long* d
   if (total == 0) return cudaSuccess;
   const unsigned blocks = static_cast<unsigned>(std::min<size_t>((total + 255) / 256, kReduceBlocks));
   copy_box_kernel<<<blocks, 256, 0, stream>>>(dst, src, c, total);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_finish_sweep(cudaStream_t stream, const FinishSweepArgs& args) {
+  if (args.n_modes < 1 || args.n_modes > kMaxFinishModes) return cudaErrorInvalidValue;
+  size_t most = 0;
+  for (int m = 0; m < args.n_modes; ++m) most = std::max(most, args.elems[m]);
+  const unsigned blocks = static_cast<unsigned>(std::max<size_t>(1, std::min<size_t>((most + 255) / 256, kReduceBlocks)));
+  finish_sweep_kernel<<<blocks, 256, 0, stream>>>(args);
   return cudaGetLastError();
 }
 
