@@ -180,8 +180,10 @@ int tp_ctx_set_option(tp_ctx* ctx, int option, long long value);
 /* Process-wide switches.  TP_GLOBAL_OPT_TTM_TMA (default 1): 0 forces the cp.async TTM kernel where the TMA pipeline
  * would be chosen (both compute the same sums in the same order).  TP_GLOBAL_OPT_TTM_PACKED (default 1): 0 sends
  * products with a short trailing extent (1 < inner < 8) to the general kernels instead of the packed-column one
- * (same sums, same order). */
-enum { TP_GLOBAL_OPT_TTM_TMA = 1, TP_GLOBAL_OPT_TTM_PACKED = 2 };
+ * (same sums, same order).  TP_GLOBAL_OPT_TTM_SPLITK (default 1): 0 sends the small nodes (at most 640 column tiles,
+ * contraction 32..512) to the streaming kernels instead of the kernel that splits the contraction over a CTA's warps
+ * (same sums to rounding: the eight partial sums are added in warp order, so the last bits differ). */
+enum { TP_GLOBAL_OPT_TTM_TMA = 1, TP_GLOBAL_OPT_TTM_PACKED = 2, TP_GLOBAL_OPT_TTM_SPLITK = 3 };
 int tp_set_global_option(int option, long long value);
 int tp_ctx_synchronize(tp_ctx* ctx);
 /* the CUDA stream the engine launches on (cudaStream_t as void*), for event timing by the caller */

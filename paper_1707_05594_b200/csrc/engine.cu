@@ -1543,6 +1543,8 @@ int tp_set_global_option(int option, long long value) {
       ttm_tma_enabled().store(value != 0, std::memory_order_relaxed);
     else if (option == TP_GLOBAL_OPT_TTM_PACKED)
       ttm_packed_enabled().store(value != 0, std::memory_order_relaxed);
+    else if (option == TP_GLOBAL_OPT_TTM_SPLITK)
+      ttm_splitk_enabled().store(value != 0, std::memory_order_relaxed);
     else
       raise(TP_ERR_BAD_ARGUMENT, "unknown global option");
   });

@@ -183,9 +183,27 @@ __global__ void gram_reduce_kernel(const double* __restrict__ partial, int split
   if (e >= rows * rows) return;
   const long long i = e / rows, j = e % rows;
   if (j > i) return;
+  // splits summed in index order; the loads of a batch are independent and issued together (one exposed L2 latency
+  // per 16 splits instead of one per split)
+  const long long plane = rows * rows;
+  const double* src = partial + e;
   double sum = 0.0;
-#pragma unroll 8
-  for (int s = 0; s < splits; ++s) sum += __ldcg(partial + static_cast<long long>(s) * rows * rows + e);
+  int s = 0;
+  for (; s + 16 <= splits; s += 16) {
+    double v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) v[u] = __ldcg(src + static_cast<long long>(s + u) * plane);
+#pragma unroll
+    for (int u = 0; u < 16; ++u) sum += v[u];
+  }
+  {
+    double v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) v[u] = (s + u < splits) ? __ldcg(src + static_cast<long long>(s + u) * plane) : 0.0;
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+      if (s + u < splits) sum += v[u];
+  }
   gram[i * rows + j] = sum;
   gram[j * rows + i] = sum;
 }

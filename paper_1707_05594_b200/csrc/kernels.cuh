@@ -52,6 +52,12 @@ cudaError_t launch_ttm(cudaStream_t stream, const double* x, long long outer, lo
 
 // Process-wide A/B switch: false forces the cp.async kernel even where the TMA pipeline is eligible.
 std::atomic<bool>& ttm_tma_enabled();
+// Few columns, contraction up to 512: one n-tile per CTA, the contraction split over its warps (ttm_splitk_kernels.cu).
+// Eligibility is a function of the shape alone.
+std::atomic<bool>& ttm_splitk_enabled();
+bool ttm_splitk_eligible(long long outer, long long len, long long inner, int kt, int k_blocks, int n_dest);
+cudaError_t launch_ttm_splitk(cudaStream_t stream, const double* x, long long outer, long long len, long long inner,
+                              const double* mfrag, const TtmFragmentLayout& f, long long new_len, double* z);
 // Short trailing extents (1 < inner < 8): columns packed across slabs, contiguous slab chunks (ttm_packed_kernels.cu).
 std::atomic<bool>& ttm_packed_enabled();
 bool ttm_packed_eligible(const double* x, long long outer, long long len, long long inner, const double* z, int kt,

@@ -449,6 +449,9 @@ cudaError_t prep_factor_fragments(cudaStream_t stream, const double* m, long lon
 cudaError_t launch_ttm(cudaStream_t stream, const double* x, long long outer, long long len, long long inner,
                        const double* mfrag, const TtmFragmentLayout& f, long long new_len, double* z, int sm_count,
                        int n_dest, const long long* dest_cuts, const long long* dest_offsets) {
+  const bool plain_dest = (!dest_cuts || (dest_cuts[0] == 0 && dest_cuts[1] == new_len)) && (!dest_offsets || dest_offsets[0] == 0);
+  if (plain_dest && ttm_splitk_eligible(outer, len, inner, f.kt, f.k_blocks, n_dest))
+    return launch_ttm_splitk(stream, x, outer, len, inner, mfrag, f, new_len, z);
   if (ttm_packed_eligible(x, outer, len, inner, z, f.kt, n_dest) && (!dest_cuts || (dest_cuts[0] == 0 && dest_cuts[1] == new_len)) &&
       (!dest_offsets || dest_offsets[0] == 0))
     return launch_ttm_packed(stream, x, outer, len, inner, mfrag, f, new_len, z, sm_count);

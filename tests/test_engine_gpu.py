@@ -64,6 +64,37 @@ def test_ttm_matches_oracle(ctx, dims, mode, new_len):
     assert np.max(np.abs(got - want)) <= 64 * EPS * np.sqrt(dims[mode]) * np.max(np.abs(m)) * np.max(np.abs(t))
 
 
+SPLITK_SHAPES = [
+    # dims, mode, new_len: few columns and a contraction of 32..512 (csrc/ttm_splitk_kernels.cu) -- the K = 40 nodes of
+    # C3, the second-level nodes of C1 / C2, ragged warp shares of the contraction, odd trailing extents, inner == 1
+    # with a ragged last n-tile, one to six m-tiles and more than one K block
+    ((400, 1000), 0, 40), ((400, 10, 100, 5), 0, 40), ((20, 200, 200), 2, 20), ((20, 200, 20), 1, 20),
+    ((96, 10, 10, 10), 0, 10), ((10, 10, 96, 10), 2, 10), ((13, 77, 9), 1, 11), ((3, 510, 16), 1, 6), ((5, 33, 8), 1, 48),
+    ((4001, 201), 1, 20), ((999, 49), 1, 5), ((7, 512, 11), 1, 44), ((1, 32, 8), 1, 1), ((2, 100, 1000), 1, 7),
+]
+
+
+@pytest.mark.parametrize("dims,mode,new_len", SPLITK_SHAPES)
+def test_ttm_split_contraction_kernel(ctx, dims, mode, new_len):
+    """The small-node kernel adds up to eight partial sums in warp order: equal to the streaming kernels' result and to the
+    oracle to a few ulps of the result scale, and bit-identical from run to run."""
+    seed = (sum(dims) * 13 + new_len) % 10000
+    t = hostgen.random_tensor(dims, seed)
+    m = hostgen.random_tensor([new_len, dims[mode]], seed + 1)
+    split = E.ttm(t, m, mode, ctx=ctx)
+    again = E.ttm(t, m, mode, ctx=ctx)
+    E.check(E.lib.tp_set_global_option(3, E.ctypes.c_longlong(0)))   # TP_GLOBAL_OPT_TTM_SPLITK off
+    try:
+        streamed = E.ttm(t, m, mode, ctx=ctx)
+    finally:
+        E.check(E.lib.tp_set_global_option(3, E.ctypes.c_longlong(1)))
+    assert np.array_equal(split, again)
+    want = ho.ttm(t, m, mode)
+    scale = EPS * np.sqrt(dims[mode]) * np.max(np.abs(m)) * np.max(np.abs(t))
+    assert np.max(np.abs(split - want)) <= 64 * scale
+    assert np.max(np.abs(split - streamed)) <= 64 * scale
+
+
 PACKED_SHAPES = [
     # dims, mode, new_len: trailing extents 2..7 behind the contracted mode, slab counts around the 32-slab tile,
     # ragged last chunks of the contraction, K blocks of one to four m-tiles and more than one K block

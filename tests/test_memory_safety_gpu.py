@@ -77,7 +77,9 @@ def repeat_identical(dev, launch, count, times=4):
 # (dims, mode, K): odd and prime extents, one short of / one past a tile, inner == 1, tiny and TMA-sized problems
 TTM_CASES = [((7, 13, 5), 1, 3), ((33, 17), 1, 9), ((33, 17), 0, 5), ((3, 31, 129), 1, 8), ((129, 40, 3), 1, 20),
              ((2, 770, 20000), 1, 24), ((40010, 50), 1, 20), ((38001, 34), 1, 33), ((5, 36, 9000), 1, 100),
-             ((1, 1, 1), 1, 1), ((63, 64, 65), 2, 13), ((16, 16, 16, 16), 2, 7)]
+             ((1, 1, 1), 1, 1), ((63, 64, 65), 2, 13), ((16, 16, 16, 16), 2, 7),
+             # the split-contraction kernel: ragged n-tiles, odd trailing extents, ragged warp shares, two K blocks
+             ((3, 77, 9), 1, 11), ((401, 1001), 0, 40), ((1001, 401), 1, 40), ((5, 510, 13), 1, 60)]
 
 
 @pytest.mark.parametrize("dims,mode,k", TTM_CASES, ids=lambda v: "x".join(map(str, v)) if isinstance(v, tuple) else str(v))
