@@ -321,6 +321,10 @@ def run_b200(args):
         return D.run_bench_rank(args, rank, world, local_rank)
 
     torch.cuda.set_device(0)
+    import ctypes
+    for item in args.global_option:
+        opt, val = item.split("=")
+        E.check(E.lib.tp_set_global_option(int(opt), ctypes.c_longlong(int(val))))
     cfg = W.CONFIGS[args.config]
     spec = cfg.spec
     cores = os.cpu_count() or 1
@@ -789,6 +793,9 @@ def main(argv=None):
     ap.add_argument("--backend", default="cuda", choices=["cuda", "numpy-test"],
                     help="numpy-test: CONTRACT TEST ONLY -- the grid executor's rank program over gloo with the tests' "
                          "NumPy stand-in for the local kernels (tests/numpy_ops.py); not a measurement")
+    ap.add_argument("--global-option", action="append", default=[], metavar="ID=VALUE",
+                    help="A/B switch: tp_set_global_option(ID, VALUE) before the run (include/tuckerplan_b200.h, "
+                         "TP_GLOBAL_OPT_*), e.g. 4=0 keeps the TMA kernel's last row tile on a padded DMMA")
     args = ap.parse_args(argv)
     if args.gpus < 1:
         ap.error("--gpus must be at least 1")

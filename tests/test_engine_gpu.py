@@ -893,6 +893,9 @@ TMA_SHAPES = [
     # several tiles per persistent CTA
     ((100000, 64), 1, 16), ((3, 64, 70000), 1, 10), ((200000, 32), 1, 5), ((20, 48, 30000), 1, 13), ((300000, 20), 1, 24),
     ((7, 33, 50000), 1, 100),
+    # last row tile at most half full (K <= 8 (KT - 1) + 4 for KT = 6, 8, 10, 13), both layouts, ragged extents
+    ((40010, 50), 1, 100), ((38001, 34), 1, 97), ((38000, 36), 1, 44), ((60000, 20), 1, 58), ((3, 40, 20000), 1, 75),
+    ((30002, 40), 1, 90), ((5, 36, 9002), 1, 99), ((2, 24, 18, 1300), 1, 42),
 ]
 
 
