@@ -182,8 +182,18 @@ int tp_ctx_set_option(tp_ctx* ctx, int option, long long value);
  * products with a short trailing extent (1 < inner < 8) to the general kernels instead of the packed-column one
  * (same sums, same order).  TP_GLOBAL_OPT_TTM_SPLITK (default 1): 0 sends the small nodes (at most 640 column tiles,
  * contraction 32..512) to the streaming kernels instead of the kernel that splits the contraction over a CTA's warps
- * (same sums to rounding: the eight partial sums are added in warp order, so the last bits differ). */
-enum { TP_GLOBAL_OPT_TTM_TMA = 1, TP_GLOBAL_OPT_TTM_PACKED = 2, TP_GLOBAL_OPT_TTM_SPLITK = 3 };
+ * (same sums to rounding: the eight partial sums are added in warp order, so the last bits differ).
+ * TP_GLOBAL_OPT_GRAM_WIDE (default 1): 0 keeps the Gram matrices of large leaves (>= 448 rows) on the 64 x 64
+ * cp.async kernel instead of the 128 x 128 TMA pipeline (same sums to rounding: the contraction range is split
+ * differently).  TP_GLOBAL_OPT_GRAM_WIDE_SPARE_SMS (default 0, 0..64): SMs that kernel's persistent grid leaves to
+ * eigen-solves running beside it during a sweep. */
+enum {
+  TP_GLOBAL_OPT_TTM_TMA = 1,
+  TP_GLOBAL_OPT_TTM_PACKED = 2,
+  TP_GLOBAL_OPT_TTM_SPLITK = 3,
+  TP_GLOBAL_OPT_GRAM_WIDE = 4,
+  TP_GLOBAL_OPT_GRAM_WIDE_SPARE_SMS = 5
+};
 int tp_set_global_option(int option, long long value);
 int tp_ctx_synchronize(tp_ctx* ctx);
 /* the CUDA stream the engine launches on (cudaStream_t as void*), for event timing by the caller */

@@ -357,12 +357,14 @@ void check_leaf_args(long long rows, long long cols, int k) {  // hooi.hpp:46-51
 }
 
 // Gram of the mode-`mode` unfolding of y into s.gram (hooi.hpp:53-54 without the unfold copy of :148-149).
-long long leaf_gram(tp_ctx* ctx, LeafScratch& s, const double* y, const std::vector<size_t>& dims, int mode, int k) {
+// `spare_sms`: SMs a persistent (wide) Gram grid leaves to eigen-solve kernels in flight on the side streams.
+long long leaf_gram(tp_ctx* ctx, LeafScratch& s, const double* y, const std::vector<size_t>& dims, int mode, int k,
+                    int spare_sms = 0) {
   long long outer, inner;
   mode_extents(dims, mode, outer, inner);
   const long long rows = static_cast<long long>(dims[mode]);
   check_leaf_args(rows, outer * inner, k);
-  const GramLayout g = gram_layout(outer, rows, inner, ctx->sm_count);
+  const GramLayout g = gram_layout(outer, rows, inner, std::max(1, ctx->sm_count - spare_sms));
   leaf_scratch_reserve(ctx, s, rows, g.workspace_doubles);
   TPB_CUDA(launch_gram(ctx->stream, y, outer, rows, inner, g, s.gram_ws, s.gram));
   ctx->own_kernels += 2;
@@ -852,7 +854,8 @@ void plan_leaf(tp_ctx* ctx, tp_plan* p, const double* y, const std::vector<size_
                int node, bool overlap) {
   const int k = static_cast<int>(p->spec.K[mode]);
   Span gram(ctx, p, kGram, node);
-  leaf_gram(ctx, p->leaf[mode], y, dims, mode, k);
+  leaf_gram(ctx, p->leaf[mode], y, dims, mode, k,
+            (overlap && p->leaves_in_flight > 0) ? gram_wide_spare_sms().load(std::memory_order_relaxed) : 0);
   gram.close();
   if (overlap) {
     TPB_CUDA(cudaEventRecord(p->gram_ready[mode], ctx->stream));
@@ -1545,6 +1548,10 @@ int tp_set_global_option(int option, long long value) {
       ttm_packed_enabled().store(value != 0, std::memory_order_relaxed);
     else if (option == TP_GLOBAL_OPT_TTM_SPLITK)
       ttm_splitk_enabled().store(value != 0, std::memory_order_relaxed);
+    else if (option == TP_GLOBAL_OPT_GRAM_WIDE)
+      gram_wide_enabled().store(value != 0, std::memory_order_relaxed);
+    else if (option == TP_GLOBAL_OPT_GRAM_WIDE_SPARE_SMS)
+      gram_wide_spare_sms().store(static_cast<int>(std::max(0LL, std::min(value, 64LL))), std::memory_order_relaxed);
     else
       raise(TP_ERR_BAD_ARGUMENT, "unknown global option");
   });

@@ -210,8 +210,35 @@ __global__ void gram_reduce_kernel(const double* __restrict__ partial, int split
 
 }  // namespace
 
+std::atomic<bool>& gram_wide_enabled() {
+  static std::atomic<bool> on{true};
+  return on;
+}
+
+std::atomic<int>& gram_wide_spare_sms() {
+  static std::atomic<int> sms{0};  // measured on C5: 0 -> 57.07 ms/iter, 4 -> 57.15, 16 -> 57.22
+  return sms;
+}
+
+namespace {
+GramLayout gram_narrow_layout(long long outer, long long rows, long long inner, int sm_count);
+}
+
 GramLayout gram_layout(long long outer, long long rows, long long inner, int sm_count) {
+  if (gram_wide_enabled().load(std::memory_order_relaxed) && gram_wide_shape(outer, rows, inner)) {
+    GramLayout g = gram_wide_layout(outer, rows, inner, sm_count);
+    // a base address that is not 16-byte aligned sends the launch back to the narrow kernel: room for its partials too
+    g.workspace_doubles = std::max(g.workspace_doubles, gram_narrow_layout(outer, rows, inner, sm_count).workspace_doubles);
+    g.sm_count = sm_count;
+    return g;
+  }
+  return gram_narrow_layout(outer, rows, inner, sm_count);
+}
+
+namespace {
+GramLayout gram_narrow_layout(long long outer, long long rows, long long inner, int sm_count) {
   GramLayout g;
+  g.sm_count = sm_count;
   g.tiles = static_cast<int>((rows + kTile - 1) / kTile);
   g.chunks = inner == 1 ? (outer + kKC - 1) / kKC : outer * ((inner + kKC - 1) / kKC);
   const long long lower_tiles = static_cast<long long>(g.tiles) * (g.tiles + 1) / 2;
@@ -238,9 +265,21 @@ GramLayout gram_layout(long long outer, long long rows, long long inner, int sm_
   g.workspace_doubles = static_cast<size_t>(g.splits) * rows * rows;
   return g;
 }
+}  // namespace
 
 cudaError_t launch_gram(cudaStream_t stream, const double* y, long long outer, long long rows, long long inner,
-                        const GramLayout& g, double* workspace, double* gram) {
+                        const GramLayout& layout, double* workspace, double* gram) {
+  GramLayout g = layout;
+  if (g.wide) {
+    if (reinterpret_cast<uintptr_t>(y) % 16 == 0 && ttm_tensor_map(y, outer, rows, inner)) {
+      cudaError_t e = launch_gram_wide(stream, y, outer, rows, inner, g, workspace, g.sm_count);
+      if (e != cudaSuccess) return e;
+      const long long total = rows * rows;
+      gram_reduce_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, stream>>>(workspace, g.splits, rows, gram);
+      return cudaGetLastError();
+    }
+    g = gram_narrow_layout(outer, rows, inner, g.sm_count);
+  }
   GramParams p;
   p.y = y;
   p.partial = workspace;

@@ -68,6 +68,9 @@ cudaError_t launch_ttm_packed(cudaStream_t stream, const double* x, long long ou
 
 // Warp-specialised TMA variant (ttm_tma_kernels.cu): used by launch_ttm for 16-byte-aligned, even extents with enough
 // columns to fill the machine.  mfrag must be the copy matching the mode (interleaved rows when inner > 1).
+// The encoded 3-D tensor map (CUtensorMap*) of x viewed as (outer, len, inner) with 16 x 16 boxes and the 128-byte
+// swizzle: dims (inner, len, outer), or (len, outer, 1) when inner == 1.  Cached per host thread; nullptr on failure.
+const void* ttm_tensor_map(const double* x, long long outer, long long len, long long inner);
 bool ttm_tma_eligible(const double* x, long long outer, long long len, long long inner, const double* z, int kt,
                       int k_blocks, int sm_count);
 cudaError_t launch_ttm_tma(cudaStream_t stream, const double* x, long long outer, long long len, long long inner,
@@ -76,12 +79,23 @@ cudaError_t launch_ttm_tma(cudaStream_t stream, const double* x, long long outer
 
 // ---- Gram of the mode-n unfolding, read in place (gram_kernels.cu) -----------
 struct GramLayout {
-  int tiles = 1;     // ceil(rows / 64)
+  int tiles = 1;     // ceil(rows / 64); wide: ceil(rows / 128)
   int splits = 1;    // deterministic split of the column (contraction) range
   long long chunks = 0;
-  size_t workspace_doubles = 0;  // splits * rows * rows
+  size_t workspace_doubles = 0;  // splits * rows * rows (wide: enough for the narrow layout too)
+  bool wide = false;  // 128 x 128 tiles on the TMA pipeline (gram_tma_kernels.cu), large leaves only
+  int sm_count = 0;   // the SMs the layout was made for (wide: the persistent grid)
 };
 GramLayout gram_layout(long long outer, long long rows, long long inner, int sm_count);
+// Process-wide A/B switch: false keeps large leaves on the 64 x 64 cp.async kernel.
+std::atomic<bool>& gram_wide_enabled();
+// SMs the wide kernel's persistent grid leaves free while eigen-solves are in flight beside it (plan walks only).
+std::atomic<int>& gram_wide_spare_sms();
+bool gram_wide_shape(long long outer, long long rows, long long inner);
+GramLayout gram_wide_layout(long long outer, long long rows, long long inner, int sm_count);
+// partial tiles only; launch_gram adds the ordered sum
+cudaError_t launch_gram_wide(cudaStream_t stream, const double* y, long long outer, long long rows, long long inner,
+                             const GramLayout& g, double* workspace, int sm_count);
 // gram (rows x rows, full symmetric storage) = sum_{a,b} Y(a,:,b) Y(a,:,b)^T, y viewed as (outer, rows, inner).
 cudaError_t launch_gram(cudaStream_t stream, const double* y, long long outer, long long rows, long long inner,
                         const GramLayout& g, double* workspace, double* gram);

@@ -409,6 +409,11 @@ cudaError_t launch_tma_kt(cudaStream_t stream, const CUtensorMap& map, const Tma
 
 }  // namespace
 
+const void* ttm_tensor_map(const double* x, long long outer, long long len, long long inner) {
+  if (!encode_tiled()) return nullptr;
+  return tensor_map_for(x, outer, len, inner);
+}
+
 bool ttm_tma_eligible(const double* x, long long outer, long long len, long long inner, const double* z, int kt,
                       int k_blocks, int sm_count) {
   if (!encode_tiled()) return false;

@@ -147,7 +147,13 @@ def test_ttm_error_codes(ctx):
 
 GRAM_SHAPES = [((6, 40), 0), ((40, 6), 1), ((5, 7, 3), 1), ((5, 7, 3), 0), ((5, 7, 3), 2), ((20, 200, 20), 1),
                ((200, 20, 20), 0), ((20, 20, 200), 2), ((10, 130, 33), 1), ((3, 65, 64), 1), ((10, 10, 96, 10), 2),
-               ((129, 100), 0), ((100, 129), 1), ((8, 48, 8, 8), 1), ((400, 7, 11), 0), ((2, 2, 2, 2, 50), 4)]
+               ((129, 100), 0), ((100, 129), 1), ((8, 48, 8, 8), 1), ((400, 7, 11), 0), ((2, 2, 2, 2, 50), 4),
+               # large leaves: 128 x 128 tiles on the TMA pipeline (>= 448 rows, >= 64 contraction chunks), all three
+               # layouts, ragged last tile rows (1..4 live row blocks), ragged contraction ends, exact multiples
+               ((3, 450, 400), 1), ((500, 40, 30), 0), ((1100, 452), 1), ((2, 600, 18, 30), 1), ((1040, 640), 1),
+               ((4, 482, 262), 1), ((1030, 546), 1), ((2, 770, 520), 1), ((7, 1000, 150), 1),
+               # odd contiguous extent: stays on the 64 x 64 kernel
+               ((3, 450, 401), 1), ((1100, 453), 1)]
 
 
 @pytest.mark.parametrize("dims,mode", GRAM_SHAPES)
