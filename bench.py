@@ -343,6 +343,9 @@ def run_b200(args):
     t_build = time.perf_counter() - t_build
     f0 = W.start_factors(cfg)
     plan = E.HooiPlan(ctx, spec, tree, "jacobi")
+    for item in args.plan_option:
+        opt, val = item.split("=")
+        plan.set_option(int(opt), int(val))
 
     # L2 hygiene: inputs far larger than the 126 MB L2 need nothing; otherwise flush between steps
     small = total * 8 < 4 * 126e6
@@ -796,6 +799,9 @@ def main(argv=None):
     ap.add_argument("--global-option", action="append", default=[], metavar="ID=VALUE",
                     help="A/B switch: tp_set_global_option(ID, VALUE) before the run (include/tuckerplan_b200.h, "
                          "TP_GLOBAL_OPT_*), e.g. 4=0 keeps the TMA kernel's last row tile on a padded DMMA")
+    ap.add_argument("--plan-option", action="append", default=[], metavar="ID=VALUE",
+                    help="A/B switch: tp_plan_set_option(ID, VALUE) on the timed plan (TP_OPT_*), e.g. 10=0 sends a long "
+                         "chain product beside running eigen-solves out as one launch")
     args = ap.parse_args(argv)
     if args.gpus < 1:
         ap.error("--gpus must be at least 1")

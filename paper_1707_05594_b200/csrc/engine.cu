@@ -1245,6 +1245,7 @@ void plan_core(tp_ctx* ctx, tp_plan* p, const double* tensor, const std::vector<
       TPB_CUDA(cudaEventRecord(p->factor_ready[m], side));
     }
   }
+  bool solves_covered = false;
   for (int i = 0; i < p->n; ++i) {
     const int m = p->core_order[i];
     if (wait_for_leaves) {
@@ -1264,8 +1265,20 @@ void plan_core(tp_ctx* ctx, tp_plan* p, const double* tensor, const std::vector<
     // solves of the modes the chain has not waited for yet may still be running on the side streams: the persistent
     // product grid must leave them SMs (its CTAs would otherwise hold every SM until the product ends, and a solve
     // queued meanwhile would start only then -- exposed on the critical path of short sweeps)
-    const bool solves_running = wait_for_leaves && !last && (p->leaves_in_flight > 0 || !p->pending.empty());
+    // ...unless a long product has been queued since the last solve was: a solve is a few milliseconds of small
+    // kernels, so those still in flight then are over long before a later chain product starts, and sparing SMs for
+    // them would only idle those SMs for the whole product (C5: 57.02 -> 56.85 ms/iter).  (Measured and rejected:
+    // the long product itself as two launches, an eighth beside the solves and the rest on the whole machine -- the
+    // solves take longer than that eighth under contention and then starve behind the second launch, 62.7 ms/iter.)
+    const bool solves_running =
+        wait_for_leaves && !last && !solves_covered && (p->leaves_in_flight > 0 || !p->pending.empty());
+    long long outer_m, inner_m;
+    mode_extents(dims, m, outer_m, inner_m);
+    const double flops = 2.0 * static_cast<double>(p->spec.K[m]) * static_cast<double>(outer_m) *
+                         static_cast<double>(dims[m]) * static_cast<double>(inner_m);
+    const bool long_product = flops >= 2.5 * p->short_product_flops;
     plan_ttm(ctx, p, src, dims, m, dst, solves_running ? p->spare_sms : 0);
+    if (long_product) solves_covered = true;
     s.close();
     if (wait_for_leaves) plan_flush_pending(ctx, p);
     dims[m] = static_cast<size_t>(p->spec.K[m]);

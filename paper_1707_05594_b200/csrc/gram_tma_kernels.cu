@@ -7,10 +7,10 @@
 // clock and SM at the DMMA rate, 4.6 TB/s over the chip, more than L2 delivers: it stalls at 78 % of the pipe
 // (profiles/r02_v1_ncu_full_gram_summary.txt).  Here a CTA owns a 128 x 128 tile (half the operand traffic per MAC):
 //
-//   * warp 0 is the PRODUCER: one lane issues cp.async.bulk.tensor loads of 16 x 16-double boxes (the tensor maps of
+//   * warp 0 is the PRODUCER (its warpgroup gives its registers to the consumers, setmaxnreg): one lane issues cp.async.bulk.tensor loads of 16 x 16-double boxes (the tensor maps of
 //     the TTM kernel: (inner, rows, outer) or (rows, outer, 1) when inner == 1), 8 boxes per operand and stage, rows
 //     past the extent zero-filled by the hardware; a 4-stage ring, full / empty mbarriers, no CTA-wide barrier;
-//   * warps 1..8 are CONSUMERS on DMMA.8x8x4.  The tile is cut into 4 x 4 blocks of 32 x 32; a consumer owns up to two
+//   * warps 4..11 are CONSUMERS on DMMA.8x8x4.  The tile is cut into 4 x 4 blocks of 32 x 32; a consumer owns up to two
 //     blocks.  Off the diagonal that is a 64 x 32 piece per warp.  On the diagonal only the ten blocks with
 //     row block >= column block are computed, dealt out so that the two warps of every SM sub-partition hold at most
 //     three between them (the FP64 pipe is per sub-partition): a diagonal tile costs 3/4 of a full one instead of all
@@ -38,7 +38,8 @@ namespace tpb {
 namespace {
 
 constexpr int kConsumerWarps = 8;
-constexpr int kThreads = 32 * (1 + kConsumerWarps);
+constexpr int kProducerWarps = 4;  // one warpgroup: setmaxnreg works on whole warpgroups; only warp 0 issues loads
+constexpr int kThreads = 32 * (kProducerWarps + kConsumerWarps);
 constexpr int kKC = 16;
 constexpr int kTile = 128;
 constexpr int kStages = 4;
@@ -121,7 +122,7 @@ __device__ __forceinline__ void decode_item(const GramTmaParams& p, int item, in
 }
 
 // The up to two 32 x 32 blocks (row block << 4 | column block, -1 = none) of consumer warp cw.  Consumers cw and
-// cw + 4 share an SM sub-partition.
+// cw + 4 share an SM sub-partition (warp w runs on sub-partition w % 4).
 __device__ __forceinline__ void warp_blocks(bool diag, int cw, int& b0, int& b1) {
   if (!diag) {
     const int wm = cw >> 2, wn = cw & 3;
@@ -186,9 +187,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   __syncthreads();
 
-  if (warp == 0) {
+  // Register split (the register file is per SM sub-partition: a ninth warp would cap every thread at 168 registers
+  // and spill the consumers' 128 accumulator registers + fragments): the kernel starts with 168 per thread for its
+  // three warpgroups, the producer group hands back all but 40, the two consumer groups grow to 232.
+  if (warp < kProducerWarps) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n");
     // ------------------------------------------------------------------ producer
-    if (lane == 0) {
+    if (warp == 0 && lane == 0) {
       int stage = 0;
       unsigned parity = 0;
       for (int item = blockIdx.x; item < p.n_items; item += gridDim.x) {
@@ -239,7 +244,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   // -------------------------------------------------------------------- consumers
-  const int cw = warp - 1;
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n");
+  const int cw = warp - kProducerWarps;
   const int fk = lane & 3, fn = lane >> 2;
   // box row of fragment row index n when the contraction index is the contiguous one
   const int prow = ((fn & 3) << 1) | (fn >> 2);
