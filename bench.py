@@ -509,9 +509,12 @@ def run_b200(args):
         ctx.synchronize()
         d = E.Decomposition(None, f0)
         w0 = time.perf_counter()
+        per_call_ms = []
         for i in range(iters):
             # call 1 makes no promise: the tensor is uploaded (and the start factors make it a cold sweep)
+            c0 = time.perf_counter()
             d = E.hooi_sweep(host_t, spec, d, tree, "jacobi", ctx=ctx, tensor_unchanged=i > 0)
+            per_call_ms.append((time.perf_counter() - c0) * 1e3)
         run_s = (time.perf_counter() - w0) / iters
         # the by-value run against the resident run of the same iterations: same subspaces to rounding
         plan.set_factors(f0)
@@ -542,7 +545,7 @@ def run_b200(args):
                "what": "whole run of the config's %d iterations through the by-value C-ABI call, upload of the tensor "
                        "(first call) included, later calls with TP_HOST_TENSOR_UNCHANGED; mean per iteration; device "
                        "allocations warm (one earlier call on the same context)" % iters,
-               "first_call_of_a_process_s": first_call_s,
+               "first_call_of_a_process_s": first_call_s, "per_call_ms": per_call_ms,
                "max_sin_principal_angle_vs_resident_run": agree,
                "by_value_every_call": {"value": every_s, "unit": "s/iter", "h2d_bytes_per_step": total * 8 + fbytes,
                                        "d2h_bytes_per_step": fbytes + cbytes, "calls": every_steps},

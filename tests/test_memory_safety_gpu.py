@@ -107,7 +107,10 @@ def test_ttm_kernels_stay_inside_their_buffers(dev, dims, mode, k, tma):
 
 
 @pytest.mark.parametrize("outer,rows,inner", [(1, 7, 1), (5, 33, 1), (3, 65, 17), (2, 128, 130), (400, 20, 1),
-                                              (1, 200, 401), (9, 63, 63)])
+                                              (1, 200, 401), (9, 63, 63),
+                                              # large leaves: the 128 x 128 TMA kernel (ragged tile rows and chunk ends)
+                                              (3, 450, 400), (1100, 452, 1), (2, 482, 518), (1, 500, 1202),
+                                              (1030, 546, 1)])
 def test_gram_kernel_stays_inside_its_buffers(dev, outer, rows, inner):
     y = hostgen.random_tensor([outer, rows, inner], 3)
     yb, yp = dev.guarded_input(y)
