@@ -186,13 +186,16 @@ int tp_ctx_set_option(tp_ctx* ctx, int option, long long value);
  * TP_GLOBAL_OPT_GRAM_WIDE (default 1): 0 keeps the Gram matrices of large leaves (>= 448 rows) on the 64 x 64
  * cp.async kernel instead of the 128 x 128 TMA pipeline (same sums to rounding: the contraction range is split
  * differently).  TP_GLOBAL_OPT_GRAM_WIDE_SPARE_SMS (default 0, 0..64): SMs that kernel's persistent grid leaves to
- * eigen-solves running beside it during a sweep. */
+ * eigen-solves running beside it during a sweep.  TP_GLOBAL_OPT_CARRY_FIRST (0 never, 1 always, 2 = default: in
+ * short sweeps): plans created afterwards walk the subtree whose products were carried over from the previous sweep
+ * first instead of last (a Jacobi sweep gives the same factors in any visiting order). */
 enum {
   TP_GLOBAL_OPT_TTM_TMA = 1,
   TP_GLOBAL_OPT_TTM_PACKED = 2,
   TP_GLOBAL_OPT_TTM_SPLITK = 3,
   TP_GLOBAL_OPT_GRAM_WIDE = 4,
-  TP_GLOBAL_OPT_GRAM_WIDE_SPARE_SMS = 5
+  TP_GLOBAL_OPT_GRAM_WIDE_SPARE_SMS = 5,
+  TP_GLOBAL_OPT_CARRY_FIRST = 6
 };
 int tp_set_global_option(int option, long long value);
 int tp_ctx_synchronize(tp_ctx* ctx);

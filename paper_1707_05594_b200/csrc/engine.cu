@@ -127,6 +127,12 @@ static tp_u64 next_tensor_stamp() {
 
 static void release_host_call_cache(tp_ctx* ctx);
 
+// Plans created from now on visit the carried subtree first: 0 never, 1 always, 2 (default) in short sweeps.
+static std::atomic<int>& carry_first_mode() {
+  static std::atomic<int> mode{2};
+  return mode;
+}
+
 namespace tpb {
 namespace {
 
@@ -723,6 +729,7 @@ struct tp_plan {
   // it is captured once and replayed, so the short sweeps of small tensors are not paced by ~100 host launches.
   int sweep_graph_mode = 2;                   // 0 off, 1 on, 2 auto: only sweeps whose tree is short (see short_sweep)
   bool short_sweep = false;                   // tree + core flops small enough for launch latency to matter
+  bool carry_first = false;                   // visit the carried subtree first (short sweeps), else last
   cudaGraphExec_t sweep_graph = nullptr;
   const double* sweep_graph_tensor = nullptr;
   tp_u64 sweep_graph_stamp = 0;
@@ -979,8 +986,11 @@ void plan_visit_order(tp_plan* p) {
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
       const bool ca = !p->on_carry.empty() && p->on_carry[a], cb = !p->on_carry.empty() && p->on_carry[b];
       // the carried path ends in the mode the core chain contracts last: its leaves are needed last, so they go last
-      // and their eigen-solves overlap the chain's large products
-      if (ca != cb) return cb;
+      // and their eigen-solves overlap the chain's large products.  In a short sweep (forked walk) it is the other
+      // way round: the carried subtree's inputs exist when the sweep starts, the leaf solve at its end is the longest
+      // dependent chain of the whole sweep (C3: 0.64 ms of 1.04) and the core waits for it -- so it is issued first
+      // and everything else fills the machine beside it.
+      if (ca != cb) return p->carry_first ? ca : cb;
       if (t.leaf(a) != t.leaf(b)) return t.leaf(a);
       return leaves[a] > leaves[b];
     });
@@ -1325,6 +1335,14 @@ void plan_choose_carry(tp_plan* p) {
     for (int id : nodes) p->on_carry[id] = 1;
     plan_visit_order(p);
     std::vector<int> key;
+    if (p->carry_first) {
+      // the carried subtree goes first so that the leaf solve at its end starts at once: take the path that ends in
+      // the dearest solve (rows x block^2; the chain's needs decide among equals)
+      const int lm = t.mode[leaf];
+      const double block = static_cast<double>(p->spec.K[lm]) + 8.0;
+      const double cost = static_cast<double>(p->spec.L[lm]) * block * block;
+      key.push_back(-static_cast<int>(std::min(cost / 64.0, 2e9)));
+    }
     for (int id : nodes) key.push_back(p->leaf_rank[t.mode[id]]);
     if (best_leaf < 0 || key < best_key) {
       best_key = key;
@@ -1561,6 +1579,8 @@ int tp_set_global_option(int option, long long value) {
       ttm_packed_enabled().store(value != 0, std::memory_order_relaxed);
     else if (option == TP_GLOBAL_OPT_TTM_SPLITK)
       ttm_splitk_enabled().store(value != 0, std::memory_order_relaxed);
+    else if (option == TP_GLOBAL_OPT_CARRY_FIRST)
+      carry_first_mode().store(static_cast<int>(std::max(0LL, std::min(value, 2LL))), std::memory_order_relaxed);
     else if (option == TP_GLOBAL_OPT_GRAM_WIDE)
       gram_wide_enabled().store(value != 0, std::memory_order_relaxed);
     else if (option == TP_GLOBAL_OPT_GRAM_WIDE_SPARE_SMS)
@@ -2000,6 +2020,11 @@ int tp_plan_create(tp_ctx* ctx, int n_modes, const tp_u64* L, const tp_u64* K, i
         if (p->tree.internal(id)) p->node_cap[id] = static_cast<size_t>(cards.out[id]);
 
       // core chain in its cheapest order; ping-pong buffers hold its largest partial product
+      {
+        const int mode = carry_first_mode().load(std::memory_order_relaxed);
+        p->carry_first = p->sweep_kind == TP_SWEEP_JACOBI &&
+                         (mode == 1 || (mode == 2 && 2.0 * static_cast<double>(cost.total_macs) < 5e10));
+      }
       plan_choose_carry(p);
       if (p->carry_nodes.empty()) {
         p->core_order = cheapest_chain_order(p->spec, p->leaf_rank, &p->core_macs_executed);
