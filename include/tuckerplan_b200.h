@@ -174,8 +174,9 @@ int tp_ctx_destroy(tp_ctx* ctx);
 /* Context options (plain values through the ABI; the library reads no environment variables).
  *   TP_CTX_OPT_STREAMED_UPLOAD_MIN_BYTES  by-value hooi_sweep calls upload tensors of at least this many bytes in
  *                                         slabs and start multiplying the slabs that have arrived (default 256 MiB)
- *   TP_CTX_OPT_TRACE_EVD                  != 0: one line per leaf and sweep on stderr with the certificate margins */
-enum { TP_CTX_OPT_STREAMED_UPLOAD_MIN_BYTES = 1, TP_CTX_OPT_TRACE_EVD = 2 };
+ *   TP_CTX_OPT_TRACE_EVD                  != 0: one line per leaf and sweep on stderr with the certificate margins
+ *   TP_CTX_OPT_DUMP_SWEEP_GRAPH           != 0: a recorded sweep's CUDA graph goes to /tmp/tpb_sweep_graph.dot (debugging) */
+enum { TP_CTX_OPT_STREAMED_UPLOAD_MIN_BYTES = 1, TP_CTX_OPT_TRACE_EVD = 2, TP_CTX_OPT_DUMP_SWEEP_GRAPH = 3 };
 int tp_ctx_set_option(tp_ctx* ctx, int option, long long value);
 /* Process-wide switches.  TP_GLOBAL_OPT_TTM_TMA (default 1): 0 forces the cp.async TTM kernel where the TMA pipeline
  * would be chosen (both compute the same sums in the same order).  TP_GLOBAL_OPT_TTM_PACKED (default 1): 0 sends

@@ -101,6 +101,7 @@ struct tp_ctx {
   // tp_ctx_set_option
   size_t streamed_upload_min_bytes = size_t{256} << 20;  // by-value calls: below this the upload is one copy
   bool trace_evd = false;                                // print every leaf's certificate margins to stderr
+  bool dump_sweep_graph = false;                         // write a recorded sweep's graph to /tmp/tpb_sweep_graph.dot
   // by-value calls with TP_HOST_TENSOR_UNCHANGED: what the cached device tensor was uploaded from, and the factors the
   // last call returned (a caller that feeds them back continues the resident run: warm solves, carried products)
   bool host_call_busy = false;                           // a by-value call is using the cache right now
@@ -1565,6 +1566,8 @@ int tp_ctx_set_option(tp_ctx* ctx, int option, long long value) {
       ctx->streamed_upload_min_bytes = static_cast<size_t>(value);
     } else if (option == TP_CTX_OPT_TRACE_EVD) {
       ctx->trace_evd = value != 0;
+    } else if (option == TP_CTX_OPT_DUMP_SWEEP_GRAPH) {
+      ctx->dump_sweep_graph = value != 0;
     } else {
       raise(TP_ERR_BAD_ARGUMENT, "unknown context option");
     }
@@ -2328,6 +2331,8 @@ int tp_plan_sweep(tp_ctx* ctx, tp_plan* p, const tp_tensor* t, tp_sweep_stats* s
             ctx->own_kernels = own0;
             ctx->library_calls = lib0;
             if (cudaStreamEndCapture(ctx->stream, &recorded) != cudaSuccess) ok = false;
+            if (ok && ctx->dump_sweep_graph && recorded)
+              cudaGraphDebugDotPrint(recorded, "/tmp/tpb_sweep_graph.dot", 0);  // TP_CTX_OPT_DUMP_SWEEP_GRAPH
             if (ok && cudaGraphInstantiate(&p->sweep_graph, recorded, 0) != cudaSuccess) ok = false;
             if (recorded) cudaGraphDestroy(recorded);
           }

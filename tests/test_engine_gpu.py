@@ -726,6 +726,39 @@ def test_config5_full_size_against_oracle(ctx):
 
 @pytest.mark.parametrize("cfg", [W.CONFIGS[1], W.scaled_config(2, [40, 36, 32, 28], [6, 5, 4, 3], 8),
                                  W.scaled_config(3, [240, 60, 60, 40], [30, 5, 10, 3], 8)], ids=lambda c: c.name)
+def test_visiting_order_of_the_carried_subtree_does_not_change_the_factors(ctx, cfg):
+    """TP_GLOBAL_OPT_CARRY_FIRST: a Jacobi sweep gives the same factors whichever subtree is walked first and whichever
+    root-to-leaf path is carried (hooi.hpp:9-12: every product uses the start-of-sweep factors) -- bit for bit, since
+    every node is still computed by the same kernel from the same operands."""
+    spec = cfg.spec
+    tree = P.optimal_tree(spec).tree
+    t = W.build_tensor_host(cfg)
+    f0 = W.start_factors(cfg)
+    dt = E.DeviceTensor.upload(ctx, t)
+    trails = {}
+    try:
+        for first in (0, 1):
+            E.check(E.lib.tp_set_global_option(6, E.ctypes.c_longlong(first)))   # plans created from now on
+            plan = E.HooiPlan(ctx, spec, tree, "jacobi")
+            plan.set_factors(f0)
+            trail = []
+            for _ in range(6):
+                plan.sweep(dt)
+                trail.append((plan.get_factors(), plan.get_core()))
+            trails[first] = trail
+            plan.close()
+    finally:
+        E.check(E.lib.tp_set_global_option(6, E.ctypes.c_longlong(2)))
+    for i, ((fa, ca), (fb, cb)) in enumerate(zip(trails[0], trails[1])):
+        for a, b in zip(fa, fb):
+            assert np.array_equal(a, b), i
+        # the core is contracted along the carried path, which differs between the two plans: same value to rounding
+        assert np.max(np.abs(ca - cb)) <= 1e-12 * np.max(np.abs(ca)), i
+    dt.free()
+
+
+@pytest.mark.parametrize("cfg", [W.CONFIGS[1], W.scaled_config(2, [40, 36, 32, 28], [6, 5, 4, 3], 8),
+                                 W.scaled_config(3, [240, 60, 60, 40], [30, 5, 10, 3], 8)], ids=lambda c: c.name)
 def test_whole_sweep_graph_is_bit_identical(ctx, cfg):
     """TP_OPT_SWEEP_GRAPH: the steady-state sweep replayed as one CUDA graph launches the same kernels with the same
     arguments as the eager sweep, so factors and core must agree bit for bit, sweep by sweep; and both match the

@@ -12,6 +12,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=5)
 ap.add_argument("--warm", type=int, default=5)
 ap.add_argument("--out", default="gpurun_out/timeline.json")
+ap.add_argument("--plan-option", action="append", default=[], metavar="ID=VALUE", help="tp_plan_set_option before the run")
 ap.add_argument("--min-us", type=float, default=20.0, help="digest: kernels at least this long")
 args = ap.parse_args()
 cfg = W.CONFIGS[args.config]
@@ -20,6 +21,8 @@ host, handle = bench.pinned_array(int(np.prod(cfg.L, dtype=np.int64)))
 dt = bench.build_on_gpu(ctx, cfg, host, os.cpu_count() or 1)
 tree = P.optimal_tree(cfg.spec).tree
 plan = E.HooiPlan(ctx, cfg.spec, tree, "jacobi")
+for item in args.plan_option:
+    plan.set_option(int(item.split("=")[0]), int(item.split("=")[1]))
 plan.set_factors(W.start_factors(cfg))
 for _ in range(args.warm):
     plan.sweep(dt)
@@ -29,7 +32,8 @@ with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) a
     ctx.synchronize()
     torch.cuda.synchronize()
 prof.export_chrome_trace(args.out + ".chrome")
-ev = [e for e in json.load(open(args.out + ".chrome"))["traceEvents"] if e.get("cat") == "kernel"]
+ev = [e for e in json.load(open(args.out + ".chrome"))["traceEvents"]
+      if e.get("cat") in ("kernel", "gpu_memcpy", "gpu_memset") and "dur" in e]
 t0 = min(e["ts"] for e in ev)
 rows = sorted(({"start_us": round(e["ts"] - t0, 1), "dur_us": round(e["dur"], 1), "stream": e["args"].get("stream"),
                 "grid": e["args"].get("grid"), "name": e["name"][:70]} for e in ev), key=lambda r: r["start_us"])
