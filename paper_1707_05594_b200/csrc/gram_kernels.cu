@@ -249,7 +249,9 @@ GramLayout gram_narrow_layout(long long outer, long long rows, long long inner, 
   // the cp.async ring holds in flight at once.
   const long long per_wave = 4LL * sm_count;
   const long long min_chunks = (g.chunks * lower_tiles <= 4 * per_wave * kStages) ? kStages : 8;
-  const long long max_splits = std::max(1LL, std::min(512LL, g.chunks / min_chunks));
+  // ... and at most 1 GiB of partial planes
+  const long long plane_cap = std::max(1LL, (1LL << 27) / std::max(1LL, rows * rows));
+  const long long max_splits = std::max(1LL, std::min({512LL, g.chunks / min_chunks, plane_cap}));
   long long best = 1, best_cost = -1;
   for (long long s = 1; s <= max_splits; ++s) {
     const long long per = (g.chunks + s - 1) / s;

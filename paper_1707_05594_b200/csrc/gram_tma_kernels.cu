@@ -379,7 +379,9 @@ GramLayout gram_wide_layout(long long outer, long long rows, long long inner, in
   // split count: replay the round-robin walk for every candidate and keep the one whose busiest CTA finishes first
   // (+ 3 chunks per item for the epilogue and the change of tile, + the ordered sum's cost per split)
   const int grid = std::max(1, sm_count);
-  const long long max_splits = std::max(1LL, std::min(32LL, g.chunks / 8));
+  // at most 1 GiB of partial planes (tall Gram matrices have tiles enough to fill the machine without splitting)
+  const long long plane_cap = std::max(1LL, (1LL << 27) / std::max(1LL, rows * rows));
+  const long long max_splits = std::max(1LL, std::min({32LL, g.chunks / 8, plane_cap}));
   long long best = 1;
   double best_time = -1.0;
   std::vector<double> load(static_cast<size_t>(grid));

@@ -152,6 +152,8 @@ GRAM_SHAPES = [((6, 40), 0), ((40, 6), 1), ((5, 7, 3), 1), ((5, 7, 3), 0), ((5, 
                # layouts, ragged last tile rows (1..4 live row blocks), ragged contraction ends, exact multiples
                ((3, 450, 400), 1), ((500, 40, 30), 0), ((1100, 452), 1), ((2, 600, 18, 30), 1), ((1040, 640), 1),
                ((4, 482, 262), 1), ((1030, 546), 1), ((2, 770, 520), 1), ((7, 1000, 150), 1),
+               # many tile rows (16, 17 with two live rows in the last)
+               ((2048, 1100), 0), ((1100, 2050), 1),
                # odd contiguous extent: stays on the 64 x 64 kernel
                ((3, 450, 401), 1), ((1100, 453), 1)]
 
