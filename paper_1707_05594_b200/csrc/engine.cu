@@ -2269,15 +2269,23 @@ bool sweep_graph_usable(const tp_ctx* ctx, const tp_plan* p, const tp_tensor* t)
   (void)ctx;
   if (p->sweep_graph_mode == 0 || (p->sweep_graph_mode == 2 && !p->short_sweep)) return false;
   if (p->sweep_kind != TP_SWEEP_JACOBI || p->arrival || !p->overlap_evd || !p->fast_evd) return false;
-  if (p->factors_from_caller || p->warm_sweeps < 2 || p->fast_rejected != 0 || t->pointer_escaped) return false;
+  if (p->factors_from_caller || p->warm_sweeps < 1 || p->fast_rejected != 0 || t->pointer_escaped) return false;
   if (p->carry_enabled && !p->carry_nodes.empty() && !p->carry_live) return false;
+  // The second sweep of a run is already the steady-state launch sequence when every leaf takes the one-launch solve
+  // AND starts it from the previous sweep's Ritz vectors (the first sweep's solves were certified); otherwise the
+  // sequence settles one sweep later (a leaf's own recording, the start block of a leaf that fell back).
+  const bool second_sweep = p->warm_sweeps < 2;
   for (int m = 0; m < p->n; ++m) {
     const LeafScratch& s = p->leaf[m];
     const long long rows = static_cast<long long>(p->spec.L[m]);
     const int k = static_cast<int>(p->spec.K[m]);
     if (s.failures >= 2 || !subspace_eligible(rows, k, plan_leaf_columns(p, m))) return false;  // full solve: cuSOLVER
     const int b = k + kSubspaceOversample;
-    if (s.use_fused && leaf_solve_fused_eligible(rows, k, b)) continue;
+    if (s.use_fused && leaf_solve_fused_eligible(rows, k, b)) {
+      if (second_sweep && !s.last_ritz) return false;
+      continue;
+    }
+    if (second_sweep) return false;
     if (static_cast<size_t>(b) > small_evd_max_block()) return false;        // cuSOLVER steps inside the iteration
     if (s.use_graph && s.graph_state != 2 && s.graph_state != -1) return false;  // its own recording comes first
     if (!s.last_ritz) return false;
