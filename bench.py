@@ -504,8 +504,13 @@ def run_b200(args):
         # one-off costs of a process, reported separately); the timed run below still moves every byte
         ctx.release_cache()
         w0 = time.perf_counter()
-        E.hooi_sweep(host_t, spec, E.Decomposition(None, f0), tree, "jacobi", ctx=ctx)
+        dw = E.hooi_sweep(host_t, spec, E.Decomposition(None, f0), tree, "jacobi", ctx=ctx)
         first_call_s = time.perf_counter() - w0
+        # ... and the rest of one whole warm-up run: the second and third calls of a process pay one-off costs of their
+        # own (lazy loading of the kernels only a warm sweep launches, the first recording of a leaf's launch
+        # sequence: 140 ms once on C3), which belong to the process, not to an iteration
+        for i in range(1, iters):
+            dw = E.hooi_sweep(host_t, spec, dw, tree, "jacobi", ctx=ctx, tensor_unchanged=True)
         ctx.synchronize()
         d = E.Decomposition(None, f0)
         w0 = time.perf_counter()
@@ -543,8 +548,9 @@ def run_b200(args):
                "h2d_bytes_per_step": (total * 8) // iters + fbytes, "d2h_bytes_per_step": fbytes + cbytes,
                "host_memory": "pinned",
                "what": "whole run of the config's %d iterations through the by-value C-ABI call, upload of the tensor "
-                       "(first call) included, later calls with TP_HOST_TENSOR_UNCHANGED; mean per iteration; device "
-                       "allocations warm (one earlier call on the same context)" % iters,
+                       "(first call) included, later calls with TP_HOST_TENSOR_UNCHANGED; mean per iteration; process "
+                       "warm (one earlier run of the same calls on the same context: allocations, lazily loaded "
+                       "kernels; the timed run uploads, starts cold and records its graphs again)" % iters,
                "first_call_of_a_process_s": first_call_s, "per_call_ms": per_call_ms,
                "max_sin_principal_angle_vs_resident_run": agree,
                "by_value_every_call": {"value": every_s, "unit": "s/iter", "h2d_bytes_per_step": total * 8 + fbytes,
