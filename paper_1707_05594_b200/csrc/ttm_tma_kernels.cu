@@ -31,6 +31,7 @@ namespace {
 constexpr int kConsumerWarps = 8;
 constexpr int kThreads = 32 * (1 + kConsumerWarps);
 constexpr int kKC = 16;  // contraction steps per stage = rows (or l-values) of one TMA box
+constexpr bool kSkewConsumers = true;
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
 
@@ -222,6 +223,16 @@ __global__ void __launch_bounds__(kThreads, (KT * NT <= 12) ? 2 : 1)
     }
   }
 
+  // The two consumer warps of an SM sub-partition (cw and cw + 4) run the same code on the same stages at the same
+  // rate, so left alone they reach every stage boundary -- barrier wait, fence, arrive, no DMMA in flight --
+  // together and the FP64 pipe of their sub-partition idles for the length of it.  Half a stage of head start for
+  // one of them lasts for the whole kernel (both advance at the pipe's pace) and puts each warp's boundary under the
+  // other's DMMAs.
+  if (kSkewConsumers && cw >= kConsumerWarps / 2) {
+    const long long t0 = clock64();
+    while (clock64() - t0 < static_cast<long long>(KT) * NT * 64) {
+    }
+  }
   int stage = 0;
   unsigned parity = 0;
   for (long long j = 0; j < my_tiles; ++j) {
